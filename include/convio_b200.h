@@ -1,0 +1,140 @@
+/*
+ * convio_b200 -- C-ABI of the B200 (sm_100a) convolution dataflow kernels.
+ *
+ * The reference package (arxiv 2012.15667 "convio", pure Python) has no FFI:
+ * its "execution" of a dataflow is the word-counting simulator.  This ABI is
+ * the device boundary *below* the reference's Python API:
+ *
+ *   reference interface replaced                      entry point here
+ *   ----------------------------------------------------------------------
+ *   dataflow.simulate(plan_direct_dataflow(...))      convio_conv_direct_f32
+ *     pkg/src/convio/dataflow.py:219-250, 316-338       (executes the schedule)
+ *   dataflow.simulate(plan_winograd_dataflow(...))    convio_conv_winograd_f32
+ *     pkg/src/convio/dataflow.py:253-310, 316-338
+ *   shared_kernel_transform=True (J_k shared)         convio_winograd_filter_transform
+ *     pkg/src/convio/dataflow.py:273, dag.py:353-383
+ *   autotune.measure -> legality of a TileConfig      convio_query
+ *     pkg/src/convio/autotune.py:173-190 (ScheduleError/InfeasibleTileError)
+ *
+ * Conventions
+ *   - Plain pointers and sizes only.  All device buffers (x, w, y, workspace)
+ *     are allocated by the caller; the library never allocates in the hot path
+ *     and keeps no pointer after return.  `stream` is a cudaStream_t (NULL =
+ *     legacy default stream); all work is ordered on it.  Calls are reentrant.
+ *   - Activations are fp32 in the layout named by `layout`:
+ *       CONVIO_LAYOUT_CHW = NCHW, CONVIO_LAYOUT_CWH = N C W H (x outer, y inner),
+ *       CONVIO_LAYOUT_HWC = NHWC (the reference's LAYOUTS axis,
+ *       pkg/src/convio/dataflow.py:23).  Output uses the same layout.
+ *   - Filters are fp32 KCRS (reference index map wt[oc, c, ky, kx],
+ *     pkg/src/convio/dag.py:262-267).
+ *   - Padding is zero-filled in the kernel (no padded copy is made).
+ *   - Return codes mirror the reference CLI's exit classes
+ *     (pkg/src/convio/cli.py:472-485):
+ *       0 OK, 2 invalid argument, 3 geometry / infeasible tile / capacity,
+ *       4 CUDA or internal error.  convio_last_error() gives the message
+ *       (thread-local, valid until the next call on the same thread).
+ */
+#ifndef CONVIO_B200_H
+#define CONVIO_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CONVIO_OK 0
+#define CONVIO_EINVAL 2
+#define CONVIO_EINFEASIBLE 3
+#define CONVIO_EINTERNAL 4
+
+#define CONVIO_LAYOUT_CHW 0
+#define CONVIO_LAYOUT_CWH 1
+#define CONVIO_LAYOUT_HWC 2
+
+#define CONVIO_ALG_DIRECT 0
+#define CONVIO_ALG_WINOGRAD 1
+
+/* One convolution layer (valid geometry after zero padding `pad`). */
+typedef struct convio_conv_desc {
+    int32_t n, c, h, w;   /* batch, input channels, input height, width (unpadded) */
+    int32_t k, r, s;      /* output channels, kernel height, kernel width */
+    int32_t stride, pad;
+    int32_t layout;       /* CONVIO_LAYOUT_* */
+} convio_conv_desc;
+
+/* Mirrors TileConfig (pkg/src/convio/dataflow.py:34-76); e = 0 for None. */
+typedef struct convio_tile {
+    int32_t x, y, z, s_b;
+    int32_t n_xt, n_yt, n_zt;
+    int32_t layout;
+    int32_t e;
+} convio_tile;
+
+/* Device projection of a tile: what convio_conv_* would launch. */
+typedef struct convio_launch_info {
+    int32_t legal;              /* 1 if launchable, else reason[] says why */
+    int32_t grid_x, grid_y, grid_z;
+    int32_t block_threads;
+    int32_t smem_bytes;         /* dynamic shared memory per block */
+    int32_t regs_per_thread;    /* from cudaFuncGetAttributes (0 if unknown) */
+    int32_t channel_chunk;      /* input channels per pipeline stage (paper alpha) */
+    int32_t stages;             /* pipeline depth */
+    int32_t smem_pitch;         /* padded row pitch of the staged input tile */
+    int32_t p, q;               /* output height, width */
+    int64_t flops;              /* algorithmic flops of the launch */
+    int64_t workspace_bytes;    /* workspace the call needs */
+    char reason[160];
+} convio_launch_info;
+
+int convio_version(void);
+const char *convio_last_error(void);
+
+/* Legality + launch shape of (desc, tile, algorithm); never launches. */
+int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t algorithm,
+                 convio_launch_info *out);
+
+/* Workspace bytes for convio_conv_* with this tile (packed / transformed filters). */
+int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *tile,
+                               int32_t algorithm);
+
+/* Repack KCRS filters to the direct kernel's C R S K layout (ws >= K*C*R*S floats). */
+int convio_pack_filter_direct(const convio_conv_desc *desc, const float *w, float *w_packed,
+                              void *stream);
+
+/* Direct convolution y = conv(x, w), the output-stationary dataflow
+ * (x*y*z outputs per block resident in registers, channel stages through
+ * shared memory).  tile == NULL picks the default device tile.  If
+ * `w_is_packed` the filter is already in convio_pack_filter_direct layout. */
+int convio_conv_direct_f32(const convio_conv_desc *desc, const convio_tile *tile,
+                           const float *x, const float *w, int32_t w_is_packed,
+                           const float *bias, int32_t relu, float *y,
+                           void *workspace, size_t workspace_bytes, void *stream);
+
+/* Winograd filter transform U[xi][c][k] = (G g G^T)[xi] for F(e x e, r x r). */
+int convio_winograd_filter_transform(const convio_conv_desc *desc, int32_t e, const float *w,
+                                     float *u, void *stream);
+
+/* Fused Winograd F(e x e, 3 x 3): input transform, element-wise batched GEMM
+ * over channels, output transform in one kernel, transformed tiles on chip.
+ * If `w_is_transformed`, w holds U from convio_winograd_filter_transform. */
+int convio_conv_winograd_f32(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,
+                             const float *x, const float *w, int32_t w_is_transformed,
+                             const float *bias, int32_t relu, float *y,
+                             void *workspace, size_t workspace_bytes, void *stream);
+
+/* The transform matrices the kernels use (row-major AT e*m, G m*r, BT m*m). */
+int convio_winograd_matrices(int32_t e, int32_t r, float *at, float *g, float *bt);
+
+/* FP32 FFMA throughput probe (the CUDA-core roofline denominator):
+ * runs `iters` FMA chains on every SM; returns flops executed in *flops. */
+int convio_ffma_peak(float *sink, int32_t blocks, int32_t iters, int64_t *flops, void *stream);
+
+/* Number of kernel launches the last convio_conv_* call on this thread issued. */
+int convio_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CONVIO_B200_H */

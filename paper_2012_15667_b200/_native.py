@@ -1,0 +1,142 @@
+"""ctypes binding of ``libconvio_b200.so`` (the C-ABI in ``include/convio_b200.h``).
+
+The library is built in-tree (``paper_2012_15667_b200/lib``) by
+``__graft_entry__.build()`` / ``make -C paper_2012_15667_b200/csrc``.  There
+is no fallback: if the library is missing every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .dataflow import LAYOUTS, InfeasibleTileError, ScheduleError
+from .model import GeometryError
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
+LIB_PATH = os.path.join(LIB_DIR, "libconvio_b200.so")
+
+ALG_DIRECT, ALG_WINOGRAD = 0, 1
+
+
+class ConvDesc(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in
+                ("n", "c", "h", "w", "k", "r", "s", "stride", "pad", "layout")]
+
+
+class Tile(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in
+                ("x", "y", "z", "s_b", "n_xt", "n_yt", "n_zt", "layout", "e")]
+
+
+class LaunchInfo(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_int32) for f in
+                ("legal", "grid_x", "grid_y", "grid_z", "block_threads", "smem_bytes",
+                 "regs_per_thread", "channel_chunk", "stages", "smem_pitch", "p", "q")] + [
+        ("flops", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+        ("reason", ctypes.c_char * 160)]
+
+    def to_dict(self) -> dict:
+        d = {f: getattr(self, f) for f, _ in self._fields_ if f != "reason"}
+        d["reason"] = self.reason.decode(errors="replace")
+        return d
+
+
+class DeviceError(RuntimeError):
+    """CUDA / internal failure inside libconvio_b200 (return code 4)."""
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load (once) and return the C-ABI library; raises if it is not built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"{LIB_PATH} is missing -- build it with `python -c 'import __graft_entry__ as g; "
+                "g.build()'` or `make -C paper_2012_15667_b200/csrc`; there is no CPU fallback")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I32, I64, SZ = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+        D, T, LI = ctypes.POINTER(ConvDesc), ctypes.POINTER(Tile), ctypes.POINTER(LaunchInfo)
+        sigs = {
+            "convio_version": ([], ctypes.c_int),
+            "convio_last_error": ([], ctypes.c_char_p),
+            "convio_last_launch_count": ([], ctypes.c_int),
+            "convio_query": ([D, T, I32, LI], ctypes.c_int),
+            "convio_workspace_bytes": ([D, T, I32], I64),
+            "convio_pack_filter_direct": ([D, P, P, P], ctypes.c_int),
+            "convio_conv_direct_f32": ([D, T, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
+            "convio_winograd_filter_transform": ([D, I32, P, P, P], ctypes.c_int),
+            "convio_conv_winograd_f32": ([D, T, I32, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
+            "convio_winograd_matrices": ([I32, I32, P, P, P], ctypes.c_int),
+            "convio_ffma_peak": ([P, I32, I32, ctypes.POINTER(I64), P], ctypes.c_int),
+        }
+        for name, (args, res) in sigs.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+        return L
+
+
+EXPORTED = (
+    "convio_version", "convio_last_error", "convio_last_launch_count", "convio_query",
+    "convio_workspace_bytes", "convio_pack_filter_direct", "convio_conv_direct_f32",
+    "convio_winograd_filter_transform", "convio_conv_winograd_f32", "convio_winograd_matrices",
+    "convio_ffma_peak",
+)
+
+
+def last_error() -> str:
+    msg = lib().convio_last_error()
+    return msg.decode(errors="replace") if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a C-ABI return code onto the reference's exception classes."""
+    if rc == 0:
+        return
+    msg = last_error() or what
+    if rc == 2:
+        raise ValueError(msg)
+    if rc == 3:
+        low = msg.lower()
+        if "resident" in low or "does not divide" in low or "not divisible" in low:
+            raise ScheduleError(msg)
+        if "larger than" in low or "unit stride" in low or "square" in low:
+            raise GeometryError(msg)
+        raise InfeasibleTileError(msg)
+    raise DeviceError(f"{what}: {msg} (rc={rc})")
+
+
+def make_tile(tile, layout: int | None = None) -> Tile | None:
+    if tile is None:
+        return None
+    t = Tile()
+    for f in ("x", "y", "z", "s_b", "n_xt", "n_yt", "n_zt"):
+        setattr(t, f, int(getattr(tile, f)))
+    t.layout = LAYOUTS.index(tile.layout) if layout is None else layout
+    t.e = int(tile.e or 0)
+    return t
+
+
+def make_desc(n, c, h, w, k, r, s, stride, pad, layout: int) -> ConvDesc:
+    return ConvDesc(n, c, h, w, k, r, s, stride, pad, layout)
+
+
+def query(desc: ConvDesc, tile: Tile | None, algorithm: int) -> tuple[int, dict]:
+    info = LaunchInfo()
+    rc = lib().convio_query(ctypes.byref(desc), ctypes.byref(tile) if tile else None,
+                            algorithm, ctypes.byref(info))
+    d = info.to_dict()
+    if rc != 0 and not d["reason"]:
+        d["reason"] = last_error()
+    return rc, d

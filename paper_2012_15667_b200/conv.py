@@ -1,0 +1,218 @@
+"""Device convolution entry points: the schedules of :mod:`.dataflow` run as
+sm_100a CUDA kernels through the C-ABI (``libconvio_b200.so``).
+
+* :func:`conv_direct`   -- output-stationary direct dataflow
+  (reference schedule ``pkg/src/convio/dataflow.py:219-250``)
+* :func:`conv_winograd` -- fused Winograd F(e x e, 3 x 3) dataflow with the
+  shared kernel transform (``dataflow.py:253-310``, ``shared_kernel_transform``)
+* :func:`winograd_filter_transform` -- ``U = G g G^T`` once per filter
+
+Tensors are PyTorch CUDA fp32 tensors with logical shape NCHW / KCRS; the
+physical activation layout (``CHW`` = NCHW, ``HWC`` = NHWC/channels_last,
+``CWH`` = N C W H) is read from the strides and is the reference's
+``LAYOUTS`` axis.  PyTorch is used for memory and streams only -- every
+output value is produced by this package's kernels; there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _native as N
+from .dataflow import LAYOUTS, TileConfig
+
+__all__ = ["conv_direct", "conv_winograd", "winograd_filter_transform", "pack_filter_direct",
+           "infer_layout", "to_layout", "empty_act", "query", "last_launch_count"]
+
+
+def _strides_for(layout: str, n: int, c: int, h: int, w: int) -> tuple[int, int, int, int]:
+    if layout == "HWC":
+        return (h * w * c, 1, w * c, c)
+    if layout == "CWH":
+        return (c * h * w, h * w, 1, h)
+    return (c * h * w, h * w, w, 1)
+
+
+def infer_layout(x: torch.Tensor) -> str:
+    """Physical layout of a logical-NCHW tensor; raises for anything else."""
+    n, c, h, w = x.shape
+    st = tuple(x.stride())
+    for lay in LAYOUTS:   # CHW first: wins when sizes make layouts coincide
+        want = _strides_for(lay, n, c, h, w)
+        if all(sz == 1 or a == b for sz, a, b in zip(x.shape, st, want)):
+            return lay
+    raise ValueError(f"tensor strides {st} match none of the layouts {LAYOUTS}")
+
+
+def empty_act(n: int, c: int, h: int, w: int, layout: str = "CHW",
+              device=None, dtype=torch.float32) -> torch.Tensor:
+    """Uninitialised activation tensor, logical NCHW, physical ``layout``."""
+    return torch.empty_strided((n, c, h, w), _strides_for(layout, n, c, h, w),
+                               device=device, dtype=dtype)
+
+
+def to_layout(x: torch.Tensor, layout: str) -> torch.Tensor:
+    """Copy ``x`` into ``layout`` (a separate, explicitly requested staging step)."""
+    if infer_layout(x) == layout:
+        return x
+    y = empty_act(*x.shape, layout=layout, device=x.device, dtype=x.dtype)
+    y.copy_(x)
+    return y
+
+
+def _check_tensor(t: torch.Tensor, name: str) -> None:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor (no CPU fallback)")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{name} must be float32, got {t.dtype}")
+
+
+def _stream_ptr(stream) -> ctypes.c_void_p:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def _ptr(t: torch.Tensor | None) -> ctypes.c_void_p | None:
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _desc(x: torch.Tensor, w: torch.Tensor, stride: int, padding: int, layout: str) -> N.ConvDesc:
+    n, c, h, wd = x.shape
+    k, c2, r, s = w.shape
+    if c2 != c:
+        raise ValueError(f"filter has {c2} input channels, input has {c}")
+    return N.make_desc(n, c, h, wd, k, r, s, stride, padding, LAYOUTS.index(layout))
+
+
+def _out_hw(h, w, r, s, stride, padding):
+    return (h + 2 * padding - r) // stride + 1, (w + 2 * padding - s) // stride + 1
+
+
+def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CHW",
+          tile: TileConfig | None = None, algorithm: str = "direct") -> dict:
+    """Device projection of ``tile`` for this layer (legality + launch shape)."""
+    n, c, h, w = x_shape
+    k, _, r, s = w_shape
+    desc = N.make_desc(n, c, h, w, k, r, s, stride, padding, LAYOUTS.index(layout))
+    alg = N.ALG_DIRECT if algorithm == "direct" else N.ALG_WINOGRAD
+    rc, info = N.query(desc, N.make_tile(tile), alg)
+    info["rc"] = rc
+    return info
+
+
+def pack_filter_direct(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """KCRS -> C R S K repack consumed by the direct kernel (cacheable per layer)."""
+    _check_tensor(w, "w")
+    w = w.contiguous()
+    k, c, r, s = w.shape
+    out = torch.empty((c, r, s, k), device=w.device, dtype=torch.float32)
+    desc = N.make_desc(1, c, r, s, k, r, s, 1, 0, 0)
+    N.check(N.lib().convio_pack_filter_direct(ctypes.byref(desc), _ptr(w), _ptr(out),
+                                              _stream_ptr(stream)), "pack_filter_direct")
+    return out
+
+
+def conv_direct(x: torch.Tensor, w: torch.Tensor, stride: int = 1, padding: int = 0,
+                tile: TileConfig | None = None, bias: torch.Tensor | None = None,
+                relu: bool = False, out: torch.Tensor | None = None, stream=None,
+                w_packed: torch.Tensor | None = None,
+                workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """``y = conv2d(x, w)`` (+bias, +ReLU) by the direct dataflow kernel.
+
+    ``tile`` is a :class:`TileConfig`; ``None`` lets the library pick its
+    default device tile.  ``w_packed`` (from :func:`pack_filter_direct`)
+    skips the per-call filter repack.  Illegal tiles raise the reference's
+    ``ScheduleError`` / ``InfeasibleTileError``.
+    """
+    _check_tensor(x, "x")
+    _check_tensor(w, "w")
+    layout = infer_layout(x)
+    if tile is not None and tile.layout != layout:
+        raise ValueError(f"tile layout {tile.layout} but input is {layout}")
+    desc = _desc(x, w, stride, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, stride, padding)
+    if out is None:
+        out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
+    else:
+        _check_tensor(out, "out")
+        if tuple(out.shape) != (desc.n, desc.k, p, q) or infer_layout(out) != layout:
+            raise ValueError("out has the wrong shape or layout")
+    if bias is not None:
+        _check_tensor(bias, "bias")
+    if w_packed is not None:
+        wsrc, is_packed, ws, ws_bytes = w_packed, 1, None, 0
+    else:
+        need = desc.k * desc.c * desc.r * desc.s
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, device=x.device, dtype=torch.float32)
+        wsrc, is_packed, ws, ws_bytes = w.contiguous(), 0, workspace, 4 * need
+    rc = N.lib().convio_conv_direct_f32(
+        ctypes.byref(desc), ctypes.byref(N.make_tile(tile)) if tile is not None else None,
+        _ptr(x), _ptr(wsrc), is_packed, _ptr(bias), int(bool(relu)), _ptr(out),
+        _ptr(ws), ws_bytes, _stream_ptr(stream))
+    N.check(rc, "conv_direct")
+    return out
+
+
+def winograd_filter_transform(w: torch.Tensor, e: int, stream=None) -> torch.Tensor:
+    """``U[xi][c][k] = (G g G^T)[xi]`` for F(e x e, 3 x 3) -- the shared J_k."""
+    _check_tensor(w, "w")
+    w = w.contiguous()
+    k, c, r, s = w.shape
+    m = e + r - 1
+    u = torch.empty((m * m, c, k), device=w.device, dtype=torch.float32)
+    desc = N.make_desc(1, c, max(r, 3), max(s, 3), k, r, s, 1, 0, 0)
+    N.check(N.lib().convio_winograd_filter_transform(ctypes.byref(desc), e, _ptr(w), _ptr(u),
+                                                     _stream_ptr(stream)),
+            "winograd_filter_transform")
+    return u
+
+
+def conv_winograd(x: torch.Tensor, w: torch.Tensor, e: int = 2, padding: int = 0,
+                  tile: TileConfig | None = None, bias: torch.Tensor | None = None,
+                  relu: bool = False, out: torch.Tensor | None = None, stream=None,
+                  u: torch.Tensor | None = None,
+                  workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """``y = conv2d(x, w)`` (3x3, stride 1) by the fused Winograd F(e, 3) kernel.
+
+    ``u`` (from :func:`winograd_filter_transform`) skips the per-call filter
+    transform.  Outputs not divisible by the tile are refused like the model
+    refuses ragged tiles.
+    """
+    _check_tensor(x, "x")
+    _check_tensor(w, "w")
+    layout = infer_layout(x)
+    if tile is not None and tile.layout != layout:
+        raise ValueError(f"tile layout {tile.layout} but input is {layout}")
+    desc = _desc(x, w, 1, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, 1, padding)
+    if out is None:
+        out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
+    else:
+        _check_tensor(out, "out")
+        if tuple(out.shape) != (desc.n, desc.k, p, q) or infer_layout(out) != layout:
+            raise ValueError("out has the wrong shape or layout")
+    if bias is not None:
+        _check_tensor(bias, "bias")
+    m = e + desc.r - 1
+    if u is not None:
+        wsrc, is_t, ws, ws_bytes = u, 1, None, 0
+    else:
+        need = m * m * desc.c * desc.k
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, device=x.device, dtype=torch.float32)
+        wsrc, is_t, ws, ws_bytes = w.contiguous(), 0, workspace, 4 * need
+    rc = N.lib().convio_conv_winograd_f32(
+        ctypes.byref(desc), ctypes.byref(N.make_tile(tile)) if tile is not None else None, e,
+        _ptr(x), _ptr(wsrc), is_t, _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes,
+        _stream_ptr(stream))
+    N.check(rc, "conv_winograd")
+    return out
+
+
+def last_launch_count() -> int:
+    """Kernel launches issued by the last conv call on this thread."""
+    return int(N.lib().convio_last_launch_count())

@@ -1,0 +1,77 @@
+// Shared device/host helpers for the convio_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/convio_b200.h"
+
+namespace convio {
+
+// ---- error plumbing (thread-local message, codes from convio_b200.h) -------
+void set_error(const char *fmt, ...);
+void clear_error();
+void note_launch();
+void reset_launches();
+
+struct Status {
+    int code;
+};
+
+#define CONVIO_CUDA_TRY(expr)                                                     \
+    do {                                                                          \
+        cudaError_t _e = (expr);                                                  \
+        if (_e != cudaSuccess) {                                                  \
+            ::convio::set_error("%s failed: %s", #expr, cudaGetErrorString(_e)); \
+            return CONVIO_EINTERNAL;                                              \
+        }                                                                         \
+    } while (0)
+
+// ---- layouts ------------------------------------------------------------------
+// Element strides of an activation tensor [n][c][h][w] stored in `layout`.
+struct ActStrides {
+    int64_t n, c, y, x;
+};
+
+__host__ __device__ inline ActStrides act_strides(int layout, int c, int h, int w) {
+    ActStrides s;
+    s.n = (int64_t)c * h * w;
+    if (layout == CONVIO_LAYOUT_HWC) {        // n h w c
+        s.c = 1; s.x = c; s.y = (int64_t)w * c;
+    } else if (layout == CONVIO_LAYOUT_CWH) { // n c w h
+        s.y = 1; s.x = h; s.c = (int64_t)h * w;
+    } else {                                  // n c h w
+        s.x = 1; s.y = w; s.c = (int64_t)h * w;
+    }
+    return s;
+}
+
+// ---- cp.async (LDGSTS) helpers ------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// 4-byte async copy; src_bytes = 0 zero-fills (halo / channel tail).
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, bool valid) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(valid ? 4 : 0));
+}
+
+// 16-byte async copy (bypasses L1); src_bytes = 0 zero-fills.
+__device__ __forceinline__ void cp_async16(void *dst, const void *src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(valid ? 16 : 0));
+}
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+inline int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+}  // namespace convio

@@ -1,0 +1,120 @@
+"""GPU parity: the sm_100a kernels vs the float64 CPU oracle (``oracle/``).
+
+Tolerances (norm-wise max error ``||y - y_ref||_inf / ||y_ref||_inf``,
+SURVEY.md §8(d)): direct FP32 <= 1e-5, Winograd F(2,3) FP32 <= 1e-4,
+F(4,3) FP32 <= 1e-3.  Every call goes through the C-ABI.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import conv_oracle as co
+from paper_2012_15667_b200 import TileConfig, ScheduleError, InfeasibleTileError
+from paper_2012_15667_b200 import conv as C
+
+pytestmark = pytest.mark.gpu
+
+TOL_DIRECT = 1e-5
+TOL_WINO = {2: 1e-4, 4: 1e-3}
+
+
+def _inputs(n, c, h, w, k, r, s, seed=0):
+    g = np.random.default_rng(seed)
+    x = g.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    g1 = np.random.default_rng(seed + 1)
+    wt = (g1.uniform(-1, 1, (k, c, r, s)) / np.sqrt(c * r * s)).astype(np.float32)
+    return x, wt
+
+
+def _dev(a, layout="CHW"):
+    t = torch.from_numpy(a).cuda()
+    return C.to_layout(t, layout) if t.dim() == 4 and layout != "CHW" else t
+
+
+DIRECT_CASES = [
+    # (n, c, h, w, k, r, stride, pad, tile)
+    (1, 64, 56, 56, 64, 3, 1, 1, TileConfig(56, 4, 64, 32768, 7, 4, 8)),
+    (1, 64, 56, 56, 64, 3, 1, 1, TileConfig(8, 8, 32, 16384, 1, 8, 4)),
+    (2, 16, 14, 14, 32, 3, 1, 1, TileConfig(14, 2, 32, 8192, 2, 2, 4)),
+    (1, 3, 32, 32, 16, 3, 1, 1, TileConfig(32, 4, 16, 8192, 4, 4, 2)),
+    (2, 32, 28, 28, 64, 3, 2, 1, TileConfig(14, 2, 16, 8192, 2, 2, 4)),
+    (1, 8, 7, 7, 16, 3, 1, 1, TileConfig(7, 7, 16, 4096, 1, 7, 4)),
+    (2, 32, 16, 16, 64, 1, 1, 0, TileConfig(16, 4, 64, 16384, 2, 4, 8)),
+    (1, 5, 9, 11, 6, 3, 1, 0, None),    # ragged: library default tile / generic path
+    (1, 3, 23, 23, 8, 5, 2, 2, None),   # 5x5 stride 2: generic kernel
+]
+
+
+@pytest.mark.parametrize("case", DIRECT_CASES, ids=[str(i) for i in range(len(DIRECT_CASES))])
+def test_direct_matches_oracle(case):
+    n, c, h, w, k, r, stride, pad, tile = case
+    x, wt = _inputs(n, c, h, w, k, r, r)
+    y = C.conv_direct(_dev(x), _dev(wt), stride=stride, padding=pad, tile=tile)
+    torch.cuda.synchronize()
+    ref = co.direct_conv(x, wt, stride, pad)
+    assert y.shape == ref.shape
+    assert co.rel_err(y.cpu().numpy(), ref) <= TOL_DIRECT
+
+
+@pytest.mark.parametrize("layout", ["HWC", "CWH"])
+def test_direct_layouts(layout):
+    x, wt = _inputs(2, 16, 28, 28, 32, 3, 3)
+    tile = TileConfig(28, 4, 32, 16384, 7, 4, 4, layout=layout)
+    y = C.conv_direct(_dev(x, layout), _dev(wt), stride=1, padding=1, tile=tile)
+    assert C.infer_layout(y) == layout
+    ref = co.direct_conv(x, wt, 1, 1)
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= TOL_DIRECT
+
+
+def test_direct_bias_relu_and_packed_filter():
+    x, wt = _inputs(1, 32, 14, 14, 16, 3, 3)
+    b = np.linspace(-0.5, 0.5, 16).astype(np.float32)
+    wp = C.pack_filter_direct(_dev(wt))
+    y = C.conv_direct(_dev(x), _dev(wt), padding=1, bias=_dev(b), relu=True, w_packed=wp,
+                      tile=TileConfig(14, 2, 16, 8192, 2, 2, 2))
+    ref = np.maximum(co.direct_conv(x, wt, 1, 1) + b[None, :, None, None], 0)
+    assert co.rel_err(y.cpu().numpy(), ref) <= TOL_DIRECT
+
+
+def test_direct_illegal_tiles_raise_reference_errors():
+    x, wt = _inputs(1, 8, 8, 8, 8, 3, 3)
+    with pytest.raises(ScheduleError):      # does not divide the output
+        C.conv_direct(_dev(x), _dev(wt), padding=1, tile=TileConfig(3, 8, 8, 4096))
+    with pytest.raises(ScheduleError):      # resident set > s_b
+        C.conv_direct(_dev(x), _dev(wt), padding=1, tile=TileConfig(8, 8, 8, 64))
+    with pytest.raises(InfeasibleTileError):  # 1024+ threads
+        C.conv_direct(_dev(x), _dev(wt), padding=1, tile=TileConfig(8, 8, 8, 8192, 8, 8, 8))
+
+
+WINO_CASES = [
+    (1, 64, 56, 56, 64, 2, TileConfig(8, 8, 32, 32768, 8, 8, 4, e=2)),
+    (1, 64, 56, 56, 64, 4, TileConfig(8, 8, 32, 32768, 4, 8, 4, e=4)),
+    (2, 16, 14, 14, 32, 2, TileConfig(14, 14, 8, 32768, 7, 7, 8, e=2)),
+    (2, 16, 16, 16, 16, 4, TileConfig(16, 8, 16, 32768, 4, 8, 4, e=4)),
+    (1, 3, 12, 12, 8, 2, None),
+    (1, 32, 28, 28, 32, 4, None),
+]
+
+
+@pytest.mark.parametrize("case", WINO_CASES, ids=[str(i) for i in range(len(WINO_CASES))])
+def test_winograd_matches_oracle(case):
+    n, c, h, w, k, e, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    y = C.conv_winograd(_dev(x), _dev(wt), e=e, padding=1, tile=tile)
+    ref = co.direct_conv(x, wt, 1, 1)
+    assert co.rel_err(y.cpu().numpy(), ref) <= TOL_WINO[e]
+    # and against the Winograd oracle itself (same transform matrices)
+    assert co.rel_err(y.cpu().numpy(), co.winograd_conv(x, wt, e, 1)) <= TOL_WINO[e]
+
+
+def test_winograd_filter_transform_matches_oracle():
+    from oracle import winograd_mats as wm
+    _, wt = _inputs(1, 8, 4, 4, 16, 3, 3)
+    for e in (2, 4):
+        u = C.winograd_filter_transform(_dev(wt), e).cpu().numpy()
+        g = wm.matrices_float(e, 3)["G"]
+        ref = np.einsum("ij,kcjl,ml->imkc", g, wt.astype(np.float64), g)
+        m = e + 2
+        ref = ref.reshape(m * m, 16, 8).transpose(0, 2, 1)
+        assert np.max(np.abs(u - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
