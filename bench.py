@@ -1,0 +1,449 @@
+"""Benchmark: per-layer conv GFLOP/s on B200 (BASELINE.json metric), JSON line out.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload resnet50|vgg16|single]
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+    python bench.py --impl reference      # the CPU path (oracle port, all host threads)
+
+Workload (default): BASELINE config 4 -- the 16 ResNet-50 3x3 convolutions at
+global batch 256, batch-sharded over the ranks (strong scaling: 256/N images
+per GPU), each layer with the algorithm + tile the lower-bound auto-tuner
+picked on the device (``paper_2012_15667_b200/tuned/b200_resnet50.json``).
+A step = filter prep + conv of all 16 layers over the local batch.  ``value``
+is the whole-job direct-equivalent conv GFLOP/s (sum over ranks of
+2*N*K*C*R*S*P*Q / the max-over-ranks step time).  Inputs are synthetic
+(``x ~ U(-1,1)``, ``w ~ U(-1,1)/sqrt(CRS)``), fp32, resident in HBM; the
+per-step working set is far larger than the 126 MB L2, so no flush is needed
+(``--workload single`` flushes L2 between steps instead).
+
+``e2e`` repeats the step through the public API with pinned-host inputs:
+H2D copy of every layer's input, conv, D2H copy of every output, all inside
+the timed region.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "conv GFLOP/s per layer & DRAM bytes vs I/O lower bound, 1/2/4/8 B200 vs CPU ref"
+L2_BYTES = 126 * 1024 * 1024
+DEFAULT_BATCH = {"resnet50": 256, "vgg16": 32, "single": 1}
+WORKLOAD_NAME = {
+    "resnet50": "ResNet-50 3x3 conv layers (16), batch-sharded (BASELINE config 4)",
+    "vgg16": "VGG-16 3x3 conv layers (13) (BASELINE config 3)",
+    "single": "single 3x3 conv N=1 C=64 56x56 K=64 s1 p1 (BASELINE config 1)",
+}
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines: list[str] = []
+        self._t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.QUERY}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self._t = threading.Thread(target=self._read, daemon=True)
+        self._t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(smax) if smax else None,
+            "reasons": sorted(reasons),
+            "samples": len(sm),
+        }
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port (C, OpenMP) on a bounded sample
+# ---------------------------------------------------------------------------
+def cpu_oracle_gflops(layers, images: int = 1, threads: int = 0):
+    """Time the C oracle (fp32 in, fp64 accumulate) over ``layers`` x ``images``.
+
+    Input generation is excluded; returns (GFLOP/s, seconds of conv work).
+    """
+    import numpy as np
+    from oracle import conv_oracle
+    rng = np.random.default_rng(0)
+    flops, busy = 0, 0.0
+    for spec in layers:
+        x = rng.uniform(-1, 1, (images, spec.c, spec.hw, spec.hw)).astype(np.float32)
+        w = (rng.uniform(-1, 1, (spec.k, spec.c, spec.r, spec.r))
+             / np.sqrt(spec.c * spec.r * spec.r)).astype(np.float32)
+        t1 = time.perf_counter()
+        conv_oracle.c_direct_conv(x, w, spec.stride, spec.pad, threads=threads)
+        busy += time.perf_counter() - t1
+        flops += spec.flops(images)
+    return flops / busy / 1e9, busy
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    """``--impl reference``: the CPU implementation of the path on host cores."""
+    if rank != 0:
+        return
+    from paper_2012_15667_b200.runner import WORKLOADS, expand
+    layers = expand(WORKLOADS[args.workload])
+    cores = os.cpu_count() or 1
+    images = 1
+    # warm-up: W passes over a small sample
+    for _ in range(args.warmup):
+        cpu_oracle_gflops(layers[:1], images, cores)
+    times, flops = [], sum(s.flops(images) for s in layers)
+    for _ in range(args.steps):
+        _, el = cpu_oracle_gflops(layers, images, cores)
+        times.append(el)
+    total = sum(times)
+    value = flops * args.steps / total / 1e9
+    sample = f"{images} image per layer instance x {len(layers)} layers per step (C oracle, fp64 accumulate)"
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * total / args.steps, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD_NAME[args.workload], "global_batch": DEFAULT_BATCH[args.workload],
+                   "sample_batch": images},
+        "cpu_baseline": {"value": round(value, 3), "unit": "GFLOP/s", "cores": cores,
+                         "kind": "port", "sample": sample},
+        "e2e": {"value": round(value, 3), "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+# ---------------------------------------------------------------------------
+def ffma_peak_tflops(torch, stream) -> float:
+    import ctypes
+    from paper_2012_15667_b200 import _native as N
+    sink = torch.zeros(148 * 64, device="cuda")
+    flops = ctypes.c_int64()
+    blocks, iters = 148 * 8, 1500
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    best = 0.0
+    for _ in range(4):
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        N.check(N.lib().convio_ffma_peak(ctypes.c_void_p(sink.data_ptr()), blocks, iters,
+                                         ctypes.byref(flops), sp))
+        b.record(stream)
+        b.synchronize()
+        best = max(best, flops.value / (a.elapsed_time(b) / 1e3) / 1e12)
+    return best
+
+
+def load_profile_traffic() -> dict:
+    """DRAM bytes per launch from the committed ncu summaries (profiles/*.json)."""
+    out = {}
+    pdir = os.path.join(ROOT, "profiles")
+    if not os.path.isdir(pdir):
+        return out
+    for fn in sorted(os.listdir(pdir)):
+        if fn.endswith("_traffic.json"):
+            try:
+                with open(os.path.join(pdir, fn)) as fh:
+                    out.update(json.load(fh))
+            except (OSError, ValueError):
+                pass
+    return out
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "single"])
+    ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--gather", action="store_true", help="all-gather outputs to every rank")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2012_15667_b200 import conv as C
+    from paper_2012_15667_b200.runner import (
+        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, shard_range,
+        gather_outputs)
+    from paper_2012_15667_b200.device import winograd_gemm_flops
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    stream = torch.cuda.current_stream(dev)
+    n_total = args.batch or DEFAULT_BATCH[args.workload]
+    lo, hi = shard_range(n_total, rank, world)
+    n_local = hi - lo
+    specs = expand(WORKLOADS[args.workload])
+    plans = load_plans(args.workload)
+    layers = [ConvLayer(s, make_weights(s, dev, 1000 + i), plans.get(s.name))
+              for i, s in enumerate(specs)]
+    xs = [make_input(s, n_local, dev, seed=7919 * (i + 1) + lo) for i, s in enumerate(specs)]
+    ys = [C.empty_act(n_local, s.k, s.out_hw, s.out_hw, "CHW", device=dev) for s in specs]
+    work_bytes = sum(x.numel() * 4 for x in xs) + sum(y.numel() * 4 for y in ys)
+    flush = work_bytes < 4 * L2_BYTES
+    scratch = torch.empty(2 * L2_BYTES // 4, device=dev) if flush else None
+
+    def step(events=None):
+        launches = 0
+        for i, layer in enumerate(layers):
+            layer.prepare(dev, stream)
+            launches += 1
+            if events is not None:
+                events[i][0].record(stream)
+            layer.run(xs[i], out=ys[i], stream=stream)
+            if events is not None:
+                events[i][1].record(stream)
+            launches += layer.launches
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+
+    # ---- device-timed region: exactly K steps --------------------------------
+    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in layers]
+          for _ in range(args.steps)]
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    launches = 0
+    barrier()
+    torch.cuda.synchronize(dev)
+    if flush:
+        total_ms = 0.0
+        for k in range(args.steps):
+            scratch.fill_(float(k))
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            launches += step(ev[k])
+            b.record(stream)
+            b.synchronize()
+            total_ms += a.elapsed_time(b)
+        barrier()
+        torch.cuda.synchronize(dev)
+    else:
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for k in range(args.steps):
+            launches += step(ev[k])
+        b.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        torch.cuda.synchronize(dev)
+        total_ms = a.elapsed_time(b)
+    clk = clocks.stop()
+    t_max_ms = max_over_ranks(total_ms)
+    flops_local = sum(s.flops(n_local) for s in specs)
+    flops_all = sum_over_ranks(float(flops_local))
+    value = flops_all * args.steps / (t_max_ms / 1e3) / 1e9
+
+    # per-layer breakdown (rank-local kernel times, median over steps)
+    per_layer = []
+    fam_time = {"direct": 0.0, "winograd": 0.0}
+    fam_flops = {"direct": 0.0, "winograd": 0.0}
+    fam_launches = {"direct": 0, "winograd": 0}
+    for i, (s, layer) in enumerate(zip(specs, layers)):
+        ts = [ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)]
+        t_med = statistics.median(ts)
+        f_dir = s.flops(n_local)
+        if layer.algorithm == "winograd":
+            f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
+        else:
+            f_alg = f_dir
+        fam_time[layer.algorithm] += sum(ts)
+        fam_flops[layer.algorithm] += f_alg * args.steps
+        fam_launches[layer.algorithm] += args.steps
+        comp_bytes = 4 * (n_local * s.c * s.hw * s.hw + s.k * s.c * s.r * s.r
+                          + n_local * s.k * s.out_hw * s.out_hw)
+        per_layer.append({
+            "layer": s.name, "algorithm": layer.algorithm + (f"F({layer.e},3)" if layer.algorithm == "winograd" else ""),
+            "tile": None if layer.tile is None else [layer.tile.x, layer.tile.y, layer.tile.z, layer.tile.s_b,
+                                                     layer.tile.n_xt, layer.tile.n_yt, layer.tile.n_zt],
+            "ms": round(t_med, 4), "gflops": round(f_dir / (t_med / 1e3) / 1e9, 1),
+            "q_dram_bytes": comp_bytes,
+        })
+
+    # ---- roofline of the dominant kernel family --------------------------------
+    dom = max(fam_time, key=fam_time.get)
+    achieved = fam_flops[dom] / (fam_time[dom] / 1e3) / 1e12 if fam_time[dom] else 0.0
+    peak = ffma_peak_tflops(torch, stream)
+    traffic_tab = load_profile_traffic()
+    traffic = traffic_tab.get(f"{args.workload}:{dom}")
+
+    # ---- end-to-end through the public API with host buffers -------------------
+    e2e = None
+    if not args.no_e2e:
+        hx = [x.cpu().pin_memory() for x in xs]
+        hy = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for y in ys]
+        dx = [torch.empty_like(x) for x in xs]
+        h2d = sum(h.numel() * 4 for h in hx)
+        d2h = sum(h.numel() * 4 for h in hy)
+
+        def e2e_step():
+            for i, layer in enumerate(layers):
+                dx[i].copy_(hx[i], non_blocking=True)
+                y = layer.forward(dx[i], out=ys[i], stream=stream)
+                hy[i].copy_(y, non_blocking=True)
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        b.record(stream)
+        b.synchronize()
+        barrier()
+        e_ms = max_over_ranks(a.elapsed_time(b))
+        e2e = {"value": round(flops_all * args.steps / (e_ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+               "h2d_bytes_per_step": int(sum_over_ranks(float(h2d))),
+               "d2h_bytes_per_step": int(sum_over_ranks(float(d2h))),
+               "ms_per_step": round(e_ms / args.steps, 3)}
+
+    gathered = None
+    if args.gather and world > 1:
+        torch.cuda.synchronize(dev)
+        barrier()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for y in ys:
+            gather_outputs(y, world)
+        b.record(stream)
+        b.synchronize()
+        gathered = {"allgather_ms_per_step": round(max_over_ranks(a.elapsed_time(b)), 3)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            cores = os.cpu_count() or 1
+            sample_layers = specs
+            gf, el = cpu_oracle_gflops(sample_layers, 1, cores)
+            cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                   "sample": f"1 image x {len(sample_layers)} layers, C oracle (oracle/conv_oracle.c), "
+                             f"{el:.1f} s"}
+        except Exception as exc:  # noqa: BLE001
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "GFLOP/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_max_ms / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {
+                "workload": WORKLOAD_NAME[args.workload], "global_batch": n_total,
+                "parallelism": f"batch-sharded x{world} (no data-path collective)",
+                "l2": ("flushed between steps" if flush else
+                       f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
+                "tuned_plans": bool(plans),
+            },
+            "e2e": e2e,
+            "roofline": {
+                "bound": "fp32", "kernel": f"{dom} conv (FFMA)",
+                "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+                "frac": round(achieved / peak, 4) if peak else None,
+                "peak_source": "live FFMA probe (convio_ffma_peak) -- no FP32 entry in MEASURED_PEAKS.json",
+                "traffic": traffic,
+            },
+            "cpu_baseline": cpu,
+            "clocks": clk,
+            "gpu_launches": launches,
+            "per_layer": per_layer,
+        }
+        if gathered:
+            line["gather"] = gathered
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

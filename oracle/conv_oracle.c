@@ -56,15 +56,20 @@ int oracle_direct_conv_f32in(const float *x, const float *wt, double *y,
             for (int ky = 0; ky < kh; ++ky) {
                 for (int kx = 0; kx < kw; ++kx) {
                     const double wv = (double)wk[(ci * kh + ky) * kw + kx];
+                    /* valid output columns for this tap: 0 <= ox*stride + kx - pad < w */
+                    int ox_lo = 0, ox_hi = q;
+                    while (ox_lo < q && ox_lo * stride + kx - pad < 0) ++ox_lo;
+                    while (ox_hi > ox_lo && (ox_hi - 1) * stride + kx - pad >= w) --ox_hi;
                     for (int oy = 0; oy < p; ++oy) {
                         const int iy = oy * stride + ky - pad;
                         if (iy < 0 || iy >= h) continue;        /* zero padding */
-                        const float *xr = xc + (long)iy * w;
+                        const float *xr = xc + (long)iy * w + kx - pad;
                         double *ar = acc + (long)oy * q;
-                        for (int ox = 0; ox < q; ++ox) {
-                            const int ix = ox * stride + kx - pad;
-                            if (ix < 0 || ix >= w) continue;
-                            ar[ox] += (double)xr[ix] * wv;
+                        if (stride == 1) {
+                            for (int ox = ox_lo; ox < ox_hi; ++ox) ar[ox] += (double)xr[ox] * wv;
+                        } else {
+                            for (int ox = ox_lo; ox < ox_hi; ++ox)
+                                ar[ox] += (double)xr[ox * stride] * wv;
                         }
                     }
                 }

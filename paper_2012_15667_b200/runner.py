@@ -1,0 +1,186 @@
+"""Per-layer runner: named CNN 3x3 conv layer sets, tuned plans, batch sharding.
+
+This is the "step after the path" of SURVEY.md §8(f) item 3: a layer list
+(ResNet-50 / VGG-16 3x3 convolutions, the BASELINE.json configs 3-4) whose
+per-layer algorithm and tile come from the lower-bound auto-tuner's device
+results (``tuned/*.json``), executed through the public conv API.
+
+Batch sharding (BASELINE config 4): rank ``g`` of ``G``
+takes images ``[g N/G, (g+1) N/G)``; filters are replicated (same seed on
+every rank); outputs stay sharded unless :func:`gather_outputs` is asked to
+collect them with an NCCL all-gather.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass
+
+import torch
+
+from .dataflow import TileConfig
+from . import conv as C
+from .device import direct_flops
+
+TUNED_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tuned")
+
+
+@dataclass(frozen=True)
+class LayerSpec:
+    name: str
+    c: int
+    hw: int          # input height = width
+    k: int
+    stride: int = 1
+    r: int = 3
+    pad: int = 1
+    count: int = 1   # identical layers in the network
+
+    @property
+    def out_hw(self) -> int:
+        return (self.hw + 2 * self.pad - self.r) // self.stride + 1
+
+    def flops(self, n: int) -> int:
+        """Direct-convolution algorithmic flops for a batch of ``n`` (one instance)."""
+        o = self.out_hw
+        return direct_flops(n, self.c, self.k, o, o, self.r, self.r)
+
+
+# ResNet-50 v1.5 bottleneck 3x3 convolutions (stride on the 3x3), 16 layers
+RESNET50_3X3 = [
+    LayerSpec("res2_3x3", 64, 56, 64, 1, count=3),
+    LayerSpec("res3_3x3_s2", 128, 56, 128, 2),
+    LayerSpec("res3_3x3", 128, 28, 128, 1, count=3),
+    LayerSpec("res4_3x3_s2", 256, 28, 256, 2),
+    LayerSpec("res4_3x3", 256, 14, 256, 1, count=5),
+    LayerSpec("res5_3x3_s2", 512, 14, 512, 2),
+    LayerSpec("res5_3x3", 512, 7, 512, 1, count=2),
+]
+
+# VGG-16: all 13 3x3 convolutions
+VGG16_3X3 = [
+    LayerSpec("conv1_1", 3, 224, 64), LayerSpec("conv1_2", 64, 224, 64),
+    LayerSpec("conv2_1", 64, 112, 128), LayerSpec("conv2_2", 128, 112, 128),
+    LayerSpec("conv3_1", 128, 56, 256), LayerSpec("conv3_2", 256, 56, 256, count=2),
+    LayerSpec("conv4_1", 256, 28, 512), LayerSpec("conv4_2", 512, 28, 512, count=2),
+    LayerSpec("conv5_1", 512, 14, 512, count=3),
+]
+
+# BASELINE config 1/2: the single ResNet 3x3 layer at N=1
+SINGLE_RESNET = [LayerSpec("res2_3x3", 64, 56, 64, 1)]
+
+WORKLOADS = {"resnet50": RESNET50_3X3, "vgg16": VGG16_3X3, "single": SINGLE_RESNET}
+
+
+def expand(layers: list[LayerSpec]) -> list[LayerSpec]:
+    """One entry per layer instance (``count`` copies)."""
+    return [spec for spec in layers for _ in range(spec.count)]
+
+
+def load_plans(workload: str) -> dict:
+    """Tuned per-layer plans ``{name: {"algorithm", "tile", "e"}}`` (empty if untuned)."""
+    path = os.path.join(TUNED_DIR, f"b200_{workload}.json")
+    if not os.path.exists(path):
+        return {}
+    with open(path) as fh:
+        raw = json.load(fh)
+    plans = {}
+    for name, p in raw.get("layers", {}).items():
+        tile = TileConfig(**p["tile"]) if p.get("tile") else None
+        plans[name] = {"algorithm": p.get("algorithm", "direct"), "tile": tile, "e": p.get("e")}
+    return plans
+
+
+class ConvLayer:
+    """One conv layer: filters on the device plus its tuned plan."""
+
+    def __init__(self, spec: LayerSpec, weight: torch.Tensor, plan: dict | None = None):
+        self.spec = spec
+        self.weight = weight
+        plan = plan or {}
+        self.algorithm = plan.get("algorithm", "direct")
+        self.tile = plan.get("tile")
+        self.e = plan.get("e") or 2
+        if self.algorithm == "winograd" and (spec.stride != 1 or spec.r != 3):
+            self.algorithm = "direct"
+            self.tile = None
+        self._ws = None
+        self.launches = 0
+
+    def filter_elems(self) -> int:
+        s = self.spec
+        if self.algorithm == "winograd":
+            m = self.e + s.r - 1
+            return m * m * s.c * s.k
+        return s.k * s.c * s.r * s.r
+
+    def prepare(self, device, stream=None) -> None:
+        """Filter prep into the layer's workspace: KCRS repack (direct) or U = G g G^T."""
+        import ctypes
+        from . import _native as N
+        s = self.spec
+        if self._ws is None or self._ws.device != torch.device(device):
+            self._ws = torch.empty(self.filter_elems(), device=device, dtype=torch.float32)
+        w = self.weight
+        desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 0)
+        sp = C._stream_ptr(stream)
+        if self.algorithm == "winograd":
+            rc = N.lib().convio_winograd_filter_transform(ctypes.byref(desc), self.e,
+                                                          C._ptr(w), C._ptr(self._ws), sp)
+        else:
+            rc = N.lib().convio_pack_filter_direct(ctypes.byref(desc), C._ptr(w),
+                                                   C._ptr(self._ws), sp)
+        N.check(rc, "filter prep")
+
+    def run(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """The conv kernel alone, on the prepared filter."""
+        s = self.spec
+        if self.algorithm == "winograd":
+            u = self._ws.view(-1)
+            y = C.conv_winograd(x, self.weight, e=self.e, padding=s.pad, tile=self.tile, out=out,
+                                stream=stream, u=u)
+        else:
+            wp = self._ws.view(s.c, s.r, s.r, s.k)
+            y = C.conv_direct(x, self.weight, stride=s.stride, padding=s.pad, tile=self.tile,
+                              out=out, stream=stream, w_packed=wp)
+        self.launches = C.last_launch_count()
+        return y
+
+    def forward(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+        """Filter prep + conv (two kernel launches)."""
+        self.prepare(x.device, stream)
+        y = self.run(x, out, stream)
+        self.launches += 1
+        return y
+
+
+def make_weights(spec: LayerSpec, device, seed: int) -> torch.Tensor:
+    """``w ~ U(-1, 1) / sqrt(C R S)``, same on every rank."""
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    w = (torch.rand((spec.k, spec.c, spec.r, spec.r), generator=g) * 2 - 1)
+    return (w / (spec.c * spec.r * spec.r) ** 0.5).to(device)
+
+
+def make_input(spec: LayerSpec, n: int, device, seed: int, layout: str = "CHW") -> torch.Tensor:
+    """``x ~ U(-1, 1)`` generated on the device (seeded per layer and rank)."""
+    g = torch.Generator(device=device).manual_seed(seed)
+    x = C.empty_act(n, spec.c, spec.hw, spec.hw, layout, device=device)
+    x.uniform_(-1.0, 1.0, generator=g)
+    return x
+
+
+def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous image range of ``rank`` (SURVEY.md §8(e) partitioning)."""
+    base, extra = divmod(n_total, world)
+    lo = rank * base + min(rank, extra)
+    return lo, lo + base + (1 if rank < extra else 0)
+
+
+def gather_outputs(y_local: torch.Tensor, world: int) -> torch.Tensor:
+    """NCCL all-gather of batch shards into the full output (only when collecting)."""
+    import torch.distributed as dist
+    out = torch.empty((world * y_local.shape[0],) + tuple(y_local.shape[1:]),
+                      device=y_local.device, dtype=y_local.dtype)
+    dist.all_gather_into_tensor(out, y_local.contiguous())
+    return out
