@@ -95,6 +95,10 @@ const char *convio_last_error(void);
 int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t algorithm,
                  convio_launch_info *out);
 
+/* The tile convio_conv_* uses when called with tile == NULL. */
+int convio_default_tile(const convio_conv_desc *desc, int32_t algorithm, int32_t e,
+                        convio_tile *out);
+
 /* Workspace bytes for convio_conv_* with this tile (packed / transformed filters). */
 int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *tile,
                                int32_t algorithm);

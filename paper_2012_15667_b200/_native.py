@@ -78,6 +78,7 @@ def lib() -> ctypes.CDLL:
             "convio_conv_winograd_f32": ([D, T, I32, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
             "convio_winograd_matrices": ([I32, I32, P, P, P], ctypes.c_int),
             "convio_ffma_peak": ([P, I32, I32, ctypes.POINTER(I64), P], ctypes.c_int),
+            "convio_default_tile": ([D, I32, I32, T], ctypes.c_int),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -91,7 +92,7 @@ EXPORTED = (
     "convio_version", "convio_last_error", "convio_last_launch_count", "convio_query",
     "convio_workspace_bytes", "convio_pack_filter_direct", "convio_conv_direct_f32",
     "convio_winograd_filter_transform", "convio_conv_winograd_f32", "convio_winograd_matrices",
-    "convio_ffma_peak",
+    "convio_ffma_peak", "convio_default_tile",
 )
 
 

@@ -6,6 +6,9 @@
 #include <algorithm>
 #include <atomic>
 #include <mutex>
+#include <unordered_map>
+#include <map>
+#include <array>
 
 #include "direct_fp32.cuh"
 #include "winograd_fp32.cuh"
@@ -26,6 +29,7 @@ void note_launch() { ++t_launches; }
 void reset_launches() { t_launches = 0; }
 
 int direct_instance_count();
+int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
 
 // ---------------------------------------------------------------------------
 // device properties (cached once per process, per device)
@@ -59,6 +63,64 @@ static const DevInfo &dev_info() {
 }
 
 static constexpr int kSmemCapBytes = 227 * 1024;
+
+// ---------------------------------------------------------------------------
+// per-kernel launch attributes, cached: the planners run on every call, so
+// the driver queries (func attributes, occupancy) must not.
+// ---------------------------------------------------------------------------
+struct FitKey {
+    const void *fn;
+    int threads;
+    size_t smem;
+    bool operator==(const FitKey &o) const {
+        return fn == o.fn && threads == o.threads && smem == o.smem;
+    }
+};
+struct FitKeyHash {
+    size_t operator()(const FitKey &k) const {
+        return std::hash<const void *>()(k.fn) ^ (std::hash<int>()(k.threads) * 31u) ^
+               (std::hash<size_t>()(k.smem) * 131u);
+    }
+};
+struct FitVal {
+    int blocks;
+    int regs;
+};
+
+int launch_fit(const void *fn, int threads, size_t smem, int *regs) {
+    static std::mutex mu;
+    static std::unordered_map<FitKey, FitVal, FitKeyHash> cache;
+    static std::unordered_map<const void *, int> regs_of;
+    const DevInfo &dev = dev_info();
+    if (!dev.ok) {
+        *regs = 0;
+        return 1;   // no device: legality of registers/occupancy unverified
+    }
+    std::lock_guard<std::mutex> lock(mu);
+    FitKey key{fn, threads, smem};
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *regs = it->second.regs;
+        return it->second.blocks;
+    }
+    auto rit = regs_of.find(fn);
+    if (rit == regs_of.end()) {
+        cudaFuncAttributes fa;
+        int r = 0;
+        if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) r = fa.numRegs;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dev.max_smem_optin);
+        cudaGetLastError();
+        rit = regs_of.emplace(fn, r).first;
+    }
+    int blocks = 0;
+    if ((int)smem > dev.max_smem_optin ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, fn, threads, smem) != cudaSuccess)
+        blocks = 0;
+    cudaGetLastError();
+    cache.emplace(key, FitVal{blocks, rit->second});
+    *regs = rit->second;
+    return blocks;
+}
 
 // ---------------------------------------------------------------------------
 // descriptor checks
@@ -98,9 +160,11 @@ static int check_desc(const convio_conv_desc *d, int *p, int *q) {
 // shared-memory pitch: smallest pitch >= width minimising bank conflicts of
 // the row reads (each lane reads base + t_y*ystep*pitch + t_x*xstep)
 // ---------------------------------------------------------------------------
-static int choose_pitch(int width, int nxt, int nyt, int nthreads, int xstep, int ystep) {
-    int best_pitch = width, best_conf = 1 << 30;
-    for (int pitch = width; pitch < width + 32; ++pitch) {
+static int choose_pitch(int width, int nxt, int nyt, int nthreads, int xstep, int ystep,
+                        int align) {
+    const int first = (width + align - 1) / align * align;
+    int best_pitch = first, best_conf = 1 << 30;
+    for (int pitch = first; pitch < first + 32; pitch += align) {
         int worst = 0;
         for (int w0 = 0; w0 < nthreads; w0 += 32) {
             int addr[32], na = 0;
@@ -186,31 +250,41 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
                     "no compiled micro-tile TX=%d TY=%d TZ=%d for %dx%d stride %d", TX, TY, TZ,
                     d->s, d->r, d->stride);
     // staging: registers hold the xyz outputs; s_b - xyz words stage inputs
-    // and filters, `ck` channels per stage, double-buffered when it fits.
+    // and filters in an NS-deep ring of `ck`-channel stages.
+    const bool vec_in = (TX * d->stride) % 4 == 0;
+    const int rs = d->r * d->s;
+    // TMA can describe the NCHW input box / packed filter box?
+    bool tma = d->layout == CONVIO_LAYOUT_CHW && d->w % 4 == 0 && ((int64_t)d->h * d->w) % 4 == 0 &&
+               d->k % 4 == 0 && t->z % 4 == 0 && t->z <= 256 && tile_h <= 256 &&
+               ((tile_w + 3) & ~3) <= 256;
+    const int align = (tma || vec_in) ? 4 : 1;
     const int pitch = choose_pitch(tile_w, t->n_xt, t->n_yt, threads, TX * d->stride,
-                                   TY * d->stride);
-    const int64_t per_ch = (int64_t)tile_h * pitch + (int64_t)d->r * d->s * t->z;
+                                   TY * d->stride, align);
+    const int64_t per_ch = (int64_t)tile_h * pitch + (int64_t)rs * t->z;
     const int64_t budget = (int64_t)t->s_b - vol;
-    int stages = budget >= 2 * per_ch ? 2 : 1;
-    int64_t ck = budget / (stages * per_ch);
-    ck = std::max<int64_t>(1, std::min<int64_t>(ck, 16));
-    ck = std::min<int64_t>(ck, d->c);
-    auto stage_bytes = [&](int64_t cks) {
-        int64_t in_stage = (cks * tile_h * pitch + 3) & ~3LL;
-        int64_t w_stage = cks * d->r * d->s * t->z;
-        return 4 * (in_stage + w_stage);
+    int stages = budget / (3 * per_ch) >= 2 ? 3 : (budget >= 2 * per_ch ? 2 : 1);
+    int64_t ck = std::max<int64_t>(1, budget / (stages * per_ch));
+    ck = std::min<int64_t>(std::min<int64_t>(ck, 16), d->c);
+    if (tma && ck * rs > 256) ck = 256 / rs;
+    auto round32 = [](int64_t v) { return (v + 31) & ~31LL; };
+    auto ring_bytes = [&](int64_t cks, int st) {
+        return 4 * st * (round32(cks * tile_h * pitch) + round32(cks * rs * t->z)) + 16 * st;
     };
-    while (ck > 1 && stages * stage_bytes(ck) > kSmemCapBytes) --ck;
-    if (stages * stage_bytes(ck) > kSmemCapBytes && stages == 2) stages = 1;
-    if (stages * stage_bytes(ck) > kSmemCapBytes)
+    while (ck > 1 && ring_bytes(ck, stages) > kSmemCapBytes) --ck;
+    while (stages > 1 && ring_bytes(ck, stages) > kSmemCapBytes) --stages;
+    if (ring_bytes(ck, stages) > kSmemCapBytes)
         return fail(CONVIO_EINFEASIBLE, "staging needs %lld B of shared memory > 227 KB",
-                    (long long)(stages * stage_bytes(ck)));
+                    (long long)ring_bytes(ck, stages));
+    if (tma && stages < 2) tma = false;
     P.bx = t->x; P.by = t->y; P.bz = t->z;
     P.nxt = t->n_xt; P.nyt = t->n_yt; P.nzt = t->n_zt;
     P.ck = (int)ck; P.stages = stages;
     P.tile_w = tile_w; P.tile_h = tile_h; P.pitch = pitch;
-    P.in_stage = (int)((ck * tile_h * pitch + 3) & ~3LL);
-    P.w_stage = (int)(ck * d->r * d->s * t->z);
+    P.in_stage = (int)round32(ck * tile_h * pitch);
+    P.w_stage = (int)round32(ck * rs * t->z);
+    P.use_tma = tma ? 1 : 0;
+    P.in_box_bytes = (int)(4 * ck * tile_h * pitch);
+    P.w_box_bytes = (int)(4 * ck * rs * t->z);
     P.tiles_x = q / t->x; P.tiles_y = p / t->y;
     pl->grid = dim3(d->k / t->z, P.tiles_x * P.tiles_y, d->n);
     if (pl->grid.y > 65535 || pl->grid.z > 65535)
@@ -218,33 +292,39 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
                     pl->grid.y, pl->grid.z);
     pl->fn = fn;
     pl->threads = threads;
-    pl->smem = (size_t)stages * stage_bytes(ck);
-    const DevInfo &dev = dev_info();
-    if (dev.ok) {
-        cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, (const void *)fn) == cudaSuccess) pl->regs = fa.numRegs;
-        if ((int)pl->smem > dev.max_smem_optin)
-            return fail(CONVIO_EINFEASIBLE, "smem %zu > device opt-in max %d", pl->smem,
-                        dev.max_smem_optin);
-        if (pl->smem > 48 * 1024)
-            cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pl->smem);
-        int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, (const void *)fn, threads,
-                                                          pl->smem) != cudaSuccess ||
-            blocks < 1) {
-            cudaGetLastError();
-            return fail(CONVIO_EINFEASIBLE,
-                        "block of %d threads x %d regs + %zu B smem does not fit an SM", threads,
-                        pl->regs, pl->smem);
-        }
-    }
+    pl->smem = (size_t)ring_bytes(ck, stages);
+    if (launch_fit((const void *)fn, threads, pl->smem, &pl->regs) < 1)
+        return fail(CONVIO_EINFEASIBLE,
+                    "block of %d threads x %d regs + %zu B smem does not fit an SM", threads,
+                    pl->regs, pl->smem);
     return CONVIO_OK;
 }
 
 // Default device tile when the caller passes none: the largest register
 // micro-tile family that divides the output, ~128-256 threads per block.
+static int default_direct_tile_search(const convio_conv_desc *d, convio_tile *out);
+
 static int default_direct_tile(const convio_conv_desc *d, convio_tile *out) {
+    static std::mutex mu;
+    static std::map<std::array<int, 10>, convio_tile> cache;
+    std::array<int, 10> key{d->n, d->c, d->h, d->w, d->k, d->r, d->s, d->stride, d->pad, d->layout};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *out = it->second;
+            return CONVIO_OK;
+        }
+    }
+    int rc = default_direct_tile_search(d, out);
+    if (rc == CONVIO_OK) {
+        std::lock_guard<std::mutex> lock(mu);
+        cache[key] = *out;
+    }
+    return rc;
+}
+
+static int default_direct_tile_search(const convio_conv_desc *d, convio_tile *out) {
     int p = 0, q = 0;
     int rc = check_desc(d, &p, &q);
     if (rc) return rc;
@@ -296,6 +376,48 @@ static int default_direct_tile(const convio_conv_desc *d, convio_tile *out) {
     }
     *out = best;
     return CONVIO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptors (driver entry point fetched once through the runtime)
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            p = nullptr;
+        }
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    if ((reinterpret_cast<uintptr_t>(P.x) & 15) || (reinterpret_cast<uintptr_t>(P.wp) & 15)) return false;
+    const int rs = P.ks * P.ks;
+    cuuint64_t gdim[4] = {(cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.c, (cuuint64_t)P.n};
+    cuuint64_t gstr[3] = {(cuuint64_t)P.w * 4, (cuuint64_t)P.h * P.w * 4,
+                          (cuuint64_t)P.c * P.h * P.w * 4};
+    cuuint32_t box[4] = {(cuuint32_t)P.pitch, (cuuint32_t)P.tile_h, (cuuint32_t)P.ck, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(tm_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float *>(P.x), gdim, gstr,
+                     box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    cuuint64_t wdim[2] = {(cuuint64_t)P.k, (cuuint64_t)P.c * rs};
+    cuuint64_t wstr[1] = {(cuuint64_t)P.k * 4};
+    cuuint32_t wbox[2] = {(cuuint32_t)P.bz, (cuuint32_t)(P.ck * rs)};
+    cuuint32_t wes[2] = {1, 1};
+    r = enc(tm_w, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(P.wp), wdim, wstr, wbox, wes,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 // generic fallback + filter packing kernels
@@ -383,7 +505,8 @@ static void fill_info_direct(const DirectPlan &pl, convio_launch_info *out,
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = 4LL * d->k * d->c * d->r * d->s;
-    out->reason[0] = 0;
+    snprintf(out->reason, sizeof(out->reason), "%s ring: %d stages x %d channels",
+             pl.P.use_tma ? "tma" : "cp.async", pl.P.stages, pl.P.ck);
 }
 
 int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t algorithm,
@@ -485,11 +608,28 @@ int convio_conv_direct_f32(const convio_conv_desc *desc, const convio_tile *tile
         const int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
         direct_conv_f32_generic_kernel<<<blocks, 256, 0, st>>>(pl.P, desc->r, desc->s);
     } else {
-        pl.fn<<<pl.grid, pl.threads, pl.smem, st>>>(pl.P);
+        CUtensorMap tm_in, tm_w;
+        memset(&tm_in, 0, sizeof(tm_in));
+        memset(&tm_w, 0, sizeof(tm_w));
+        if (pl.P.use_tma && !make_direct_tensor_maps(pl.P, &tm_in, &tm_w)) pl.P.use_tma = 0;
+        pl.fn<<<pl.grid, pl.threads, pl.smem, st>>>(pl.P, tm_in, tm_w);
     }
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
+}
+
+int convio_default_tile(const convio_conv_desc *desc, int32_t algorithm, int32_t e,
+                        convio_tile *out) {
+    clear_error();
+    if (!out) {
+        set_error("null output");
+        return CONVIO_EINVAL;
+    }
+    if (algorithm == CONVIO_ALG_DIRECT) return default_direct_tile(desc, out);
+    if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_default_tile(desc, e, out);
+    set_error("unknown algorithm %d", algorithm);
+    return CONVIO_EINVAL;
 }
 
 int convio_ffma_peak(float *sink, int32_t blocks, int32_t iters, int64_t *flops, void *stream) {

@@ -16,6 +16,11 @@ void clear_error();
 void note_launch();
 void reset_launches();
 
+// Blocks of `fn` that fit one SM with this launch shape (cached per
+// (fn, threads, smem)); sets *regs.  Returns 1 without checking when no
+// device is present (CPU-only legality queries).
+int launch_fit(const void *fn, int threads, size_t smem, int *regs);
+
 struct Status {
     int code;
 };

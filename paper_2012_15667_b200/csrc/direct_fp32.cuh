@@ -6,16 +6,26 @@
 // Thread = an x/n_xt * y/n_yt * z/n_zt register micro-tile (TX, TY, TZ):
 //          TX consecutive output columns of TY consecutive rows for TZ
 //          consecutive output channels.
-// Stage  = `ck` input channels (the paper's alpha, reference alpha = 1): the
-//          x' * y' input footprint (halo zero-filled -> padding is never
-//          materialised) and the ck*R*S*z filter slice, streamed global ->
-//          shared with cp.async (LDGSTS) into a 1- or 2-deep ring.
+// Stage  = `ck` input channels (the paper's alpha; reference alpha = 1): the
+//          x' * y' input footprint and the ck*R*S*z filter slice.  The
+//          footprint's halo is zero-filled by the copy engine, so padding is
+//          never materialised.
+// Pipe   = an NS-deep ring of stages in shared memory.
+//          TMA path (NCHW, 16-byte-aligned strides): one elected thread
+//          issues cp.async.bulk.tensor (4-D input box, 2-D filter box) that
+//          completes on a per-stage mbarrier; consumer warps wait on the
+//          "full" barrier and release the slot through an "empty" barrier --
+//          no block-wide barrier in the main loop.
+//          cp.async path (other layouts / unaligned strides): LDGSTS
+//          multistage ring, one __syncthreads per stage.
 // Inner  = per (channel, ky): KS*TZ weights to registers, then per output
 //          row a register row segment of ST*(TX-1)+KS inputs reused across
 //          the KS taps ("shift" reuse) -> KS*TX*TZ FFMA per row segment.
 // Every output accumulates in (c, ky, kx) order, the reference DAG's
 // left-deep summation order (pkg/src/convio/dag.py:274-284), in fp32 FMA.
 #pragma once
+
+#include <cudaTypedefs.h>
 
 #include "common.cuh"
 
@@ -32,18 +42,80 @@ struct DirectParams {
     int bx, by, bz;           // block output tile
     int nxt, nyt, nzt;        // threads per axis
     int ck;                   // channels per stage
-    int stages;               // 1 or 2
+    int stages;               // ring depth NS (1..4)
     int tile_w, tile_h;       // input footprint x', y'
     int pitch;                // smem row pitch (floats)
-    int in_stage;             // floats per input stage
-    int w_stage;              // floats per weight stage
+    int in_stage;             // floats per input stage (128-B multiple)
+    int w_stage;              // floats per weight stage (128-B multiple)
     int tiles_x, tiles_y;
     int relu;
+    int use_tma;              // 1: TMA + mbarrier ring, 0: cp.async ring
+    int in_box_bytes, w_box_bytes;
 };
 
+// ---- mbarrier / TMA primitives (PTX) ------------------------------------------
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+                                            int c3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void load_row(float (&v)[N], const float *src) {
+    // 16-byte vector loads when the row segment is aligned (pitch % 4 == 0
+    // and the thread's column offset % 4 == 0 are guaranteed by the host).
+#pragma unroll
+    for (int t = 0; t + 4 <= N; t += 4) {
+        const float4 f = *reinterpret_cast<const float4 *>(src + t);
+        v[t] = f.x; v[t + 1] = f.y; v[t + 2] = f.z; v[t + 3] = f.w;
+    }
+    constexpr int rem = N & 3;
+    constexpr int base = N - rem;
+    if constexpr (rem >= 2) {
+        const float2 f = *reinterpret_cast<const float2 *>(src + base);
+        v[base] = f.x; v[base + 1] = f.y;
+    }
+    if constexpr (rem & 1) v[N - 1] = src[N - 1];
+}
+
 template <int KS, int ST, int TX, int TY, int TZ>
-__global__ void direct_conv_f32_kernel(const DirectParams P) {
-    extern __shared__ __align__(16) float smem[];
+__global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
+                                       const __grid_constant__ CUtensorMap tm_in,
+                                       const __grid_constant__ CUtensorMap tm_w) {
+    extern __shared__ __align__(128) float smem[];
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
     const int t_x = tid % P.nxt;
@@ -58,15 +130,25 @@ __global__ void direct_conv_f32_kernel(const DirectParams P) {
     const int ox0 = xt * P.bx, oy0 = yt * P.by;
     const int ix0 = ox0 * ST - P.pad, iy0 = oy0 * ST - P.pad;
 
+    const int NS = P.stages;
     float *in_s = smem;
-    float *w_s = smem + P.stages * P.in_stage;
+    float *w_s = smem + NS * P.in_stage;
+    uint64_t *full = reinterpret_cast<uint64_t *>(w_s + NS * P.w_stage);
+    uint64_t *empty = full + NS;
+    const int nwarps = (nthr + 31) >> 5;
     const float *xb = P.x + (int64_t)img * P.xs.n;
-    const int taps_z = KS * KS * P.bz;
     const int nchunks = (P.c + P.ck - 1) / P.ck;
 
-    auto load_chunk = [&](int chunk, int buf) {
+    // ---- producers ---------------------------------------------------------
+    auto tma_issue = [&](int chunk, int slot) {   // one thread
+        uint64_t *bar = full + slot;
+        mbar_arrive_expect_tx(bar, P.in_box_bytes + P.w_box_bytes);
+        tma_load_4d(in_s + slot * P.in_stage, &tm_in, ix0, iy0, chunk * P.ck, img, bar);
+        tma_load_2d(w_s + slot * P.w_stage, &tm_w, k0, chunk * P.ck * KS * KS, bar);
+    };
+    auto cp_issue = [&](int chunk, int slot) {    // all threads
         const int c0 = chunk * P.ck;
-        float *din = in_s + buf * P.in_stage;
+        float *din = in_s + slot * P.in_stage;
         const int total = P.ck * P.tile_h * P.tile_w;
         for (int i = tid; i < total; i += nthr) {
             int cc, r, col;
@@ -91,33 +173,31 @@ __global__ void direct_conv_f32_kernel(const DirectParams P) {
             const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx * P.xs.x : P.x;
             cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
         }
-        float *dw = w_s + buf * P.w_stage;
+        float *dw = w_s + slot * P.w_stage;
         const int rows = P.ck * KS * KS;   // (cc, tap) rows of bz filters
         if ((P.bz & 3) == 0 && (P.k & 3) == 0) {
             const int per_row = P.bz >> 2;
             const int tot = rows * per_row;
             for (int i = tid; i < tot; i += nthr) {
                 const int row = i / per_row, j = (i - row * per_row) << 2;
-                const int cc = row / (KS * KS), tap = row - cc * (KS * KS);
-                const int gc = c0 + cc;
+                const int gc = c0 + row / (KS * KS);
                 const bool v = gc < P.c;
-                const float *src = v ? P.wp + ((int64_t)gc * KS * KS + tap) * P.k + k0 + j : P.wp;
+                const float *src = v ? P.wp + ((int64_t)c0 * KS * KS + row) * P.k + k0 + j : P.wp;
                 cp_async16(dw + row * P.bz + j, src, v);
             }
         } else {
             const int tot = rows * P.bz;
             for (int i = tid; i < tot; i += nthr) {
                 const int row = i / P.bz, j = i - row * P.bz;
-                const int cc = row / (KS * KS), tap = row - cc * (KS * KS);
-                const int gc = c0 + cc;
+                const int gc = c0 + row / (KS * KS);
                 const bool v = gc < P.c;
-                const float *src = v ? P.wp + ((int64_t)gc * KS * KS + tap) * P.k + k0 + j : P.wp;
+                const float *src = v ? P.wp + ((int64_t)c0 * KS * KS + row) * P.k + k0 + j : P.wp;
                 cp_async4(dw + row * P.bz + j, src, v);
             }
         }
-        (void)taps_z;
     };
 
+    // ---- consumers ---------------------------------------------------------
     float acc[TY][TZ][TX];
 #pragma unroll
     for (int i = 0; i < TY; ++i)
@@ -127,13 +207,15 @@ __global__ void direct_conv_f32_kernel(const DirectParams P) {
             for (int xx = 0; xx < TX; ++xx) acc[i][zz][xx] = 0.0f;
 
     constexpr int SEG = ST * (TX - 1) + KS;
+    constexpr bool VEC_IN = ((TX * ST) % 4) == 0;
     const int in_off = (t_y * TY * ST) * P.pitch + t_x * TX * ST;
     const int w_off = t_z * TZ;
 
-    auto compute_chunk = [&](int buf) {
-        const float *ins = in_s + buf * P.in_stage + in_off;
-        const float *wss = w_s + buf * P.w_stage + w_off;
+    auto compute_chunk = [&](int slot) {
+        const float *ins = in_s + slot * P.in_stage + in_off;
+        const float *wss = w_s + slot * P.w_stage + w_off;
         const int ch_stride = P.tile_h * P.pitch;
+#pragma unroll 1
         for (int cc = 0; cc < P.ck; ++cc) {
             const float *in_c = ins + cc * ch_stride;
             const float *w_c = wss + cc * (KS * KS) * P.bz;
@@ -165,8 +247,12 @@ __global__ void direct_conv_f32_kernel(const DirectParams P) {
                 for (int i = 0; i < TY; ++i) {
                     const float *row = in_c + (i * ST + ky) * P.pitch;
                     float xr[SEG];
+                    if constexpr (VEC_IN) {
+                        load_row<SEG>(xr, row);
+                    } else {
 #pragma unroll
-                    for (int t = 0; t < SEG; ++t) xr[t] = row[t];
+                        for (int t = 0; t < SEG; ++t) xr[t] = row[t];
+                    }
 #pragma unroll
                     for (int kx = 0; kx < KS; ++kx)
 #pragma unroll
@@ -179,29 +265,57 @@ __global__ void direct_conv_f32_kernel(const DirectParams P) {
         }
     };
 
-    if (P.stages >= 2) {
-        load_chunk(0, 0);
-        cp_async_commit();
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            if (chunk + 1 < nchunks) {
-                load_chunk(chunk + 1, (chunk + 1) & 1);
-                cp_async_commit();
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
+    if (P.use_tma) {
+        if (tid == 0) {
+            for (int s = 0; s < NS; ++s) {
+                mbar_init(full + s, 1);
+                mbar_init(empty + s, nwarps);
             }
-            __syncthreads();
-            compute_chunk(chunk & 1);
-            __syncthreads();
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_in)));
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_w)));
+            for (int s = 0; s < NS - 1 && s < nchunks; ++s) tma_issue(s, s);
+        }
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const int slot = chunk % NS;
+            mbar_wait(full + slot, (chunk / NS) & 1);
+            compute_chunk(slot);
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(empty + slot);
+            // refill the slot consumed one iteration ago with chunk + NS - 1
+            const int next = chunk + NS - 1;
+            if (tid == 0 && next < nchunks) {
+                const int nslot = next % NS;
+                if (next >= NS) mbar_wait(empty + nslot, ((next / NS) - 1) & 1);
+                tma_issue(next, nslot);
+            }
         }
     } else {
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            load_chunk(chunk, 0);
+        const int pre = NS > 1 ? NS - 1 : 1;
+        for (int s = 0; s < pre; ++s) {
+            if (s < nchunks) cp_issue(s, s);
             cp_async_commit();
-            cp_async_wait<0>();
-            __syncthreads();
-            compute_chunk(0);
-            __syncthreads();
+        }
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            // the group of `chunk` is complete once at most NS-2 newer groups pend
+            if (NS >= 4) cp_async_wait<2>();
+            else if (NS == 3) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncthreads();   // chunk visible to all; slot (chunk-1)%NS free
+            if (NS >= 2) {
+                const int next = chunk + NS - 1;
+                if (next < nchunks) cp_issue(next, next % NS);
+                cp_async_commit();
+            }
+            compute_chunk(chunk % NS);
+            if (NS == 1) {
+                __syncthreads();
+                if (chunk + 1 < nchunks) cp_issue(chunk + 1, 0);
+                cp_async_commit();
+            }
         }
     }
 
@@ -243,9 +357,12 @@ __global__ void direct_conv_f32_generic_kernel(const DirectParams P, int kh, int
 // Repack KCRS -> C R S K.
 __global__ void pack_filter_direct_kernel(const float *w, float *wp, int k, int c, int rs);
 
-using DirectKernelFn = void (*)(const DirectParams);
+using DirectKernelFn = void (*)(const DirectParams, const CUtensorMap, const CUtensorMap);
 
 // Lookup of the compiled instances: nullptr if (KS, ST, TX, TY, TZ) absent.
 DirectKernelFn find_direct_kernel(int ks, int st, int tx, int ty, int tz);
+
+// Build the TMA descriptors of a plan (host); false if TMA cannot describe it.
+bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w);
 
 }  // namespace convio

@@ -2,6 +2,9 @@
 // projection of a TileConfig, and the C entry points.
 #include <stdarg.h>
 #include <algorithm>
+#include <array>
+#include <map>
+#include <mutex>
 
 #include "winograd_fp32.cuh"
 
@@ -237,26 +240,13 @@ static int plan_winograd(const convio_conv_desc *d, const convio_tile *t, int e,
     pl->threads = threads;
     pl->smem = (size_t)bytes(ck, stages);
     pl->e = e;
-    int count = 0;
-    if (cudaGetDeviceCount(&count) == cudaSuccess && count > 0) {
-        cudaFuncAttributes fa;
-        if (cudaFuncGetAttributes(&fa, (const void *)fn) == cudaSuccess) pl->regs = fa.numRegs;
-        if (pl->smem > 48 * 1024)
-            cudaFuncSetAttribute((const void *)fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)pl->smem);
-        int blocks = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, (const void *)fn, threads,
-                                                          pl->smem) != cudaSuccess ||
-            blocks < 1) {
-            cudaGetLastError();
-            return fail(CONVIO_EINFEASIBLE, "block of %d threads x %d regs + %zu B smem does not fit an SM",
-                        threads, pl->regs, pl->smem);
-        }
-    } else {
-        cudaGetLastError();
-    }
+    if (launch_fit((const void *)fn, threads, pl->smem, &pl->regs) < 1)
+        return fail(CONVIO_EINFEASIBLE, "block of %d threads x %d regs + %zu B smem does not fit an SM",
+                    threads, pl->regs, pl->smem);
     return CONVIO_OK;
 }
+
+int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
 
 static int default_winograd_tile(const convio_conv_desc *d, int e, convio_tile *out) {
     int p = 0, q = 0;
@@ -316,6 +306,26 @@ static int default_winograd_tile(const convio_conv_desc *d, int e, convio_tile *
     }
     *out = bt;
     return CONVIO_OK;
+}
+
+int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out) {
+    static std::mutex mu;
+    static std::map<std::array<int, 11>, convio_tile> cache;
+    std::array<int, 11> key{d->n, d->c, d->h, d->w, d->k, d->r, d->s, d->stride, d->pad, d->layout, e};
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) {
+            *out = it->second;
+            return CONVIO_OK;
+        }
+    }
+    int rc = default_winograd_tile(d, e, out);
+    if (rc == CONVIO_OK) {
+        std::lock_guard<std::mutex> lock(mu);
+        cache[key] = *out;
+    }
+    return rc;
 }
 
 int winograd_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out) {
@@ -404,7 +414,7 @@ int convio_conv_winograd_f32(const convio_conv_desc *desc, const convio_tile *ti
     }
     convio_tile chosen;
     if (!tile) {
-        int rc = default_winograd_tile(desc, e, &chosen);
+        int rc = winograd_default_tile(desc, e, &chosen);
         if (rc) return rc;
         tile = &chosen;
     }

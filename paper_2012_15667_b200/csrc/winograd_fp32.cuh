@@ -128,7 +128,7 @@ template <int E, int TZ, int TP, int UPT>
 __global__ void winograd_f32_kernel(const WinoParams P) {
     constexpr int M = E + 2;
     constexpr int MM = M * M;
-    extern __shared__ __align__(16) float smem[];
+    extern __shared__ __align__(128) float smem[];
     const int tid = threadIdx.x;
     const int nthr = blockDim.x;
 

@@ -22,20 +22,18 @@ from paper_2012_15667_b200 import _native as N  # noqa: E402
 
 
 def timeit(fn, reps=20, warm=5):
+    """Mean device time of back-to-back launches (host overhead overlapped)."""
     for _ in range(warm):
         fn()
     torch.cuda.synchronize()
-    ts = []
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record()
     for _ in range(reps):
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record()
         fn()
-        b.record()
-        b.synchronize()
-        ts.append(a.elapsed_time(b) / 1e3)
-    ts.sort()
-    return ts[len(ts) // 2]
+    b.record()
+    b.synchronize()
+    return a.elapsed_time(b) / 1e3 / reps
 
 
 def ffma_peak():
