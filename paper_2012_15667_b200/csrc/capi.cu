@@ -256,9 +256,10 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
     // TMA can describe the NCHW input box / packed filter box?
     bool tma = d->layout == CONVIO_LAYOUT_CHW && d->w % 4 == 0 && ((int64_t)d->h * d->w) % 4 == 0 &&
                d->k % 4 == 0 && t->z % 4 == 0 && t->z <= 256 && tile_h <= 256 &&
-               ((tile_w + 3) & ~3) <= 256;
+               ((tile_w + 6) & ~3) <= 256;
     const int align = (tma || vec_in) ? 4 : 1;
-    const int pitch = choose_pitch(tile_w, t->n_xt, t->n_yt, threads, TX * d->stride,
+    // rows are staged from a 16-byte-aligned column: up to 3 extra leading columns
+    const int pitch = choose_pitch(tile_w + 3, t->n_xt, t->n_yt, threads, TX * d->stride,
                                    TY * d->stride, align);
     const int64_t per_ch = (int64_t)tile_h * pitch + (int64_t)rs * t->z;
     const int64_t budget = (int64_t)t->s_b - vol;

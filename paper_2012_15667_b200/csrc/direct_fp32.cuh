@@ -27,6 +27,8 @@
 
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace convio {
@@ -76,40 +78,49 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2,
+// `map` is the generic address of a __grid_constant__ kernel parameter; it
+// must be taken at kernel scope (a by-reference lambda capture would copy
+// the descriptor to local memory, which TMA cannot read).
+__device__ __forceinline__ void tma_load_4d(void *dst, uint64_t map, int c0, int c1, int c2,
                                             int c3, uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, int c0, int c1,
+__device__ __forceinline__ void tma_load_2d(void *dst, uint64_t map, int c0, int c1,
                                             uint64_t *bar) {
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
 
-template <int N>
-__device__ __forceinline__ void load_row(float (&v)[N], const float *src) {
-    // 16-byte vector loads when the row segment is aligned (pitch % 4 == 0
-    // and the thread's column offset % 4 == 0 are guaranteed by the host).
-#pragma unroll
-    for (int t = 0; t + 4 <= N; t += 4) {
-        const float4 f = *reinterpret_cast<const float4 *>(src + t);
-        v[t] = f.x; v[t + 1] = f.y; v[t + 2] = f.z; v[t + 3] = f.w;
+// v[t] = src[SH + t] for t < N: the widest aligned load at each position
+// (LDS.128 / .64 / .32 on a 16-byte-aligned `src`; the host guarantees
+// pitch % 4 == 0 and a 4-aligned thread column offset), exactly N registers.
+template <int N, int SH, int P = SH>
+__device__ __forceinline__ void load_row_exact(float (&v)[N], const float *src) {
+    if constexpr (P < SH + N) {
+        if constexpr (P % 4 == 0 && P + 4 <= SH + N) {
+            const float4 f = *reinterpret_cast<const float4 *>(src + P);
+            v[P - SH] = f.x; v[P - SH + 1] = f.y; v[P - SH + 2] = f.z; v[P - SH + 3] = f.w;
+            load_row_exact<N, SH, P + 4>(v, src);
+        } else if constexpr (P % 2 == 0 && P + 2 <= SH + N) {
+            const float2 f = *reinterpret_cast<const float2 *>(src + P);
+            v[P - SH] = f.x; v[P - SH + 1] = f.y;
+            load_row_exact<N, SH, P + 2>(v, src);
+        } else {
+            v[P - SH] = src[P];
+            load_row_exact<N, SH, P + 1>(v, src);
+        }
     }
-    constexpr int rem = N & 3;
-    constexpr int base = N - rem;
-    if constexpr (rem >= 2) {
-        const float2 f = *reinterpret_cast<const float2 *>(src + base);
-        v[base] = f.x; v[base + 1] = f.y;
-    }
-    if constexpr (rem & 1) v[N - 1] = src[N - 1];
 }
+
+template <int V>
+using IntC = std::integral_constant<int, V>;
 
 template <int KS, int ST, int TX, int TY, int TZ>
 __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
@@ -128,7 +139,14 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
     const int yt = blockIdx.y / P.tiles_x;
     const int img = blockIdx.z;
     const int ox0 = xt * P.bx, oy0 = yt * P.by;
-    const int ix0 = ox0 * ST - P.pad, iy0 = oy0 * ST - P.pad;
+    const int iy0 = oy0 * ST - P.pad;
+    // the staged footprint starts at a 16-byte-aligned column (TMA requires
+    // the innermost box coordinate to be a multiple of 4 floats); `shift`
+    // is the offset of the true footprint start inside the staged row
+    const int ix0 = ox0 * ST - P.pad;
+    const int shift = ((ix0 % 4) + 4) % 4;
+    const int ix0a = ix0 - shift;
+    const int stage_w = P.tile_w + shift;
 
     const int NS = P.stages;
     float *in_s = smem;
@@ -140,35 +158,37 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
     const int nchunks = (P.c + P.ck - 1) / P.ck;
 
     // ---- producers ---------------------------------------------------------
+    const uint64_t map_in = reinterpret_cast<uint64_t>(&tm_in);
+    const uint64_t map_w = reinterpret_cast<uint64_t>(&tm_w);
     auto tma_issue = [&](int chunk, int slot) {   // one thread
         uint64_t *bar = full + slot;
         mbar_arrive_expect_tx(bar, P.in_box_bytes + P.w_box_bytes);
-        tma_load_4d(in_s + slot * P.in_stage, &tm_in, ix0, iy0, chunk * P.ck, img, bar);
-        tma_load_2d(w_s + slot * P.w_stage, &tm_w, k0, chunk * P.ck * KS * KS, bar);
+        tma_load_4d(in_s + slot * P.in_stage, map_in, ix0a, iy0, chunk * P.ck, img, bar);
+        tma_load_2d(w_s + slot * P.w_stage, map_w, k0, chunk * P.ck * KS * KS, bar);
     };
     auto cp_issue = [&](int chunk, int slot) {    // all threads
         const int c0 = chunk * P.ck;
         float *din = in_s + slot * P.in_stage;
-        const int total = P.ck * P.tile_h * P.tile_w;
+        const int total = P.ck * P.tile_h * stage_w;
         for (int i = tid; i < total; i += nthr) {
             int cc, r, col;
             if (P.layout == CONVIO_LAYOUT_HWC) {          // channels contiguous
                 cc = i % P.ck;
                 const int t = i / P.ck;
-                col = t % P.tile_w;
-                r = t / P.tile_w;
+                col = t % stage_w;
+                r = t / stage_w;
             } else if (P.layout == CONVIO_LAYOUT_CWH) {   // rows contiguous
                 r = i % P.tile_h;
                 const int t = i / P.tile_h;
-                col = t % P.tile_w;
-                cc = t / P.tile_w;
+                col = t % stage_w;
+                cc = t / stage_w;
             } else {                                      // columns contiguous
-                col = i % P.tile_w;
-                const int t = i / P.tile_w;
+                col = i % stage_w;
+                const int t = i / stage_w;
                 r = t % P.tile_h;
                 cc = t / P.tile_h;
             }
-            const int gc = c0 + cc, gy = iy0 + r, gx = ix0 + col;
+            const int gc = c0 + cc, gy = iy0 + r, gx = ix0a + col;
             const bool v = gc < P.c && gy >= 0 && gy < P.h && gx >= 0 && gx < P.w;
             const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx * P.xs.x : P.x;
             cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
@@ -211,7 +231,11 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
     const int in_off = (t_y * TY * ST) * P.pitch + t_x * TX * ST;
     const int w_off = t_z * TZ;
 
-    auto compute_chunk = [&](int slot) {
+    // SH = the block's staged-row shift (compile-time inside, dispatched once
+    // per chunk so the register row loads stay exact-width vector loads)
+    auto compute_chunk_sh = [&](int slot, auto sh_tag) {
+        constexpr int SH = decltype(sh_tag)::value;
+        (void)SH;
         const float *ins = in_s + slot * P.in_stage + in_off;
         const float *wss = w_s + slot * P.w_stage + w_off;
         const int ch_stride = P.tile_h * P.pitch;
@@ -248,10 +272,10 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
                     const float *row = in_c + (i * ST + ky) * P.pitch;
                     float xr[SEG];
                     if constexpr (VEC_IN) {
-                        load_row<SEG>(xr, row);
+                        load_row_exact<SEG, SH>(xr, row);
                     } else {
 #pragma unroll
-                        for (int t = 0; t < SEG; ++t) xr[t] = row[t];
+                        for (int t = 0; t < SEG; ++t) xr[t] = row[shift + t];
                     }
 #pragma unroll
                     for (int kx = 0; kx < KS; ++kx)
@@ -262,6 +286,18 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
                                 acc[i][zz][xx] = fmaf(xr[xx * ST + kx], wr[kx][zz], acc[i][zz][xx]);
                 }
             }
+        }
+    };
+    auto compute_chunk = [&](int slot) {
+        if constexpr (VEC_IN) {
+            switch (shift) {   // block-uniform
+                case 0: compute_chunk_sh(slot, IntC<0>{}); break;
+                case 1: compute_chunk_sh(slot, IntC<1>{}); break;
+                case 2: compute_chunk_sh(slot, IntC<2>{}); break;
+                default: compute_chunk_sh(slot, IntC<3>{}); break;
+            }
+        } else {
+            compute_chunk_sh(slot, IntC<0>{});
         }
     };
 
@@ -275,8 +311,8 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
         }
         __syncthreads();
         if (tid == 0) {
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_in)));
-            asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(&tm_w)));
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_in));
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_w));
             for (int s = 0; s < NS - 1 && s < nchunks; ++s) tma_issue(s, s);
         }
         for (int chunk = 0; chunk < nchunks; ++chunk) {
