@@ -1,0 +1,146 @@
+"""Lower-bound auto-tuning of every layer of a workload on the device.
+
+    python scripts/tune_layers.py --workload resnet50 --n 64 --budget 128 \
+        [--exhaustive-cap 0] [--out paper_2012_15667_b200/tuned/b200_resnet50.json]
+
+Per distinct layer and per algorithm (direct, Winograd F(2,3), F(4,3)):
+  1. the Table-1 searching domain of the B200 machine model (reference
+     ``build_space``) restricted to its legal device projection;
+  2. the model's analytic tile (``optimal_tile_dc/wa``) and its device time
+     if it has a projection;
+  3. the reference tuner (``tune``: GBR cost model + random walks) with
+     ``backend="device"``;
+  4. optionally the exhaustive oracle over the legal projection
+     (``--exhaustive-cap``), for the pruned-vs-exhaustive comparison.
+The fastest (algorithm, tile) per layer is written as the layer's plan.
+"""
+
+import argparse
+import json
+import math
+import os
+import sys
+import time
+import warnings
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2012_15667_b200 import device_tuner as DT  # noqa: E402
+from paper_2012_15667_b200.autotune import tune, exhaustive_oracle, random_search  # noqa: E402
+from paper_2012_15667_b200.dataflow import optimal_tile_dc, optimal_tile_wa, InfeasibleTileError  # noqa: E402
+from paper_2012_15667_b200.device import b200_hw_model, shape_of  # noqa: E402
+from paper_2012_15667_b200.model import WinogradParams  # noqa: E402
+from paper_2012_15667_b200.runner import WORKLOADS, TUNED_DIR  # noqa: E402
+
+
+def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
+    t0 = time.time()
+    try:
+        space = DT.device_space(shape, hw, alg, wp)
+    except InfeasibleTileError as exc:
+        return {"error": str(exc)}
+    out = {"legal_space": space.size, "unconstrained": space.unconstrained_size}
+    # the model's analytic pick
+    try:
+        mt = optimal_tile_dc(shape, hw) if alg == "direct" else optimal_tile_wa(shape, wp, hw)
+        mcost = DT.measure_device(mt, shape, hw, alg, wp)
+        out["model_tile"] = {"tile": mt.to_dict(), "seconds": None if math.isinf(mcost) else mcost}
+    except InfeasibleTileError as exc:
+        out["model_tile"] = {"error": str(exc)}
+    n_s = min(16, max(2, budget // 4))
+    sess = tune(shape, hw, alg, min(budget, space.size), seed, winograd=wp, n_s=min(n_s, space.size),
+                space=space, backend="device")
+    best = sess.best
+    out["tuner"] = {"best": best.config.to_dict() if best else None,
+                    "seconds": best.cost if best else None,
+                    "measurements": len(sess.measurements), "iterations": sess.iterations,
+                    "stopped_by": sess.stopped_by,
+                    "measurements_to_best": (best.index + 1) if best else None,
+                    "wall_s": round(time.time() - t0, 1)}
+    rs_cfg, rs_cost = random_search(space, min(budget, space.size), seed, backend="device")
+    out["random_search"] = {"best": rs_cfg.to_dict() if rs_cfg else None,
+                            "seconds": None if math.isinf(rs_cost) else rs_cost}
+    if exhaustive_cap and space.size <= exhaustive_cap:
+        t1 = time.time()
+        ex_cfg, ex_cost = exhaustive_oracle(space, cap=exhaustive_cap, backend="device")
+        out["exhaustive"] = {"best": ex_cfg.to_dict() if ex_cfg else None,
+                             "seconds": None if math.isinf(ex_cost) else ex_cost,
+                             "wall_s": round(time.time() - t1, 1)}
+    log(f"    {alg}{'' if wp is None else wp.e}: legal {space.size}, tuner best "
+        f"{out['tuner']['seconds']} in {out['tuner']['measurements']} meas "
+        f"({out['tuner']['wall_s']} s), random {out['random_search']['seconds']}"
+        + (f", exhaustive {out['exhaustive']['seconds']}" if "exhaustive" in out else ""))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="resnet50")
+    ap.add_argument("--n", type=int, default=64)
+    ap.add_argument("--budget", type=int, default=128)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--exhaustive-cap", type=int, default=0)
+    ap.add_argument("--algs", default="direct,winograd2,winograd4")
+    ap.add_argument("--layers", default="")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    warnings.simplefilter("ignore")
+    torch.cuda.init()
+    hw = b200_hw_model()
+    out_path = args.out or os.path.join(TUNED_DIR, f"b200_{args.workload}.json")
+    result = {"workload": args.workload, "n_tune": args.n, "budget": args.budget,
+              "hw_model": {"s": hw.s, "s_sm": hw.s_sm, "n_p": hw.n_p},
+              "device": torch.cuda.get_device_name(), "layers": {}}
+    if os.path.exists(out_path):
+        with open(out_path) as fh:
+            prev = json.load(fh)
+        if prev.get("n_tune") == args.n:
+            result["layers"].update(prev.get("layers", {}))
+
+    def log(msg):
+        print(msg, flush=True)
+
+    wanted = set(args.layers.split(",")) if args.layers else None
+    for spec in WORKLOADS[args.workload]:
+        if wanted and spec.name not in wanted:
+            continue
+        DT.set_padding(spec.pad)
+        shape = shape_of(args.n, spec.c, spec.hw, spec.hw, spec.k, spec.r, spec.stride, spec.pad)
+        log(f"{spec.name}: {shape}")
+        cands = {}
+        for alg in args.algs.split(","):
+            if alg == "direct":
+                cands["direct"] = tune_one(shape, hw, "direct", None, args.budget, args.seed,
+                                           args.exhaustive_cap, log)
+            elif alg.startswith("winograd") and spec.stride == 1 and spec.r == 3:
+                e = int(alg[len("winograd"):])
+                cands[alg] = tune_one(shape, hw, "winograd", WinogradParams(e, 3), args.budget,
+                                      args.seed, args.exhaustive_cap, log)
+        best_key, best_t = None, math.inf
+        for key, c in cands.items():
+            t = (c.get("tuner") or {}).get("seconds")
+            if t is not None and t < best_t:
+                best_key, best_t = key, t
+        if best_key is None:
+            log(f"  no legal plan for {spec.name}")
+            continue
+        tile = cands[best_key]["tuner"]["best"]
+        flops = spec.flops(args.n)
+        result["layers"][spec.name] = {
+            "algorithm": "direct" if best_key == "direct" else "winograd",
+            "e": None if best_key == "direct" else int(best_key[len("winograd"):]),
+            "tile": tile, "seconds": best_t, "gflops_direct_equiv": round(flops / best_t / 1e9, 1),
+            "candidates": cands,
+        }
+        log(f"  -> {best_key} {tile} {best_t * 1e3:.3f} ms {flops / best_t / 1e12:.2f} TFLOP/s")
+        os.makedirs(os.path.dirname(out_path), exist_ok=True)
+        with open(out_path, "w") as fh:
+            json.dump(result, fh, indent=1, sort_keys=True)
+    print(f"wrote {out_path}")
+
+
+if __name__ == "__main__":
+    main()
