@@ -178,9 +178,18 @@ def shard_range(n_total: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def gather_outputs(y_local: torch.Tensor, world: int) -> torch.Tensor:
-    """NCCL all-gather of batch shards into the full output (only when collecting)."""
+    """All-gather of equal batch shards into the full output (only when collecting).
+
+    NCCL (NVLink / NVSwitch) on GPUs via ``all_gather_into_tensor``; the list
+    form on backends without it (gloo, used by the CPU tests).
+    """
     import torch.distributed as dist
-    out = torch.empty((world * y_local.shape[0],) + tuple(y_local.shape[1:]),
-                      device=y_local.device, dtype=y_local.dtype)
-    dist.all_gather_into_tensor(out, y_local.contiguous())
-    return out
+    y_local = y_local.contiguous()
+    if dist.get_backend() == "nccl":
+        out = torch.empty((world * y_local.shape[0],) + tuple(y_local.shape[1:]),
+                          device=y_local.device, dtype=y_local.dtype)
+        dist.all_gather_into_tensor(out, y_local)
+        return out
+    parts = [torch.empty_like(y_local) for _ in range(world)]
+    dist.all_gather(parts, y_local)
+    return torch.cat(parts, 0)

@@ -1,0 +1,125 @@
+"""The C-ABI library on a CPU-only machine: it loads, exports every symbol the
+header declares, and its host-side planning (legality of a TileConfig's
+device projection, transform matrices) answers without a GPU.  No kernel is
+launched here."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import winograd_mats as wm
+from paper_2012_15667_b200 import _native as N
+from paper_2012_15667_b200 import TileConfig
+from paper_2012_15667_b200.conv import query
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "convio_b200.h")
+
+
+def _declared():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(convio_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    lib = N.lib()
+    names = _declared()
+    assert "convio_conv_direct_f32" in names and "convio_query" in names
+    for name in names:
+        assert hasattr(lib, name), name
+    assert set(names) == set(N.EXPORTED)
+    assert lib.convio_version() >= 100
+
+
+def test_struct_layouts_match_header():
+    assert ctypes.sizeof(N.ConvDesc) == 10 * 4
+    assert ctypes.sizeof(N.Tile) == 9 * 4
+    assert N.LaunchInfo.flops.offset % 8 == 0
+
+
+def test_query_legal_and_illegal_projections():
+    ok = query((1, 64, 56, 56), (64, 64, 3, 3), 1, 1, "CHW", TileConfig(56, 4, 64, 32768, 7, 4, 8))
+    assert ok["rc"] == 0 and ok["legal"] == 1
+    assert (ok["grid_x"], ok["grid_y"], ok["grid_z"]) == (1, 14, 1)
+    assert ok["block_threads"] == 224 and ok["p"] == ok["q"] == 56
+    assert ok["flops"] == 231211008
+    assert "tma" in ok["reason"]          # NCHW with 16-byte strides: TMA ring
+    assert 1 <= ok["stages"] <= 4 and ok["channel_chunk"] >= 1
+    # resident set above s_b -> ScheduleError class (rc 3)
+    bad = query((1, 64, 56, 56), (64, 64, 3, 3), 1, 1, "CHW", TileConfig(56, 4, 64, 2000, 7, 4, 8))
+    assert bad["rc"] == 3 and "resident" in bad["reason"]
+    # ragged tile refused like the model refuses it
+    rag = query((1, 64, 56, 56), (64, 64, 3, 3), 1, 1, "CHW", TileConfig(5, 4, 64, 32768, 5, 4, 8))
+    assert rag["rc"] == 3 and "divide" in rag["reason"]
+    # 14x14 maps: 56-byte rows cannot be a TMA box -> cp.async ring
+    small = query((1, 256, 14, 14), (256, 256, 3, 3), 1, 1, "CHW",
+                  TileConfig(14, 14, 32, 16384, 2, 7, 16))
+    assert small["rc"] == 0 and "cp.async" in small["reason"]
+
+
+def test_winograd_projection():
+    ok = query((1, 64, 56, 56), (64, 64, 3, 3), 1, 1, "CHW",
+               TileConfig(8, 8, 32, 32768, 8, 8, 4, e=2), "winograd")
+    assert ok["rc"] == 0 and ok["block_threads"] == 256
+    assert ok["flops"] == 2 * 16 * 28 * 28 * 64 * 64
+    stride2 = query((1, 64, 56, 56), (64, 64, 3, 3), 2, 1, "CHW",
+                    TileConfig(4, 4, 32, 32768, 2, 2, 4, e=2), "winograd")
+    assert stride2["rc"] == 3 and "stride" in stride2["reason"]
+
+
+def test_default_tiles_are_legal():
+    lib = N.lib()
+    for n, c, h, k, st in [(8, 64, 56, 64, 1), (4, 256, 14, 256, 1), (2, 128, 28, 128, 2)]:
+        d = N.make_desc(n, c, h, h, k, 3, 3, st, 1, 0)
+        t = N.Tile()
+        assert lib.convio_default_tile(ctypes.byref(d), 0, 0, ctypes.byref(t)) == 0
+        rc, info = N.query(d, t, N.ALG_DIRECT)
+        assert rc == 0 and info["legal"] == 1
+
+
+@pytest.mark.parametrize("e", [2, 4])
+def test_kernel_transform_matrices_match_oracle(e):
+    m = e + 2
+    at = np.zeros(e * m, np.float32)
+    g = np.zeros(m * 3, np.float32)
+    bt = np.zeros(m * m, np.float32)
+    rc = N.lib().convio_winograd_matrices(e, 3, at.ctypes.data, g.ctypes.data, bt.ctypes.data)
+    assert rc == 0
+    mats = wm.matrices_float(e, 3)
+    assert np.array_equal(at.reshape(e, m), mats["AT"].astype(np.float32))
+    assert np.allclose(g.reshape(m, 3), mats["G"], rtol=0, atol=1e-7)
+    assert np.array_equal(bt.reshape(m, m), mats["BT"].astype(np.float32))
+
+
+def test_error_codes_map_to_reference_exceptions():
+    from paper_2012_15667_b200.dataflow import ScheduleError, InfeasibleTileError
+    lib = N.lib()
+    d = N.make_desc(1, 4, 8, 8, 4, 3, 3, 1, 1, 0)
+    info = N.LaunchInfo()
+    rc = lib.convio_query(ctypes.byref(d), ctypes.byref(N.make_tile(TileConfig(3, 8, 4, 4096))),
+                          0, ctypes.byref(info))
+    with pytest.raises(ScheduleError):
+        N.check(rc)
+    rc = lib.convio_query(ctypes.byref(d), ctypes.byref(N.make_tile(TileConfig(8, 8, 4, 8192, 1, 1, 4))),
+                          0, ctypes.byref(info))
+    with pytest.raises(InfeasibleTileError):
+        N.check(rc)
+    bad = N.make_desc(0, 4, 8, 8, 4, 3, 3, 1, 1, 0)
+    rc = lib.convio_query(ctypes.byref(bad), ctypes.byref(N.make_tile(TileConfig(8, 8, 4, 8192))),
+                          0, ctypes.byref(info))
+    with pytest.raises(ValueError):
+        N.check(rc)
+
+
+def test_no_cpu_fallback_for_conv():
+    torch = pytest.importorskip("torch")
+    from paper_2012_15667_b200 import conv as C
+    x = torch.zeros(1, 2, 4, 4)
+    w = torch.zeros(2, 2, 3, 3)
+    with pytest.raises(ValueError, match="CUDA"):
+        C.conv_direct(x, w, padding=1)
+    with pytest.raises(ValueError, match="CUDA"):
+        C.conv_winograd(x, w, e=2, padding=1)
