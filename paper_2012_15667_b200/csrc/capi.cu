@@ -87,6 +87,21 @@ struct FitVal {
     int regs;
 };
 
+int kernel_regs(const void *fn) {
+    static std::mutex mu;
+    static std::unordered_map<const void *, int> regs_of;
+    if (!dev_info().ok) return 0;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = regs_of.find(fn);
+    if (it != regs_of.end()) return it->second;
+    cudaFuncAttributes fa;
+    int r = 0;
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) r = fa.numRegs;
+    cudaGetLastError();
+    regs_of.emplace(fn, r);
+    return r;
+}
+
 int launch_fit(const void *fn, int threads, size_t smem, int *regs) {
     static std::mutex mu;
     static std::unordered_map<FitKey, FitVal, FitKeyHash> cache;
@@ -263,16 +278,46 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
                                    TY * d->stride, align);
     const int64_t per_ch = (int64_t)tile_h * pitch + (int64_t)rs * t->z;
     const int64_t budget = (int64_t)t->s_b - vol;
-    int stages = budget / (3 * per_ch) >= 2 ? 3 : (budget >= 2 * per_ch ? 2 : 1);
-    int64_t ck = std::max<int64_t>(1, budget / (stages * per_ch));
-    ck = std::min<int64_t>(std::min<int64_t>(ck, 16), d->c);
-    if (tma && ck * rs > 256) ck = 256 / rs;
     auto round32 = [](int64_t v) { return (v + 31) & ~31LL; };
     auto ring_bytes = [&](int64_t cks, int st) {
         return 4 * st * (round32(cks * tile_h * pitch) + round32(cks * rs * t->z)) + 16 * st;
     };
-    while (ck > 1 && ring_bytes(ck, stages) > kSmemCapBytes) --ck;
-    while (stages > 1 && ring_bytes(ck, stages) > kSmemCapBytes) --stages;
+    // s_b - xyz bounds the staging ring; inside that bound pick (stages, ck)
+    // for resident warps first (latency hiding), then fewer barriers per
+    // channel: warps/SM from registers x threads, smem, 2048 threads, 32 blocks
+    int regs_guess = kernel_regs((const void *)fn);
+    if (regs_guess <= 0) regs_guess = 128;
+    const int warps_per_block = (threads + 31) / 32;
+    const int regs_per_warp = ((regs_guess * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / std::max(1, regs_per_warp * warps_per_block);
+    const int by_threads = 2048 / threads;
+    int best_st = 1;
+    int64_t best_ck = 1;
+    double best_score = -1;
+    for (int st = 1; st <= 3; ++st) {
+        for (int64_t cks = 1; cks <= std::min<int64_t>(16, d->c); cks *= 2) {
+            if (st * cks * per_ch > budget && !(st == 1 && cks == 1)) continue;
+            if (tma && cks * rs > 256) continue;
+            const int64_t bytes = ring_bytes(cks, st);
+            if (bytes > kSmemCapBytes) continue;
+            const int by_smem = (int)((228 * 1024) / (bytes + 1024));
+            const int blocks = std::min(std::min(by_regs, by_threads), std::min(by_smem, 32));
+            if (blocks < 1) continue;
+            const int warps = blocks * warps_per_block;
+            // 12 resident warps/SM (3 per scheduler) first, then a pipelined ring
+            // (2-3 stages: TMA needs >= 2), then channels per barrier
+            const double score = std::min(warps, 12) * 1000.0 + (st >= 2 ? 500.0 : 0.0) +
+                                 (st == 3 ? 100.0 : 0.0) +
+                                 std::min<int64_t>(cks * (st > 1 ? st - 1 : 1), 16) * 10.0;
+            if (score > best_score) {
+                best_score = score;
+                best_st = st;
+                best_ck = cks;
+            }
+        }
+    }
+    int stages = best_st;
+    int64_t ck = best_ck;
     if (ring_bytes(ck, stages) > kSmemCapBytes)
         return fail(CONVIO_EINFEASIBLE, "staging needs %lld B of shared memory > 227 KB",
                     (long long)ring_bytes(ck, stages));
@@ -286,6 +331,10 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
     P.use_tma = tma ? 1 : 0;
     P.in_box_bytes = (int)(4 * ck * tile_h * pitch);
     P.w_box_bytes = (int)(4 * ck * rs * t->z);
+    {
+        const int per_row = t->z / 4;
+        P.w_row_shift = (t->z % 4 == 0 && (per_row & (per_row - 1)) == 0) ? __builtin_ctz(per_row) : -1;
+    }
     P.tiles_x = q / t->x; P.tiles_y = p / t->y;
     pl->grid = dim3(d->k / t->z, P.tiles_x * P.tiles_y, d->n);
     if (pl->grid.y > 65535 || pl->grid.z > 65535)

@@ -20,6 +20,8 @@ void reset_launches();
 // (fn, threads, smem)); sets *regs.  Returns 1 without checking when no
 // device is present (CPU-only legality queries).
 int launch_fit(const void *fn, int threads, size_t smem, int *regs);
+// Registers per thread of a kernel (cached); 0 without a device.
+int kernel_regs(const void *fn);
 
 struct Status {
     int code;

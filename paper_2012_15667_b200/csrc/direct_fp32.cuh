@@ -53,6 +53,7 @@ struct DirectParams {
     int relu;
     int use_tma;              // 1: TMA + mbarrier ring, 0: cp.async ring
     int in_box_bytes, w_box_bytes;
+    int w_row_shift;          // log2(bz/4) if a power of two, else -1
 };
 
 // ---- mbarrier / TMA primitives (PTX) ------------------------------------------
@@ -169,37 +170,64 @@ __global__ void direct_conv_f32_kernel(const __grid_constant__ DirectParams P,
     auto cp_issue = [&](int chunk, int slot) {    // all threads
         const int c0 = chunk * P.ck;
         float *din = in_s + slot * P.in_stage;
-        const int total = P.ck * P.tile_h * stage_w;
-        for (int i = tid; i < total; i += nthr) {
-            int cc, r, col;
-            if (P.layout == CONVIO_LAYOUT_HWC) {          // channels contiguous
-                cc = i % P.ck;
-                const int t = i / P.ck;
-                col = t % stage_w;
-                r = t / stage_w;
-            } else if (P.layout == CONVIO_LAYOUT_CWH) {   // rows contiguous
-                r = i % P.tile_h;
-                const int t = i / P.tile_h;
-                col = t % stage_w;
-                cc = t / stage_w;
-            } else {                                      // columns contiguous
-                col = i % stage_w;
-                const int t = i / stage_w;
-                r = t % P.tile_h;
-                cc = t / P.tile_h;
+        if (P.layout == CONVIO_LAYOUT_CHW && nthr >= 32) {
+            // warp-per-row(s): lanes run along the contiguous columns, one
+            // uniform division per row instead of three per element
+            const int lane = tid & 31, warp = tid >> 5, nfull = nthr >> 5;
+            const int lpr = stage_w <= 8 ? 8 : (stage_w <= 16 ? 16 : 32);   // lanes per row
+            const int rpi = 32 / lpr;                                      // rows per warp pass
+            const int segs = (stage_w + 31) >> 5;
+            const int rows = P.ck * P.tile_h;
+            const int sub = lane / lpr, lcol = lane - sub * lpr;
+            if (warp < nfull) {
+                for (int it = warp; it * rpi < rows * segs; it += nfull) {
+                    const int rs = it * rpi + sub;
+                    if (rs >= rows * segs) break;
+                    const int row = segs == 1 ? rs : rs / segs;
+                    const int col = (segs == 1 ? 0 : (rs - row * segs) * 32) + lcol;
+                    if (col >= stage_w) continue;
+                    const int cc = row / P.tile_h, r = row - cc * P.tile_h;
+                    const int gc = c0 + cc, gy = iy0 + r, gx = ix0a + col;
+                    const bool v = gc < P.c && gy >= 0 && gy < P.h && gx >= 0 && gx < P.w;
+                    const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx : P.x;
+                    cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
+                }
             }
-            const int gc = c0 + cc, gy = iy0 + r, gx = ix0a + col;
-            const bool v = gc < P.c && gy >= 0 && gy < P.h && gx >= 0 && gx < P.w;
-            const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx * P.xs.x : P.x;
-            cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
+        } else {
+            const int total = P.ck * P.tile_h * stage_w;
+            for (int i = tid; i < total; i += nthr) {
+                int cc, r, col;
+                if (P.layout == CONVIO_LAYOUT_HWC) {          // channels contiguous
+                    cc = i % P.ck;
+                    const int t = i / P.ck;
+                    col = t % stage_w;
+                    r = t / stage_w;
+                } else if (P.layout == CONVIO_LAYOUT_CWH) {   // rows contiguous
+                    r = i % P.tile_h;
+                    const int t = i / P.tile_h;
+                    col = t % stage_w;
+                    cc = t / stage_w;
+                } else {                                      // columns contiguous
+                    col = i % stage_w;
+                    const int t = i / stage_w;
+                    r = t % P.tile_h;
+                    cc = t / P.tile_h;
+                }
+                const int gc = c0 + cc, gy = iy0 + r, gx = ix0a + col;
+                const bool v = gc < P.c && gy >= 0 && gy < P.h && gx >= 0 && gx < P.w;
+                const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx * P.xs.x : P.x;
+                cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
+            }
         }
         float *dw = w_s + slot * P.w_stage;
         const int rows = P.ck * KS * KS;   // (cc, tap) rows of bz filters
         if ((P.bz & 3) == 0 && (P.k & 3) == 0) {
             const int per_row = P.bz >> 2;
             const int tot = rows * per_row;
+            const int sh = P.w_row_shift;   // log2(per_row) when a power of two, else -1
             for (int i = tid; i < tot; i += nthr) {
-                const int row = i / per_row, j = (i - row * per_row) << 2;
+                const int row = sh >= 0 ? (i >> sh) : i / per_row;
+                const int j = (i - row * per_row) << 2;
                 const int gc = c0 + row / (KS * KS);
                 const bool v = gc < P.c;
                 const float *src = v ? P.wp + ((int64_t)c0 * KS * KS + row) * P.k + k0 + j : P.wp;
