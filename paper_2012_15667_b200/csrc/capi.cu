@@ -446,6 +446,15 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                             const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, dim, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w) {
     auto enc = encode_fn();
     if (!enc) return false;

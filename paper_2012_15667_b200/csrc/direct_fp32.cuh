@@ -90,6 +90,14 @@ __device__ __forceinline__ void tma_load_4d(void *dst, uint64_t map, int c0, int
         "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void *dst, uint64_t map, int c0, int c1, int c2,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d(void *dst, uint64_t map, int c0, int c1,
                                             uint64_t *bar) {
     asm volatile(
@@ -428,5 +436,7 @@ DirectKernelFn find_direct_kernel(int ks, int st, int tx, int ty, int tz);
 
 // Build the TMA descriptors of a plan (host); false if TMA cannot describe it.
 bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w);
+bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                             const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es);
 
 }  // namespace convio

@@ -199,39 +199,67 @@ static int plan_winograd(const convio_conv_desc *d, const convio_tile *t, int e,
     P.px = t->x / e; P.npos = npos; P.npg = npos / TP; P.nzg = t->z / TZ;
     P.units = best_units;
     P.tile_w = t->x + 2; P.tile_h = t->y + 2;
-    P.pitch = P.tile_w | 1;               // odd pitch: conflict-free patch reads
-    P.u_pitch = (t->z + 3) & ~3;
-    if (P.u_pitch % 32 == 0) P.u_pitch += 4;   // rows of different xi on different banks
+    bool tma = d->layout == CONVIO_LAYOUT_CHW && d->w % 4 == 0 && ((int64_t)d->h * d->w) % 4 == 0 &&
+               d->k % 4 == 0 && t->z % 4 == 0 && t->z <= 256 && P.tile_h <= 256 &&
+               ((P.tile_w + 6) & ~3) <= 256;
+    // staged rows start at a 16-byte-aligned column: up to 3 leading extras
+    P.pitch = ((P.tile_w + 3 + 3) & ~3) | (tma ? 0 : 1);
+    if (tma) P.pitch = (P.tile_w + 3 + 3) & ~3;
+    P.u_pitch = t->z;                      // U slice is the dense [xi][cc][z] box
     P.v_pitch = (npos + 3) & ~3;
     if (P.v_pitch % 32 == 0) P.v_pitch += 4;
     P.o_pitch = npos | 1;
-    // channels per stage from the budget left after the register-resident
-    // accumulators (m^2 * npos * z words)
-    const int64_t per_ch = (int64_t)P.tile_h * P.pitch + (int64_t)mm * P.u_pitch + (int64_t)mm * P.v_pitch;
+    auto round32 = [](int64_t v) { return (v + 31) & ~31LL; };
+    const int64_t per_ch = (int64_t)P.tile_h * P.pitch + (int64_t)mm * t->z;
     const int64_t budget = (int64_t)t->s_b - (int64_t)mm * npos * t->z;
-    int stages = budget >= 2 * per_ch ? 2 : 1;
-    int64_t ck = budget > 0 ? budget / (stages * per_ch) : 1;
-    ck = std::max<int64_t>(1, std::min<int64_t>(ck, 16));
-    ck = std::min<int64_t>(ck, d->c);
     auto bytes = [&](int64_t cks, int st) {
-        const int64_t in_stage = (cks * P.tile_h * P.pitch + 3) & ~3LL;
-        const int64_t u_stage = cks * mm * P.u_pitch;
-        const int64_t v = cks * mm * P.v_pitch;
-        const int64_t pipe = st * (in_stage + u_stage) + v;
+        const int64_t ring = st * (round32(cks * P.tile_h * P.pitch) + round32(cks * mm * t->z));
+        const int64_t v = 2 * round32(cks * mm * P.v_pitch);
         const int64_t exch = (int64_t)mm * t->z * P.o_pitch;
-        return 4 * std::max(pipe, exch);
+        return 4 * (round32(std::max(ring + v, exch)) + 4 * st);
     };
-    const int64_t cap = 227 * 1024;
-    while (ck > 1 && bytes(ck, stages) > cap) --ck;
-    if (bytes(ck, stages) > cap && stages == 2) stages = 1;
-    if (bytes(ck, stages) > cap)
+    // occupancy first (12 warps/SM), then a pipelined ring, then channels per stage
+    int regs_guess = kernel_regs((const void *)fn);
+    if (regs_guess <= 0) regs_guess = 128;
+    const int warps_per_block = (threads + 31) / 32;
+    const int regs_per_warp = ((regs_guess * 32 + 255) / 256) * 256;
+    const int by_regs = 65536 / std::max(1, regs_per_warp * warps_per_block);
+    const int by_threads = 2048 / threads;
+    int stages = 1;
+    int64_t ck = 1;
+    double ring_score = -1;
+    for (int st = 1; st <= 3; ++st) {
+        for (int64_t cks = 1; cks <= std::min<int64_t>(16, d->c); cks *= 2) {
+            if (st * cks * per_ch > budget && !(st == 1 && cks == 1)) continue;
+            const int64_t by = bytes(cks, st);
+            if (by > 227 * 1024) continue;
+            const int by_smem = (int)((228 * 1024) / (by + 1024));
+            const int blocks = std::min(std::min(by_regs, by_threads), std::min(by_smem, 32));
+            if (blocks < 1) continue;
+            const double score = std::min(blocks * warps_per_block, 12) * 1000.0 +
+                                 (st >= 2 ? 500.0 : 0.0) + (st == 3 ? 100.0 : 0.0) +
+                                 std::min<int64_t>(cks * (st > 1 ? st - 1 : 1), 16) * 10.0;
+            if (score > ring_score) {
+                ring_score = score;
+                stages = st;
+                ck = cks;
+            }
+        }
+    }
+    if (bytes(ck, stages) > 227 * 1024)
         return fail(CONVIO_EINFEASIBLE, "Winograd staging needs %lld B of shared memory > 227 KB",
                     (long long)bytes(ck, stages));
+    if (tma && stages < 2) tma = false;
     P.ck = (int)ck;
     P.stages = stages;
-    P.in_stage = (int)((ck * P.tile_h * P.pitch + 3) & ~3LL);
-    P.u_stage = (int)(ck * mm * P.u_pitch);
-    P.v_floats = (int)(ck * mm * P.v_pitch);
+    P.in_stage = (int)round32(ck * P.tile_h * P.pitch);
+    P.u_stage = (int)round32(ck * mm * t->z);
+    P.v_floats = (int)round32(ck * mm * P.v_pitch);
+    P.use_tma = tma ? 1 : 0;
+    P.in_box_bytes = (int)(4 * ck * P.tile_h * P.pitch);
+    P.u_box_bytes = (int)(4 * ck * mm * t->z);
+    P.bar_off = (int)round32(std::max<int64_t>(stages * (P.in_stage + P.u_stage) + 2LL * P.v_floats,
+                                               (int64_t)mm * t->z * P.o_pitch));
     P.tiles_x = q / t->x; P.tiles_y = p / t->y;
     pl->grid = dim3(d->k / t->z, P.tiles_x * P.tiles_y, d->n);
     if (pl->grid.y > 65535 || pl->grid.z > 65535)
@@ -247,6 +275,23 @@ static int plan_winograd(const convio_conv_desc *d, const convio_tile *t, int e,
 }
 
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
+
+static bool make_winograd_tensor_maps(const WinoParams &P, int e, CUtensorMap *tm_in, CUtensorMap *tm_u) {
+    // the input box exactly as the direct kernel's (same 16-byte-aligned start rule)
+    DirectParams D;
+    memset(&D, 0, sizeof(D));
+    D.x = P.x; D.wp = P.u; D.n = P.n; D.c = P.c; D.h = P.h; D.w = P.w; D.k = P.k;
+    D.pitch = P.pitch; D.tile_h = P.tile_h; D.ck = P.ck; D.ks = 1; D.bz = P.bz;
+    CUtensorMap dummy;
+    if (!make_direct_tensor_maps(D, tm_in, &dummy)) return false;
+    const int mm = (e + 2) * (e + 2);
+    if (reinterpret_cast<uintptr_t>(P.u) & 15) return false;
+    cuuint64_t dim[3] = {(cuuint64_t)P.k, (cuuint64_t)P.c, (cuuint64_t)mm};
+    cuuint64_t str[2] = {(cuuint64_t)P.k * 4, (cuuint64_t)P.c * P.k * 4};
+    cuuint32_t box[3] = {(cuuint32_t)P.bz, (cuuint32_t)P.ck, (cuuint32_t)mm};
+    cuuint32_t es[3] = {1, 1, 1};
+    return encode_tensor_map_tiled(tm_u, 3, const_cast<float *>(P.u), dim, str, box, es);
+}
 
 static int default_winograd_tile(const convio_conv_desc *d, int e, convio_tile *out) {
     int p = 0, q = 0;
@@ -440,7 +485,11 @@ int convio_conv_winograd_f32(const convio_conv_desc *desc, const convio_tile *ti
         note_launch();
     }
     pl.P.x = x; pl.P.u = u; pl.P.bias = bias; pl.P.y = y; pl.P.relu = relu;
-    pl.fn<<<pl.grid, pl.threads, pl.smem, (cudaStream_t)stream>>>(pl.P);
+    CUtensorMap tm_in, tm_u;
+    memset(&tm_in, 0, sizeof(tm_in));
+    memset(&tm_u, 0, sizeof(tm_u));
+    if (pl.P.use_tma && !make_winograd_tensor_maps(pl.P, e, &tm_in, &tm_u)) pl.P.use_tma = 0;
+    pl.fn<<<pl.grid, pl.threads, pl.smem, (cudaStream_t)stream>>>(pl.P, tm_in, tm_u);
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;

@@ -4,11 +4,13 @@
 //
 // Block  = an x*y*z output sub-block: NPOS = (x/e)(y/e) tile positions.
 // Stage  = ck input channels: (x+2)(y+2) input footprint (zero-filled halo)
-//          and the ck*m^2*z transformed-filter slice U, cp.async -> smem,
-//          double-buffered.
-// Step 1 = input transform V = B^T d B of every (channel, position) into
-//          smem (the kernel transform is shared: U from
-//          convio_winograd_filter_transform, i.e. shared_kernel_transform).
+//          and the m^2*ck*z transformed-filter slice U in an NS-deep smem
+//          ring: TMA (4-D input box + 3-D U box, mbarrier complete_tx) when
+//          the strides allow, else a cp.async ring.
+// Step 1 = input transform V = B^T d B of every (channel, position) into a
+//          double-buffered smem V (the kernel transform is shared: U from
+//          convio_winograd_filter_transform, i.e. shared_kernel_transform);
+//          one block barrier per stage.
 // Step 2+3 = m^2 independent GEMMs accumulated over channels in registers:
 //          the (xi, position group of TP, z group of TZ) units are dealt
 //          round-robin to the block's threads (UPT units each), so any thread
@@ -18,7 +20,7 @@
 //          (z, position) gets A^T Pi A, + bias/ReLU, stored to HBM.
 #pragma once
 
-#include "common.cuh"
+#include "direct_fp32.cuh"   // mbarrier / TMA primitives
 
 namespace convio {
 
@@ -43,6 +45,9 @@ struct WinoParams {
     int o_pitch;             // floats per (xi, z) row of the exchange buffer
     int tiles_x, tiles_y;
     int relu;
+    int use_tma;
+    int in_box_bytes, u_box_bytes;
+    int bar_off;             // float offset of the mbarriers in smem
 };
 
 template <int E>
@@ -125,7 +130,9 @@ struct WinoMats<4> {
 };
 
 template <int E, int TZ, int TP, int UPT>
-__global__ void winograd_f32_kernel(const WinoParams P) {
+__global__ void winograd_f32_kernel(const __grid_constant__ WinoParams P,
+                                    const __grid_constant__ CUtensorMap tm_in,
+                                    const __grid_constant__ CUtensorMap tm_u) {
     constexpr int M = E + 2;
     constexpr int MM = M * M;
     extern __shared__ __align__(128) float smem[];
@@ -137,70 +144,87 @@ __global__ void winograd_f32_kernel(const WinoParams P) {
     const int yt = blockIdx.y / P.tiles_x;
     const int img = blockIdx.z;
     const int ox0 = xt * P.bx, oy0 = yt * P.by;
-    const int ix0 = ox0 - P.pad, iy0 = oy0 - P.pad;
+    const int iy0 = oy0 - P.pad;
+    const int ix0 = ox0 - P.pad;
+    const int shift = ((ix0 % 4) + 4) % 4;   // staged rows start 16-byte aligned
+    const int ix0a = ix0 - shift;
+    const int stage_w = P.tile_w + shift;
 
+    const int NS = P.stages;
     float *in_s = smem;
-    float *u_s = in_s + P.stages * P.in_stage;
-    float *v_s = u_s + P.stages * P.u_stage;
+    float *u_s = in_s + NS * P.in_stage;
+    float *v_s = u_s + NS * P.u_stage;          // 2 buffers of v_floats
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + P.bar_off);
+    uint64_t *empty = full + NS;
+    const int nwarps = (nthr + 31) >> 5;
     const float *xb = P.x + (int64_t)img * P.xs.n;
     const int nchunks = (P.c + P.ck - 1) / P.ck;
+    const uint64_t map_in = reinterpret_cast<uint64_t>(&tm_in);
+    const uint64_t map_u = reinterpret_cast<uint64_t>(&tm_u);
 
-    auto load_chunk = [&](int chunk, int buf) {
+    auto tma_issue = [&](int chunk, int slot) {   // one thread
+        uint64_t *bar = full + slot;
+        mbar_arrive_expect_tx(bar, P.in_box_bytes + P.u_box_bytes);
+        tma_load_4d(in_s + slot * P.in_stage, map_in, ix0a, iy0, chunk * P.ck, img, bar);
+        tma_load_3d(u_s + slot * P.u_stage, map_u, k0, chunk * P.ck, 0, bar);
+    };
+    auto cp_issue = [&](int chunk, int slot) {    // all threads
         const int c0 = chunk * P.ck;
-        float *din = in_s + buf * P.in_stage;
-        const int total = P.ck * P.tile_h * P.tile_w;
+        float *din = in_s + slot * P.in_stage;
+        const int total = P.ck * P.tile_h * stage_w;
         for (int i = tid; i < total; i += nthr) {
             int cc, r, col;
             if (P.layout == CONVIO_LAYOUT_HWC) {
                 cc = i % P.ck;
                 const int t = i / P.ck;
-                col = t % P.tile_w;
-                r = t / P.tile_w;
+                col = t % stage_w;
+                r = t / stage_w;
             } else if (P.layout == CONVIO_LAYOUT_CWH) {
                 r = i % P.tile_h;
                 const int t = i / P.tile_h;
-                col = t % P.tile_w;
-                cc = t / P.tile_w;
+                col = t % stage_w;
+                cc = t / stage_w;
             } else {
-                col = i % P.tile_w;
-                const int t = i / P.tile_w;
+                col = i % stage_w;
+                const int t = i / stage_w;
                 r = t % P.tile_h;
                 cc = t / P.tile_h;
             }
-            const int gc = c0 + cc, gy = iy0 + r, gx = ix0 + col;
+            const int gc = c0 + cc, gy = iy0 + r, gx = ix0a + col;
             const bool v = gc < P.c && gy >= 0 && gy < P.h && gx >= 0 && gx < P.w;
             const float *src = v ? xb + gc * P.xs.c + gy * P.xs.y + gx * P.xs.x : P.x;
             cp_async4(din + (cc * P.tile_h + r) * P.pitch + col, src, v);
         }
-        float *du = u_s + buf * P.u_stage;
-        const int rows = P.ck * MM;   // (cc, xi) rows of bz values
+        // U slice -> [xi][cc][z] (the TMA box layout)
+        float *du = u_s + slot * P.u_stage;
+        const int rows = MM * P.ck;
         if ((P.bz & 3) == 0 && (P.k & 3) == 0) {
             const int per_row = P.bz >> 2;
             const int tot = rows * per_row;
             for (int i = tid; i < tot; i += nthr) {
                 const int row = i / per_row, j = (i - row * per_row) << 2;
-                const int cc = row / MM, xi = row - cc * MM;
+                const int xi = row / P.ck, cc = row - xi * P.ck;
                 const int gc = c0 + cc;
                 const bool v = gc < P.c;
                 const float *src = v ? P.u + ((int64_t)xi * P.c + gc) * P.k + k0 + j : P.u;
-                cp_async16(du + row * P.u_pitch + j, src, v);
+                cp_async16(du + row * P.bz + j, src, v);
             }
         } else {
             const int tot = rows * P.bz;
             for (int i = tid; i < tot; i += nthr) {
                 const int row = i / P.bz, j = i - row * P.bz;
-                const int cc = row / MM, xi = row - cc * MM;
+                const int xi = row / P.ck, cc = row - xi * P.ck;
                 const int gc = c0 + cc;
                 const bool v = gc < P.c;
                 const float *src = v ? P.u + ((int64_t)xi * P.c + gc) * P.k + k0 + j : P.u;
-                cp_async4(du + row * P.u_pitch + j, src, v);
+                cp_async4(du + row * P.bz + j, src, v);
             }
         }
     };
 
     // step 1: V[cc][xi][pos] = (B^T d B)[xi] for every (channel, position)
-    auto transform_inputs = [&](int buf) {
-        const float *din = in_s + buf * P.in_stage;
+    auto transform_inputs = [&](int slot, float *vbuf) {
+        const float *din = in_s + slot * P.in_stage + shift;
         const int tasks = P.ck * P.npos;
         for (int t = tid; t < tasks; t += nthr) {
             const int cc = t / P.npos, pos = t - cc * P.npos;
@@ -212,7 +236,7 @@ __global__ void winograd_f32_kernel(const WinoParams P) {
 #pragma unroll
                 for (int j = 0; j < M; ++j) d[i][j] = src[i * P.pitch + j];
             WinoMats<E>::input(d, v);
-            float *dst = v_s + cc * MM * P.v_pitch + pos;
+            float *dst = vbuf + cc * MM * P.v_pitch + pos;
 #pragma unroll
             for (int i = 0; i < M; ++i)
 #pragma unroll
@@ -243,27 +267,27 @@ __global__ void winograd_f32_kernel(const WinoParams P) {
 #pragma unroll
             for (int b = 0; b < TP; ++b) acc[j][a][b] = 0.0f;
 
-    // steps 2+3: acc[z][pos] += U[cc][xi][z] * V[cc][xi][pos]
-    auto gemm = [&](int buf) {
-        const float *ub = u_s + buf * P.u_stage;
-        const int ustep = MM * P.u_pitch, vstep = MM * P.v_pitch;
+    // steps 2+3: acc[z][pos] += U[xi][cc][z] * V[cc][xi][pos]
+    auto gemm = [&](int slot, const float *vbuf) {
+        const float *ub = u_s + slot * P.u_stage;
+        const int vstep = MM * P.v_pitch;
 #pragma unroll
         for (int j = 0; j < UPT; ++j) {
             if (!u_ok[j]) continue;
-            const float *us = ub + u_xi[j] * P.u_pitch + u_z[j];
-            const float *vs = v_s + u_xi[j] * P.v_pitch + u_p[j];
-#pragma unroll 2
+            const float *us = ub + u_xi[j] * P.ck * P.bz + u_z[j];
+            const float *vs = vbuf + u_xi[j] * P.v_pitch + u_p[j];
+#pragma unroll 4
             for (int cc = 0; cc < P.ck; ++cc) {
                 float ur[TZ], vr[TP];
                 if constexpr (TZ % 4 == 0) {
 #pragma unroll
                     for (int q = 0; q < TZ; q += 4) {
-                        const float4 t = *reinterpret_cast<const float4 *>(us + cc * ustep + q);
+                        const float4 t = *reinterpret_cast<const float4 *>(us + cc * P.bz + q);
                         ur[q] = t.x; ur[q + 1] = t.y; ur[q + 2] = t.z; ur[q + 3] = t.w;
                     }
                 } else {
 #pragma unroll
-                    for (int q = 0; q < TZ; ++q) ur[q] = us[cc * ustep + q];
+                    for (int q = 0; q < TZ; ++q) ur[q] = us[cc * P.bz + q];
                 }
                 if constexpr (TP % 4 == 0) {
 #pragma unroll
@@ -289,35 +313,60 @@ __global__ void winograd_f32_kernel(const WinoParams P) {
         }
     };
 
-    if (P.stages >= 2) {
-        load_chunk(0, 0);
-        cp_async_commit();
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            if (chunk + 1 < nchunks) {
-                load_chunk(chunk + 1, (chunk + 1) & 1);
-                cp_async_commit();
-                cp_async_wait<1>();
-            } else {
-                cp_async_wait<0>();
+    if (P.use_tma) {
+        if (tid == 0) {
+            for (int s2 = 0; s2 < NS; ++s2) {
+                mbar_init(full + s2, 1);
+                mbar_init(empty + s2, nwarps);
             }
-            __syncthreads();
-            transform_inputs(chunk & 1);
-            __syncthreads();
-            gemm(chunk & 1);
-            __syncthreads();
+            asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        }
+        __syncthreads();
+        if (tid == 0)
+            for (int s2 = 0; s2 < NS - 1 && s2 < nchunks; ++s2) tma_issue(s2, s2);
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            const int slot = chunk % NS;
+            float *vbuf = v_s + (chunk & 1) * P.v_floats;
+            mbar_wait(full + slot, (chunk / NS) & 1);
+            transform_inputs(slot, vbuf);
+            __syncthreads();   // V[chunk&1] complete; V[(chunk-1)&1] readers done
+            gemm(slot, vbuf);
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(empty + slot);
+            const int next = chunk + NS - 1;
+            if (tid == 0 && next < nchunks) {
+                const int nslot = next % NS;
+                if (next >= NS) mbar_wait(empty + nslot, ((next / NS) - 1) & 1);
+                tma_issue(next, nslot);
+            }
         }
     } else {
-        for (int chunk = 0; chunk < nchunks; ++chunk) {
-            load_chunk(chunk, 0);
+        const int pre = NS > 1 ? NS - 1 : 1;
+        for (int s2 = 0; s2 < pre; ++s2) {
+            if (s2 < nchunks) cp_issue(s2, s2);
             cp_async_commit();
-            cp_async_wait<0>();
+        }
+        for (int chunk = 0; chunk < nchunks; ++chunk) {
+            float *vbuf = v_s + (chunk & 1) * P.v_floats;
+            if (NS >= 3) cp_async_wait<1>();
+            else cp_async_wait<0>();
+            __syncthreads();   // chunk landed for all; slot (chunk-1)%NS and V buffers free
+            if (NS >= 2) {
+                const int next = chunk + NS - 1;
+                if (next < nchunks) cp_issue(next, next % NS);
+                cp_async_commit();
+            }
+            transform_inputs(chunk % NS, vbuf);
             __syncthreads();
-            transform_inputs(0);
-            __syncthreads();
-            gemm(0);
-            __syncthreads();
+            gemm(chunk % NS, vbuf);
+            if (NS == 1) {
+                __syncthreads();
+                if (chunk + 1 < nchunks) cp_issue(chunk + 1, 0);
+                cp_async_commit();
+            }
         }
     }
+    __syncthreads();
 
     // step 4: exchange through smem O[xi][z][pos], then A^T Pi A per (z, pos)
     float *o_s = smem;
@@ -358,7 +407,7 @@ __global__ void winograd_f32_kernel(const WinoParams P) {
     }
 }
 
-using WinoKernelFn = void (*)(const WinoParams);
+using WinoKernelFn = void (*)(const WinoParams, const CUtensorMap, const CUtensorMap);
 WinoKernelFn find_winograd_kernel(int e, int tz, int tp, int upt);
 
 int winograd_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
