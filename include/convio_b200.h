@@ -55,6 +55,7 @@ extern "C" {
 
 #define CONVIO_ALG_DIRECT 0
 #define CONVIO_ALG_WINOGRAD 1
+#define CONVIO_ALG_IGEMM_TF32 2   /* tcgen05 implicit GEMM, TF32 in / FP32 accumulate */
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {
@@ -127,6 +128,20 @@ int convio_conv_winograd_f32(const convio_conv_desc *desc, const convio_tile *ti
                              const float *x, const float *w, int32_t w_is_transformed,
                              const float *bias, int32_t relu, float *y,
                              void *workspace, size_t workspace_bytes, void *stream);
+
+/* Repack KCRS filters to [R*S][K][C] for the tcgen05 implicit GEMM. */
+int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float *w_packed,
+                             void *stream);
+
+/* Direct convolution as an implicit GEMM on the 5th-gen tensor cores
+ * (tcgen05.mma kind::tf32, accumulators in TMEM, TMA SWIZZLE_128B operand
+ * staging).  NHWC (CONVIO_LAYOUT_HWC) activations, C % 32 == 0, stride 1,
+ * tile z in {64,128,256}, x*y <= 128 (ceil(128/(x*y)) images stacked per MMA
+ * tile).  Inputs are consumed at TF32 precision, accumulation is FP32.
+ * Replaces the same schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
+int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
+                           const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
+                           float *y, void *workspace, size_t workspace_bytes, void *stream);
 
 /* The transform matrices the kernels use (row-major AT e*m, G m*r, BT m*m). */
 int convio_winograd_matrices(int32_t e, int32_t r, float *at, float *g, float *bt);

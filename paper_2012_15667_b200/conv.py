@@ -23,7 +23,8 @@ import torch
 from . import _native as N
 from .dataflow import LAYOUTS, TileConfig
 
-__all__ = ["conv_direct", "conv_winograd", "winograd_filter_transform", "pack_filter_direct",
+__all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "winograd_filter_transform",
+           "pack_filter_direct", "pack_filter_igemm",
            "infer_layout", "to_layout", "empty_act", "query", "last_launch_count"]
 
 
@@ -97,7 +98,8 @@ def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CH
     n, c, h, w = x_shape
     k, _, r, s = w_shape
     desc = N.make_desc(n, c, h, w, k, r, s, stride, padding, LAYOUTS.index(layout))
-    alg = N.ALG_DIRECT if algorithm == "direct" else N.ALG_WINOGRAD
+    alg = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
+           "igemm_tf32": N.ALG_IGEMM_TF32}[algorithm]
     rc, info = N.query(desc, N.make_tile(tile), alg)
     info["rc"] = rc
     return info
@@ -210,6 +212,54 @@ def conv_winograd(x: torch.Tensor, w: torch.Tensor, e: int = 2, padding: int = 0
         _ptr(x), _ptr(wsrc), is_t, _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes,
         _stream_ptr(stream))
     N.check(rc, "conv_winograd")
+    return out
+
+
+def pack_filter_igemm(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """KCRS -> [R*S][K][C] for the tcgen05 implicit GEMM (K-major B operand)."""
+    _check_tensor(w, "w")
+    w = w.contiguous()
+    k, c, r, s = w.shape
+    out = torch.empty((r * s, k, c), device=w.device, dtype=torch.float32)
+    desc = N.make_desc(1, c, r, s, k, r, s, 1, 0, 2)
+    N.check(N.lib().convio_pack_filter_igemm(ctypes.byref(desc), _ptr(w), _ptr(out),
+                                             _stream_ptr(stream)), "pack_filter_igemm")
+    return out
+
+
+def conv_igemm_tf32(x: torch.Tensor, w: torch.Tensor, padding: int = 0,
+                    tile: TileConfig | None = None, bias: torch.Tensor | None = None,
+                    relu: bool = False, out: torch.Tensor | None = None, stream=None,
+                    w_packed: torch.Tensor | None = None,
+                    workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Direct conv as a tcgen05 implicit GEMM: TF32 inputs, FP32 accumulation in TMEM.
+
+    ``x`` must be channels-last (layout ``HWC``), ``C % 32 == 0``, stride 1,
+    ``tile.z in {64, 128, 256}``, ``tile.x * tile.y <= 128``.  Results differ
+    from FP32 by TF32 input rounding (tolerance 5e-3).
+    """
+    _check_tensor(x, "x")
+    _check_tensor(w, "w")
+    layout = infer_layout(x)
+    if layout != "HWC":
+        raise ValueError("conv_igemm_tf32 needs a channels-last (HWC) input")
+    if tile is None:
+        raise ValueError("conv_igemm_tf32 needs an explicit tile")
+    desc = _desc(x, w, 1, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, 1, padding)
+    if out is None:
+        out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
+    if w_packed is not None:
+        wsrc, is_packed, ws, ws_bytes = w_packed, 1, None, 0
+    else:
+        need = desc.k * desc.c * desc.r * desc.s
+        if workspace is None or workspace.numel() < need:
+            workspace = torch.empty(need, device=x.device, dtype=torch.float32)
+        wsrc, is_packed, ws, ws_bytes = w.contiguous(), 0, workspace, 4 * need
+    rc = N.lib().convio_conv_igemm_tf32(
+        ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), _ptr(x), _ptr(wsrc), is_packed,
+        _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes, _stream_ptr(stream))
+    N.check(rc, "conv_igemm_tf32")
     return out
 
 

@@ -30,6 +30,7 @@ void reset_launches() { t_launches = 0; }
 
 int direct_instance_count();
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
+int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
 
 // ---------------------------------------------------------------------------
 // device properties (cached once per process, per device)
@@ -446,13 +447,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
-                             const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
+bool encode_tensor_map_tiled_ex(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                                const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es,
+                                bool swizzle128) {
     auto enc = encode_fn();
     if (!enc) return false;
     return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank, base, dim, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                             const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
+    return encode_tensor_map_tiled_ex(map, rank, base, dim, strides, box, es, false);
 }
 
 bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w) {
@@ -583,6 +591,7 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
         return rc;
     }
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_query(desc, tile, out);
+    if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out);
     set_error("unknown algorithm %d", algorithm);
     return CONVIO_EINVAL;
 }
@@ -593,6 +602,7 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
     if (!desc) return -1;
     if (algorithm == CONVIO_ALG_DIRECT) return 4LL * desc->k * desc->c * desc->r * desc->s;
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_workspace_bytes(desc, tile);
+    if (algorithm == CONVIO_ALG_IGEMM_TF32) return 4LL * desc->k * desc->c * desc->r * desc->s;
     return -1;
 }
 

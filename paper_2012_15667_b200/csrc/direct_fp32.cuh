@@ -438,5 +438,8 @@ DirectKernelFn find_direct_kernel(int ks, int st, int tx, int ty, int tz);
 bool make_direct_tensor_maps(const DirectParams &P, CUtensorMap *tm_in, CUtensorMap *tm_w);
 bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
                              const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es);
+bool encode_tensor_map_tiled_ex(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                                const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es,
+                                bool swizzle128);
 
 }  // namespace convio

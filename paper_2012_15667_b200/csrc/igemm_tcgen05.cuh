@@ -1,0 +1,217 @@
+// Direct convolution as an implicit GEMM on the 5th-generation tensor cores
+// (tcgen05, kind::tf32, FP32 accumulate in TMEM) -- the "TF32 tcgen05 variant
+// for the dense contraction stage" of the north star, same output-stationary
+// block (x*y pixels x z channels per CTA) as the FP32 dataflow
+// (reference pkg/src/convio/dataflow.py:219-250).
+//
+//   GEMM view  D[m][n] += A[m][kk] * B[n][kk]
+//     m  = pixel of the block (x*y pixels of up to `imgs` stacked images),
+//     n  = output channel (z = BN per CTA),
+//     kk = (tap r,s ; input-channel c), walked as 9 taps x C/32 blocks.
+//   A    = NHWC input box [imgs][y][x][32 ch] for tap (r,s): one TMA 4-D load
+//          per k-block, zero-filled halo (= padding), SWIZZLE_128B, i.e. the
+//          canonical K-major UMMA layout (128-B rows, 1024-B swizzle atoms).
+//   B    = packed filters [RS][K][C] box [BN][32 ch], same layout.
+//   MMA  = one elected thread issues 4 x tcgen05.mma (M=128, N=BN, K=8) per
+//          k-block; tcgen05.commit releases the smem stage to the TMA thread.
+//   D    = 128 lanes x BN fp32 columns in TMEM; 4 warps tcgen05.ld their 32
+//          lanes and store NHWC rows (+ bias / ReLU).
+// Rows of the A tile beyond x*y*imgs are don't-care (never stored).
+#pragma once
+
+#include "direct_fp32.cuh"
+
+namespace convio {
+
+struct IgemmParams {
+    const float *bias;
+    float *y;
+    int n, c, h, w, k, p, q, pad, stride;
+    int bx, by, imgs;          // block: bx * by pixels of `imgs` images (<= 128 rows)
+    int tiles_x, tiles_y, img_groups;
+    int kblocks;               // 9 * C / 32 (R*S taps x channel blocks)
+    int cblocks;               // C / 32
+    int ks;                    // kernel edge
+    int stages;
+    int relu;
+};
+
+// ---- tcgen05 / UMMA primitives ----------------------------------------------------
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
+    // K-major, SWIZZLE_128B: 128-B rows, 8-row (1024-B) atoms -> SBO = 1024 B.
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFF);        // start address
+    d |= (uint64_t)1 << 16;                             // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;                   // SBO
+    d |= (uint64_t)1 << 46;                             // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                             // layout: SWIZZLE_128B
+    return d;
+}
+
+template <int BN>
+__device__ __forceinline__ constexpr uint32_t idesc_tf32_m128() {
+    return (1u << 4)          // D format F32
+           | (2u << 7)        // A format TF32
+           | (2u << 10)       // B format TF32
+           | ((uint32_t)(BN >> 3) << 17)
+           | ((uint32_t)(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ld_32x32b(uint32_t taddr, float (&v)[N]);
+
+template <>
+__device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32]) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int BN>
+__global__ void __launch_bounds__(128, 1)
+    igemm_tf32_tcgen05_kernel(const __grid_constant__ IgemmParams P,
+                              const __grid_constant__ CUtensorMap tm_x,
+                              const __grid_constant__ CUtensorMap tm_w) {
+    constexpr int A_BYTES = 128 * 128;       // 128 rows x 32 fp32
+    constexpr int B_BYTES = BN * 128;        // BN rows x 32 fp32
+    constexpr int STAGE = A_BYTES + B_BYTES;
+    constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for SWIZZLE_128B atoms
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int NS = P.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint64_t *empty = full + NS;
+    uint64_t *done = empty + NS;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int k0 = blockIdx.x * BN;
+    const int xt = blockIdx.y % P.tiles_x;
+    const int rest = blockIdx.y / P.tiles_x;
+    const int yt = rest % P.tiles_y;
+    const int ig = rest / P.tiles_y;
+    const int ox0 = xt * P.bx, oy0 = yt * P.by, img0 = ig * P.imgs;
+    const uint64_t map_x = reinterpret_cast<uint64_t>(&tm_x);
+    const uint64_t map_w = reinterpret_cast<uint64_t>(&tm_w);
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_w));
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (tid == 0) {
+        // ---- TMA producer ---------------------------------------------------------
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+            const int s = kb % NS;
+            if (kb >= NS) mbar_wait(empty + s, ((kb / NS) - 1) & 1);
+            const int tap = kb / P.cblocks, cb = kb - tap * P.cblocks;
+            const int r = tap / P.ks, sx = tap - r * P.ks;
+            uint8_t *a = smem + s * STAGE;
+            uint8_t *b = a + A_BYTES;
+            mbar_arrive_expect_tx(full + s, (uint32_t)(P.bx * P.by * P.imgs * 128 + B_BYTES));
+            tma_load_4d(a, map_x, cb * 32, ox0 * P.stride + sx - P.pad, oy0 * P.stride + r - P.pad,
+                        img0, full + s);
+            tma_load_3d(b, map_w, cb * 32, k0, tap, full + s);
+        }
+    } else if (tid == 32) {
+        // ---- MMA issuer (single thread) -------------------------------------------
+        constexpr uint32_t idesc = idesc_tf32_m128<BN>();
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+            const int s = kb % NS;
+            mbar_wait(full + s, (kb / NS) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t a = smem_u32(smem + s * STAGE);
+            const uint32_t b = a + A_BYTES;
+            const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(b);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)   // K = 8 tf32 = 32 B per MMA
+                umma_tf32(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                          (kb | kk) != 0);
+            umma_commit(empty + s);
+        }
+        umma_commit(done);
+    }
+    // ---- epilogue: TMEM -> registers -> NHWC global ---------------------------------
+    mbar_wait(done, 0);
+    __syncwarp();   // the producer / MMA lanes rejoin their warps before .sync.aligned loads
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int m = warp * 32 + lane;                 // D row = TMEM lane = pixel
+    const int per_img = P.bx * P.by;
+    const int im = m / per_img, pix = m - im * per_img;
+    const int py = pix / P.bx, px = pix - py * P.bx;
+    const int img = img0 + im, oy = oy0 + py, ox = ox0 + px;
+    const bool valid = m < per_img * P.imgs && img < P.n && oy < P.p && ox < P.q;
+    float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+        float v[32];
+        tmem_ld_32x32b<32>(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+        if (valid) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+                float4 o;
+                o.x = v[j] + (P.bias ? __ldg(P.bias + k0 + c0 + j) : 0.0f);
+                o.y = v[j + 1] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 1) : 0.0f);
+                o.z = v[j + 2] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 2) : 0.0f);
+                o.w = v[j + 3] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 3) : 0.0f);
+                if (P.relu) {
+                    o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
+                    o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                }
+                *reinterpret_cast<float4 *>(dst + c0 + j) = o;
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace convio

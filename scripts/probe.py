@@ -113,6 +113,20 @@ def main():
         print(f"{name} direct best: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s  {tile} "
               f"regs={info['regs_per_thread']} smem={info['smem_bytes']} ck={info['channel_chunk']}",
               flush=True)
+        if c % 32 == 0:
+            xh = C.to_layout(x, "HWC")
+            wq = C.pack_filter_igemm(w)
+            for bx, by in ((28, 4), (14, 8), (hw, min(hw, 128 // hw)), (7, 7)):
+                for bn in (64, 128, 256):
+                    if k % bn or hw % bx or hw % by or bx * by > 128:
+                        continue
+                    tile = TileConfig(bx, by, bn, 32768, 1, 1, 1, layout="HWC")
+                    try:
+                        t = timeit(lambda: C.conv_igemm_tf32(xh, w, padding=1, tile=tile, w_packed=wq))
+                        print(f"{name} tcgen05 tf32 {bx}x{by}x{bn}: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s",
+                              flush=True)
+                    except Exception as exc:  # noqa: BLE001
+                        print(f"{name} tcgen05 {bx}x{by}x{bn}: {exc}", flush=True)
         for e in (2, 4):
             try:
                 u = C.winograd_filter_transform(w, e)

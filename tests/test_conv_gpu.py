@@ -118,3 +118,24 @@ def test_winograd_filter_transform_matches_oracle():
         m = e + 2
         ref = ref.reshape(m * m, 16, 8).transpose(0, 2, 1)
         assert np.max(np.abs(u - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
+
+
+TOL_TF32 = 5e-3
+
+IGEMM_CASES = [
+    (2, 64, 56, 56, 64, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
+    (2, 64, 56, 56, 128, TileConfig(14, 8, 128, 32768, 1, 1, 1, layout="HWC")),
+    (3, 128, 14, 14, 256, TileConfig(14, 7, 256, 32768, 1, 1, 1, layout="HWC")),
+    (5, 32, 7, 7, 64, TileConfig(7, 7, 64, 32768, 1, 1, 1, layout="HWC")),   # 2 images / tile
+]
+
+
+@pytest.mark.parametrize("case", IGEMM_CASES, ids=[str(i) for i in range(len(IGEMM_CASES))])
+def test_igemm_tcgen05_tf32_matches_oracle(case):
+    n, c, h, w, k, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    y = C.conv_igemm_tf32(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, bias=_dev(b))
+    ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
+    assert C.infer_layout(y) == "HWC"
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= TOL_TF32
