@@ -210,6 +210,7 @@ def main() -> None:
     ap.add_argument("--gather", action="store_true", help="all-gather outputs to every rank")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -225,7 +226,7 @@ def main() -> None:
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
         WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, shard_range,
-        gather_outputs)
+        gather_outputs, CUDA_CORE_ALGORITHMS)
     from paper_2012_15667_b200.device import winograd_gemm_flops
 
     torch.cuda.set_device(local_rank)
@@ -257,109 +258,180 @@ def main() -> None:
     lo, hi = shard_range(n_total, rank, world)
     n_local = hi - lo
     specs = expand(WORKLOADS[args.workload])
+    weights = [make_weights(s, dev, 1000 + i) for i, s in enumerate(specs)]
+    flops_local = sum(s.flops(n_local) for s in specs)
+    flops_all = sum_over_ranks(float(flops_local))
+
+    class Arm:
+        """One plan set: per-layer ConvLayers, inputs in each plan's layout, outputs."""
+
+        def __init__(self, plans):
+            self.plans = plans
+            self.layers = [ConvLayer(s, weights[i], plans.get(s.name)) for i, s in enumerate(specs)]
+            self.xs = [make_input(s, n_local, dev, seed=7919 * (i + 1) + lo, layout=lay.layout)
+                       for i, (s, lay) in enumerate(zip(specs, self.layers))]
+            self.ys = [C.empty_act(n_local, s.k, s.out_hw, s.out_hw, lay.layout, device=dev)
+                       for s, lay in zip(specs, self.layers)]
+            self.work_bytes = sum(x.numel() * 4 for x in self.xs) + sum(y.numel() * 4 for y in self.ys)
+
+        def step(self, events=None):
+            launches = 0
+            for i, layer in enumerate(self.layers):
+                layer.prepare(dev, stream)
+                launches += 1
+                if events is not None:
+                    events[i][0].record(stream)
+                layer.run(self.xs[i], out=self.ys[i], stream=stream)
+                if events is not None:
+                    events[i][1].record(stream)
+                launches += layer.launches
+            return launches
+
+        def timed(self, steps, flush_buf=None):
+            """K device-timed steps (barrier + sync both sides); per-layer events."""
+            ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in self.layers]
+                  for _ in range(steps)]
+            launches = 0
+            barrier()
+            torch.cuda.synchronize(dev)
+            if flush_buf is not None:
+                total = 0.0
+                for k in range(steps):
+                    flush_buf.fill_(float(k))
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    launches += self.step(ev[k])
+                    b.record(stream)
+                    b.synchronize()
+                    total += a.elapsed_time(b)
+            else:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for k in range(steps):
+                    launches += self.step(ev[k])
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                total = a.elapsed_time(b)
+            barrier()
+            torch.cuda.synchronize(dev)
+            return total, ev, launches
+
+        def breakdown(self, ev, steps):
+            rows, fam = [], {}
+            for i, (s, layer) in enumerate(zip(specs, self.layers)):
+                ts = [ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(steps)]
+                t_med = statistics.median(ts)
+                f_dir = s.flops(n_local)
+                if layer.algorithm == "winograd":
+                    f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
+                    name = f"winograd F({layer.e},3)"
+                else:
+                    f_alg = f_dir
+                    name = layer.algorithm
+                agg = fam.setdefault(name, {"ms": 0.0, "flops": 0.0, "launches": 0, "layers": set()})
+                agg["ms"] += sum(ts)
+                agg["flops"] += f_alg * steps
+                agg["launches"] += steps
+                agg["layers"].add(s.name)
+                comp = 4 * (n_local * s.c * s.hw * s.hw + s.k * s.c * s.r * s.r
+                            + n_local * s.k * s.out_hw * s.out_hw)
+                t = layer.tile
+                rows.append({
+                    "layer": s.name, "algorithm": name,
+                    "tile": None if t is None else [t.x, t.y, t.z, t.s_b, t.n_xt, t.n_yt, t.n_zt, t.layout],
+                    "ms": round(t_med, 4), "gflops": round(f_dir / (t_med / 1e3) / 1e9, 1),
+                    "q_dram_bytes": comp,
+                })
+            return rows, fam
+
     plans = load_plans(args.workload)
-    layers = [ConvLayer(s, make_weights(s, dev, 1000 + i), plans.get(s.name))
-              for i, s in enumerate(specs)]
-    xs = [make_input(s, n_local, dev, seed=7919 * (i + 1) + lo) for i, s in enumerate(specs)]
-    ys = [C.empty_act(n_local, s.k, s.out_hw, s.out_hw, "CHW", device=dev) for s in specs]
-    work_bytes = sum(x.numel() * 4 for x in xs) + sum(y.numel() * 4 for y in ys)
-    flush = work_bytes < 4 * L2_BYTES
+    arm = Arm(plans)
+    flush = arm.work_bytes < 4 * L2_BYTES
     scratch = torch.empty(2 * L2_BYTES // 4, device=dev) if flush else None
-
-    def step(events=None):
-        launches = 0
-        for i, layer in enumerate(layers):
-            layer.prepare(dev, stream)
-            launches += 1
-            if events is not None:
-                events[i][0].record(stream)
-            layer.run(xs[i], out=ys[i], stream=stream)
-            if events is not None:
-                events[i][1].record(stream)
-            launches += layer.launches
-        return launches
-
     for _ in range(args.warmup):
-        step()
+        arm.step()
     torch.cuda.synchronize(dev)
 
     # ---- device-timed region: exactly K steps --------------------------------
-    ev = [[[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in layers]
-          for _ in range(args.steps)]
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    launches = 0
-    barrier()
-    torch.cuda.synchronize(dev)
-    if flush:
-        total_ms = 0.0
-        for k in range(args.steps):
-            scratch.fill_(float(k))
-            a = torch.cuda.Event(enable_timing=True)
-            b = torch.cuda.Event(enable_timing=True)
-            a.record(stream)
-            launches += step(ev[k])
-            b.record(stream)
-            b.synchronize()
-            total_ms += a.elapsed_time(b)
-        barrier()
-        torch.cuda.synchronize(dev)
-    else:
-        a = torch.cuda.Event(enable_timing=True)
-        b = torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for k in range(args.steps):
-            launches += step(ev[k])
-        b.record(stream)
-        torch.cuda.synchronize(dev)
-        barrier()
-        torch.cuda.synchronize(dev)
-        total_ms = a.elapsed_time(b)
+    total_ms, ev, launches = arm.timed(args.steps, scratch)
     clk = clocks.stop()
     t_max_ms = max_over_ranks(total_ms)
-    flops_local = sum(s.flops(n_local) for s in specs)
-    flops_all = sum_over_ranks(float(flops_local))
     value = flops_all * args.steps / (t_max_ms / 1e3) / 1e9
+    per_layer, fam = arm.breakdown(ev, args.steps)
 
-    # per-layer breakdown (rank-local kernel times, median over steps)
-    per_layer = []
-    fam_time = {"direct": 0.0, "winograd": 0.0}
-    fam_flops = {"direct": 0.0, "winograd": 0.0}
-    fam_launches = {"direct": 0, "winograd": 0}
-    for i, (s, layer) in enumerate(zip(specs, layers)):
-        ts = [ev[k][i][0].elapsed_time(ev[k][i][1]) for k in range(args.steps)]
-        t_med = statistics.median(ts)
-        f_dir = s.flops(n_local)
-        if layer.algorithm == "winograd":
-            f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
-        else:
-            f_alg = f_dir
-        fam_time[layer.algorithm] += sum(ts)
-        fam_flops[layer.algorithm] += f_alg * args.steps
-        fam_launches[layer.algorithm] += args.steps
-        comp_bytes = 4 * (n_local * s.c * s.hw * s.hw + s.k * s.c * s.r * s.r
-                          + n_local * s.k * s.out_hw * s.out_hw)
-        per_layer.append({
-            "layer": s.name, "algorithm": layer.algorithm + (f"F({layer.e},3)" if layer.algorithm == "winograd" else ""),
-            "tile": None if layer.tile is None else [layer.tile.x, layer.tile.y, layer.tile.z, layer.tile.s_b,
-                                                     layer.tile.n_xt, layer.tile.n_yt, layer.tile.n_zt],
-            "ms": round(t_med, 4), "gflops": round(f_dir / (t_med / 1e3) / 1e9, 1),
-            "q_dram_bytes": comp_bytes,
-        })
-
-    # ---- roofline of the dominant kernel family --------------------------------
-    dom = max(fam_time, key=fam_time.get)
-    achieved = fam_flops[dom] / (fam_time[dom] / 1e3) / 1e12 if fam_time[dom] else 0.0
-    peak = ffma_peak_tflops(torch, stream)
+    # ---- roofline of the dominant kernel (largest share of the step) ------------
+    dom = max(fam, key=lambda k: fam[k]["ms"])
+    d = fam[dom]
+    achieved = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] else 0.0
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except (OSError, ValueError):
+        pass
     traffic_tab = load_profile_traffic()
-    traffic = traffic_tab.get(f"{args.workload}:{dom}")
+    if dom.startswith("igemm"):
+        # tensor pipe: dense TF32 = 1/2 of the measured bf16 rate; 3xTF32 issues 3 MMAs per flop
+        mma_per_flop = 3 if dom == "igemm_3xtf32" else 1
+        bf16 = peaks.get("bf16_tflops") or 1590.0
+        peak = bf16 / 2
+        roofline = {
+            "bound": "tensor", "kernel": f"{dom} (tcgen05.mma kind::tf32)",
+            "achieved": round(achieved * mma_per_flop, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+            "frac": round(achieved * mma_per_flop / peak, 4),
+            "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)" if peaks.get("bf16_tflops")
+                            else "fallback 1.59 PFLOP/s bf16 / 2"),
+            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom}"),
+        }
+    else:
+        peak = ffma_peak_tflops(torch, stream)
+        roofline = {
+            "bound": "fp32", "kernel": f"{dom} conv (FFMA)",
+            "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4) if peak else None,
+            "peak_source": "live FFMA probe (convio_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
+            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom}"),
+        }
+    roofline["layers"] = sorted(d["layers"])
+    roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)
+
+    # ---- variants: paper-faithful FP32 CUDA cores only, and reduced-precision TF32 ----
+    variants = {}
+    if not args.no_variants:
+        for vname, allowed in (("fp32_cuda_cores", CUDA_CORE_ALGORITHMS),
+                               ("tf32_tcgen05", ("igemm_tf32",))):
+            vplans = load_plans(args.workload, allowed)
+            if not vplans:
+                continue
+            varm = Arm(vplans)
+            for _ in range(2):
+                varm.step()
+            vt, vev, _ = varm.timed(args.steps, scratch)
+            vt = max_over_ranks(vt)
+            rows, _ = varm.breakdown(vev, args.steps)
+            variants[vname] = {
+                "value": round(flops_all * args.steps / (vt / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+                "ms_per_step": round(vt / args.steps, 4),
+                "tolerance": "5e-3 (TF32 inputs)" if vname.startswith("tf32") else "1e-5 direct / 1e-4..1e-3 Winograd",
+                "per_layer": [{k: r[k] for k in ("layer", "algorithm", "ms", "gflops")} for r in rows],
+            }
+            del varm
+    layers, xs, ys = arm.layers, arm.xs, arm.ys
+    work_bytes = arm.work_bytes
 
     # ---- end-to-end through the public API with host buffers -------------------
     e2e = None
     if not args.no_e2e:
-        hx = [x.cpu().pin_memory() for x in xs]
-        hy = [torch.empty(y.shape, dtype=torch.float32).pin_memory() for y in ys]
+        hx = [torch.empty_strided(x.shape, x.stride(), dtype=torch.float32, pin_memory=True).copy_(x)
+              for x in xs]
+        hy = [torch.empty_strided(y.shape, y.stride(), dtype=torch.float32, pin_memory=True)
+              for y in ys]
         dx = [torch.empty_like(x) for x in xs]
         h2d = sum(h.numel() * 4 for h in hx)
         d2h = sum(h.numel() * 4 for h in hy)
@@ -424,15 +496,12 @@ def main() -> None:
                 "l2": ("flushed between steps" if flush else
                        f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
                 "tuned_plans": bool(plans),
+                "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
+                         "(FFMA) or 3xTF32 tcgen05 implicit GEMM (FP32-level accuracy)",
             },
             "e2e": e2e,
-            "roofline": {
-                "bound": "fp32", "kernel": f"{dom} conv (FFMA)",
-                "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4) if peak else None,
-                "peak_source": "live FFMA probe (convio_ffma_peak) -- no FP32 entry in MEASURED_PEAKS.json",
-                "traffic": traffic,
-            },
+            "roofline": roofline,
+            "variants": variants,
             "cpu_baseline": cpu,
             "clocks": clk,
             "gpu_launches": launches,

@@ -56,6 +56,7 @@ extern "C" {
 #define CONVIO_ALG_DIRECT 0
 #define CONVIO_ALG_WINOGRAD 1
 #define CONVIO_ALG_IGEMM_TF32 2   /* tcgen05 implicit GEMM, TF32 in / FP32 accumulate */
+#define CONVIO_ALG_IGEMM_3XTF32 3 /* tcgen05 implicit GEMM, 3xTF32 split: FP32-level accuracy */
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {
@@ -142,6 +143,13 @@ int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float
 int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                            const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
                            float *y, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Same implicit GEMM with each operand split into hi = rna_tf32(v) and
+ * lo = v - hi (3 MMAs per k-step: hi*lo + lo*hi + hi*hi): FP32-level
+ * accuracy on the tensor cores.  z in {64, 128}. */
+int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
+                             const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
+                             float *y, void *workspace, size_t workspace_bytes, void *stream);
 
 /* The transform matrices the kernels use (row-major AT e*m, G m*r, BT m*m). */
 int convio_winograd_matrices(int32_t e, int32_t r, float *at, float *g, float *bt);

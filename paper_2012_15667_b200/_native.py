@@ -17,7 +17,7 @@ from .model import GeometryError
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libconvio_b200.so")
 
-ALG_DIRECT, ALG_WINOGRAD, ALG_IGEMM_TF32 = 0, 1, 2
+ALG_DIRECT, ALG_WINOGRAD, ALG_IGEMM_TF32, ALG_IGEMM_3XTF32 = 0, 1, 2, 3
 
 
 class ConvDesc(ctypes.Structure):
@@ -81,6 +81,7 @@ def lib() -> ctypes.CDLL:
             "convio_default_tile": ([D, I32, I32, T], ctypes.c_int),
             "convio_pack_filter_igemm": ([D, P, P, P], ctypes.c_int),
             "convio_conv_igemm_tf32": ([D, T, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
+            "convio_conv_igemm_3xtf32": ([D, T, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -95,6 +96,7 @@ EXPORTED = (
     "convio_workspace_bytes", "convio_pack_filter_direct", "convio_conv_direct_f32",
     "convio_winograd_filter_transform", "convio_conv_winograd_f32", "convio_winograd_matrices",
     "convio_ffma_peak", "convio_default_tile", "convio_pack_filter_igemm", "convio_conv_igemm_tf32",
+    "convio_conv_igemm_3xtf32",
 )
 
 

@@ -99,7 +99,7 @@ def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CH
     k, _, r, s = w_shape
     desc = N.make_desc(n, c, h, w, k, r, s, stride, padding, LAYOUTS.index(layout))
     alg = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
-           "igemm_tf32": N.ALG_IGEMM_TF32}[algorithm]
+           "igemm_tf32": N.ALG_IGEMM_TF32, "igemm_3xtf32": N.ALG_IGEMM_3XTF32}[algorithm]
     rc, info = N.query(desc, N.make_tile(tile), alg)
     info["rc"] = rc
     return info
@@ -231,12 +231,15 @@ def conv_igemm_tf32(x: torch.Tensor, w: torch.Tensor, padding: int = 0,
                     tile: TileConfig | None = None, bias: torch.Tensor | None = None,
                     relu: bool = False, out: torch.Tensor | None = None, stream=None,
                     w_packed: torch.Tensor | None = None,
-                    workspace: torch.Tensor | None = None) -> torch.Tensor:
-    """Direct conv as a tcgen05 implicit GEMM: TF32 inputs, FP32 accumulation in TMEM.
+                    workspace: torch.Tensor | None = None, stride: int = 1,
+                    split: bool = False) -> torch.Tensor:
+    """Direct conv as a tcgen05 implicit GEMM, FP32 accumulation in TMEM.
 
-    ``x`` must be channels-last (layout ``HWC``), ``C % 32 == 0``, stride 1,
-    ``tile.z in {64, 128, 256}``, ``tile.x * tile.y <= 128``.  Results differ
-    from FP32 by TF32 input rounding (tolerance 5e-3).
+    ``x`` must be channels-last (layout ``HWC``), ``C % 32 == 0``, stride 1/2,
+    ``tile.x * tile.y <= 128``.  ``split=False``: TF32 inputs, ``tile.z in
+    {64,128,256}``, tolerance 5e-3.  ``split=True``: 3xTF32
+    (hi/lo operand split, 3 MMAs per k-step) -- FP32-level accuracy,
+    ``tile.z in {64,128}``.
     """
     _check_tensor(x, "x")
     _check_tensor(w, "w")
@@ -245,8 +248,8 @@ def conv_igemm_tf32(x: torch.Tensor, w: torch.Tensor, padding: int = 0,
         raise ValueError("conv_igemm_tf32 needs a channels-last (HWC) input")
     if tile is None:
         raise ValueError("conv_igemm_tf32 needs an explicit tile")
-    desc = _desc(x, w, 1, padding, layout)
-    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, 1, padding)
+    desc = _desc(x, w, stride, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, stride, padding)
     if out is None:
         out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
     if w_packed is not None:
@@ -256,10 +259,10 @@ def conv_igemm_tf32(x: torch.Tensor, w: torch.Tensor, padding: int = 0,
         if workspace is None or workspace.numel() < need:
             workspace = torch.empty(need, device=x.device, dtype=torch.float32)
         wsrc, is_packed, ws, ws_bytes = w.contiguous(), 0, workspace, 4 * need
-    rc = N.lib().convio_conv_igemm_tf32(
-        ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), _ptr(x), _ptr(wsrc), is_packed,
-        _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes, _stream_ptr(stream))
-    N.check(rc, "conv_igemm_tf32")
+    fn = N.lib().convio_conv_igemm_3xtf32 if split else N.lib().convio_conv_igemm_tf32
+    rc = fn(ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), _ptr(x), _ptr(wsrc), is_packed,
+            _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes, _stream_ptr(stream))
+    N.check(rc, "conv_igemm_3xtf32" if split else "conv_igemm_tf32")
     return out
 
 

@@ -30,7 +30,7 @@ void reset_launches() { t_launches = 0; }
 
 int direct_instance_count();
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
-int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
+int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, bool split);
 
 // ---------------------------------------------------------------------------
 // device properties (cached once per process, per device)
@@ -591,7 +591,8 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
         return rc;
     }
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_query(desc, tile, out);
-    if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out);
+    if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out, false);
+    if (algorithm == CONVIO_ALG_IGEMM_3XTF32) return igemm_query(desc, tile, out, true);
     set_error("unknown algorithm %d", algorithm);
     return CONVIO_EINVAL;
 }
@@ -602,7 +603,8 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
     if (!desc) return -1;
     if (algorithm == CONVIO_ALG_DIRECT) return 4LL * desc->k * desc->c * desc->r * desc->s;
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_workspace_bytes(desc, tile);
-    if (algorithm == CONVIO_ALG_IGEMM_TF32) return 4LL * desc->k * desc->c * desc->r * desc->s;
+    if (algorithm == CONVIO_ALG_IGEMM_TF32 || algorithm == CONVIO_ALG_IGEMM_3XTF32)
+        return 4LL * desc->k * desc->c * desc->r * desc->s;
     return -1;
 }
 

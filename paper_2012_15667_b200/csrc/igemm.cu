@@ -9,11 +9,18 @@ namespace convio {
 
 using IgemmFn = void (*)(const IgemmParams, const CUtensorMap, const CUtensorMap);
 
-static IgemmFn igemm_kernel(int bn) {
+static IgemmFn igemm_kernel(int bn, bool split) {
+    if (split) {
+        switch (bn) {
+            case 64: return &igemm_tf32_tcgen05_kernel<64, true>;
+            case 128: return &igemm_tf32_tcgen05_kernel<128, true>;
+            default: return nullptr;
+        }
+    }
     switch (bn) {
-        case 64: return &igemm_tf32_tcgen05_kernel<64>;
-        case 128: return &igemm_tf32_tcgen05_kernel<128>;
-        case 256: return &igemm_tf32_tcgen05_kernel<256>;
+        case 64: return &igemm_tf32_tcgen05_kernel<64, false>;
+        case 128: return &igemm_tf32_tcgen05_kernel<128, false>;
+        case 256: return &igemm_tf32_tcgen05_kernel<256, false>;
         default: return nullptr;
     }
 }
@@ -37,10 +44,12 @@ struct IgemmPlan {
     size_t smem = 0;
     int regs = 0;
     int bn = 0;
+    int threads = 128;
+    bool split = false;
 };
 
 static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
-                      size_t rlen) {
+                      size_t rlen, bool split) {
     auto fail = [&](int code, const char *fmt, ...) {
         va_list ap;
         va_start(ap, fmt);
@@ -59,7 +68,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (d->layout != CONVIO_LAYOUT_HWC)
         return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM needs the HWC (NHWC) layout");
     if (t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
-    if (d->stride != 1) return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM is compiled for stride 1");
+    if (d->stride > 2) return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM supports stride 1 and 2");
     if (d->r != d->s) return fail(CONVIO_EINFEASIBLE, "square kernels only");
     if (d->c % 32) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of 32 (one 128-B K block)", d->c);
     if (t->x < 1 || t->y < 1 || t->z < 1 || t->s_b < 1)
@@ -67,24 +76,29 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (q % t->x || p % t->y || d->k % t->z)
         return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
-    const int tile_w = t->x + d->s - 1, tile_h = t->y + d->r - 1;
+    const int tile_w = d->stride * (t->x - 1) + d->s, tile_h = d->stride * (t->y - 1) + d->r;
     const int64_t resident = (int64_t)t->x * t->y * t->z + (int64_t)tile_w * tile_h + (int64_t)d->r * d->s * t->z;
     if (resident > t->s_b)
         return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     const int bn = t->z;
-    IgemmFn fn = igemm_kernel(bn);
-    if (!fn) return fail(CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
+    IgemmFn fn = igemm_kernel(bn, split);
+    if (!fn)
+        return fail(CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128%s}, got %d",
+                    split ? "" : ", 256", bn);
     const int px = t->x * t->y;
     if (px > 128) return fail(CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the M=128 MMA tile", px);
-    if (t->x > 256 || t->y > 256) return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
+    if (t->x * d->stride > 256 || t->y * d->stride > 256)
+        return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
     const int imgs = std::max(1, std::min(128 / px, d->n));
-    // ring depth from the staging budget (outputs live in TMEM, s_b words stage A and B)
-    const int stage_words = 128 * 32 + bn * 32;
-    int stages = std::max(2, std::min(6, t->s_b / stage_words));
+    // ring depth: the outputs live in TMEM (not in the s_b budget of the
+    // register/smem machine model), so the TMA ring takes what shared memory
+    // allows -- up to 6 stages of (A, B[, A_lo, B_lo]) k-blocks
+    const int stage_words = (128 * 32 + bn * 32) * (split ? 2 : 1);
+    int stages = 6;
     const size_t stage_bytes = (size_t)4 * stage_words;
     while (stages > 2 && stages * stage_bytes + 2048 > 227 * 1024) --stages;
-    const size_t smem = stages * stage_bytes + 1024 + 256;
+    const size_t smem = stages * stage_bytes + 1024 + 512;
     if (smem > 227 * 1024) return fail(CONVIO_EINFEASIBLE, "tcgen05 ring needs %zu B smem", smem);
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
@@ -99,8 +113,11 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     pl->fn = fn;
     pl->smem = smem;
     pl->bn = bn;
-    if (launch_fit((const void *)fn, 128, smem, &pl->regs) < 1)
-        return fail(CONVIO_EINFEASIBLE, "tcgen05 block (128 threads, %zu B smem) does not fit", smem);
+    pl->split = split;
+    pl->threads = split ? 256 : 128;
+    if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
+        return fail(CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
+                    pl->threads, smem);
     return CONVIO_OK;
 }
 
@@ -110,9 +127,12 @@ static bool make_igemm_maps(const IgemmPlan &pl, const float *x, const float *wq
     if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15)) return false;
     cuuint64_t xd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.n};
     cuuint64_t xs[3] = {(cuuint64_t)P.c * 4, (cuuint64_t)P.w * P.c * 4, (cuuint64_t)P.h * P.w * P.c * 4};
-    cuuint32_t xb[4] = {32, (cuuint32_t)P.bx, (cuuint32_t)P.by, (cuuint32_t)P.imgs};
+    // stride: box spans stride*(pixels) input positions, traversal stride picks every stride-th
+    cuuint32_t xb[4] = {32, (cuuint32_t)(P.bx * P.stride), (cuuint32_t)(P.by * P.stride),
+                        (cuuint32_t)P.imgs};
+    cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    if (!encode_tensor_map_tiled_ex(tx, 4, const_cast<float *>(x), xd, xs, xb, es, true)) return false;
+    if (!encode_tensor_map_tiled_ex(tx, 4, const_cast<float *>(x), xd, xs, xb, xes, true)) return false;
     const int rs = P.ks * P.ks;
     cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)rs};
     cuuint64_t ws[2] = {(cuuint64_t)P.c * 4, (cuuint64_t)P.k * P.c * 4};
@@ -120,13 +140,13 @@ static bool make_igemm_maps(const IgemmPlan &pl, const float *x, const float *wq
     return encode_tensor_map_tiled_ex(tw, 3, const_cast<float *>(wq), wd, ws, wb, es, true);
 }
 
-int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out) {
+int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, bool split) {
     IgemmPlan pl;
-    int rc = plan_igemm(d, t, &pl, out->reason, sizeof(out->reason));
+    int rc = plan_igemm(d, t, &pl, out->reason, sizeof(out->reason), split);
     if (rc) return rc;
     out->legal = 1;
     out->grid_x = pl.grid.x; out->grid_y = pl.grid.y; out->grid_z = pl.grid.z;
-    out->block_threads = 128;
+    out->block_threads = pl.threads;
     out->smem_bytes = (int)pl.smem;
     out->regs_per_thread = pl.regs;
     out->channel_chunk = 32;
@@ -134,8 +154,8 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = 4LL * d->k * d->c * d->r * d->s;
-    snprintf(out->reason, sizeof(out->reason), "tcgen05 tf32: M=128 (%d px x %d img), N=%d, %d stages",
-             pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
+    snprintf(out->reason, sizeof(out->reason), "tcgen05 %s: M=128 (%d px x %d img), N=%d, %d stages",
+             split ? "3xtf32" : "tf32", pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
     return CONVIO_OK;
 }
 
@@ -160,9 +180,9 @@ int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float
     return CONVIO_OK;
 }
 
-int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
-                           const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
-                           float *y, void *workspace, size_t workspace_bytes, void *stream) {
+static int conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
+                      const float *w, int32_t w_is_packed, const float *bias, int32_t relu, float *y,
+                      void *workspace, size_t workspace_bytes, void *stream, bool split) {
     clear_error();
     reset_launches();
     if (!x || !w || !y || !tile) {
@@ -171,7 +191,7 @@ int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile
     }
     IgemmPlan pl;
     char why[160];
-    int rc = plan_igemm(desc, tile, &pl, why, sizeof(why));
+    int rc = plan_igemm(desc, tile, &pl, why, sizeof(why), split);
     if (rc) return rc;
     const float *wq = w;
     if (!w_is_packed) {
@@ -194,10 +214,24 @@ int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile
     pl.P.bias = bias;
     pl.P.y = y;
     pl.P.relu = relu;
-    pl.fn<<<pl.grid, 128, pl.smem, (cudaStream_t)stream>>>(pl.P, tx, tw);
+    pl.fn<<<pl.grid, pl.threads, pl.smem, (cudaStream_t)stream>>>(pl.P, tx, tw);
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
+}
+
+int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
+                           const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
+                           float *y, void *workspace, size_t workspace_bytes, void *stream) {
+    return conv_igemm(desc, tile, x, w, w_is_packed, bias, relu, y, workspace, workspace_bytes,
+                      stream, false);
+}
+
+int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
+                             const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
+                             float *y, void *workspace, size_t workspace_bytes, void *stream) {
+    return conv_igemm(desc, tile, x, w, w_is_packed, bias, relu, y, workspace, workspace_bytes,
+                      stream, true);
 }
 
 }  // extern "C"

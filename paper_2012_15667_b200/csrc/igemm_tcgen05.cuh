@@ -95,14 +95,18 @@ __device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int BN>
-__global__ void __launch_bounds__(128, 1)
+// SPLIT = 3xTF32: each operand is split into hi = rna_tf32(v) and lo = v - hi
+// by 4 converter warps, and every k-step issues A_hi*B_lo + A_lo*B_hi +
+// A_hi*B_hi -- FP32-level accuracy (~2^-21) on the tensor cores.
+template <int BN, bool SPLIT>
+__global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     igemm_tf32_tcgen05_kernel(const __grid_constant__ IgemmParams P,
                               const __grid_constant__ CUtensorMap tm_x,
                               const __grid_constant__ CUtensorMap tm_w) {
     constexpr int A_BYTES = 128 * 128;       // 128 rows x 32 fp32
     constexpr int B_BYTES = BN * 128;        // BN rows x 32 fp32
-    constexpr int STAGE = A_BYTES + B_BYTES;
+    // stage: [A | B] (TMA; hi after conversion) then, when split, [A_lo | B_lo]
+    constexpr int STAGE = (A_BYTES + B_BYTES) * (SPLIT ? 2 : 1);
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for SWIZZLE_128B atoms
@@ -111,7 +115,8 @@ __global__ void __launch_bounds__(128, 1)
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
     uint64_t *empty = full + NS;
     uint64_t *done = empty + NS;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+    uint64_t *conv = done + 1;                        // split: converted[NS]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(conv + NS);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -130,6 +135,8 @@ __global__ void __launch_bounds__(128, 1)
             mbar_init(empty + s, 1);
         }
         mbar_init(done, 1);
+        if (SPLIT)
+            for (int s = 0; s < NS; ++s) mbar_init(conv + s, 4);   // 4 converter warps
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_w));
@@ -155,6 +162,7 @@ __global__ void __launch_bounds__(128, 1)
             uint8_t *a = smem + s * STAGE;
             uint8_t *b = a + A_BYTES;
             mbar_arrive_expect_tx(full + s, (uint32_t)(P.bx * P.by * P.imgs * 128 + B_BYTES));
+            // stride > 1: the map's traversal strides pick every stride-th pixel
             tma_load_4d(a, map_x, cb * 32, ox0 * P.stride + sx - P.pad, oy0 * P.stride + r - P.pad,
                         img0, full + s);
             tma_load_3d(b, map_w, cb * 32, k0, tap, full + s);
@@ -164,20 +172,61 @@ __global__ void __launch_bounds__(128, 1)
         constexpr uint32_t idesc = idesc_tf32_m128<BN>();
         for (int kb = 0; kb < P.kblocks; ++kb) {
             const int s = kb % NS;
-            mbar_wait(full + s, (kb / NS) & 1);
+            mbar_wait(SPLIT ? conv + s : full + s, (kb / NS) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t a = smem_u32(smem + s * STAGE);
             const uint32_t b = a + A_BYTES;
             const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(b);
+            if constexpr (SPLIT) {
+                const uint64_t adl = umma_desc_sw128(a + A_BYTES + B_BYTES);
+                const uint64_t bdl = umma_desc_sw128(b + A_BYTES + B_BYTES);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk)   // K = 8 tf32 = 32 B per MMA
-                umma_tf32(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                          (kb | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk) {
+                    const uint64_t o = (uint64_t)(kk * 2);
+                    umma_tf32(tmem, ad + o, bdl + o, idesc, (kb | kk) != 0);   // small terms first
+                    umma_tf32(tmem, adl + o, bd + o, idesc, 1);
+                    umma_tf32(tmem, ad + o, bd + o, idesc, 1);
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)   // K = 8 tf32 = 32 B per MMA
+                    umma_tf32(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                              (kb | kk) != 0);
+            }
             umma_commit(empty + s);
         }
         umma_commit(done);
+    } else if (SPLIT && warp >= 4) {
+        // ---- converter warps: hi = rna_tf32(v) in place, lo = v - hi alongside -------
+        const int ct = tid - 128;                    // 0..127
+        constexpr int VEC = (A_BYTES + B_BYTES) / 16;
+        for (int kb = 0; kb < P.kblocks; ++kb) {
+            const int s = kb % NS;
+            mbar_wait(full + s, (kb / NS) & 1);
+            float4 *hi = reinterpret_cast<float4 *>(smem + s * STAGE);
+            float4 *lo = reinterpret_cast<float4 *>(smem + s * STAGE + A_BYTES + B_BYTES);
+            for (int i = ct; i < VEC; i += 128) {
+                float4 v = hi[i], h, l;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.x)) : "f"(v.x));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.y)) : "f"(v.y));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.z)) : "f"(v.z));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.w)) : "f"(v.w));
+                l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+                hi[i] = h;
+                lo[i] = l;
+            }
+            // generic-proxy stores -> visible to the tensor core's async proxy
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(conv + s);
+        }
     }
     // ---- epilogue: TMEM -> registers -> NHWC global ---------------------------------
+    if (SPLIT && warp >= 4) {        // converters have no TMEM lanes to drain
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncthreads();
+        return;
+    }
     mbar_wait(done, 0);
     __syncwarp();   // the producer / MMA lanes rejoin their warps before .sync.aligned loads
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");

@@ -76,6 +76,48 @@ def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
     return out
 
 
+def tune_igemm(shape, spec, split, log):
+    """Tensor-core projection: small exhaustive device search over (x, y, z).
+
+    The Table-1 prune is derived for the FFMA machine model (outputs in
+    registers); the tcgen05 kernel keeps outputs in TMEM, so its own small
+    space (x | Q, y | P, x*y <= 128, z in {64, 128[, 256]}) is searched whole.
+    """
+    import math as _m
+    from paper_2012_15667_b200.dataflow import TileConfig
+    from paper_2012_15667_b200 import conv as C
+    if spec.c % 32 or spec.stride > 2:
+        return {"error": "needs C % 32 == 0 and stride <= 2"}
+    q = shape.w_out
+    p = shape.h_out
+    zs = [z for z in ((64, 128) if split else (64, 128, 256)) if spec.k % z == 0]
+    best, best_t, tried = None, _m.inf, 0
+    x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
+    xh = C.to_layout(x, "HWC")
+    w = torch.empty((spec.k, spec.c, spec.r, spec.r), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
+    wq = C.pack_filter_igemm(w)
+    for bx in [d for d in range(1, q + 1) if q % d == 0]:
+        for by in [d for d in range(1, p + 1) if p % d == 0]:
+            if bx * by > 128 or bx * by < 32:
+                continue
+            for z in zs:
+                tile = TileConfig(bx, by, z, 32768, 1, 1, 1, layout="HWC")
+                try:
+                    t = DT.device_time(lambda: C.conv_igemm_tf32(xh, w, padding=spec.pad, tile=tile,
+                                                                  w_packed=wq, stride=spec.stride,
+                                                                  split=split))
+                except Exception:  # noqa: BLE001 -- illegal projection
+                    continue
+                tried += 1
+                if t < best_t:
+                    best, best_t = tile, t
+    key = "igemm_3xtf32" if split else "igemm_tf32"
+    log(f"    {key}: {tried} tiles, best {best} {best_t}")
+    return {"tuner": {"best": best.to_dict() if best else None,
+                      "seconds": best_t if best else None, "measurements": tried},
+            "space": "exhaustive tcgen05 projection"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="resnet50")
@@ -83,7 +125,7 @@ def main():
     ap.add_argument("--budget", type=int, default=128)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--exhaustive-cap", type=int, default=0)
-    ap.add_argument("--algs", default="direct,winograd2,winograd4")
+    ap.add_argument("--algs", default="direct,winograd2,winograd4,igemm_3xtf32,igemm_tf32")
     ap.add_argument("--layers", default="")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -110,11 +152,13 @@ def main():
         DT.set_padding(spec.pad)
         shape = shape_of(args.n, spec.c, spec.hw, spec.hw, spec.k, spec.r, spec.stride, spec.pad)
         log(f"{spec.name}: {shape}")
-        cands = {}
+        cands = dict(result["layers"].get(spec.name, {}).get("candidates", {}))
         for alg in args.algs.split(","):
             if alg == "direct":
                 cands["direct"] = tune_one(shape, hw, "direct", None, args.budget, args.seed,
                                            args.exhaustive_cap, log)
+            elif alg.startswith("igemm"):
+                cands[alg] = tune_igemm(shape, spec, alg == "igemm_3xtf32", log)
             elif alg.startswith("winograd") and spec.stride == 1 and spec.r == 3:
                 e = int(alg[len("winograd"):])
                 cands[alg] = tune_one(shape, hw, "winograd", WinogradParams(e, 3), args.budget,
@@ -122,6 +166,8 @@ def main():
         best_key, best_t = None, math.inf
         for key, c in cands.items():
             t = (c.get("tuner") or {}).get("seconds")
+            if key == "igemm_tf32":      # reduced precision: never the layer's FP32 plan
+                continue
             if t is not None and t < best_t:
                 best_key, best_t = key, t
         if best_key is None:
@@ -130,8 +176,8 @@ def main():
         tile = cands[best_key]["tuner"]["best"]
         flops = spec.flops(args.n)
         result["layers"][spec.name] = {
-            "algorithm": "direct" if best_key == "direct" else "winograd",
-            "e": None if best_key == "direct" else int(best_key[len("winograd"):]),
+            "algorithm": best_key if not best_key.startswith("winograd") else "winograd",
+            "e": int(best_key[len("winograd"):]) if best_key.startswith("winograd") else None,
             "tile": tile, "seconds": best_t, "gflops_direct_equiv": round(flops / best_t / 1e9, 1),
             "candidates": cands,
         }

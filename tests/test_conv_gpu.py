@@ -139,3 +139,29 @@ def test_igemm_tcgen05_tf32_matches_oracle(case):
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
     assert C.infer_layout(y) == "HWC"
     assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= TOL_TF32
+
+
+def test_igemm_tcgen05_tf32_stride2():
+    x, wt = _inputs(2, 64, 28, 28, 128, 3, 3)
+    tile = TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")
+    y = C.conv_igemm_tf32(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, stride=2)
+    ref = co.direct_conv(x, wt, 2, 1)
+    assert y.shape == ref.shape
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= TOL_TF32
+
+
+SPLIT_CASES = [
+    (2, 64, 56, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
+    (2, 256, 14, 14, 128, 1, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
+    (3, 64, 7, 7, 64, 1, TileConfig(7, 7, 64, 32768, 1, 1, 1, layout="HWC")),
+    (2, 128, 28, 28, 128, 2, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
+]
+
+
+@pytest.mark.parametrize("case", SPLIT_CASES, ids=[str(i) for i in range(len(SPLIT_CASES))])
+def test_igemm_tcgen05_3xtf32_meets_fp32_tolerance(case):
+    n, c, h, w, k, stride, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    y = C.conv_igemm_tf32(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, stride=stride, split=True)
+    ref = co.direct_conv(x, wt, stride, 1)
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= TOL_DIRECT
