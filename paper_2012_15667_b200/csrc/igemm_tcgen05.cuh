@@ -211,7 +211,12 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.y)) : "f"(v.y));
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.z)) : "f"(v.z));
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.w)) : "f"(v.w));
+                // lo is itself rounded to TF32 (not left to the MMA's truncation)
                 l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.x)) : "f"(l.x));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.y)) : "f"(l.y));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.z)) : "f"(l.z));
+                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.w)) : "f"(l.w));
                 hi[i] = h;
                 lo[i] = l;
             }
