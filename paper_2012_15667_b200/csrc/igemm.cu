@@ -91,12 +91,14 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (t->x * d->stride > 256 || t->y * d->stride > 256)
         return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
     const int imgs = std::max(1, std::min(128 / px, d->n));
-    // ring depth: the outputs live in TMEM (not in the s_b budget of the
-    // register/smem machine model), so the TMA ring takes what shared memory
-    // allows -- up to 6 stages of (A, B[, A_lo, B_lo]) k-blocks
+    // ring depth: the outputs live in TMEM, so s_b only sizes the TMA ring:
+    // ring bytes <= 6 * s_b (s_b = 16384 words -> 96 KB, two CTAs per SM;
+    // 32768 -> 192 KB, one deep-ring CTA per SM), 2..6 stages
     const int stage_words = (128 * 32 + bn * 32) * (split ? 2 : 1);
-    int stages = 6;
     const size_t stage_bytes = (size_t)4 * stage_words;
+    const size_t ring_cap = std::min<size_t>((size_t)6 * t->s_b, 227 * 1024 - 2048);
+    int stages = (int)std::min<size_t>(6, ring_cap / stage_bytes);
+    if (stages < 2) stages = 2;
     while (stages > 2 && stages * stage_bytes + 2048 > 227 * 1024) --stages;
     const size_t smem = stages * stage_bytes + 1024 + 512;
     if (smem > 227 * 1024) return fail(CONVIO_EINFEASIBLE, "tcgen05 ring needs %zu B smem", smem);

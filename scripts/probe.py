@@ -54,6 +54,7 @@ def ffma_peak():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=32)
+    ap.add_argument("--only-tc", action="store_true", help="skip the FFMA / Winograd searches")
     args = ap.parse_args()
     torch.backends.cudnn.benchmark = True
     torch.backends.cudnn.allow_tf32 = False
@@ -67,6 +68,8 @@ def main():
     ]
     n = args.n
     for name, c, hw, k, st in layers:
+        if args.only_tc and c % 32:
+            continue
         x = torch.randn(n, c, hw, hw, device="cuda")
         w = torch.randn(k, c, 3, 3, device="cuda") / (c * 9) ** 0.5
         flops = 2.0 * n * k * c * 9 * hw * hw
@@ -74,9 +77,11 @@ def main():
         print(f"{name} cudnn fp32: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s", flush=True)
         wp = C.pack_filter_direct(w)
         cands = []
+        if args.only_tc:
+            cands = None
         for TX in (8, 7, 4):
             for TZ in (8, 16, 4):
-                for TY in (1, 2):
+                for TY in ((1, 2) if not args.only_tc else ()):
                     for nzt in (4, 8, 16):
                         z = TZ * nzt
                         if k % z:
@@ -96,7 +101,7 @@ def main():
                                     cands.append(TileConfig(x_, y_, z, sb, nxt, nyt, nzt))
         best = None
         t0 = time.time()
-        for tile in cands:
+        for tile in (cands or []):
             info = C.query(x.shape, w.shape, 1, 1, "CHW", tile)
             if info["rc"] != 0:
                 continue
@@ -109,6 +114,8 @@ def main():
                 best = (t, tile, info)
             if time.time() - t0 > 60:
                 break
+        if best is None:
+            best = (float("nan"), None, {"regs_per_thread": 0, "smem_bytes": 0, "channel_chunk": 0})
         t, tile, info = best
         print(f"{name} direct best: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s  {tile} "
               f"regs={info['regs_per_thread']} smem={info['smem_bytes']} ck={info['channel_chunk']}",
@@ -120,14 +127,22 @@ def main():
                 for bn in (64, 128, 256):
                     if k % bn or hw % bx or hw % by or bx * by > 128:
                         continue
-                    tile = TileConfig(bx, by, bn, 32768, 1, 1, 1, layout="HWC")
-                    try:
-                        t = timeit(lambda: C.conv_igemm_tf32(xh, w, padding=1, tile=tile, w_packed=wq))
-                        print(f"{name} tcgen05 tf32 {bx}x{by}x{bn}: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s",
-                              flush=True)
-                    except Exception as exc:  # noqa: BLE001
-                        print(f"{name} tcgen05 {bx}x{by}x{bn}: {exc}", flush=True)
-        for e in (2, 4):
+                    for sb in (16384, 32768):
+                        for split in (False, True):
+                            if split and bn == 256:
+                                continue
+                            tile = TileConfig(bx, by, bn, sb, 1, 1, 1, layout="HWC")
+                            try:
+                                t = timeit(lambda: C.conv_igemm_tf32(xh, w, padding=1, tile=tile,
+                                                                      w_packed=wq, split=split))
+                                info = C.query(xh.shape, w.shape, 1, 1, "HWC", tile,
+                                               "igemm_3xtf32" if split else "igemm_tf32")
+                                print(f"{name} tcgen05 {'3xtf32' if split else 'tf32'} {bx}x{by}x{bn} "
+                                      f"sb={sb}: {t*1e3:.3f} ms {flops/t/1e12:.2f} TFLOP/s "
+                                      f"[{info['reason']}]", flush=True)
+                            except Exception as exc:  # noqa: BLE001
+                                print(f"{name} tcgen05 {bx}x{by}x{bn}: {exc}", flush=True)
+        for e in ((2, 4) if not args.only_tc else ()):
             try:
                 u = C.winograd_filter_transform(w, e)
                 t = timeit(lambda: C.conv_winograd(x, w, e=e, padding=1, u=u))

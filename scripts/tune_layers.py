@@ -100,8 +100,8 @@ def tune_igemm(shape, spec, split, log):
         for by in [d for d in range(1, p + 1) if p % d == 0]:
             if bx * by > 128 or bx * by < 32:
                 continue
-            for z in zs:
-                tile = TileConfig(bx, by, z, 32768, 1, 1, 1, layout="HWC")
+            for z, sb in [(z, sb) for z in zs for sb in (16384, 32768)]:
+                tile = TileConfig(bx, by, z, sb, 1, 1, 1, layout="HWC")
                 try:
                     t = DT.device_time(lambda: C.conv_igemm_tf32(xh, w, padding=spec.pad, tile=tile,
                                                                   w_packed=wq, stride=spec.stride,
