@@ -231,23 +231,26 @@ def main() -> None:
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    if world > 1:
+    # under torchrun (MASTER_ADDR set) the process group is created even for one
+    # rank, so the max-over-ranks / barrier path is the same code at N=1 and N=8
+    if world > 1 or "MASTER_ADDR" in os.environ:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+    distributed = dist.is_available() and dist.is_initialized()
 
     def barrier():
-        if world > 1:
+        if distributed:
             dist.barrier()
 
     def max_over_ranks(v: float) -> float:
-        if world == 1:
+        if not distributed:
             return v
         t = torch.tensor([v], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
     def sum_over_ranks(v: float) -> float:
-        if world == 1:
+        if not distributed:
             return v
         t = torch.tensor([v], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -459,7 +462,7 @@ def main() -> None:
                "ms_per_step": round(e_ms / args.steps, 3)}
 
     gathered = None
-    if args.gather and world > 1:
+    if args.gather and distributed:
         torch.cuda.synchronize(dev)
         barrier()
         a = torch.cuda.Event(enable_timing=True)
@@ -510,7 +513,7 @@ def main() -> None:
         if gathered:
             line["gather"] = gathered
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if distributed:
         dist.destroy_process_group()
 
 

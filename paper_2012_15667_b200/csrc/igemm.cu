@@ -14,6 +14,7 @@ static IgemmFn igemm_kernel(int bn, bool split) {
         switch (bn) {
             case 64: return &igemm_tf32_tcgen05_kernel<64, true>;
             case 128: return &igemm_tf32_tcgen05_kernel<128, true>;
+            case 256: return &igemm_tf32_tcgen05_kernel<256, true>;
             default: return nullptr;
         }
     }
@@ -84,8 +85,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     const int bn = t->z;
     IgemmFn fn = igemm_kernel(bn, split);
     if (!fn)
-        return fail(CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128%s}, got %d",
-                    split ? "" : ", 256", bn);
+        return fail(CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
     const int px = t->x * t->y;
     if (px > 128) return fail(CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the M=128 MMA tile", px);
     if (t->x * d->stride > 256 || t->y * d->stride > 256)

@@ -95,9 +95,10 @@ __device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// SPLIT = 3xTF32: each operand is split into hi = rna_tf32(v) and lo = v - hi
-// by 4 converter warps, and every k-step issues A_hi*B_lo + A_lo*B_hi +
-// A_hi*B_hi -- FP32-level accuracy (~2^-21) on the tensor cores.
+// SPLIT = 3xTF32: each operand is split into hi = tf32(v) (the raw operand,
+// read by the tensor core with the low mantissa bits dropped) and
+// lo = rna_tf32(v - hi) written by 4 converter warps; every k-step issues
+// A_hi*B_lo + A_lo*B_hi + A_hi*B_hi -- FP32-level accuracy on the tensor cores.
 template <int BN, bool SPLIT>
 __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     igemm_tf32_tcgen05_kernel(const __grid_constant__ IgemmParams P,
@@ -197,27 +198,28 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
         }
         umma_commit(done);
     } else if (SPLIT && warp >= 4) {
-        // ---- converter warps: hi = rna_tf32(v) in place, lo = v - hi alongside -------
+        // ---- converter warps: lo = v - tf32(v) alongside the raw operand --------------
+        // The tensor core reads the raw fp32 operand as TF32 by dropping the low
+        // 13 mantissa bits, so hi = v & ~0x1fff needs no store: only lo is
+        // written (itself rounded to TF32), halving the conversion's smem traffic.
         const int ct = tid - 128;                    // 0..127
         constexpr int VEC = (A_BYTES + B_BYTES) / 16;
         for (int kb = 0; kb < P.kblocks; ++kb) {
             const int s = kb % NS;
             mbar_wait(full + s, (kb / NS) & 1);
-            float4 *hi = reinterpret_cast<float4 *>(smem + s * STAGE);
+            const float4 *hi = reinterpret_cast<const float4 *>(smem + s * STAGE);
             float4 *lo = reinterpret_cast<float4 *>(smem + s * STAGE + A_BYTES + B_BYTES);
             for (int i = ct; i < VEC; i += 128) {
-                float4 v = hi[i], h, l;
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.x)) : "f"(v.x));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.y)) : "f"(v.y));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.z)) : "f"(v.z));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.w)) : "f"(v.w));
-                // lo is itself rounded to TF32 (not left to the MMA's truncation)
-                l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+                const float4 v = hi[i];
+                float4 l;
+                l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+                l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+                l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+                l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.x)) : "f"(l.x));
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.y)) : "f"(l.y));
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.z)) : "f"(l.z));
                 asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.w)) : "f"(l.w));
-                hi[i] = h;
                 lo[i] = l;
             }
             // generic-proxy stores -> visible to the tensor core's async proxy

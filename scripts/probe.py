@@ -129,8 +129,6 @@ def main():
                         continue
                     for sb in (16384, 32768):
                         for split in (False, True):
-                            if split and bn == 256:
-                                continue
                             tile = TileConfig(bx, by, bn, sb, 1, 1, 1, layout="HWC")
                             try:
                                 t = timeit(lambda: C.conv_igemm_tf32(xh, w, padding=1, tile=tile,

@@ -90,7 +90,7 @@ def tune_igemm(shape, spec, split, log):
         return {"error": "needs C % 32 == 0 and stride <= 2"}
     q = shape.w_out
     p = shape.h_out
-    zs = [z for z in ((64, 128) if split else (64, 128, 256)) if spec.k % z == 0]
+    zs = [z for z in (64, 128, 256) if spec.k % z == 0]
     best, best_t, tried = None, _m.inf, 0
     x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
     xh = C.to_layout(x, "HWC")
