@@ -57,6 +57,15 @@ extern "C" {
 #define CONVIO_ALG_WINOGRAD 1
 #define CONVIO_ALG_IGEMM_TF32 2   /* tcgen05 implicit GEMM, TF32 in / FP32 accumulate */
 #define CONVIO_ALG_IGEMM_3XTF32 3 /* tcgen05 implicit GEMM, 3xTF32 split: FP32-level accuracy */
+#define CONVIO_ALG_IGEMM_BF16 4   /* tcgen05 implicit GEMM, BF16 operands / FP32 accumulate */
+#define CONVIO_ALG_WINOGRAD_TC_TF32 5   /* Winograd, element-wise GEMMs on tcgen05 (TF32) */
+#define CONVIO_ALG_WINOGRAD_TC_3XTF32 6 /* ... 3xTF32 (FP32-level GEMM accuracy) */
+#define CONVIO_ALG_WINOGRAD_TC_BF16 7   /* ... BF16 transformed operands */
+
+/* Operand precision of the tcgen05 contractions (FP32 accumulate always). */
+#define CONVIO_PREC_TF32 0
+#define CONVIO_PREC_3XTF32 1
+#define CONVIO_PREC_BF16 2
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {
@@ -150,6 +159,41 @@ int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile
 int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                              const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
                              float *y, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Generic form of the two calls above plus BF16 (CONVIO_PREC_*).  For BF16
+ * the fp32 activations are converted to bf16 NHWC in the workspace first
+ * (C % 64 == 0), filters packed to bf16 [R*S][K][C] unless `w_is_packed`
+ * (then w holds convio_pack_filter_igemm_bf16 output).  Replaces the same
+ * schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
+int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
+                      const float *x, const void *w, int32_t w_is_packed, const float *bias,
+                      int32_t relu, float *y, void *workspace, size_t workspace_bytes, void *stream);
+
+/* KCRS fp32 -> [R*S][K][C] bf16 (round to nearest even). */
+int convio_pack_filter_igemm_bf16(const convio_conv_desc *desc, const float *w, void *w_packed,
+                                  void *stream);
+
+/* dst[i] = bf16_rne(src[i]), both 16-byte aligned. */
+int convio_convert_bf16(const float *src, void *dst, int64_t n, void *stream);
+
+/* Tensor-core Winograd filter transform U[xi][k][c] = (G g G^T)[xi]
+ * (fp32 for TF32/3xTF32, bf16 for BF16) -- the shared kernel transform
+ * (dataflow.py:273 shared_kernel_transform=True, dag.py:353-383). */
+int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e, int32_t precision,
+                                        const float *w, void *u, void *stream);
+
+/* Winograd F(e x e, 3 x 3), e in {2, 4}, with step 3 (the element-wise
+ * products summed over channels, dag.py:384-401) as (e+2)^2 batched GEMMs
+ * M[xi][t][k] = sum_c V[xi][t][c] U[xi][k][c] on tcgen05 in one launch, and
+ * the input/output transforms as HBM-streaming kernels; the batch is chunked
+ * so each chunk's V and M stay in L2.  NHWC, stride 1, C % 32 (% 64 for
+ * BF16) == 0; tile->z in {64,128,256} is the GEMM's N tile, tile->s_b sizes
+ * the TMA ring, tile->e must equal e (tile == NULL: defaults).
+ * Replaces plan_winograd_dataflow + simulate (dataflow.py:253-338). */
+int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,
+                          int32_t precision, const float *x, const void *w, int32_t w_is_transformed,
+                          const float *bias, int32_t relu, float *y, void *workspace,
+                          size_t workspace_bytes, void *stream);
 
 /* The transform matrices the kernels use (row-major AT e*m, G m*r, BT m*m). */
 int convio_winograd_matrices(int32_t e, int32_t r, float *at, float *g, float *bt);

@@ -18,6 +18,10 @@ LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
 LIB_PATH = os.path.join(LIB_DIR, "libconvio_b200.so")
 
 ALG_DIRECT, ALG_WINOGRAD, ALG_IGEMM_TF32, ALG_IGEMM_3XTF32 = 0, 1, 2, 3
+ALG_IGEMM_BF16 = 4
+ALG_WINOGRAD_TC_TF32, ALG_WINOGRAD_TC_3XTF32, ALG_WINOGRAD_TC_BF16 = 5, 6, 7
+PREC_TF32, PREC_3XTF32, PREC_BF16 = 0, 1, 2
+PRECISIONS = {"tf32": PREC_TF32, "3xtf32": PREC_3XTF32, "bf16": PREC_BF16}
 
 
 class ConvDesc(ctypes.Structure):
@@ -82,6 +86,12 @@ def lib() -> ctypes.CDLL:
             "convio_pack_filter_igemm": ([D, P, P, P], ctypes.c_int),
             "convio_conv_igemm_tf32": ([D, T, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
             "convio_conv_igemm_3xtf32": ([D, T, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
+            "convio_conv_igemm": ([D, T, I32, P, P, I32, P, I32, P, P, SZ, P], ctypes.c_int),
+            "convio_pack_filter_igemm_bf16": ([D, P, P, P], ctypes.c_int),
+            "convio_convert_bf16": ([P, P, I64, P], ctypes.c_int),
+            "convio_winograd_filter_transform_tc": ([D, I32, I32, P, P, P], ctypes.c_int),
+            "convio_winograd_bgemm": ([D, T, I32, I32, P, P, I32, P, I32, P, P, SZ, P],
+                                      ctypes.c_int),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -96,7 +106,8 @@ EXPORTED = (
     "convio_workspace_bytes", "convio_pack_filter_direct", "convio_conv_direct_f32",
     "convio_winograd_filter_transform", "convio_conv_winograd_f32", "convio_winograd_matrices",
     "convio_ffma_peak", "convio_default_tile", "convio_pack_filter_igemm", "convio_conv_igemm_tf32",
-    "convio_conv_igemm_3xtf32",
+    "convio_conv_igemm_3xtf32", "convio_conv_igemm", "convio_pack_filter_igemm_bf16",
+    "convio_convert_bf16", "convio_winograd_filter_transform_tc", "convio_winograd_bgemm",
 )
 
 

@@ -23,8 +23,9 @@ import torch
 from . import _native as N
 from .dataflow import LAYOUTS, TileConfig
 
-__all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "winograd_filter_transform",
-           "pack_filter_direct", "pack_filter_igemm",
+__all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "conv_igemm", "conv_winograd_tc",
+           "winograd_filter_transform", "winograd_filter_transform_tc",
+           "pack_filter_direct", "pack_filter_igemm", "pack_filter_igemm_bf16",
            "infer_layout", "to_layout", "empty_act", "query", "last_launch_count"]
 
 
@@ -92,14 +93,20 @@ def _out_hw(h, w, r, s, stride, padding):
     return (h + 2 * padding - r) // stride + 1, (w + 2 * padding - s) // stride + 1
 
 
+ALGORITHMS = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
+              "igemm_tf32": N.ALG_IGEMM_TF32, "igemm_3xtf32": N.ALG_IGEMM_3XTF32,
+              "igemm_bf16": N.ALG_IGEMM_BF16, "winograd_tc_tf32": N.ALG_WINOGRAD_TC_TF32,
+              "winograd_tc_3xtf32": N.ALG_WINOGRAD_TC_3XTF32,
+              "winograd_tc_bf16": N.ALG_WINOGRAD_TC_BF16}
+
+
 def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CHW",
           tile: TileConfig | None = None, algorithm: str = "direct") -> dict:
     """Device projection of ``tile`` for this layer (legality + launch shape)."""
     n, c, h, w = x_shape
     k, _, r, s = w_shape
     desc = N.make_desc(n, c, h, w, k, r, s, stride, padding, LAYOUTS.index(layout))
-    alg = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
-           "igemm_tf32": N.ALG_IGEMM_TF32, "igemm_3xtf32": N.ALG_IGEMM_3XTF32}[algorithm]
+    alg = ALGORITHMS[algorithm]
     rc, info = N.query(desc, N.make_tile(tile), alg)
     info["rc"] = rc
     return info
@@ -263,6 +270,125 @@ def conv_igemm_tf32(x: torch.Tensor, w: torch.Tensor, padding: int = 0,
     rc = fn(ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), _ptr(x), _ptr(wsrc), is_packed,
             _ptr(bias), int(bool(relu)), _ptr(out), _ptr(ws), ws_bytes, _stream_ptr(stream))
     N.check(rc, "conv_igemm_3xtf32" if split else "conv_igemm_tf32")
+    return out
+
+
+def pack_filter_igemm_bf16(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """KCRS fp32 -> [R*S][K][C] bf16 for the BF16 tcgen05 implicit GEMM."""
+    _check_tensor(w, "w")
+    w = w.contiguous()
+    k, c, r, s = w.shape
+    out = torch.empty((r * s, k, c), device=w.device, dtype=torch.bfloat16)
+    desc = N.make_desc(1, c, r, s, k, r, s, 1, 0, 2)
+    N.check(N.lib().convio_pack_filter_igemm_bf16(ctypes.byref(desc), _ptr(w), _ptr(out),
+                                                  _stream_ptr(stream)), "pack_filter_igemm_bf16")
+    return out
+
+
+def _precision(precision: str) -> int:
+    try:
+        return N.PRECISIONS[precision]
+    except KeyError:
+        raise ValueError(f"precision must be one of {sorted(N.PRECISIONS)}, got {precision!r}")
+
+
+def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int = 1,
+               tile: TileConfig | None = None, precision: str = "3xtf32",
+               bias: torch.Tensor | None = None, relu: bool = False,
+               out: torch.Tensor | None = None, stream=None,
+               w_packed: torch.Tensor | None = None,
+               workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Direct conv as a tcgen05 implicit GEMM at ``precision`` ("tf32",
+    "3xtf32" or "bf16"; FP32 accumulation in TMEM).  Channels-last input,
+    ``C % 32 == 0`` (``% 64`` for bf16).  For bf16 the activations are
+    converted to bf16 in the workspace by the library; ``w_packed`` must come
+    from :func:`pack_filter_igemm_bf16` (bf16) or :func:`pack_filter_igemm`.
+    Tolerances: 3xtf32 1e-5, tf32 5e-3, bf16 3e-2.
+    """
+    _check_tensor(x, "x")
+    _check_tensor(w, "w")
+    prec = _precision(precision)
+    layout = infer_layout(x)
+    if layout != "HWC":
+        raise ValueError("conv_igemm needs a channels-last (HWC) input")
+    if tile is None:
+        raise ValueError("conv_igemm needs an explicit tile")
+    desc = _desc(x, w, stride, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, stride, padding)
+    if out is None:
+        out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
+    need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), None,
+                                              N.ALG_IGEMM_TF32 + prec))
+    wsrc, is_packed = (w_packed, 1) if w_packed is not None else (w.contiguous(), 0)
+    if w_packed is not None and prec != N.PREC_BF16:
+        need = 0
+    if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
+        workspace = torch.empty(need, device=x.device, dtype=torch.uint8)
+    rc = N.lib().convio_conv_igemm(
+        ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), prec, _ptr(x), _ptr(wsrc),
+        is_packed, _ptr(bias), int(bool(relu)), _ptr(out), _ptr(workspace) if need else None,
+        need, _stream_ptr(stream))
+    N.check(rc, f"conv_igemm[{precision}]")
+    return out
+
+
+def winograd_filter_transform_tc(w: torch.Tensor, e: int, precision: str = "3xtf32",
+                                 stream=None) -> torch.Tensor:
+    """``U[xi][k][c] = (G g G^T)[xi]`` (K-major B operand of the tensor-core
+    Winograd GEMMs; bf16 for ``precision="bf16"``)."""
+    _check_tensor(w, "w")
+    prec = _precision(precision)
+    w = w.contiguous()
+    k, c, r, s = w.shape
+    m = e + r - 1
+    u = torch.empty((m * m, k, c), device=w.device,
+                    dtype=torch.bfloat16 if prec == N.PREC_BF16 else torch.float32)
+    desc = N.make_desc(1, c, 8, 8, k, r, s, 1, 1, 2)
+    N.check(N.lib().convio_winograd_filter_transform_tc(ctypes.byref(desc), e, prec, _ptr(w),
+                                                        _ptr(u), _stream_ptr(stream)),
+            "winograd_filter_transform_tc")
+    return u
+
+
+def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int = 1,
+                     tile: TileConfig | None = None, precision: str = "3xtf32",
+                     bias: torch.Tensor | None = None, relu: bool = False,
+                     out: torch.Tensor | None = None, stream=None,
+                     u: torch.Tensor | None = None,
+                     workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """Winograd F(e x e, 3 x 3) with the element-wise batched GEMM on tcgen05
+    (``convio_winograd_bgemm``).  Channels-last input, stride 1.  ``u`` from
+    :func:`winograd_filter_transform_tc` (same precision) skips the filter
+    transform.  Ragged outputs (P, Q not multiples of e) are handled by
+    zero-padded tiles.  Tolerances: 3xtf32 as the FP32 Winograd (F(2,3) 1e-4,
+    F(4,3) 1e-3), tf32 5e-3, bf16 3e-2.
+    """
+    _check_tensor(x, "x")
+    _check_tensor(w, "w")
+    prec = _precision(precision)
+    layout = infer_layout(x)
+    if layout != "HWC":
+        raise ValueError("conv_winograd_tc needs a channels-last (HWC) input")
+    desc = _desc(x, w, 1, padding, layout)
+    p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, 1, padding)
+    if out is None:
+        out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
+    if tile is not None:
+        ct = N.make_tile(tile, 2)
+    else:   # library default: N tile 128 (64 if K is not a multiple), 96 KB ring
+        ct = N.Tile(e, e, 128 if desc.k % 128 == 0 else 64, 16384, 1, 1, 1, 2, e)
+    alg = N.ALG_WINOGRAD_TC_TF32 + prec
+    need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), ctypes.byref(ct), alg))
+    if need < 0:
+        rc, _ = N.query(desc, ct, alg)
+        N.check(rc if rc else 3, "conv_winograd_tc")
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.empty(max(need, 1), device=x.device, dtype=torch.uint8)
+    wsrc, is_t = (u, 1) if u is not None else (w.contiguous(), 0)
+    rc = N.lib().convio_winograd_bgemm(
+        ctypes.byref(desc), ctypes.byref(ct), e, prec, _ptr(x), _ptr(wsrc), is_t,
+        _ptr(bias), int(bool(relu)), _ptr(out), _ptr(workspace), need, _stream_ptr(stream))
+    N.check(rc, f"conv_winograd_tc[{precision}]")
     return out
 
 

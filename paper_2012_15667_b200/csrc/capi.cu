@@ -30,7 +30,11 @@ void reset_launches() { t_launches = 0; }
 
 int direct_instance_count();
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
-int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, bool split);
+int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, int kind);
+int64_t igemm_workspace_bytes(const convio_conv_desc *d, int kind);
+int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t precision,
+                  convio_launch_info *out);
+int64_t wino_tc_workspace_bytes(const convio_conv_desc *d, const convio_tile *t, int32_t precision);
 
 // ---------------------------------------------------------------------------
 // device properties (cached once per process, per device)
@@ -458,6 +462,16 @@ bool encode_tensor_map_tiled_ex(CUtensorMap *map, int rank, void *base, const cu
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+bool encode_tensor_map_bf16_sw128(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                                  const cuuint64_t *strides, const cuuint32_t *box,
+                                  const cuuint32_t *es) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, base, dim, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
                              const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es) {
     return encode_tensor_map_tiled_ex(map, rank, base, dim, strides, box, es, false);
@@ -591,8 +605,11 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
         return rc;
     }
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_query(desc, tile, out);
-    if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out, false);
-    if (algorithm == CONVIO_ALG_IGEMM_3XTF32) return igemm_query(desc, tile, out, true);
+    if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out, 0);
+    if (algorithm == CONVIO_ALG_IGEMM_3XTF32) return igemm_query(desc, tile, out, 1);
+    if (algorithm == CONVIO_ALG_IGEMM_BF16) return igemm_query(desc, tile, out, 2);
+    if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
+        return wino_tc_query(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32, out);
     set_error("unknown algorithm %d", algorithm);
     return CONVIO_EINVAL;
 }
@@ -603,8 +620,11 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
     if (!desc) return -1;
     if (algorithm == CONVIO_ALG_DIRECT) return 4LL * desc->k * desc->c * desc->r * desc->s;
     if (algorithm == CONVIO_ALG_WINOGRAD) return winograd_workspace_bytes(desc, tile);
-    if (algorithm == CONVIO_ALG_IGEMM_TF32 || algorithm == CONVIO_ALG_IGEMM_3XTF32)
-        return 4LL * desc->k * desc->c * desc->r * desc->s;
+    if (algorithm == CONVIO_ALG_IGEMM_TF32 || algorithm == CONVIO_ALG_IGEMM_3XTF32 ||
+        algorithm == CONVIO_ALG_IGEMM_BF16)
+        return igemm_workspace_bytes(desc, algorithm - CONVIO_ALG_IGEMM_TF32);
+    if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
+        return wino_tc_workspace_bytes(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32);
     return -1;
 }
 

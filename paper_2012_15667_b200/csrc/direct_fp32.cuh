@@ -448,5 +448,8 @@ bool encode_tensor_map_tiled(CUtensorMap *map, int rank, void *base, const cuuin
 bool encode_tensor_map_tiled_ex(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
                                 const cuuint64_t *strides, const cuuint32_t *box, const cuuint32_t *es,
                                 bool swizzle128);
+bool encode_tensor_map_bf16_sw128(CUtensorMap *map, int rank, void *base, const cuuint64_t *dim,
+                                  const cuuint64_t *strides, const cuuint32_t *box,
+                                  const cuuint32_t *es);
 
 }  // namespace convio

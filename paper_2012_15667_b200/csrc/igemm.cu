@@ -1,5 +1,8 @@
-// Host side of the tcgen05 implicit-GEMM convolution (TF32 in, FP32 accumulate):
-// device projection of a TileConfig, filter packing, TMA descriptors, launch.
+// Host side of the tcgen05 implicit-GEMM convolution (TF32 / 3xTF32 / BF16 in,
+// FP32 accumulate): device projection of a TileConfig, filter packing, TMA
+// descriptors, launch; plus the batched launcher the tensor-core Winograd
+// path uses for its element-wise GEMMs (winograd_tc.cu).
+#include <cuda_bf16.h>
 #include <stdarg.h>
 #include <algorithm>
 
@@ -7,57 +10,110 @@
 
 namespace convio {
 
-using IgemmFn = void (*)(const IgemmParams, const CUtensorMap, const CUtensorMap);
-
-static IgemmFn igemm_kernel(int bn, bool split) {
-    if (split) {
-        switch (bn) {
-            case 64: return &igemm_tf32_tcgen05_kernel<64, true>;
-            case 128: return &igemm_tf32_tcgen05_kernel<128, true>;
-            case 256: return &igemm_tf32_tcgen05_kernel<256, true>;
-            default: return nullptr;
-        }
-    }
+template <int KIND>
+static IgemmFn igemm_kernel_kind(int bn) {
     switch (bn) {
-        case 64: return &igemm_tf32_tcgen05_kernel<64, false>;
-        case 128: return &igemm_tf32_tcgen05_kernel<128, false>;
-        case 256: return &igemm_tf32_tcgen05_kernel<256, false>;
+        case 64: return &igemm_tcgen05_kernel<64, KIND>;
+        case 128: return &igemm_tcgen05_kernel<128, KIND>;
+        case 256: return &igemm_tcgen05_kernel<256, KIND>;
         default: return nullptr;
     }
 }
 
-// KCRS -> [R*S][K][C]
-__global__ void pack_filter_igemm_kernel(const float *w, float *wq, int k, int c, int rs) {
+static IgemmFn igemm_kernel(int bn, int kind) {
+    if (kind == KIND_3XTF32) return igemm_kernel_kind<KIND_3XTF32>(bn);
+    if (kind == KIND_BF16) return igemm_kernel_kind<KIND_BF16>(bn);
+    return igemm_kernel_kind<KIND_TF32>(bn);
+}
+
+static const char *kind_name(int kind) {
+    return kind == KIND_3XTF32 ? "3xtf32" : (kind == KIND_BF16 ? "bf16" : "tf32");
+}
+
+// KCRS -> [R*S][K][C] (fp32 or bf16, round-to-nearest-even)
+template <typename T>
+__global__ void pack_filter_igemm_kernel(const float *w, T *wq, int k, int c, int rs) {
     const int64_t total = (int64_t)k * c * rs;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int cc = i % c;
         const int kk = (i / c) % k;
         const int tap = i / ((int64_t)c * k);
-        wq[i] = w[((int64_t)kk * c + cc) * rs + tap];
+        const float v = w[((int64_t)kk * c + cc) * rs + tap];
+        if constexpr (sizeof(T) == 2)
+            wq[i] = __float2bfloat16_rn(v);
+        else
+            wq[i] = v;
     }
 }
 
-struct IgemmPlan {
-    IgemmParams P;
-    IgemmFn fn = nullptr;
-    dim3 grid;
-    size_t smem = 0;
-    int regs = 0;
-    int bn = 0;
-    int threads = 128;
-    bool split = false;
-};
+// fp32 -> bf16 (RNE), 8 elements per thread-step when aligned
+__global__ void convert_bf16_kernel(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
+                                    int64_t n) {
+    const int64_t n8 = n / 8;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += step) {
+        const float4 a = reinterpret_cast<const float4 *>(src)[2 * i];
+        const float4 b = reinterpret_cast<const float4 *>(src)[2 * i + 1];
+        __nv_bfloat162 o[4] = {__floats2bfloat162_rn(a.x, a.y), __floats2bfloat162_rn(a.z, a.w),
+                               __floats2bfloat162_rn(b.x, b.y), __floats2bfloat162_rn(b.z, b.w)};
+        reinterpret_cast<uint4 *>(dst)[i] = *reinterpret_cast<uint4 *>(o);
+    }
+    for (int64_t i = n8 * 8 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += step)
+        dst[i] = __float2bfloat16_rn(src[i]);
+}
+
+static int vfail(char *reason, size_t rlen, int code, const char *fmt, va_list ap) {
+    vsnprintf(reason, rlen, fmt, ap);
+    set_error("%s", reason);
+    return code;
+}
+
+static int pfail(char *reason, size_t rlen, int code, const char *fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    int rc = vfail(reason, rlen, code, fmt, ap);
+    va_end(ap);
+    return rc;
+}
+
+// Ring depth, smem and occupancy shared by the conv and batched plans.  The
+// outputs live in TMEM, so s_b only sizes the TMA ring: ring bytes <= 6*s_b
+// (s_b = 16384 words -> 96 KB, two CTAs per SM; 32768 -> 192 KB, one deep-ring
+// CTA per SM), 2..6 stages.
+static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, char *reason, size_t rlen) {
+    IgemmFn fn = igemm_kernel(bn, kind);
+    if (!fn)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d",
+                     bn);
+    const size_t stage_bytes = (size_t)(128 * 128 + bn * 128) * (kind == KIND_3XTF32 ? 2 : 1);
+    const size_t ring_cap = std::min<size_t>((size_t)6 * s_b, 227 * 1024 - 2048);
+    int stages = (int)std::min<size_t>(6, ring_cap / stage_bytes);
+    if (stages < 2) stages = 2;
+    while (stages > 2 && stages * stage_bytes + 2048 > 227 * 1024) --stages;
+    const size_t smem = stages * stage_bytes + 1024 + 512;
+    if (smem > 227 * 1024)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 ring needs %zu B smem", smem);
+    pl->P.stages = stages;
+    pl->fn = fn;
+    pl->smem = smem;
+    pl->bn = bn;
+    pl->kind = kind;
+    pl->threads = kind == KIND_3XTF32 ? 256 : 128;
+    if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
+                     pl->threads, smem);
+    return CONVIO_OK;
+}
 
 static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
-                      size_t rlen, bool split) {
+                      size_t rlen, int kind) {
     auto fail = [&](int code, const char *fmt, ...) {
         va_list ap;
         va_start(ap, fmt);
-        vsnprintf(reason, rlen, fmt, ap);
+        int rc = vfail(reason, rlen, code, fmt, ap);
         va_end(ap);
-        set_error("%s", reason);
-        return code;
+        return rc;
     };
     if (!d || !t) return fail(CONVIO_EINVAL, "null descriptor or tile");
     if (d->n < 1 || d->c < 1 || d->h < 1 || d->w < 1 || d->k < 1 || d->r < 1 || d->s < 1 ||
@@ -71,7 +127,9 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
     if (d->stride > 2) return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM supports stride 1 and 2");
     if (d->r != d->s) return fail(CONVIO_EINFEASIBLE, "square kernels only");
-    if (d->c % 32) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of 32 (one 128-B K block)", d->c);
+    const int cb = kind == KIND_BF16 ? 64 : 32;
+    if (d->c % cb)
+        return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d (one 128-B K block)", d->c, cb);
     if (t->x < 1 || t->y < 1 || t->z < 1 || t->s_b < 1)
         return fail(CONVIO_EINFEASIBLE, "tile fields must be >= 1");
     if (q % t->x || p % t->y || d->k % t->z)
@@ -82,88 +140,154 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (resident > t->s_b)
         return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
-    const int bn = t->z;
-    IgemmFn fn = igemm_kernel(bn, split);
-    if (!fn)
-        return fail(CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
     const int px = t->x * t->y;
     if (px > 128) return fail(CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the M=128 MMA tile", px);
     if (t->x * d->stride > 256 || t->y * d->stride > 256)
         return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
-    const int imgs = std::max(1, std::min(128 / px, d->n));
-    // ring depth: the outputs live in TMEM, so s_b only sizes the TMA ring:
-    // ring bytes <= 6 * s_b (s_b = 16384 words -> 96 KB, two CTAs per SM;
-    // 32768 -> 192 KB, one deep-ring CTA per SM), 2..6 stages
-    const int stage_words = (128 * 32 + bn * 32) * (split ? 2 : 1);
-    const size_t stage_bytes = (size_t)4 * stage_words;
-    const size_t ring_cap = std::min<size_t>((size_t)6 * t->s_b, 227 * 1024 - 2048);
-    int stages = (int)std::min<size_t>(6, ring_cap / stage_bytes);
-    if (stages < 2) stages = 2;
-    while (stages > 2 && stages * stage_bytes + 2048 > 227 * 1024) --stages;
-    const size_t smem = stages * stage_bytes + 1024 + 512;
-    if (smem > 227 * 1024) return fail(CONVIO_EINFEASIBLE, "tcgen05 ring needs %zu B smem", smem);
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
+    int rc = plan_ring(pl, t->z, kind, t->s_b, reason, rlen);
+    if (rc) return rc;
+    const int imgs = std::max(1, std::min(128 / px, d->n));
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
     P.pad = d->pad; P.stride = d->stride; P.ks = d->r;
     P.bx = t->x; P.by = t->y; P.imgs = imgs;
     P.tiles_x = q / t->x; P.tiles_y = p / t->y; P.img_groups = (d->n + imgs - 1) / imgs;
-    P.cblocks = d->c / 32; P.kblocks = d->r * d->s * P.cblocks;
-    P.stages = stages;
-    pl->grid = dim3(d->k / bn, P.tiles_x * P.tiles_y * P.img_groups, 1);
+    P.cblocks = d->c / cb; P.kblocks = d->r * d->s * P.cblocks;
+    pl->grid = dim3(d->k / pl->bn, P.tiles_x * P.tiles_y * P.img_groups, 1);
     if (pl->grid.y > 65535) return fail(CONVIO_EINFEASIBLE, "grid exceeds launch limits");
-    pl->fn = fn;
-    pl->smem = smem;
-    pl->bn = bn;
-    pl->split = split;
-    pl->threads = split ? 256 : 128;
-    if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
-        return fail(CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
-                    pl->threads, smem);
     return CONVIO_OK;
 }
 
-static bool make_igemm_maps(const IgemmPlan &pl, const float *x, const float *wq, CUtensorMap *tx,
+// M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c]: V is an "image" per xi of
+// 1 x T pixels, U the filter of tap xi.
+int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, int k, IgemmPlan *pl,
+                       char *reason, size_t rlen) {
+    const int cb = kind == KIND_BF16 ? 64 : 32;
+    if (c % cb)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", c, cb);
+    if (k % bn)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "K=%d is not a multiple of z=%d", k, bn);
+    IgemmParams &P = pl->P;
+    memset(&P, 0, sizeof(P));
+    int rc = plan_ring(pl, bn, kind, s_b, reason, rlen);
+    if (rc) return rc;
+    P.n = xi; P.c = c; P.h = 1; P.w = t_count; P.k = k; P.p = 1; P.q = t_count;
+    P.pad = 0; P.stride = 1; P.ks = 1;
+    P.bx = 128; P.by = 1; P.imgs = 1;
+    P.tiles_x = (t_count + 127) / 128; P.tiles_y = 1; P.img_groups = xi;
+    P.cblocks = c / cb; P.kblocks = P.cblocks;
+    P.batched = 1;
+    pl->grid = dim3(k / bn, P.tiles_x * xi, 1);
+    if (pl->grid.y > 65535)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "grid exceeds launch limits");
+    return CONVIO_OK;
+}
+
+static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, CUtensorMap *tx,
                             CUtensorMap *tw) {
     const IgemmParams &P = pl.P;
     if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15)) return false;
+    const bool bf = pl.kind == KIND_BF16;
+    const cuuint64_t es_b = bf ? 2 : 4;
+    const cuuint32_t cb = bf ? 64 : 32;
     cuuint64_t xd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.n};
-    cuuint64_t xs[3] = {(cuuint64_t)P.c * 4, (cuuint64_t)P.w * P.c * 4, (cuuint64_t)P.h * P.w * P.c * 4};
+    cuuint64_t xs[3] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.w * P.c * es_b,
+                        (cuuint64_t)P.h * P.w * P.c * es_b};
     // stride: box spans stride*(pixels) input positions, traversal stride picks every stride-th
-    cuuint32_t xb[4] = {32, (cuuint32_t)(P.bx * P.stride), (cuuint32_t)(P.by * P.stride),
+    cuuint32_t xb[4] = {cb, (cuuint32_t)(P.bx * P.stride), (cuuint32_t)(P.by * P.stride),
                         (cuuint32_t)P.imgs};
     cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
-    if (!encode_tensor_map_tiled_ex(tx, 4, const_cast<float *>(x), xd, xs, xb, xes, true)) return false;
-    const int rs = P.ks * P.ks;
-    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)rs};
-    cuuint64_t ws[2] = {(cuuint64_t)P.c * 4, (cuuint64_t)P.k * P.c * 4};
-    cuuint32_t wb[3] = {32, (cuuint32_t)pl.bn, 1};
-    return encode_tensor_map_tiled_ex(tw, 3, const_cast<float *>(wq), wd, ws, wb, es, true);
+    const int taps = P.batched ? P.n : P.ks * P.ks;
+    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps};
+    cuuint64_t ws[2] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.k * P.c * es_b};
+    cuuint32_t wb[3] = {cb, (cuuint32_t)pl.bn, 1};
+    if (bf)
+        return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
+               encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), wd, ws, wb, es);
+    return encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true) &&
+           encode_tensor_map_tiled_ex(tw, 3, const_cast<void *>(wq), wd, ws, wb, es, true);
 }
 
-int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, bool split) {
+int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
+                 cudaStream_t stream) {
+    CUtensorMap tx, tw;
+    if (!make_igemm_maps(pl, x, wq, &tx, &tw)) {
+        set_error("TMA descriptors cannot describe these tensors (alignment)");
+        return CONVIO_EINFEASIBLE;
+    }
+    pl.P.bias = bias;
+    pl.P.y = y;
+    pl.P.relu = relu;
+    pl.fn<<<pl.grid, pl.threads, pl.smem, stream>>>(pl.P, tx, tw);
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
+}
+
+int launch_convert_bf16(const float *src, void *dst, int64_t n, cudaStream_t stream) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n / 8 + 255) / 256, 148 * 16));
+    convert_bf16_kernel<<<blocks, 256, 0, stream>>>(src, (__nv_bfloat16 *)dst, n);
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
+}
+
+static inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+int64_t igemm_workspace_bytes(const convio_conv_desc *d, int kind) {
+    const int64_t wbytes = (int64_t)d->k * d->c * d->r * d->s * (kind == KIND_BF16 ? 2 : 4);
+    if (kind != KIND_BF16) return wbytes;
+    return (int64_t)align256(wbytes) + 2LL * d->n * d->c * d->h * d->w;
+}
+
+int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, int kind) {
     IgemmPlan pl;
-    int rc = plan_igemm(d, t, &pl, out->reason, sizeof(out->reason), split);
+    int rc = plan_igemm(d, t, &pl, out->reason, sizeof(out->reason), kind);
     if (rc) return rc;
     out->legal = 1;
     out->grid_x = pl.grid.x; out->grid_y = pl.grid.y; out->grid_z = pl.grid.z;
     out->block_threads = pl.threads;
     out->smem_bytes = (int)pl.smem;
     out->regs_per_thread = pl.regs;
-    out->channel_chunk = 32;
+    out->channel_chunk = kind == KIND_BF16 ? 64 : 32;
     out->stages = pl.P.stages;
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
-    out->workspace_bytes = 4LL * d->k * d->c * d->r * d->s;
+    out->workspace_bytes = igemm_workspace_bytes(d, kind);
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s: M=128 (%d px x %d img), N=%d, %d stages",
-             split ? "3xtf32" : "tf32", pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
+             kind_name(kind), pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
+    return CONVIO_OK;
+}
+
+int launch_pack_filter_igemm(const convio_conv_desc *desc, const float *w, void *wq, int bf16,
+                             cudaStream_t stream) {
+    const int64_t total = (int64_t)desc->k * desc->c * desc->r * desc->s;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
+    if (bf16)
+        pack_filter_igemm_kernel<__nv_bfloat16><<<blocks, 256, 0, stream>>>(
+            w, (__nv_bfloat16 *)wq, desc->k, desc->c, desc->r * desc->s);
+    else
+        pack_filter_igemm_kernel<float><<<blocks, 256, 0, stream>>>(w, (float *)wq, desc->k, desc->c,
+                                                                    desc->r * desc->s);
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
 }
 
 }  // namespace convio
 
 using namespace convio;
+
+static int prec_kind(int32_t precision) {
+    switch (precision) {
+        case CONVIO_PREC_TF32: return KIND_TF32;
+        case CONVIO_PREC_3XTF32: return KIND_3XTF32;
+        case CONVIO_PREC_BF16: return KIND_BF16;
+        default: return -1;
+    }
+}
 
 extern "C" {
 
@@ -173,67 +297,89 @@ int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float
         set_error("null argument");
         return CONVIO_EINVAL;
     }
-    const int64_t total = (int64_t)desc->k * desc->c * desc->r * desc->s;
-    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
-    pack_filter_igemm_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(w, wq, desc->k, desc->c,
-                                                                      desc->r * desc->s);
-    note_launch();
-    CONVIO_CUDA_TRY(cudaGetLastError());
-    return CONVIO_OK;
+    return launch_pack_filter_igemm(desc, w, wq, 0, (cudaStream_t)stream);
 }
 
-static int conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
-                      const float *w, int32_t w_is_packed, const float *bias, int32_t relu, float *y,
-                      void *workspace, size_t workspace_bytes, void *stream, bool split) {
+int convio_pack_filter_igemm_bf16(const convio_conv_desc *desc, const float *w, void *wq,
+                                  void *stream) {
+    clear_error();
+    if (!desc || !w || !wq) {
+        set_error("null argument");
+        return CONVIO_EINVAL;
+    }
+    return launch_pack_filter_igemm(desc, w, wq, 1, (cudaStream_t)stream);
+}
+
+int convio_convert_bf16(const float *src, void *dst, int64_t n, void *stream) {
+    clear_error();
+    if (!src || !dst || n < 0) {
+        set_error("null argument or negative count");
+        return CONVIO_EINVAL;
+    }
+    if ((reinterpret_cast<uintptr_t>(src) & 15) || (reinterpret_cast<uintptr_t>(dst) & 15)) {
+        set_error("convio_convert_bf16 needs 16-byte aligned buffers");
+        return CONVIO_EINVAL;
+    }
+    if (n == 0) return CONVIO_OK;
+    return launch_convert_bf16(src, dst, n, (cudaStream_t)stream);
+}
+
+int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
+                      const float *x, const void *w, int32_t w_is_packed, const float *bias,
+                      int32_t relu, float *y, void *workspace, size_t workspace_bytes, void *stream) {
     clear_error();
     reset_launches();
-    if (!x || !w || !y || !tile) {
-        set_error("null tensor pointer or tile");
+    const int kind = prec_kind(precision);
+    if (kind < 0) {
+        set_error("unknown precision %d", precision);
+        return CONVIO_EINVAL;
+    }
+    if (!x || !w || !y || !tile || !desc) {
+        set_error("null tensor pointer, descriptor or tile");
         return CONVIO_EINVAL;
     }
     IgemmPlan pl;
     char why[160];
-    int rc = plan_igemm(desc, tile, &pl, why, sizeof(why), split);
+    int rc = plan_igemm(desc, tile, &pl, why, sizeof(why), kind);
     if (rc) return rc;
-    const float *wq = w;
+    cudaStream_t st = (cudaStream_t)stream;
+    const bool bf = kind == KIND_BF16;
+    const size_t wbytes = (size_t)desc->k * desc->c * desc->r * desc->s * (bf ? 2 : 4);
+    const size_t need = (size_t)igemm_workspace_bytes(desc, kind);
+    const size_t need_here = bf ? need : (w_is_packed ? 0 : need);
+    if (need_here && (!workspace || workspace_bytes < need_here)) {
+        set_error("workspace of %zu bytes needed (%s)", need_here,
+                  bf ? "bf16 filter + bf16 activations" : "packed filter");
+        return CONVIO_EINVAL;
+    }
+    const void *wq = w;
     if (!w_is_packed) {
-        const size_t need = 4ULL * desc->k * desc->c * desc->r * desc->s;
-        if (!workspace || workspace_bytes < need) {
-            set_error("workspace of %zu bytes needed for the packed filter", need);
-            return CONVIO_EINVAL;
-        }
-        rc = convio_pack_filter_igemm(desc, w, (float *)workspace, stream);
+        rc = launch_pack_filter_igemm(desc, (const float *)w, workspace, bf, st);
         if (rc) return rc;
-        wq = (const float *)workspace;
-        reset_launches();
-        note_launch();
+        wq = workspace;
     }
-    CUtensorMap tx, tw;
-    if (!make_igemm_maps(pl, x, wq, &tx, &tw)) {
-        set_error("TMA descriptors cannot describe these tensors (alignment)");
-        return CONVIO_EINFEASIBLE;
+    const void *xa = x;
+    if (bf) {
+        void *xb = (uint8_t *)workspace + align256(wbytes);
+        rc = launch_convert_bf16(x, xb, (int64_t)desc->n * desc->c * desc->h * desc->w, st);
+        if (rc) return rc;
+        xa = xb;
     }
-    pl.P.bias = bias;
-    pl.P.y = y;
-    pl.P.relu = relu;
-    pl.fn<<<pl.grid, pl.threads, pl.smem, (cudaStream_t)stream>>>(pl.P, tx, tw);
-    note_launch();
-    CONVIO_CUDA_TRY(cudaGetLastError());
-    return CONVIO_OK;
+    return igemm_launch(pl, xa, wq, bias, relu, y, st);
 }
 
 int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                            const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
                            float *y, void *workspace, size_t workspace_bytes, void *stream) {
-    return conv_igemm(desc, tile, x, w, w_is_packed, bias, relu, y, workspace, workspace_bytes,
-                      stream, false);
+    return convio_conv_igemm(desc, tile, CONVIO_PREC_TF32, x, w, w_is_packed, bias, relu, y,
+                             workspace, workspace_bytes, stream);
 }
 
 int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                              const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
                              float *y, void *workspace, size_t workspace_bytes, void *stream) {
-    return conv_igemm(desc, tile, x, w, w_is_packed, bias, relu, y, workspace, workspace_bytes,
-                      stream, true);
+    return convio_conv_igemm(desc, tile, CONVIO_PREC_3XTF32, x, w, w_is_packed, bias, relu, y,
+                             workspace, workspace_bytes, stream);
 }
 
 }  // extern "C"

@@ -1,22 +1,28 @@
 // Direct convolution as an implicit GEMM on the 5th-generation tensor cores
-// (tcgen05, kind::tf32, FP32 accumulate in TMEM) -- the "TF32 tcgen05 variant
-// for the dense contraction stage" of the north star, same output-stationary
+// (tcgen05, FP32 accumulate in TMEM) -- the "TF32/BF16 tcgen05 variant for
+// the dense contraction stage" of the north star, same output-stationary
 // block (x*y pixels x z channels per CTA) as the FP32 dataflow
 // (reference pkg/src/convio/dataflow.py:219-250).
 //
 //   GEMM view  D[m][n] += A[m][kk] * B[n][kk]
 //     m  = pixel of the block (x*y pixels of up to `imgs` stacked images),
 //     n  = output channel (z = BN per CTA),
-//     kk = (tap r,s ; input-channel c), walked as 9 taps x C/32 blocks.
-//   A    = NHWC input box [imgs][y][x][32 ch] for tap (r,s): one TMA 4-D load
+//     kk = (tap r,s ; input-channel c), walked as R*S taps x C/CB blocks
+//          (CB = 32 fp32 or 64 bf16 channels = one 128-B row).
+//   A    = NHWC input box [imgs][y][x][CB ch] for tap (r,s): one TMA 4-D load
 //          per k-block, zero-filled halo (= padding), SWIZZLE_128B, i.e. the
 //          canonical K-major UMMA layout (128-B rows, 1024-B swizzle atoms).
-//   B    = packed filters [RS][K][C] box [BN][32 ch], same layout.
-//   MMA  = one elected thread issues 4 x tcgen05.mma (M=128, N=BN, K=8) per
-//          k-block; tcgen05.commit releases the smem stage to the TMA thread.
+//   B    = packed filters [RS][K][C] box [BN][CB ch], same layout.
+//   MMA  = one elected thread issues 4 x tcgen05.mma (M=128, N=BN, K=32 B)
+//          per k-block; tcgen05.commit releases the smem stage to the TMA thread.
 //   D    = 128 lanes x BN fp32 columns in TMEM; 4 warps tcgen05.ld their 32
 //          lanes and store NHWC rows (+ bias / ReLU).
 // Rows of the A tile beyond x*y*imgs are don't-care (never stored).
+//
+// Batched mode (P.batched, Winograd's element-wise GEMMs, dataflow.py:253-310
+// step 3): the "image" axis is the Winograd element xi, the pixel axis the
+// tile index t, R = S = 1, and the filter box's third coordinate is xi, so
+// one launch computes M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c] for all xi.
 #pragma once
 
 #include "direct_fp32.cuh"
@@ -34,7 +40,11 @@ struct IgemmParams {
     int ks;                    // kernel edge
     int stages;
     int relu;
+    int batched;               // 1: Winograd element-wise GEMMs (see header)
 };
+
+// operand kinds of the tcgen05 contraction
+enum IgemmKind : int { KIND_TF32 = 0, KIND_3XTF32 = 1, KIND_BF16 = 2 };
 
 // ---- tcgen05 / UMMA primitives ----------------------------------------------------
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
@@ -48,11 +58,12 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {
     return d;
 }
 
-template <int BN>
-__device__ __forceinline__ constexpr uint32_t idesc_tf32_m128() {
+template <int BN, int KIND>
+__device__ __forceinline__ constexpr uint32_t idesc_m128() {
+    // kind::tf32: A/B format 2 (TF32); kind::f16: A/B format 1 (BF16)
     return (1u << 4)          // D format F32
-           | (2u << 7)        // A format TF32
-           | (2u << 10)       // B format TF32
+           | ((KIND == KIND_BF16 ? 1u : 2u) << 7)
+           | ((KIND == KIND_BF16 ? 1u : 2u) << 10)
            | ((uint32_t)(BN >> 3) << 17)
            | ((uint32_t)(128 >> 4) << 24);
 }
@@ -68,9 +79,40 @@ __device__ __forceinline__ void umma_tf32(uint32_t tmem_d, uint64_t a, uint64_t 
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+__device__ __forceinline__ void umma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                      smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ float4 lds128(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(addr));
+    return v;
+}
+
+// store v rounded to TF32 (cvt.rna), explicit shared window
+__device__ __forceinline__ void sts128_tf32(uint32_t addr, float4 v) {
+    uint32_t a, b, c, d;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(v.x));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(v.y));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(c) : "f"(v.z));
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(d) : "f"(v.w));
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};\n" ::"r"(addr), "r"(a), "r"(b), "r"(c),
+                 "r"(d)
                  : "memory");
 }
 
@@ -95,17 +137,20 @@ __device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-// SPLIT = 3xTF32: each operand is split into hi = tf32(v) (the raw operand,
+// KIND_3XTF32: each operand is split into hi = tf32(v) (the raw operand,
 // read by the tensor core with the low mantissa bits dropped) and
 // lo = rna_tf32(v - hi) written by 4 converter warps; every k-step issues
 // A_hi*B_lo + A_lo*B_hi + A_hi*B_hi -- FP32-level accuracy on the tensor cores.
-template <int BN, bool SPLIT>
-__global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
-    igemm_tf32_tcgen05_kernel(const __grid_constant__ IgemmParams P,
+// KIND_BF16: operands are bf16 in HBM (64 channels per 128-B row), kind::f16.
+template <int BN, int KIND>
+__global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
+    igemm_tcgen05_kernel(const __grid_constant__ IgemmParams P,
                               const __grid_constant__ CUtensorMap tm_x,
                               const __grid_constant__ CUtensorMap tm_w) {
-    constexpr int A_BYTES = 128 * 128;       // 128 rows x 32 fp32
-    constexpr int B_BYTES = BN * 128;        // BN rows x 32 fp32
+    constexpr bool SPLIT = KIND == KIND_3XTF32;
+    constexpr int A_BYTES = 128 * 128;       // 128 rows x 128 B (32 fp32 / 64 bf16)
+    constexpr int B_BYTES = BN * 128;        // BN rows x 128 B
+    constexpr int CB = KIND == KIND_BF16 ? 64 : 32;   // channels per k-block
     // stage: [A | B] (TMA; hi after conversion) then, when split, [A_lo | B_lo]
     constexpr int STAGE = (A_BYTES + B_BYTES) * (SPLIT ? 2 : 1);
     constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
@@ -155,25 +200,34 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
 
     if (tid == 0) {
         // ---- TMA producer ---------------------------------------------------------
+        int s = 0, tap = 0, cb = 0;
+        uint32_t ph = 0;
         for (int kb = 0; kb < P.kblocks; ++kb) {
-            const int s = kb % NS;
-            if (kb >= NS) mbar_wait(empty + s, ((kb / NS) - 1) & 1);
-            const int tap = kb / P.cblocks, cb = kb - tap * P.cblocks;
+            if (kb >= NS) mbar_wait(empty + s, ph ^ 1);
             const int r = tap / P.ks, sx = tap - r * P.ks;
             uint8_t *a = smem + s * STAGE;
             uint8_t *b = a + A_BYTES;
             mbar_arrive_expect_tx(full + s, (uint32_t)(P.bx * P.by * P.imgs * 128 + B_BYTES));
             // stride > 1: the map's traversal strides pick every stride-th pixel
-            tma_load_4d(a, map_x, cb * 32, ox0 * P.stride + sx - P.pad, oy0 * P.stride + r - P.pad,
+            tma_load_4d(a, map_x, cb * CB, ox0 * P.stride + sx - P.pad, oy0 * P.stride + r - P.pad,
                         img0, full + s);
-            tma_load_3d(b, map_w, cb * 32, k0, tap, full + s);
+            tma_load_3d(b, map_w, cb * CB, k0, P.batched ? img0 : tap, full + s);
+            if (++cb == P.cblocks) {
+                cb = 0;
+                ++tap;
+            }
+            if (++s == NS) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     } else if (tid == 32) {
         // ---- MMA issuer (single thread) -------------------------------------------
-        constexpr uint32_t idesc = idesc_tf32_m128<BN>();
+        constexpr uint32_t idesc = idesc_m128<BN, KIND>();
+        int s = 0;
+        uint32_t ph = 0;
         for (int kb = 0; kb < P.kblocks; ++kb) {
-            const int s = kb % NS;
-            mbar_wait(SPLIT ? conv + s : full + s, (kb / NS) & 1);
+            mbar_wait(SPLIT ? conv + s : full + s, ph);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t a = smem_u32(smem + s * STAGE);
             const uint32_t b = a + A_BYTES;
@@ -188,6 +242,11 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
                     umma_tf32(tmem, adl + o, bd + o, idesc, 1);
                     umma_tf32(tmem, ad + o, bd + o, idesc, 1);
                 }
+            } else if constexpr (KIND == KIND_BF16) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk)   // K = 16 bf16 = 32 B per MMA
+                    umma_bf16(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                              (kb | kk) != 0);
             } else {
 #pragma unroll
                 for (int kk = 0; kk < 4; ++kk)   // K = 8 tf32 = 32 B per MMA
@@ -195,6 +254,10 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
                               (kb | kk) != 0);
             }
             umma_commit(empty + s);
+            if (++s == NS) {
+                s = 0;
+                ph ^= 1;
+            }
         }
         umma_commit(done);
     } else if (SPLIT && warp >= 4) {
@@ -203,29 +266,35 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
         // 13 mantissa bits, so hi = v & ~0x1fff needs no store: only lo is
         // written (itself rounded to TF32), halving the conversion's smem traffic.
         const int ct = tid - 128;                    // 0..127
-        constexpr int VEC = (A_BYTES + B_BYTES) / 16;
+        constexpr int PER = (A_BYTES + B_BYTES) / 16 / 128;   // float4 per converter thread
+        int s = 0;
+        uint32_t ph = 0;
         for (int kb = 0; kb < P.kblocks; ++kb) {
-            const int s = kb % NS;
-            mbar_wait(full + s, (kb / NS) & 1);
-            const float4 *hi = reinterpret_cast<const float4 *>(smem + s * STAGE);
-            float4 *lo = reinterpret_cast<float4 *>(smem + s * STAGE + A_BYTES + B_BYTES);
-            for (int i = ct; i < VEC; i += 128) {
-                const float4 v = hi[i];
+            mbar_wait(full + s, ph);
+            // explicit shared-window addressing (LDS/STS, not generic LD/ST);
+            // all loads first so their latencies overlap
+            const uint32_t hi_s = smem_u32(smem + s * STAGE) + ct * 16;
+            const uint32_t lo_s = hi_s + A_BYTES + B_BYTES;
+            float4 v[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) v[j] = lds128(hi_s + j * 128 * 16);
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
                 float4 l;
-                l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
-                l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
-                l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
-                l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.x)) : "f"(l.x));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.y)) : "f"(l.y));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.z)) : "f"(l.z));
-                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&l.w)) : "f"(l.w));
-                lo[i] = l;
+                l.x = v[j].x - __uint_as_float(__float_as_uint(v[j].x) & 0xffffe000u);
+                l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
+                l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
+                l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
+                sts128_tf32(lo_s + j * 128 * 16, l);
             }
             // generic-proxy stores -> visible to the tensor core's async proxy
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive(conv + s);
+            if (++s == NS) {
+                s = 0;
+                ph ^= 1;
+            }
         }
     }
     // ---- epilogue: TMEM -> registers -> NHWC global ---------------------------------
@@ -269,5 +338,25 @@ __global__ void __launch_bounds__(SPLIT ? 256 : 128, 1)
     if (warp == 0)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
 }
+
+// ---- host-side plan (igemm.cu) -------------------------------------------------
+using IgemmFn = void (*)(const IgemmParams, const CUtensorMap, const CUtensorMap);
+
+struct IgemmPlan {
+    IgemmParams P;
+    IgemmFn fn = nullptr;
+    dim3 grid;
+    size_t smem = 0;
+    int regs = 0;
+    int bn = 0;
+    int threads = 128;
+    int kind = KIND_TF32;
+};
+
+// M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c] (Winograd step 3) in one launch
+int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, int k, IgemmPlan *pl,
+                       char *reason, size_t rlen);
+int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
+                 cudaStream_t stream);
 
 }  // namespace convio

@@ -1,0 +1,446 @@
+// Winograd F(e x e, 3 x 3) with the element-wise batched GEMM on the tensor
+// cores (tcgen05) -- the north star's "TF32/BF16 tcgen05 variant for ...
+// Winograd's batched GEMM".  The four steps of the reference DAG
+// (pkg/src/convio/dag.py:302-403; schedule dataflow.py:253-310):
+//
+//   1. input transform   V[xi][t][c] = (B^T d_{t,c} B)[xi]      (winograd_input_tc_kernel)
+//   2. kernel transform  U[xi][k][c] = (G g_{k,c} G^T)[xi]      (winograd_filter_tc_kernel,
+//                                                                 once per filter: shared)
+//   3. products + sum    M[xi][t][k] = sum_c V[xi][t][c] U[xi][k][c]
+//                        -> m^2 GEMMs of T x K x C in ONE tcgen05 launch
+//                           (igemm_tcgen05_kernel, batched mode)
+//   4. output transform  y_{t,k} = A^T M_{t,k} A (+ bias, ReLU)  (winograd_output_tc_kernel)
+//
+// t = (image, tile row, tile col) with e x e output tiles; NHWC activations.
+// The batch is processed in chunks of images sized so the chunk's V and M
+// (the transformed tiles) stay resident in the 126 MB L2: HBM sees the input
+// read once and the output written once, the transformed tensors live on
+// chip (L2) between the three launches.
+#include <cuda_bf16.h>
+#include <stdarg.h>
+#include <algorithm>
+
+#include "igemm_tcgen05.cuh"
+
+namespace convio {
+
+// The same Lavin & Gray matrices as winograd.cu / oracle/winograd_mats.py,
+// written out so the zero coefficients cost nothing.
+template <int E>
+struct WinoTf;
+
+template <>
+struct WinoTf<2> {   // F(2x2, 3x3), m = 4
+    static constexpr int M = 4;
+    template <typename T>
+    __device__ __forceinline__ static void bt(const T (&d)[4], T (&o)[4]) {
+        o[0] = d[0] - d[2];
+        o[1] = d[1] + d[2];
+        o[2] = d[2] - d[1];
+        o[3] = d[1] - d[3];
+    }
+    __device__ __forceinline__ static void at(const float (&m)[4], float (&y)[2]) {
+        y[0] = m[0] + m[1] + m[2];
+        y[1] = m[1] - m[2] - m[3];
+    }
+    __device__ __forceinline__ static void g(const float (&w)[3], float (&o)[4]) {
+        o[0] = w[0];
+        o[1] = 0.5f * (w[0] + w[1] + w[2]);
+        o[2] = 0.5f * (w[0] - w[1] + w[2]);
+        o[3] = w[2];
+    }
+};
+
+template <>
+struct WinoTf<4> {   // F(4x4, 3x3), m = 6
+    static constexpr int M = 6;
+    template <typename T>
+    __device__ __forceinline__ static void bt(const T (&d)[6], T (&o)[6]) {
+        o[0] = fmaf(4.0f, d[0], fmaf(-5.0f, d[2], d[4]));
+        o[1] = fmaf(-4.0f, d[1] + d[2], d[3] + d[4]);
+        o[2] = fmaf(4.0f, d[1] - d[2], d[4] - d[3]);
+        o[3] = fmaf(2.0f, d[3] - d[1], d[4] - d[2]);
+        o[4] = fmaf(2.0f, d[1] - d[3], d[4] - d[2]);
+        o[5] = fmaf(4.0f, d[1], fmaf(-5.0f, d[3], d[5]));
+    }
+    __device__ __forceinline__ static void at(const float (&m)[6], float (&y)[4]) {
+        const float a = m[1] + m[2], b = m[1] - m[2], c = m[3] + m[4], d = m[3] - m[4];
+        y[0] = m[0] + a + c;
+        y[1] = fmaf(2.0f, d, b);
+        y[2] = fmaf(4.0f, c, a);
+        y[3] = fmaf(8.0f, d, b) + m[5];
+    }
+    __device__ __forceinline__ static void g(const float (&w)[3], float (&o)[6]) {
+        o[0] = 0.25f * w[0];
+        o[1] = (-1.0f / 6.0f) * (w[0] + w[1] + w[2]);
+        o[2] = (-1.0f / 6.0f) * (w[0] - w[1] + w[2]);
+        o[3] = (1.0f / 24.0f) * w[0] + (1.0f / 12.0f) * w[1] + (1.0f / 6.0f) * w[2];
+        o[4] = (1.0f / 24.0f) * w[0] - (1.0f / 12.0f) * w[1] + (1.0f / 6.0f) * w[2];
+        o[5] = w[2];
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ void store_elem(T *p, float v) {
+    if constexpr (sizeof(T) == 2)
+        *p = __float2bfloat16_rn(v);
+    else
+        *p = v;
+}
+
+struct WinoTcGeom {
+    int n, c, h, w, k, pad;
+    int p, q;            // output
+    int tiles_y, tiles_x;
+    int img0, imgs;      // chunk
+};
+
+// Step 1: one thread per (tile, channel); channels fastest so every load and
+// every V store is a coalesced 128-B warp access.
+template <int E, typename T>
+__global__ void __launch_bounds__(256) winograd_input_tc_kernel(const float *__restrict__ x,
+                                                                T *__restrict__ v, WinoTcGeom g) {
+    constexpr int M = WinoTf<E>::M;
+    const int64_t tpi = (int64_t)g.tiles_y * g.tiles_x;
+    const int64_t t_count = tpi * g.imgs;
+    const int64_t total = t_count * g.c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(i % g.c);
+        const int64_t t = i / g.c;
+        const int img = (int)(t / tpi);
+        const int rem = (int)(t - img * tpi);
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        const int iy0 = ty * E - g.pad, ix0 = tx * E - g.pad;
+        const float *xb = x + ((int64_t)(g.img0 + img) * g.h * g.w) * g.c + c;
+        float d[M][M];
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            const int iy = iy0 + a;
+            const bool rok = iy >= 0 && iy < g.h;
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                const int ix = ix0 + b;
+                d[a][b] = (rok && ix >= 0 && ix < g.w) ? __ldg(xb + ((int64_t)iy * g.w + ix) * g.c) : 0.0f;
+            }
+        }
+        // columns: tmp[a][j] = (B^T d)[a][j]
+        float tmp[M][M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            float col[M], o[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) col[a] = d[a][j];
+            WinoTf<E>::bt(col, o);
+#pragma unroll
+            for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
+        }
+        const int64_t xi_stride = t_count * g.c;
+        T *vp = v + t * g.c + c;
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            float o[M];
+            WinoTf<E>::bt(tmp[a], o);   // rows: (B^T d B)[a][b]
+#pragma unroll
+            for (int b = 0; b < M; ++b) store_elem(vp + (a * M + b) * xi_stride, o[b]);
+        }
+    }
+}
+
+// Step 2: U[xi][k][c] = (G g G^T)[xi], one thread per (k, c), c fastest.
+template <int E, typename T>
+__global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__restrict__ u, int k,
+                                          int c) {
+    constexpr int M = WinoTf<E>::M;
+    const int64_t pairs = (int64_t)k * c;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float *g = w + i * 9;   // KCRS: (k, c) pairs are contiguous 3x3 filters
+        float t[M][3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            float col[3] = {g[j], g[3 + j], g[6 + j]}, o[M];
+            WinoTf<E>::g(col, o);
+#pragma unroll
+            for (int a = 0; a < M; ++a) t[a][j] = o[a];
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            float o[M];
+            WinoTf<E>::g(t[a], o);
+#pragma unroll
+            for (int b = 0; b < M; ++b) store_elem(u + (int64_t)(a * M + b) * pairs + i, o[b]);
+        }
+    }
+}
+
+// Step 4: one thread per (tile, output channel), k fastest (coalesced M
+// loads and NHWC stores); bias + ReLU fused; ragged tiles masked.
+template <int E>
+__global__ void __launch_bounds__(256) winograd_output_tc_kernel(const float *__restrict__ mm,
+                                                                 const float *__restrict__ bias,
+                                                                 float *__restrict__ y, WinoTcGeom g,
+                                                                 int relu) {
+    constexpr int M = WinoTf<E>::M;
+    const int64_t tpi = (int64_t)g.tiles_y * g.tiles_x;
+    const int64_t t_count = tpi * g.imgs;
+    const int64_t total = t_count * g.k;
+    const int64_t xi_stride = t_count * g.k;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i % g.k);
+        const int64_t t = i / g.k;
+        const int img = (int)(t / tpi);
+        const int rem = (int)(t - img * tpi);
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        const float *mp = mm + t * g.k + k;
+        float tmp[E][M];
+#pragma unroll
+        for (int b = 0; b < M; ++b) {
+            float col[M], o[E];
+#pragma unroll
+            for (int a = 0; a < M; ++a) col[a] = __ldg(mp + (a * M + b) * xi_stride);
+            WinoTf<E>::at(col, o);
+#pragma unroll
+            for (int a = 0; a < E; ++a) tmp[a][b] = o[a];
+        }
+        const float bv = bias ? __ldg(bias + k) : 0.0f;
+        float *yb = y + ((int64_t)(g.img0 + img) * g.p * g.q) * g.k + k;
+#pragma unroll
+        for (int a = 0; a < E; ++a) {
+            float o[E];
+            WinoTf<E>::at(tmp[a], o);
+            const int oy = ty * E + a;
+#pragma unroll
+            for (int b = 0; b < E; ++b) {
+                const int ox = tx * E + b;
+                if (oy < g.p && ox < g.q) {
+                    float r = o[b] + bv;
+                    yb[((int64_t)oy * g.q + ox) * g.k] = relu ? fmaxf(r, 0.0f) : r;
+                }
+            }
+        }
+    }
+}
+
+static int kind_of_prec(int32_t precision) {
+    switch (precision) {
+        case CONVIO_PREC_TF32: return KIND_TF32;
+        case CONVIO_PREC_3XTF32: return KIND_3XTF32;
+        case CONVIO_PREC_BF16: return KIND_BF16;
+        default: return -1;
+    }
+}
+
+static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
+
+// L2 budget for one chunk's transformed tiles (V + M): about half the 126 MB
+// L2, leaving room for the input/output streams and the filter.
+static constexpr size_t kChunkL2Bytes = 56ull << 20;
+
+struct WinoTcPlan {
+    WinoTcGeom g;
+    int e, m, kind, bn, s_b;
+    int chunk_imgs;
+    size_t u_bytes, v_bytes, m_bytes;   // per chunk for V and M
+};
+
+static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, int32_t precision,
+                        WinoTcPlan *pl, char *reason, size_t rlen) {
+    auto fail = [&](int code, const char *fmt, ...) {
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(reason, rlen, fmt, ap);
+        va_end(ap);
+        set_error("%s", reason);
+        return code;
+    };
+    if (!d) return fail(CONVIO_EINVAL, "null descriptor");
+    const int kind = kind_of_prec(precision);
+    if (kind < 0) return fail(CONVIO_EINVAL, "unknown precision %d", precision);
+    if (e != 2 && e != 4) return fail(CONVIO_EINFEASIBLE, "Winograd e must be 2 or 4 (got %d)", e);
+    if (d->n < 1 || d->c < 1 || d->h < 1 || d->w < 1 || d->k < 1 || d->pad < 0)
+        return fail(CONVIO_EINVAL, "descriptor fields must be >= 1 (pad >= 0)");
+    if (d->r != 3 || d->s != 3) return fail(CONVIO_EINFEASIBLE, "Winograd needs a 3x3 kernel");
+    if (d->stride != 1)
+        return fail(CONVIO_EINFEASIBLE, "Winograd requires stride 1 (reference WinogradParams.check_shape)");
+    if (d->layout != CONVIO_LAYOUT_HWC)
+        return fail(CONVIO_EINFEASIBLE, "tensor-core Winograd needs the HWC (NHWC) layout");
+    const int p = d->h + 2 * d->pad - 2, q = d->w + 2 * d->pad - 2;
+    if (p < 1 || q < 1) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
+    const int cb = kind == KIND_BF16 ? 64 : 32;
+    if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
+    int bn = t ? t->z : (d->k % 128 == 0 ? 128 : 64);
+    int s_b = t ? t->s_b : 16384;
+    if (t && t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
+    if (t && t->e != e) return fail(CONVIO_EINVAL, "tile e=%d differs from e=%d", t->e, e);
+    if (bn != 64 && bn != 128 && bn != 256)
+        return fail(CONVIO_EINFEASIBLE, "tcgen05 Winograd needs z in {64, 128, 256}, got %d", bn);
+    if (d->k % bn) return fail(CONVIO_EINFEASIBLE, "z=%d does not divide K=%d", bn, d->k);
+    const int m = e + 2;
+    const size_t es = kind == KIND_BF16 ? 2 : 4;
+    WinoTcGeom &g = pl->g;
+    g.n = d->n; g.c = d->c; g.h = d->h; g.w = d->w; g.k = d->k; g.pad = d->pad;
+    g.p = p; g.q = q;
+    g.tiles_y = (p + e - 1) / e; g.tiles_x = (q + e - 1) / e;
+    const size_t tpi = (size_t)g.tiles_y * g.tiles_x;
+    const size_t per_img = tpi * m * m * ((size_t)d->c * es + (size_t)d->k * 4);
+    int chunk = (int)std::max<size_t>(1, kChunkL2Bytes / per_img);
+    chunk = std::min(chunk, d->n);
+    // keep the GEMM's T axis within the TMA box-coordinate / grid limits
+    while (chunk > 1 && (size_t)chunk * tpi > (size_t)1 << 24) chunk /= 2;
+    if ((size_t)chunk * tpi >= ((size_t)1 << 31)) return fail(CONVIO_EINFEASIBLE, "too many tiles");
+    pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b;
+    pl->chunk_imgs = chunk;
+    pl->u_bytes = al256((size_t)m * m * d->k * d->c * es);
+    pl->v_bytes = al256((size_t)m * m * chunk * tpi * d->c * es);
+    pl->m_bytes = al256((size_t)m * m * chunk * tpi * d->k * 4);
+    return CONVIO_OK;
+}
+
+static int launch_filter_tc(const WinoTcPlan &pl, const float *w, void *u, cudaStream_t st) {
+    const int64_t pairs = (int64_t)pl.g.k * pl.g.c;
+    const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
+    const bool bf = pl.kind == KIND_BF16;
+    if (pl.e == 2) {
+        if (bf) winograd_filter_tc_kernel<2, __nv_bfloat16><<<blocks, 256, 0, st>>>(w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c);
+        else winograd_filter_tc_kernel<2, float><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+    } else {
+        if (bf) winograd_filter_tc_kernel<4, __nv_bfloat16><<<blocks, 256, 0, st>>>(w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c);
+        else winograd_filter_tc_kernel<4, float><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+    }
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
+}
+
+static int grid_for(int64_t work) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 16));
+}
+
+int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t precision,
+                  convio_launch_info *out) {
+    WinoTcPlan pl;
+    const int e = t ? t->e : 0;
+    int rc = plan_wino_tc(d, t, e, precision, &pl, out->reason, sizeof(out->reason));
+    if (rc) return rc;
+    IgemmPlan gp;
+    const int tc = pl.chunk_imgs * pl.g.tiles_y * pl.g.tiles_x;
+    rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.m * pl.m, tc, d->c, d->k, &gp, out->reason,
+                            sizeof(out->reason));
+    if (rc) return rc;
+    out->legal = 1;
+    out->grid_x = gp.grid.x; out->grid_y = gp.grid.y; out->grid_z = gp.grid.z;
+    out->block_threads = gp.threads;
+    out->smem_bytes = (int)gp.smem;
+    out->regs_per_thread = gp.regs;
+    out->channel_chunk = pl.kind == KIND_BF16 ? 64 : 32;
+    out->stages = gp.P.stages;
+    out->p = pl.g.p; out->q = pl.g.q;
+    const int64_t tiles = (int64_t)d->n * pl.g.tiles_y * pl.g.tiles_x;
+    out->flops = 2LL * pl.m * pl.m * tiles * d->k * d->c;   // element-wise GEMM flops
+    out->workspace_bytes = (int64_t)(pl.u_bytes + pl.v_bytes + pl.m_bytes);
+    snprintf(out->reason, sizeof(out->reason),
+             "tcgen05 Winograd F(%d,3) %s: %d GEMMs of T=%d (chunk %d img) x K=%d x C=%d, N=%d",
+             pl.e, pl.kind == KIND_BF16 ? "bf16" : (pl.kind == KIND_3XTF32 ? "3xtf32" : "tf32"),
+             pl.m * pl.m, tc, pl.chunk_imgs, d->k, d->c, pl.bn);
+    return CONVIO_OK;
+}
+
+int64_t wino_tc_workspace_bytes(const convio_conv_desc *d, const convio_tile *t, int32_t precision) {
+    WinoTcPlan pl;
+    char why[160];
+    if (!t) {   // no tile: enough for the library default of either e
+        int64_t best = -1;
+        for (int e : {2, 4})
+            if (!plan_wino_tc(d, nullptr, e, precision, &pl, why, sizeof(why)))
+                best = std::max<int64_t>(best, (int64_t)(pl.u_bytes + pl.v_bytes + pl.m_bytes));
+        return best;
+    }
+    if (plan_wino_tc(d, t, t->e, precision, &pl, why, sizeof(why))) return -1;
+    return (int64_t)(pl.u_bytes + pl.v_bytes + pl.m_bytes);
+}
+
+}  // namespace convio
+
+using namespace convio;
+
+extern "C" {
+
+int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e, int32_t precision,
+                                        const float *w, void *u, void *stream) {
+    clear_error();
+    reset_launches();
+    WinoTcPlan pl;
+    char why[160];
+    int rc = plan_wino_tc(desc, nullptr, e, precision, &pl, why, sizeof(why));
+    if (rc) return rc;
+    if (!w || !u) {
+        set_error("null filter pointer");
+        return CONVIO_EINVAL;
+    }
+    return launch_filter_tc(pl, w, u, (cudaStream_t)stream);
+}
+
+int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,
+                          int32_t precision, const float *x, const void *w, int32_t w_is_transformed,
+                          const float *bias, int32_t relu, float *y, void *workspace,
+                          size_t workspace_bytes, void *stream) {
+    clear_error();
+    reset_launches();
+    WinoTcPlan pl;
+    char why[160];
+    int rc = plan_wino_tc(desc, tile, e, precision, &pl, why, sizeof(why));
+    if (rc) return rc;
+    if (!x || !w || !y) {
+        set_error("null tensor pointer");
+        return CONVIO_EINVAL;
+    }
+    const size_t need = pl.u_bytes + pl.v_bytes + pl.m_bytes;
+    if (!workspace || workspace_bytes < need) {
+        set_error("workspace of %zu bytes needed (U + chunk V + chunk M)", need);
+        return CONVIO_EINVAL;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    uint8_t *ws = (uint8_t *)workspace;
+    const void *u = w;
+    if (!w_is_transformed) {
+        rc = launch_filter_tc(pl, (const float *)w, ws, st);
+        if (rc) return rc;
+        u = ws;
+    }
+    void *v = ws + pl.u_bytes;
+    float *mm = (float *)(ws + pl.u_bytes + pl.v_bytes);
+    const int tpi = pl.g.tiles_y * pl.g.tiles_x;
+    const bool bf = pl.kind == KIND_BF16;
+    for (int img0 = 0; img0 < desc->n; img0 += pl.chunk_imgs) {
+        WinoTcGeom g = pl.g;
+        g.img0 = img0;
+        g.imgs = std::min(pl.chunk_imgs, desc->n - img0);
+        const int tc = g.imgs * tpi;
+        const int gin = grid_for((int64_t)tc * g.c), gout = grid_for((int64_t)tc * g.k);
+        if (pl.e == 2) {
+            if (bf) winograd_input_tc_kernel<2, __nv_bfloat16><<<gin, 256, 0, st>>>(x, (__nv_bfloat16 *)v, g);
+            else winograd_input_tc_kernel<2, float><<<gin, 256, 0, st>>>(x, (float *)v, g);
+        } else {
+            if (bf) winograd_input_tc_kernel<4, __nv_bfloat16><<<gin, 256, 0, st>>>(x, (__nv_bfloat16 *)v, g);
+            else winograd_input_tc_kernel<4, float><<<gin, 256, 0, st>>>(x, (float *)v, g);
+        }
+        note_launch();
+        CONVIO_CUDA_TRY(cudaGetLastError());
+        IgemmPlan gp;
+        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.m * pl.m, tc, g.c, g.k, &gp, why, sizeof(why));
+        if (rc) return rc;
+        rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);
+        if (rc) return rc;
+        if (pl.e == 2)
+            winograd_output_tc_kernel<2><<<gout, 256, 0, st>>>(mm, bias, y, g, relu);
+        else
+            winograd_output_tc_kernel<4><<<gout, 256, 0, st>>>(mm, bias, y, g, relu);
+        note_launch();
+        CONVIO_CUDA_TRY(cudaGetLastError());
+    }
+    return CONVIO_OK;
+}
+
+}  // extern "C"

@@ -158,6 +158,7 @@ def test_igemm_tcgen05_tf32_stride2():
 
 SPLIT_CASES = [
     (2, 64, 56, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
+    (2, 128, 14, 14, 256, 1, TileConfig(14, 7, 256, 32768, 1, 1, 1, layout="HWC")),
     (2, 256, 14, 14, 128, 1, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
     (3, 64, 7, 7, 64, 1, TileConfig(7, 7, 64, 32768, 1, 1, 1, layout="HWC")),
     (2, 128, 28, 28, 128, 2, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
@@ -182,3 +183,119 @@ def test_direct_fp32_error_at_long_reductions(c):
     x, wt = _inputs(1, c, 14, 14, 64, 3, 3)
     y = C.conv_direct(_dev(x), _dev(wt), padding=1, tile=TileConfig(14, 14, 32, 16384, 2, 7, 4))
     assert co.rel_err(y.cpu().numpy(), co.direct_conv(x, wt, 1, 1)) <= tol_fp32(c)
+
+
+# ---- BF16 tcgen05 implicit GEMM (kind::f16) -------------------------------------
+TOL_BF16 = 3e-2
+
+BF16_CASES = [
+    (2, 64, 56, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
+    (2, 128, 28, 28, 256, 2, TileConfig(14, 7, 256, 32768, 1, 1, 1, layout="HWC")),
+    (5, 128, 7, 7, 128, 1, TileConfig(7, 7, 128, 16384, 1, 1, 1, layout="HWC")),
+]
+
+
+@pytest.mark.parametrize("case", BF16_CASES, ids=[str(i) for i in range(len(BF16_CASES))])
+def test_igemm_tcgen05_bf16_matches_oracle(case):
+    n, c, h, w, k, stride, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile,
+                     precision="bf16", bias=_dev(b), relu=True)
+    ref = np.maximum(co.direct_conv(x, wt, stride, 1) + b[None, :, None, None], 0)
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= TOL_BF16
+    assert err > 1e-6   # really computed at bf16 (not a silent fp32 path)
+    # pre-packed bf16 filter gives the same result
+    wp = C.pack_filter_igemm_bf16(_dev(wt))
+    assert wp.dtype == torch.bfloat16
+    y2 = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile,
+                      precision="bf16", bias=_dev(b), relu=True, w_packed=wp)
+    assert torch.equal(y, y2)
+
+
+def test_igemm_generic_entry_matches_split_entry():
+    x, wt = _inputs(2, 64, 28, 28, 64, 3, 3)
+    tile = TileConfig(14, 4, 64, 16384, 1, 1, 1, layout="HWC")
+    y1 = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision="3xtf32")
+    y2 = C.conv_igemm_tf32(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, split=True)
+    assert torch.equal(y1, y2)
+
+
+def test_igemm_bf16_rejects_c_not_multiple_of_64():
+    x, wt = _inputs(1, 32, 14, 14, 64, 3, 3)
+    with pytest.raises(InfeasibleTileError):
+        C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, precision="bf16",
+                     tile=TileConfig(14, 7, 64, 16384, 1, 1, 1, layout="HWC"))
+
+
+# ---- Winograd with the element-wise GEMMs on tcgen05 ------------------------------
+WTC_CASES = [
+    # (n, c, h, w, k, e, precision, z)
+    (2, 64, 56, 56, 64, 4, "3xtf32", 64),
+    (2, 64, 56, 56, 64, 2, "3xtf32", 64),
+    (3, 128, 14, 14, 256, 4, "3xtf32", 128),
+    (4, 256, 7, 7, 128, 2, "3xtf32", 128),    # ragged: 7 = 3*2 + 1
+    (4, 256, 7, 7, 128, 4, "3xtf32", 128),    # ragged: 7 = 4 + 3
+    (2, 64, 28, 28, 128, 4, "tf32", 128),
+    (2, 64, 28, 28, 128, 2, "tf32", 128),
+    (2, 128, 28, 28, 256, 4, "bf16", 256),
+    (3, 64, 13, 13, 64, 2, "bf16", 64),
+    (2, 128, 14, 14, 256, 4, "3xtf32", 256),
+]
+# Reduced-precision Winograd: the operand rounding error is amplified by the
+# transforms (F(4,3)'s B^T / G entries up to 5 and 1/6..1/24), so the stated
+# tolerances are looser than the direct conv's at the same precision:
+#   tf32: F(2,3) 5e-3, F(4,3) 2e-2;  bf16: F(2,3) 5e-2, F(4,3) 1.5e-1.
+TOL_WTC = {("tf32", 2): 5e-3, ("tf32", 4): 2e-2, ("bf16", 2): 5e-2, ("bf16", 4): 1.5e-1}
+
+
+@pytest.mark.parametrize("case", WTC_CASES, ids=[str(i) for i in range(len(WTC_CASES))])
+def test_winograd_tc_matches_oracle(case):
+    n, c, h, w, k, e, prec, z = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    tile = TileConfig(e, e, z, 16384, 1, 1, 1, layout="HWC", e=e)
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision=prec,
+                           bias=_dev(b))
+    ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
+    assert C.infer_layout(y) == "HWC"
+    tol = TOL_WTC.get((prec, e), TOL_WINO[e] * max(1.0, (c / 64) ** 0.5))
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= tol, (err, tol)
+
+
+def test_winograd_tc_pretransformed_filter_and_relu():
+    x, wt = _inputs(2, 64, 28, 28, 64, 3, 3)
+    u = C.winograd_filter_transform_tc(_dev(wt), 4, "3xtf32")
+    assert tuple(u.shape) == (36, 64, 64)
+    y1 = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, relu=True)
+    y2 = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, relu=True, u=u)
+    assert torch.equal(y1, y2)
+    ref = np.maximum(co.direct_conv(x, wt, 1, 1), 0)
+    assert co.rel_err(y1.contiguous().cpu().numpy(), ref) <= TOL_WINO[4]
+
+
+def test_winograd_tc_filter_transform_matches_oracle():
+    from oracle import winograd_mats as wm
+    _, wt = _inputs(1, 32, 4, 4, 64, 3, 3)
+    for e in (2, 4):
+        u = C.winograd_filter_transform_tc(_dev(wt), e, "3xtf32").cpu().numpy()
+        g = wm.matrices_float(e, 3)["G"]
+        m = e + 2
+        ref = np.einsum("ij,kcjl,ml->imkc", g, wt.astype(np.float64), g).reshape(m * m, 64, 32)
+        assert np.max(np.abs(u - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
+
+
+def test_winograd_tc_chunks_the_batch_through_l2():
+    # enough images that V + M exceed one L2 chunk: several chunks, same answer
+    x, wt = _inputs(24, 64, 56, 56, 64, 3, 3)
+    info = C.query(x.shape, wt.shape, 1, 1, "HWC", TileConfig(4, 4, 64, 16384, 1, 1, 1,
+                   layout="HWC", e=4), algorithm="winograd_tc_3xtf32")
+    assert info["rc"] == 0 and "chunk" in info["reason"]
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, precision="3xtf32")
+    assert C.last_launch_count() > 4   # filter + 3 launches per chunk, > 1 chunk
+    ref = co.direct_conv(x[:2], wt, 1, 1)
+    assert co.rel_err(y[:2].contiguous().cpu().numpy(), ref) <= TOL_WINO[4]
+    ref_last = co.direct_conv(x[-2:], wt, 1, 1)
+    assert co.rel_err(y[-2:].contiguous().cpu().numpy(), ref_last) <= TOL_WINO[4]
