@@ -330,6 +330,9 @@ def main() -> None:
                 if layer.algorithm == "winograd":
                     f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
                     name = f"winograd F({layer.e},3)"
+                elif layer.algorithm.startswith("winograd_tc"):
+                    f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
+                    name = f"{layer.algorithm} F({layer.e},3)"
                 else:
                     f_alg = f_dir
                     name = layer.algorithm
@@ -378,19 +381,25 @@ def main() -> None:
     except (OSError, ValueError):
         pass
     traffic_tab = load_profile_traffic()
-    if dom.startswith("igemm"):
-        # tensor pipe: dense TF32 = 1/2 of the measured bf16 rate; 3xTF32 issues 3 MMAs per flop
-        mma_per_flop = 3 if dom == "igemm_3xtf32" else 1
+    if dom.startswith("igemm") or dom.startswith("winograd_tc"):
+        # tensor pipe: dense TF32 = 1/2 of the measured bf16 rate; 3xTF32 issues 3 MMAs per
+        # algorithmic flop; BF16 runs at the bf16 rate
+        prec = dom.split()[0].rsplit("_", 1)[-1]
+        mma_per_flop = 3 if prec == "3xtf32" else 1
         bf16 = peaks.get("bf16_tflops") or 1590.0
-        peak = bf16 / 2
+        peak = bf16 if prec == "bf16" else bf16 / 2
+        kind = "kind::f16 (bf16)" if prec == "bf16" else "kind::tf32"
+        what = ("implicit GEMM" if dom.startswith("igemm") else
+                "Winograd pipeline: input transform + batched GEMM + output transform, "
+                "flops = element-wise GEMM flops")
         roofline = {
-            "bound": "tensor", "kernel": f"{dom} (tcgen05.mma kind::tf32)",
+            "bound": "tensor", "kernel": f"{dom} (tcgen05.mma {kind}; {what})",
             "achieved": round(achieved * mma_per_flop, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved * mma_per_flop / peak, 4),
             "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
-            "peak_source": ("MEASURED_PEAKS.json bf16_tflops / 2 (dense TF32 rate)" if peaks.get("bf16_tflops")
-                            else "fallback 1.59 PFLOP/s bf16 / 2"),
-            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom}"),
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec == "bf16" else " / 2 (dense TF32 rate)")
+                            if peaks.get("bf16_tflops") else "fallback 1.59 PFLOP/s bf16"),
+            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom.split()[0]}"),
         }
     else:
         peak = ffma_peak_tflops(torch, stream)
@@ -408,7 +417,8 @@ def main() -> None:
     variants = {}
     if not args.no_variants:
         for vname, allowed in (("fp32_cuda_cores", CUDA_CORE_ALGORITHMS),
-                               ("tf32_tcgen05", ("igemm_tf32",))):
+                               ("tf32_tcgen05", ("igemm_tf32", "winograd_tc_tf32")),
+                               ("bf16_tcgen05", ("igemm_bf16", "winograd_tc_bf16"))):
             vplans = load_plans(args.workload, allowed)
             if not vplans:
                 continue
@@ -421,7 +431,9 @@ def main() -> None:
             variants[vname] = {
                 "value": round(flops_all * args.steps / (vt / 1e3) / 1e9, 3), "unit": "GFLOP/s",
                 "ms_per_step": round(vt / args.steps, 4),
-                "tolerance": "5e-3 (TF32 inputs)" if vname.startswith("tf32") else "1e-5 direct / 1e-4..1e-3 Winograd",
+                "tolerance": {"tf32_tcgen05": "5e-3 direct, 5e-3..2e-2 Winograd (TF32 operands)",
+                              "bf16_tcgen05": "3e-2 direct, 5e-2..1.5e-1 Winograd (BF16 operands)"}.get(
+                                  vname, "1e-5 direct / 1e-4..1e-3 Winograd"),
                 "per_layer": [{k: r[k] for k in ("layer", "algorithm", "ms", "gflops")} for r in rows],
             }
             del varm
@@ -500,7 +512,8 @@ def main() -> None:
                        f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
                 "tuned_plans": bool(plans),
                 "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
-                         "(FFMA) or 3xTF32 tcgen05 implicit GEMM (FP32-level accuracy)",
+                         "(FFMA), 3xTF32 tcgen05 implicit GEMM or 3xTF32 tcgen05 Winograd "
+                         "(FP32-level GEMM accuracy)",
             },
             "e2e": e2e,
             "roofline": roofline,

@@ -147,7 +147,9 @@ int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float
  * (tcgen05.mma kind::tf32, accumulators in TMEM, TMA SWIZZLE_128B operand
  * staging).  NHWC (CONVIO_LAYOUT_HWC) activations, C % 32 == 0, stride 1,
  * tile z in {64,128,256}, x*y <= 128 (ceil(128/(x*y)) images stacked per MMA
- * tile).  Inputs are consumed at TF32 precision, accumulation is FP32.
+ * tile).  tile->n_zt selects the kernel: 1 = one 128-row tile per CTA,
+ * 2 = persistent CTA pair (cta_group::2, M = 256, each CTA stages z/2 filter
+ * rows, double-buffered TMEM accumulators); n_xt = n_yt = 1.  Inputs are consumed at TF32 precision, accumulation is FP32.
  * Replaces the same schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
 int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                            const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
@@ -188,7 +190,8 @@ int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e,
  * the input/output transforms as HBM-streaming kernels; the batch is chunked
  * so each chunk's V and M stay in L2.  NHWC, stride 1, C % 32 (% 64 for
  * BF16) == 0; tile->z in {64,128,256} is the GEMM's N tile, tile->s_b sizes
- * the TMA ring, tile->e must equal e (tile == NULL: defaults).
+ * the TMA ring, tile->n_zt in {1, 2} picks the single-CTA / CTA-pair GEMM
+ * kernel, tile->e must equal e (tile == NULL: defaults).
  * Replaces plan_winograd_dataflow + simulate (dataflow.py:253-338). */
 int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,
                           int32_t precision, const float *x, const void *w, int32_t w_is_transformed,

@@ -304,6 +304,9 @@ def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int =
     converted to bf16 in the workspace by the library; ``w_packed`` must come
     from :func:`pack_filter_igemm_bf16` (bf16) or :func:`pack_filter_igemm`.
     Tolerances: 3xtf32 1e-5, tf32 5e-3, bf16 3e-2.
+    ``tile.n_zt`` selects the kernel: 1 = one 128-pixel tile per CTA, 2 = the
+    persistent CTA pair (``tcgen05.mma.cta_group::2``, M = 256, z/2 filter
+    rows staged per CTA, double-buffered TMEM accumulators).
     """
     _check_tensor(x, "x")
     _check_tensor(w, "w")
@@ -375,8 +378,9 @@ def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int 
         out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
     if tile is not None:
         ct = N.make_tile(tile, 2)
-    else:   # library default: N tile 128 (64 if K is not a multiple), 96 KB ring
-        ct = N.Tile(e, e, 128 if desc.k % 128 == 0 else 64, 16384, 1, 1, 1, 2, e)
+    else:   # library default: widest N tile dividing K, CTA-pair kernel
+        z = 256 if desc.k % 256 == 0 else (128 if desc.k % 128 == 0 else 64)
+        ct = N.Tile(e, e, z, 16384, 1, 1, 2, 2, e)
     alg = N.ALG_WINOGRAD_TC_TF32 + prec
     need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), ctypes.byref(ct), alg))
     if need < 0:

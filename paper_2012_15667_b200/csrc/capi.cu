@@ -31,6 +31,10 @@ void reset_launches() { t_launches = 0; }
 int direct_instance_count();
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
 int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, int kind);
+bool nhwc_tile(const convio_conv_desc *d, const convio_tile *t);
+int direct_nhwc_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
+int direct_nhwc_run(const convio_conv_desc *d, const convio_tile *t, const float *x, const float *wp,
+                    const float *bias, int relu, float *y, cudaStream_t stream);
 int64_t igemm_workspace_bytes(const convio_conv_desc *d, int kind);
 int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t precision,
                   convio_launch_info *out);
@@ -105,6 +109,30 @@ int kernel_regs(const void *fn) {
     cudaGetLastError();
     regs_of.emplace(fn, r);
     return r;
+}
+
+int device_sms() { return dev_info().ok ? dev_info().sms : 148; }
+
+// Cluster kernels (CTA pairs): one block per SM by construction; check the
+// block's registers and shared memory against the SM and opt in to the smem.
+int launch_fit_cluster(const void *fn, int threads, size_t smem, int *regs) {
+    const DevInfo &dev = dev_info();
+    if (!dev.ok) {
+        *regs = 0;
+        return 1;
+    }
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    *regs = fa.numRegs;
+    if ((int)smem > dev.max_smem_optin || fa.numRegs * threads > 65536) return 0;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return 1;
 }
 
 int launch_fit(const void *fn, int threads, size_t smem, int *regs) {
@@ -599,6 +627,15 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
     }
     memset(out, 0, sizeof(*out));
     if (algorithm == CONVIO_ALG_DIRECT) {
+        if (nhwc_tile(desc, tile)) {
+            int p, q;
+            int rc = check_desc(desc, &p, &q);
+            if (rc) {
+                snprintf(out->reason, sizeof(out->reason), "%s", t_err);
+                return rc;
+            }
+            return direct_nhwc_query(desc, tile, out);
+        }
         DirectPlan pl;
         int rc = plan_direct(desc, tile, &pl, out->reason, sizeof(out->reason));
         if (rc == CONVIO_OK) fill_info_direct(pl, out, desc);
@@ -664,6 +701,20 @@ int convio_conv_direct_f32(const convio_conv_desc *desc, const convio_tile *tile
     DirectPlan pl;
     char why[160];
     bool generic = false;
+    if (nhwc_tile(desc, tile)) {   // channels-last stacked-pixel kernel (direct_nhwc.cuh)
+        const float *wpk = w;
+        if (!w_is_packed) {
+            const size_t need = 4ULL * desc->k * desc->c * desc->r * desc->s;
+            if (!workspace || workspace_bytes < need) {
+                set_error("workspace of %zu bytes needed for the packed filter", need);
+                return CONVIO_EINVAL;
+            }
+            rc = convio_pack_filter_direct(desc, w, (float *)workspace, stream);
+            if (rc) return rc;
+            wpk = (const float *)workspace;
+        }
+        return direct_nhwc_run(desc, tile, x, wpk, bias, relu, y, st);
+    }
     if (!tile) {
         if (default_direct_tile(desc, &chosen) == CONVIO_OK) {
             tile = &chosen;

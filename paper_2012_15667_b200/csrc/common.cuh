@@ -20,6 +20,10 @@ void reset_launches();
 // (fn, threads, smem)); sets *regs.  Returns 1 without checking when no
 // device is present (CPU-only legality queries).
 int launch_fit(const void *fn, int threads, size_t smem, int *regs);
+// Same for a cluster (CTA-pair) kernel: 1 if one block fits an SM.
+int launch_fit_cluster(const void *fn, int threads, size_t smem, int *regs);
+// SMs of the current device (148 without a device).
+int device_sms();
 // Registers per thread of a kernel (cached); 0 without a device.
 int kernel_regs(const void *fn);
 

@@ -6,7 +6,9 @@
 #include <stdarg.h>
 #include <algorithm>
 
-#include "igemm_tcgen05.cuh"
+#include <stdlib.h>
+
+#include "igemm_pair.cuh"
 
 namespace convio {
 
@@ -24,6 +26,22 @@ static IgemmFn igemm_kernel(int bn, int kind) {
     if (kind == KIND_3XTF32) return igemm_kernel_kind<KIND_3XTF32>(bn);
     if (kind == KIND_BF16) return igemm_kernel_kind<KIND_BF16>(bn);
     return igemm_kernel_kind<KIND_TF32>(bn);
+}
+
+template <int KIND>
+static PairFn pair_kernel_kind(int bn) {
+    switch (bn) {
+        case 64: return &igemm_pair_kernel<64, KIND>;
+        case 128: return &igemm_pair_kernel<128, KIND>;
+        case 256: return &igemm_pair_kernel<256, KIND>;
+        default: return nullptr;
+    }
+}
+
+static PairFn pair_kernel(int bn, int kind) {
+    if (kind == KIND_3XTF32) return pair_kernel_kind<KIND_3XTF32>(bn);
+    if (kind == KIND_BF16) return pair_kernel_kind<KIND_BF16>(bn);
+    return pair_kernel_kind<KIND_TF32>(bn);
 }
 
 static const char *kind_name(int kind) {
@@ -81,7 +99,35 @@ static int pfail(char *reason, size_t rlen, int code, const char *fmt, ...) {
 // outputs live in TMEM, so s_b only sizes the TMA ring: ring bytes <= 6*s_b
 // (s_b = 16384 words -> 96 KB, two CTAs per SM; 32768 -> 192 KB, one deep-ring
 // CTA per SM), 2..6 stages.
-static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, char *reason, size_t rlen) {
+// pair = true: the persistent CTA-pair kernel (igemm_pair.cuh), selected by a
+// tile with n_zt == 2 (two CTAs share the z = BN output channels of one MMA);
+// n_zt == 1: one 128-row tile per CTA (igemm_tcgen05.cuh).
+static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *reason, size_t rlen) {
+    if (pair) {
+        // persistent pair: one CTA per SM, the whole shared memory is the ring
+        PairFn pfn = pair_kernel(bn, kind);
+        if (!pfn)
+            return pfail(reason, rlen, CONVIO_EINFEASIBLE,
+                         "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
+        const size_t stage_bytes = (size_t)(128 * 128 + (bn / 2) * 128) * (kind == KIND_3XTF32 ? 2 : 1);
+        const size_t budget = 227 * 1024 - 1024 - 512;
+        int stages = (int)std::min<size_t>(8, budget / stage_bytes);
+        if (stages < 2)
+            return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair ring does not fit");
+        pl->P.stages = stages;
+        pl->pair = true;
+        pl->pfn = pfn;
+        pl->fn = nullptr;
+        pl->smem = stages * stage_bytes + 1024 + 512;
+        pl->bn = bn;
+        pl->kind = kind;
+        pl->threads = kind == KIND_3XTF32 ? 384 : 256;
+        if (launch_fit_cluster((const void *)pfn, pl->threads, pl->smem, &pl->regs) < 1)
+            return pfail(reason, rlen, CONVIO_EINFEASIBLE,
+                         "tcgen05 pair block (%d threads, %zu B smem) does not fit", pl->threads,
+                         pl->smem);
+        return CONVIO_OK;
+    }
     IgemmFn fn = igemm_kernel(bn, kind);
     if (!fn)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d",
@@ -103,6 +149,19 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, char *reason, siz
     if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
                      pl->threads, smem);
+    return CONVIO_OK;
+}
+
+// persistent grid: one CTA pair per TPC (fewer if there are fewer work items)
+static int finish_pair_grid(IgemmPlan *pl) {
+    const int pairs = (pl->blocks_per_group + 1) / 2;
+    const int64_t items = (int64_t)pl->groups * pairs * (pl->P.k / pl->bn);
+    if (items >= ((int64_t)1 << 31)) {
+        set_error("too many work items");
+        return CONVIO_EINFEASIBLE;
+    }
+    const int64_t clusters = std::max<int64_t>(1, std::min<int64_t>(items, device_sms() / 2));
+    pl->grid = dim3((unsigned)(2 * clusters), 1, 1);
     return CONVIO_OK;
 }
 
@@ -146,7 +205,10 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
-    int rc = plan_ring(pl, t->z, kind, t->s_b, reason, rlen);
+    if (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2))
+        return fail(CONVIO_EINFEASIBLE,
+                    "tcgen05 tiles take n_xt = n_yt = 1 and n_zt in {1 (one CTA), 2 (CTA pair)}");
+    int rc = plan_ring(pl, t->z, kind, t->s_b, t->n_zt == 2, reason, rlen);
     if (rc) return rc;
     const int imgs = std::max(1, std::min(128 / px, d->n));
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
@@ -154,6 +216,9 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     P.bx = t->x; P.by = t->y; P.imgs = imgs;
     P.tiles_x = q / t->x; P.tiles_y = p / t->y; P.img_groups = (d->n + imgs - 1) / imgs;
     P.cblocks = d->c / cb; P.kblocks = d->r * d->s * P.cblocks;
+    pl->groups = 1;
+    pl->blocks_per_group = P.tiles_x * P.tiles_y * P.img_groups;
+    if (pl->pair) return finish_pair_grid(pl);
     pl->grid = dim3(d->k / pl->bn, P.tiles_x * P.tiles_y * P.img_groups, 1);
     if (pl->grid.y > 65535) return fail(CONVIO_EINFEASIBLE, "grid exceeds launch limits");
     return CONVIO_OK;
@@ -161,8 +226,8 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
 
 // M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c]: V is an "image" per xi of
 // 1 x T pixels, U the filter of tap xi.
-int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, int k, IgemmPlan *pl,
-                       char *reason, size_t rlen) {
+int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count, int c, int k,
+                       IgemmPlan *pl, char *reason, size_t rlen) {
     const int cb = kind == KIND_BF16 ? 64 : 32;
     if (c % cb)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", c, cb);
@@ -170,7 +235,7 @@ int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, in
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "K=%d is not a multiple of z=%d", k, bn);
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
-    int rc = plan_ring(pl, bn, kind, s_b, reason, rlen);
+    int rc = plan_ring(pl, bn, kind, s_b, pair, reason, rlen);
     if (rc) return rc;
     P.n = xi; P.c = c; P.h = 1; P.w = t_count; P.k = k; P.p = 1; P.q = t_count;
     P.pad = 0; P.stride = 1; P.ks = 1;
@@ -178,6 +243,9 @@ int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, in
     P.tiles_x = (t_count + 127) / 128; P.tiles_y = 1; P.img_groups = xi;
     P.cblocks = c / cb; P.kblocks = P.cblocks;
     P.batched = 1;
+    pl->groups = xi;
+    pl->blocks_per_group = P.tiles_x;
+    if (pl->pair) return finish_pair_grid(pl);
     pl->grid = dim3(k / bn, P.tiles_x * xi, 1);
     if (pl->grid.y > 65535)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "grid exceeds launch limits");
@@ -202,7 +270,7 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     const int taps = P.batched ? P.n : P.ks * P.ks;
     cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps};
     cuuint64_t ws[2] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.k * P.c * es_b};
-    cuuint32_t wb[3] = {cb, (cuuint32_t)pl.bn, 1};
+    cuuint32_t wb[3] = {cb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1};
     if (bf)
         return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
                encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), wd, ws, wb, es);
@@ -220,6 +288,19 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
     pl.P.bias = bias;
     pl.P.y = y;
     pl.P.relu = relu;
+    if (pl.pair) {
+        PairParams PP;
+        PP.g = pl.P;
+        PP.groups = pl.groups;
+        PP.blocks_per_group = pl.blocks_per_group;
+        PP.pairs_per_group = (pl.blocks_per_group + 1) / 2;
+        PP.nblocks = pl.P.k / pl.bn;
+        PP.items = PP.groups * PP.pairs_per_group * PP.nblocks;
+        pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
+        note_launch();
+        CONVIO_CUDA_TRY(cudaGetLastError());
+        return CONVIO_OK;
+    }
     pl.fn<<<pl.grid, pl.threads, pl.smem, stream>>>(pl.P, tx, tw);
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
@@ -256,8 +337,9 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
-    snprintf(out->reason, sizeof(out->reason), "tcgen05 %s: M=128 (%d px x %d img), N=%d, %d stages",
-             kind_name(kind), pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
+    snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages",
+             kind_name(kind), pl.pair ? " CTA pair (persistent)" : "", pl.pair ? 256 : 128,
+             pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
     return CONVIO_OK;
 }
 

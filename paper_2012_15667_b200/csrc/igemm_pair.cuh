@@ -1,0 +1,395 @@
+// Persistent CTA-pair implicit GEMM on tcgen05 (cta_group::2, M = 256).
+//
+// Same GEMM view as igemm_tcgen05.cuh (D[m][n] += A[m][kk] * B[n][kk], m =
+// pixels, n = output channels, kk = taps x channel blocks), re-organised for
+// the B200 tensor-core / L2 balance:
+//
+//  * A cluster of two CTAs on one TPC shares one M = 256 x N = BN MMA: each
+//    CTA stages its own 128-pixel A block and HALF of the BN filter rows; the
+//    leader's single thread issues tcgen05.mma.cta_group::2, which reads both
+//    CTAs' shared memory.  Per-SM operand traffic (TMA from L2 and smem reads
+//    by the tensor core) drops from (128 + BN) to (128 + BN/2) rows per k-block.
+//  * Persistent: one pair per TPC walks the (pixel-pair, n-block) work list
+//    (n fastest, so the pair re-reads its A block from L2 while it is hot).
+//  * The TMEM accumulator is double-buffered (2 x BN columns): the epilogue
+//    warps drain tile i while the MMA issuer accumulates tile i+1.
+//
+// Warp roles (per CTA):  warp 0 = TMA producer, warp 1 = MMA issuer (leader
+// CTA) + TMEM allocator, warps 4..7 = epilogue (TMEM lane quadrants 0..3),
+// warps 8..11 = 3xTF32 converters (KIND_3XTF32 only).
+//
+// Synchronisation (s = ring stage, a = accumulator buffer):
+//   full[s]   leader: TMA bytes of BOTH CTAs (non-split; .cta_group::2 TMA
+//             signals the leader's barrier) / own bytes (split)
+//   conv[s]   leader, count 8: the 4 converter warps of each CTA (split)
+//   empty[s]  each CTA, via tcgen05.commit multicast to both CTAs
+//   tfull[a]  each CTA, via tcgen05.commit multicast (accumulator ready)
+//   tempty[a] leader, count 8: the 4 epilogue warps of each CTA
+#pragma once
+
+#include "igemm_tcgen05.cuh"
+
+namespace convio {
+
+struct PairParams {
+    IgemmParams g;          // geometry as in the single-CTA kernel
+    int groups;             // 1 (conv) or xi (batched Winograd GEMMs)
+    int blocks_per_group;   // pixel blocks per group
+    int pairs_per_group;    // ceil(blocks_per_group / 2)
+    int nblocks;            // K / BN
+    int items;              // groups * pairs_per_group * nblocks
+};
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+// shared::cluster address of the same variable in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+// wait with cluster-scope acquire (arrivals from the peer CTA)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
+    uint32_t done = 0, polls = 0;
+    while (true) {
+        asm volatile(
+            "{\n"
+            ".reg .pred P1;\n"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, P1;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        if (++polls > (1u << 28)) asm volatile("trap;");
+    }
+}
+
+// TMA load whose completion is signalled on the LEADER CTA's barrier (peer bit cleared)
+__device__ __forceinline__ void tma_load_4d_pair(void *dst, uint64_t map, int c0, int c1, int c2, int c3,
+                                                 uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_pair(void *dst, uint64_t map, int c0, int c1, int c2,
+                                                 uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+
+template <int BN, int KIND>
+__device__ __forceinline__ constexpr uint32_t idesc_m256() {
+    return (1u << 4) | ((KIND == KIND_BF16 ? 1u : 2u) << 7) | ((KIND == KIND_BF16 ? 1u : 2u) << 10) |
+           ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+}
+
+template <int KIND>
+__device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                          uint32_t accumulate) {
+    if constexpr (KIND == KIND_BF16) {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    } else {
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    }
+}
+
+__device__ __forceinline__ void umma_commit_pair(uint64_t *bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)3)
+        : "memory");
+}
+
+// Pixel-block origin of block `blk` of group `grp` (conv: group 0, blocks
+// enumerate (img group, tile row, tile col); batched: group = xi, blocks are
+// 128-tile runs of the T axis).  Out-of-range blocks land beyond the tensor,
+// so TMA fills zeros and the epilogue masks every row.
+__device__ __forceinline__ void pair_block_origin(const IgemmParams &P, int grp, int blk, int &ox0,
+                                                  int &oy0, int &img0) {
+    if (P.batched) {
+        ox0 = blk * P.bx;
+        oy0 = 0;
+        img0 = grp;
+    } else {
+        const int xt = blk % P.tiles_x;
+        const int rest = blk / P.tiles_x;
+        const int yt = rest % P.tiles_y;
+        const int ig = rest / P.tiles_y;
+        ox0 = xt * P.bx;
+        oy0 = yt * P.by;
+        img0 = ig * P.imgs;
+    }
+}
+
+template <int BN, int KIND>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 ? 384 : 256, 1)
+    igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
+                      const __grid_constant__ CUtensorMap tm_w) {
+    constexpr bool SPLIT = KIND == KIND_3XTF32;
+    constexpr int HB = BN / 2;                        // filter rows staged per CTA
+    constexpr int A_BYTES = 128 * 128;
+    constexpr int B_BYTES = HB * 128;
+    constexpr int STAGE = (A_BYTES + B_BYTES) * (SPLIT ? 2 : 1);
+    constexpr int CB = KIND == KIND_BF16 ? 64 : 32;
+    constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    const IgemmParams &P = PP.g;
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int NS = P.stages;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint64_t *empty = full + NS;
+    uint64_t *conv = empty + NS;
+    uint64_t *tfull = conv + NS;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int cluster_id = blockIdx.x >> 1;
+    const int nclusters = gridDim.x >> 1;
+    const uint64_t map_x = reinterpret_cast<uint64_t>(&tm_x);
+    const uint64_t map_w = reinterpret_cast<uint64_t>(&tm_w);
+
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+            mbar_init(conv + s, 8);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(tfull + a, 1);
+            mbar_init(tempty + a, 8);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_w));
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    // work item -> (group, pair, n-block); n fastest
+    auto decode = [&](int item, int &grp, int &pair, int &nb) {
+        nb = item % PP.nblocks;
+        const int rest = item / PP.nblocks;
+        pair = rest % PP.pairs_per_group;
+        grp = rest / PP.pairs_per_group;
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer (both CTAs) -------------------------------------------
+            const uint32_t a_rows_bytes = (uint32_t)(P.bx * P.by * P.imgs * 128);
+            const uint32_t cta_bytes = a_rows_bytes + B_BYTES;
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int item = cluster_id; item < PP.items; item += nclusters) {
+                int grp, pair, nb;
+                decode(item, grp, pair, nb);
+                int ox0, oy0, img0;
+                pair_block_origin(P, grp, pair * 2 + (int)rank, ox0, oy0, img0);
+                const int n0 = nb * BN + (int)rank * HB;
+                int tap = 0, cb = 0;
+                for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+                    if (it >= NS) mbar_wait(empty + s, ph ^ 1);
+                    const int r = tap / P.ks, sx = tap - r * P.ks;
+                    uint8_t *a = smem + s * STAGE;
+                    uint8_t *b = a + A_BYTES;
+                    const int xc = ox0 * P.stride + sx - P.pad, yc = oy0 * P.stride + r - P.pad;
+                    const int wc = P.batched ? img0 : tap;
+                    if constexpr (SPLIT) {   // own barrier: the converters need a local signal
+                        mbar_arrive_expect_tx(full + s, cta_bytes);
+                        tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
+                        tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
+                    } else {                 // both CTAs' bytes complete on the leader's barrier
+                        if (leader) mbar_arrive_expect_tx(full + s, 2 * cta_bytes);
+                        tma_load_4d_pair(a, map_x, cb * CB, xc, yc, img0, full + s);
+                        tma_load_3d_pair(b, map_w, cb * CB, n0, wc, full + s);
+                    }
+                    if (++cb == P.cblocks) {
+                        cb = 0;
+                        ++tap;
+                    }
+                    if (++s == NS) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ---- MMA issuer (leader CTA, one thread) -----------------------------------
+            constexpr uint32_t idesc = idesc_m256<BN, KIND>();
+            int s = 0;
+            uint32_t ph = 0;
+            int t = 0;
+            for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
+                const int acc = t & 1;
+                if (t >= 2) mbar_wait_cluster(tempty + acc, ((t >> 1) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                const uint32_t d = tmem + (uint32_t)(acc * BN);
+                for (int kb = 0; kb < P.kblocks; ++kb) {
+                    if constexpr (SPLIT) mbar_wait_cluster(conv + s, ph);
+                    else mbar_wait(full + s, ph);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t a = smem_u32(smem + s * STAGE);
+                    const uint32_t b = a + A_BYTES;
+                    const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(b);
+                    if constexpr (SPLIT) {
+                        const uint64_t adl = umma_desc_sw128(a + A_BYTES + B_BYTES);
+                        const uint64_t bdl = umma_desc_sw128(b + A_BYTES + B_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t o = (uint64_t)(kk * 2);
+                            umma_pair<KIND>(d, ad + o, bdl + o, idesc, (kb | kk) != 0);
+                            umma_pair<KIND>(d, adl + o, bd + o, idesc, 1);
+                            umma_pair<KIND>(d, ad + o, bd + o, idesc, 1);
+                        }
+                    } else {
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk)
+                            umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                                            (kb | kk) != 0);
+                    }
+                    umma_commit_pair(empty + s);
+                    if (++s == NS) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                umma_commit_pair(tfull + acc);
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---- epilogue: TMEM -> registers -> NHWC global, both CTAs ------------------
+        const int q = warp - 4;                       // TMEM lane quadrant
+        const int m = q * 32 + lane;                  // pixel row of this CTA's A block
+        const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+        int t = 0;
+        for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
+            int grp, pair, nb;
+            decode(item, grp, pair, nb);
+            const int acc = t & 1;
+            mbar_wait(tfull + acc, (t >> 1) & 1);
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int blk = pair * 2 + (int)rank;
+            int ox0, oy0, img0;
+            pair_block_origin(P, grp, blk, ox0, oy0, img0);
+            const int per_img = P.bx * P.by;
+            const int im = m / per_img, pix = m - im * per_img;
+            const int py = pix / P.bx, px = pix - py * P.bx;
+            const int img = img0 + im, oy = oy0 + py, ox = ox0 + px;
+            const bool valid = blk < PP.blocks_per_group && m < per_img * P.imgs && img < P.n &&
+                               oy < P.p && ox < P.q;
+            const int k0 = nb * BN;
+            float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                float v[32];
+                tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                if (valid) {
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4) {
+                        float4 o;
+                        o.x = v[j] + (P.bias ? __ldg(P.bias + k0 + c0 + j) : 0.0f);
+                        o.y = v[j + 1] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 1) : 0.0f);
+                        o.z = v[j + 2] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 2) : 0.0f);
+                        o.w = v[j + 3] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 3) : 0.0f);
+                        if (P.relu) {
+                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
+                            o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
+                        }
+                        *reinterpret_cast<float4 *>(dst + c0 + j) = o;
+                    }
+                }
+            }
+            // accumulator buffer drained: tell the leader's MMA issuer
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
+        }
+    } else if (SPLIT && warp >= 8) {
+        // ---- converters: lo = v - tf32(v) of this CTA's stage (3xTF32) -------------
+        const int ct = tid - 256;                    // 0..127
+        constexpr int PER = (A_BYTES + B_BYTES) / 16 / 128;
+        const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int item = cluster_id; item < PP.items; item += nclusters) {
+            for (int kb = 0; kb < P.kblocks; ++kb) {
+                mbar_wait(full + s, ph);
+                const uint32_t hi_s = smem_u32(smem + s * STAGE) + ct * 16;
+                const uint32_t lo_s = hi_s + A_BYTES + B_BYTES;
+                float4 v[PER];
+#pragma unroll
+                for (int j = 0; j < PER; ++j) v[j] = lds128(hi_s + j * 128 * 16);
+#pragma unroll
+                for (int j = 0; j < PER; ++j) {
+                    float4 l;
+                    l.x = v[j].x - __uint_as_float(__float_as_uint(v[j].x) & 0xffffe000u);
+                    l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
+                    l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
+                    l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
+                    sts128_tf32(lo_s + j * 128 * 16, l);
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(conv_leader + (uint32_t)(s * 8));
+                if (++s == NS) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    }
+    // ---- teardown ---------------------------------------------------------------------
+    __syncwarp();   // role lanes rejoin their warps before the .aligned cluster barrier
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync_all();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+}  // namespace convio

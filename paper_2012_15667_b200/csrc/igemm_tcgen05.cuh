@@ -342,9 +342,15 @@ __global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
 // ---- host-side plan (igemm.cu) -------------------------------------------------
 using IgemmFn = void (*)(const IgemmParams, const CUtensorMap, const CUtensorMap);
 
+struct PairParams;   // igemm_pair.cuh
+using PairFn = void (*)(const PairParams, const CUtensorMap, const CUtensorMap);
+
 struct IgemmPlan {
     IgemmParams P;
     IgemmFn fn = nullptr;
+    bool pair = false;       // persistent CTA-pair kernel (igemm_pair.cuh)
+    PairFn pfn = nullptr;
+    int groups = 1, blocks_per_group = 0;
     dim3 grid;
     size_t smem = 0;
     int regs = 0;
@@ -354,8 +360,8 @@ struct IgemmPlan {
 };
 
 // M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c] (Winograd step 3) in one launch
-int plan_igemm_batched(int kind, int bn, int s_b, int xi, int t_count, int c, int k, IgemmPlan *pl,
-                       char *reason, size_t rlen);
+int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count, int c, int k,
+                       IgemmPlan *pl, char *reason, size_t rlen);
 int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
                  cudaStream_t stream);
 

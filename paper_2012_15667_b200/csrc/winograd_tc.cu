@@ -241,6 +241,7 @@ static constexpr size_t kChunkL2Bytes = 56ull << 20;
 struct WinoTcPlan {
     WinoTcGeom g;
     int e, m, kind, bn, s_b;
+    bool pair;
     int chunk_imgs;
     size_t u_bytes, v_bytes, m_bytes;   // per chunk for V and M
 };
@@ -270,8 +271,12 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     if (p < 1 || q < 1) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
     const int cb = kind == KIND_BF16 ? 64 : 32;
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
-    int bn = t ? t->z : (d->k % 128 == 0 ? 128 : 64);
+    int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));
     int s_b = t ? t->s_b : 16384;
+    const bool pair = t ? t->n_zt == 2 : true;
+    if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2)))
+        return fail(CONVIO_EINFEASIBLE,
+                    "tcgen05 Winograd tiles take n_xt = n_yt = 1 and n_zt in {1, 2 (CTA pair)}");
     if (t && t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
     if (t && t->e != e) return fail(CONVIO_EINVAL, "tile e=%d differs from e=%d", t->e, e);
     if (bn != 64 && bn != 128 && bn != 256)
@@ -290,7 +295,7 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     // keep the GEMM's T axis within the TMA box-coordinate / grid limits
     while (chunk > 1 && (size_t)chunk * tpi > (size_t)1 << 24) chunk /= 2;
     if ((size_t)chunk * tpi >= ((size_t)1 << 31)) return fail(CONVIO_EINFEASIBLE, "too many tiles");
-    pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b;
+    pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b; pl->pair = pair;
     pl->chunk_imgs = chunk;
     pl->u_bytes = al256((size_t)m * m * d->k * d->c * es);
     pl->v_bytes = al256((size_t)m * m * chunk * tpi * d->c * es);
@@ -326,7 +331,7 @@ int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t preci
     if (rc) return rc;
     IgemmPlan gp;
     const int tc = pl.chunk_imgs * pl.g.tiles_y * pl.g.tiles_x;
-    rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.m * pl.m, tc, d->c, d->k, &gp, out->reason,
+    rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, d->c, d->k, &gp, out->reason,
                             sizeof(out->reason));
     if (rc) return rc;
     out->legal = 1;
@@ -429,7 +434,7 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
         IgemmPlan gp;
-        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.m * pl.m, tc, g.c, g.k, &gp, why, sizeof(why));
+        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, g.c, g.k, &gp, why, sizeof(why));
         if (rc) return rc;
         rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);
         if (rc) return rc;

@@ -81,8 +81,22 @@ def expand(layers: list[LayerSpec]) -> list[LayerSpec]:
 # Algorithms whose results meet the FP32 tolerance (1e-5 normwise vs the float64
 # oracle; Winograd F(e,3) is looser by construction, 1e-4 / 1e-3) -- the
 # headline plan picks among these; "igemm_tf32" is the reduced-precision variant.
-FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32")
+FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32")
 CUDA_CORE_ALGORITHMS = ("direct", "winograd")
+
+
+def candidate_algorithm(key: str) -> tuple[str, int | None]:
+    """Tuned-candidate key -> (algorithm, e): ``direct`` / ``direct_nhwc`` (FFMA
+    direct, NCHW register micro-tiles / channels-last stacked pixels), ``winograd2|4`` (FFMA
+    Winograd), ``winograd_tc_<prec>_e2|4`` (tensor-core Winograd), ``igemm_<prec>``."""
+    if key.startswith("winograd_tc_"):
+        prec, _, e = key[len("winograd_tc_"):].partition("_e")
+        return f"winograd_tc_{prec}", int(e)
+    if key.startswith("winograd"):
+        return "winograd", int(key[len("winograd"):])
+    if key == "direct_nhwc":   # the channels-last FFMA direct kernel (an HWC "direct" tile)
+        return "direct", None
+    return key, None
 
 
 def load_plans(workload: str, allowed=FP32_ALGORITHMS) -> dict:
@@ -99,14 +113,12 @@ def load_plans(workload: str, allowed=FP32_ALGORITHMS) -> dict:
     for name, entry in raw.get("layers", {}).items():
         best, best_t = None, float("inf")
         for key, cand in entry.get("candidates", {}).items():
-            alg = ("direct" if key == "direct" else "winograd" if key.startswith("winograd")
-                   else key)
+            alg, e = candidate_algorithm(key)
             tuned = cand.get("tuner") or {}
             t = tuned.get("seconds")
             if alg not in allowed or t is None or not tuned.get("best"):
                 continue
             if t < best_t:
-                e = int(key[len("winograd"):]) if key.startswith("winograd") else None
                 best, best_t = {"algorithm": alg, "tile": TileConfig(**tuned["best"]), "e": e}, t
         if best is None and entry.get("algorithm") in allowed and entry.get("tile"):
             best = {"algorithm": entry["algorithm"], "tile": TileConfig(**entry["tile"]),
@@ -125,12 +137,21 @@ class ConvLayer:
         plan = plan or {}
         self.algorithm = plan.get("algorithm", "direct")
         self.tile = plan.get("tile")
-        self.e = plan.get("e") or 2
-        if self.algorithm == "winograd" and (spec.stride != 1 or spec.r != 3):
+        self.e = plan.get("e") or (self.tile.e if self.tile is not None and self.tile.e else 2)
+        if self.algorithm.startswith("winograd") and (spec.stride != 1 or spec.r != 3):
             self.algorithm = "direct"
             self.tile = None
         self._ws = None
+        self._run_ws = None
         self.launches = 0
+
+    @property
+    def precision(self) -> str | None:
+        """Operand precision of a tensor-core plan (tf32 / 3xtf32 / bf16), else None."""
+        for prefix in ("igemm_", "winograd_tc_"):
+            if self.algorithm.startswith(prefix):
+                return self.algorithm[len(prefix):]
+        return None
 
     @property
     def layout(self) -> str:
@@ -139,7 +160,7 @@ class ConvLayer:
 
     def filter_elems(self) -> int:
         s = self.spec
-        if self.algorithm == "winograd":
+        if self.algorithm.startswith("winograd"):
             m = self.e + s.r - 1
             return m * m * s.c * s.k
         return s.k * s.c * s.r * s.r
@@ -149,12 +170,22 @@ class ConvLayer:
         import ctypes
         from . import _native as N
         s = self.spec
-        if self._ws is None or self._ws.device != torch.device(device):
-            self._ws = torch.empty(self.filter_elems(), device=device, dtype=torch.float32)
+        prec = self.precision
+        dtype = torch.bfloat16 if prec == "bf16" else torch.float32
+        if self._ws is None or self._ws.device != torch.device(device) or self._ws.dtype != dtype:
+            self._ws = torch.empty(self.filter_elems(), device=device, dtype=dtype)
         w = self.weight
-        desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 0)
+        desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0,
+                           2 if prec else 0)
         sp = C._stream_ptr(stream)
-        if self.algorithm == "winograd":
+        if self.algorithm.startswith("winograd_tc"):
+            rc = N.lib().convio_winograd_filter_transform_tc(ctypes.byref(desc), self.e,
+                                                             N.PRECISIONS[prec], C._ptr(w),
+                                                             C._ptr(self._ws), sp)
+        elif self.algorithm == "igemm_bf16":
+            rc = N.lib().convio_pack_filter_igemm_bf16(ctypes.byref(desc), C._ptr(w),
+                                                       C._ptr(self._ws), sp)
+        elif self.algorithm == "winograd":
             rc = N.lib().convio_winograd_filter_transform(ctypes.byref(desc), self.e,
                                                           C._ptr(w), C._ptr(self._ws), sp)
         elif self.algorithm.startswith("igemm"):
@@ -168,7 +199,23 @@ class ConvLayer:
     def run(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """The conv kernel alone, on the prepared filter."""
         s = self.spec
-        if self.algorithm == "winograd":
+        if self.algorithm.startswith("winograd_tc"):
+            if self._run_ws is None or self._run_ws.device != x.device:
+                info = C.query(tuple(x.shape), tuple(self.weight.shape), 1, s.pad, "HWC",
+                               self.tile, self.algorithm)
+                self._run_ws = torch.empty(max(1, info["workspace_bytes"]), device=x.device,
+                                           dtype=torch.uint8)
+            y = C.conv_winograd_tc(x, self.weight, e=self.e, padding=s.pad, tile=self.tile,
+                                   precision=self.precision, out=out, stream=stream,
+                                   u=self._ws, workspace=self._run_ws)
+        elif self.algorithm == "igemm_bf16":
+            if self._run_ws is None or self._run_ws.device != x.device:
+                self._run_ws = torch.empty(2 * x.numel() + (1 << 20), device=x.device,
+                                           dtype=torch.uint8)
+            y = C.conv_igemm(x, self.weight, padding=s.pad, stride=s.stride, tile=self.tile,
+                             precision="bf16", out=out, stream=stream, w_packed=self._ws,
+                             workspace=self._run_ws)
+        elif self.algorithm == "winograd":
             u = self._ws.view(-1)
             y = C.conv_winograd(x, self.weight, e=self.e, padding=s.pad, tile=self.tile, out=out,
                                 stream=stream, u=u)

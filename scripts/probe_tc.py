@@ -39,7 +39,7 @@ def timeit(fn, reps=10, warm=3):
     return a.elapsed_time(b) / 1e3 / reps
 
 
-def igemm_tile(spec, z):
+def igemm_tile(spec, z, nzt=1):
     o = spec.out_hw
     # largest x*y <= 128 block with x | Q, y | P, preferring full rows
     best = None
@@ -53,7 +53,7 @@ def igemm_tile(spec, z):
             if best is None or key > best[0]:
                 best = (key, x, y)
     _, x, y = best
-    return TileConfig(x, y, z, 32768, 1, 1, 1, layout="HWC")
+    return TileConfig(x, y, z, 32768, 1, 1, nzt, layout="HWC")
 
 
 def build(spec, kind, n, x, w, wcache):
@@ -62,9 +62,10 @@ def build(spec, kind, n, x, w, wcache):
     if alg.startswith("igemm_"):
         prec = alg[len("igemm_"):]
         z = int(rest[0]) if rest else 128
+        nzt = int(rest[1]) if len(rest) > 1 else 2
         if spec.k % z:
             return None
-        tile = igemm_tile(spec, z)
+        tile = igemm_tile(spec, z, nzt)
         key = ("ig", prec == "bf16")
         if key not in wcache:
             wcache[key] = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
@@ -80,13 +81,14 @@ def build(spec, kind, n, x, w, wcache):
         prec = alg[len("winograd_tc_"):]
         e = int(rest[0]) if rest else 4
         z = int(rest[1]) if len(rest) > 1 else 128
+        nzt = int(rest[2]) if len(rest) > 2 else 2
         if spec.k % z:
             return None
         key = ("wtc", prec, e)
         if key not in wcache:
             wcache[key] = C.winograd_filter_transform_tc(w, e, prec)
         u = wcache[key]
-        tile = TileConfig(e, e, z, 16384, 1, 1, 1, layout="HWC", e=e)
+        tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
         out = C.empty_act(n, spec.k, spec.out_hw, spec.out_hw, "HWC", device="cuda")
         info = C.query(x.shape, w.shape, 1, 1, "HWC", tile, "winograd_tc_" + prec)
         if info["rc"]:
@@ -95,6 +97,17 @@ def build(spec, kind, n, x, w, wcache):
         ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
         return lambda: C.conv_winograd_tc(x, w, e=e, padding=1, tile=tile, precision=prec, u=u,
                                           out=out, workspace=ws)
+    if alg == "direct_nhwc":
+        z = int(rest[0]) if rest else 128
+        if spec.k % z or spec.c % 32:
+            return None
+        t = igemm_tile(spec, z)
+        tile = TileConfig(t.x, t.y, z, 32768, 1, 1, 1, layout="HWC")
+        if "dwp" not in wcache:
+            wcache["dwp"] = C.pack_filter_direct(w)
+        out = C.empty_act(n, spec.k, spec.out_hw, spec.out_hw, "HWC", device="cuda")
+        return lambda: C.conv_direct(x, w, stride=spec.stride, padding=1, tile=tile,
+                                     w_packed=wcache["dwp"], out=out)
     if alg.startswith("cudnn"):
         tf32 = alg == "cudnn_tf32"
         xc = x.contiguous(memory_format=torch.channels_last)
@@ -144,7 +157,7 @@ def main():
             torch.cuda.synchronize()
             print("ran", args.one, spec.name)
             continue
-        ref = build(spec, "igemm_3xtf32:128" if spec.k % 128 == 0 else "igemm_3xtf32:64",
+        ref = build(spec, "igemm_3xtf32:128:1" if spec.k % 128 == 0 else "igemm_3xtf32:64:1",
                     args.n, x, w, wcache)().clone()
         flops = spec.flops(args.n)
         for kind in args.kinds.split(","):

@@ -33,7 +33,8 @@ from paper_2012_15667_b200.autotune import tune, exhaustive_oracle, random_searc
 from paper_2012_15667_b200.dataflow import optimal_tile_dc, optimal_tile_wa, InfeasibleTileError  # noqa: E402
 from paper_2012_15667_b200.device import b200_hw_model, shape_of  # noqa: E402
 from paper_2012_15667_b200.model import WinogradParams  # noqa: E402
-from paper_2012_15667_b200.runner import WORKLOADS, TUNED_DIR  # noqa: E402
+from paper_2012_15667_b200.runner import (WORKLOADS, TUNED_DIR, FP32_ALGORITHMS,  # noqa: E402
+                                           candidate_algorithm)
 
 
 def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
@@ -76,18 +77,21 @@ def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
     return out
 
 
-def tune_igemm(shape, spec, split, log):
-    """Tensor-core projection: small exhaustive device search over (x, y, z).
+def tune_igemm(shape, spec, prec, log):
+    """Tensor-core projection: small exhaustive device search over (x, y, z, kernel).
 
     The Table-1 prune is derived for the FFMA machine model (outputs in
-    registers); the tcgen05 kernel keeps outputs in TMEM, so its own small
-    space (x | Q, y | P, x*y <= 128, z in {64, 128[, 256]}) is searched whole.
+    registers); the tcgen05 kernels keep outputs in TMEM, so their own small
+    space (x | Q, y | P, 32 <= x*y <= 128, z in {64, 128, 256}, n_zt in
+    {1 (one CTA, s_b 16384 / 32768 ring), 2 (persistent CTA pair)}) is
+    searched whole.
     """
     import math as _m
     from paper_2012_15667_b200.dataflow import TileConfig
     from paper_2012_15667_b200 import conv as C
-    if spec.c % 32 or spec.stride > 2:
-        return {"error": "needs C % 32 == 0 and stride <= 2"}
+    cb = 64 if prec == "bf16" else 32
+    if spec.c % cb or spec.stride > 2:
+        return {"error": f"needs C % {cb} == 0 and stride <= 2"}
     q = shape.w_out
     p = shape.h_out
     zs = [z for z in (64, 128, 256) if spec.k % z == 0]
@@ -95,24 +99,105 @@ def tune_igemm(shape, spec, split, log):
     x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
     xh = C.to_layout(x, "HWC")
     w = torch.empty((spec.k, spec.c, spec.r, spec.r), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
-    wq = C.pack_filter_igemm(w)
+    wq = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
+    out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
+    ws = torch.empty(2 * xh.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
+    variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
     for bx in [d for d in range(1, q + 1) if q % d == 0]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
             if bx * by > 128 or bx * by < 32:
                 continue
-            for z, sb in [(z, sb) for z in zs for sb in (16384, 32768)]:
-                tile = TileConfig(bx, by, z, sb, 1, 1, 1, layout="HWC")
+            for z, sb, nzt in variants:
+                tile = TileConfig(bx, by, z, sb, 1, 1, nzt, layout="HWC")
                 try:
-                    t = DT.device_time(lambda: C.conv_igemm_tf32(xh, w, padding=spec.pad, tile=tile,
-                                                                  w_packed=wq, stride=spec.stride,
-                                                                  split=split))
+                    t = DT.device_time(lambda: C.conv_igemm(xh, w, padding=spec.pad, tile=tile,
+                                                             precision=prec, w_packed=wq,
+                                                             stride=spec.stride, out=out,
+                                                             workspace=ws))
                 except Exception:  # noqa: BLE001 -- illegal projection
                     continue
                 tried += 1
                 if t < best_t:
                     best, best_t = tile, t
-    key = "igemm_3xtf32" if split else "igemm_tf32"
-    log(f"    {key}: {tried} tiles, best {best} {best_t}")
+    log(f"    igemm_{prec}: {tried} tiles, best {best} {best_t}")
+    return {"tuner": {"best": best.to_dict() if best else None,
+                      "seconds": best_t if best else None, "measurements": tried},
+            "space": "exhaustive tcgen05 projection"}
+
+
+def tune_direct_nhwc(shape, spec, log):
+    """Channels-last FFMA direct kernel (stacked pixels): exhaustive device
+    search over its own space (x | Q, y | P, 32 <= x*y <= 128, z in {64, 128},
+    s_b in {16384, 32768}), threads = library layout (1, 1, 1).  Like the
+    tensor-core kernels it lies outside Table 1 (z^2 R <= s_b assumes the
+    paper's x*y ~ R*z block shape; this block is 128 stacked pixels x z)."""
+    import math as _m
+    from paper_2012_15667_b200.dataflow import TileConfig
+    from paper_2012_15667_b200 import conv as C
+    if spec.c % 32 or spec.stride > 2:
+        return {"error": "needs C % 32 == 0 and stride <= 2"}
+    q, p = shape.w_out, shape.h_out
+    x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
+    xh = C.to_layout(x, "HWC")
+    w = torch.empty((spec.k, spec.c, spec.r, spec.r), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
+    wp = C.pack_filter_direct(w)
+    out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
+    best, best_t, tried = None, _m.inf, 0
+    for bx in [d for d in range(1, q + 1) if q % d == 0]:
+        for by in [d for d in range(1, p + 1) if p % d == 0]:
+            if bx * by > 128 or bx * by < 32:
+                continue
+            for z in [z for z in (64, 128) if spec.k % z == 0]:
+                for sb in (16384, 32768):
+                    tile = TileConfig(bx, by, z, sb, 1, 1, 1, layout="HWC")
+                    try:
+                        t = DT.device_time(lambda: C.conv_direct(xh, w, stride=spec.stride,
+                                                                  padding=spec.pad, tile=tile,
+                                                                  w_packed=wp, out=out))
+                    except Exception:  # noqa: BLE001 -- illegal projection
+                        continue
+                    tried += 1
+                    if t < best_t:
+                        best, best_t = tile, t
+    log(f"    direct_nhwc: {tried} tiles, best {best} {best_t}")
+    return {"tuner": {"best": best.to_dict() if best else None,
+                      "seconds": best_t if best else None, "measurements": tried},
+            "space": "exhaustive channels-last FFMA projection"}
+
+
+def tune_winograd_tc(shape, spec, prec, e, log):
+    """Tensor-core Winograd: exhaustive over (z, n_zt); the GEMM's M tile is
+    fixed at 128 Winograd tiles per CTA (256 per pair)."""
+    import math as _m
+    from paper_2012_15667_b200.dataflow import TileConfig
+    from paper_2012_15667_b200 import conv as C
+    cb = 64 if prec == "bf16" else 32
+    if spec.c % cb or spec.stride != 1 or spec.r != 3:
+        return {"error": f"needs C % {cb} == 0, stride 1, 3x3"}
+    x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
+    xh = C.to_layout(x, "HWC")
+    w = torch.empty((spec.k, spec.c, 3, 3), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
+    u = C.winograd_filter_transform_tc(w, e, prec)
+    out = C.empty_act(shape.n, spec.k, shape.h_out, shape.w_out, "HWC", device="cuda")
+    best, best_t, tried = None, _m.inf, 0
+    for z in [z for z in (64, 128, 256) if spec.k % z == 0]:
+        for nzt in (1, 2):
+            tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
+            info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
+                           f"winograd_tc_{prec}")
+            if info["rc"]:
+                continue
+            ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
+            try:
+                t = DT.device_time(lambda: C.conv_winograd_tc(xh, w, e=e, padding=spec.pad, tile=tile,
+                                                               precision=prec, u=u, out=out,
+                                                               workspace=ws))
+            except Exception:  # noqa: BLE001
+                continue
+            tried += 1
+            if t < best_t:
+                best, best_t = tile, t
+    log(f"    winograd_tc_{prec}_e{e}: {tried} tiles, best {best} {best_t}")
     return {"tuner": {"best": best.to_dict() if best else None,
                       "seconds": best_t if best else None, "measurements": tried},
             "space": "exhaustive tcgen05 projection"}
@@ -125,7 +210,9 @@ def main():
     ap.add_argument("--budget", type=int, default=128)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--exhaustive-cap", type=int, default=0)
-    ap.add_argument("--algs", default="direct,winograd2,winograd4,igemm_3xtf32,igemm_tf32")
+    ap.add_argument("--algs", default="direct,direct_nhwc,winograd2,winograd4,igemm_3xtf32,igemm_tf32,"
+                    "igemm_bf16,winograd_tc_3xtf32_e2,winograd_tc_3xtf32_e4,"
+                    "winograd_tc_tf32_e4,winograd_tc_bf16_e4")
     ap.add_argument("--layers", default="")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -157,8 +244,14 @@ def main():
             if alg == "direct":
                 cands["direct"] = tune_one(shape, hw, "direct", None, args.budget, args.seed,
                                            args.exhaustive_cap, log)
+            elif alg == "direct_nhwc":
+                cands[alg] = tune_direct_nhwc(shape, spec, log)
             elif alg.startswith("igemm"):
-                cands[alg] = tune_igemm(shape, spec, alg == "igemm_3xtf32", log)
+                cands[alg] = tune_igemm(shape, spec, alg[len("igemm_"):], log)
+            elif alg.startswith("winograd_tc_"):
+                if spec.stride == 1 and spec.r == 3:
+                    prec, _, e = alg[len("winograd_tc_"):].partition("_e")
+                    cands[alg] = tune_winograd_tc(shape, spec, prec, int(e), log)
             elif alg.startswith("winograd") and spec.stride == 1 and spec.r == 3:
                 e = int(alg[len("winograd"):])
                 cands[alg] = tune_one(shape, hw, "winograd", WinogradParams(e, 3), args.budget,
@@ -166,7 +259,8 @@ def main():
         best_key, best_t = None, math.inf
         for key, c in cands.items():
             t = (c.get("tuner") or {}).get("seconds")
-            if key == "igemm_tf32":      # reduced precision: never the layer's FP32 plan
+            alg_k, _ = candidate_algorithm(key)
+            if alg_k not in FP32_ALGORITHMS:   # reduced precision: never the layer's FP32 plan
                 continue
             if t is not None and t < best_t:
                 best_key, best_t = key, t
@@ -175,9 +269,9 @@ def main():
             continue
         tile = cands[best_key]["tuner"]["best"]
         flops = spec.flops(args.n)
+        best_alg, best_e = candidate_algorithm(best_key)
         result["layers"][spec.name] = {
-            "algorithm": best_key if not best_key.startswith("winograd") else "winograd",
-            "e": int(best_key[len("winograd"):]) if best_key.startswith("winograd") else None,
+            "algorithm": best_alg, "e": best_e,
             "tile": tile, "seconds": best_t, "gflops_direct_equiv": round(flops / best_t / 1e9, 1),
             "candidates": cands,
         }

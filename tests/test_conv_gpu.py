@@ -214,6 +214,36 @@ def test_igemm_tcgen05_bf16_matches_oracle(case):
     assert torch.equal(y, y2)
 
 
+PAIR_CASES = [
+    # (n, c, h, w, k, stride, precision, tile) -- n_zt = 2: persistent CTA pair
+    (2, 64, 56, 56, 64, 1, "3xtf32", TileConfig(28, 4, 64, 32768, 1, 1, 2, layout="HWC")),
+    (3, 128, 14, 14, 256, 1, "3xtf32", TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC")),
+    (3, 64, 28, 28, 128, 2, "3xtf32", TileConfig(14, 7, 128, 32768, 1, 1, 2, layout="HWC")),
+    (5, 32, 7, 7, 64, 1, "tf32", TileConfig(7, 7, 64, 32768, 1, 1, 2, layout="HWC")),  # odd block count
+    (3, 128, 14, 14, 256, 1, "tf32", TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC")),
+    (4, 128, 28, 28, 256, 2, "bf16", TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC")),
+    (1, 64, 14, 14, 128, 1, "bf16", TileConfig(14, 2, 128, 32768, 1, 1, 2, layout="HWC")),  # 7 blocks
+]
+TOL_PREC = {"tf32": TOL_TF32, "bf16": TOL_BF16}
+
+
+@pytest.mark.parametrize("case", PAIR_CASES, ids=[str(i) for i in range(len(PAIR_CASES))])
+def test_igemm_cta_pair_matches_oracle_and_single_cta(case):
+    n, c, h, w, k, stride, prec, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile, precision=prec,
+                     bias=_dev(b))
+    ref = co.direct_conv(x, wt, stride, 1) + b[None, :, None, None]
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= TOL_PREC.get(prec, tol_fp32(c)), err
+    single = TileConfig(tile.x, tile.y, tile.z, tile.s_b, 1, 1, 1, layout="HWC")
+    y1 = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=single,
+                      precision=prec, bias=_dev(b))
+    # same products, same per-output summation order: identical up to MMA-internal order
+    assert co.rel_err(y.contiguous().cpu().numpy(), y1.contiguous().cpu().numpy()) <= 1e-5
+
+
 def test_igemm_generic_entry_matches_split_entry():
     x, wt = _inputs(2, 64, 28, 28, 64, 3, 3)
     tile = TileConfig(14, 4, 64, 16384, 1, 1, 1, layout="HWC")
@@ -255,7 +285,7 @@ def test_winograd_tc_matches_oracle(case):
     n, c, h, w, k, e, prec, z = case
     x, wt = _inputs(n, c, h, w, k, 3, 3)
     b = np.linspace(-0.25, 0.25, k).astype(np.float32)
-    tile = TileConfig(e, e, z, 16384, 1, 1, 1, layout="HWC", e=e)
+    tile = TileConfig(e, e, z, 16384, 1, 1, 2 if n % 2 else 1, layout="HWC", e=e)
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision=prec,
                            bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
@@ -299,3 +329,38 @@ def test_winograd_tc_chunks_the_batch_through_l2():
     assert co.rel_err(y[:2].contiguous().cpu().numpy(), ref) <= TOL_WINO[4]
     ref_last = co.direct_conv(x[-2:], wt, 1, 1)
     assert co.rel_err(y[-2:].contiguous().cpu().numpy(), ref_last) <= TOL_WINO[4]
+
+
+# ---- channels-last FP32 direct kernel (stacked pixels, TMA ring) -----------------
+NHWC_CASES = [
+    # (n, c, h, w, k, stride, tile) -- n_xt*n_yt = 16, n_zt = 16, z in {64, 128}
+    (2, 64, 56, 56, 64, 1, TileConfig(28, 4, 64, 32768, 4, 4, 16, layout="HWC")),
+    (2, 64, 56, 56, 128, 1, TileConfig(56, 2, 128, 32768, 8, 2, 16, layout="HWC")),
+    (3, 128, 14, 14, 128, 1, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
+    (5, 64, 7, 7, 64, 1, TileConfig(7, 7, 64, 16384, 1, 1, 1, layout="HWC")),   # 2 images / block
+    (2, 128, 28, 28, 128, 2, TileConfig(14, 7, 128, 32768, 1, 1, 1, layout="HWC")),
+    (2, 32, 16, 16, 64, 1, TileConfig(16, 8, 64, 16384, 4, 4, 16, layout="HWC")),
+    (3, 256, 7, 7, 128, 1, TileConfig(7, 7, 128, 32768, 1, 1, 1, layout="HWC")),   # library threads
+    (3, 64, 14, 14, 64, 2, TileConfig(7, 7, 64, 32768, 1, 1, 1, layout="HWC")),
+]
+
+
+@pytest.mark.parametrize("case", NHWC_CASES, ids=[str(i) for i in range(len(NHWC_CASES))])
+def test_direct_nhwc_matches_oracle(case):
+    n, c, h, w, k, stride, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.5, 0.5, k).astype(np.float32)
+    info = C.query(x.shape, wt.shape, stride, 1, "HWC", tile)
+    assert info["rc"] == 0 and "channels-last" in info["reason"], info
+    y = C.conv_direct(_dev(x, "HWC"), _dev(wt), stride=stride, padding=1, tile=tile, bias=_dev(b),
+                      relu=True)
+    assert C.infer_layout(y) == "HWC"
+    ref = np.maximum(co.direct_conv(x, wt, stride, 1) + b[None, :, None, None], 0)
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= tol_fp32(c)
+
+
+def test_direct_nhwc_illegal_tiles():
+    x, wt = _inputs(1, 48, 14, 14, 64, 3, 3)   # C not a multiple of 32
+    with pytest.raises(InfeasibleTileError):
+        C.conv_direct(_dev(x, "HWC"), _dev(wt), padding=1,
+                      tile=TileConfig(14, 7, 64, 32768, 1, 1, 1, layout="HWC"))
