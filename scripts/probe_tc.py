@@ -49,7 +49,8 @@ def igemm_tile(spec, z, nzt=1):
         for y in range(1, o + 1):
             if o % y or x * y > 128:
                 continue
-            key = (x * y, x)
+            rows = (128 // (x * y)) * x * y      # images stacked to fill the 128-row tile
+            key = (rows, x * y, x)
             if best is None or key > best[0]:
                 best = (key, x, y)
     _, x, y = best

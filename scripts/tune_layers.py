@@ -77,6 +77,14 @@ def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
     return out
 
 
+def block_ok(bx, by, n):
+    """Pixel blocks of the stacked-pixel kernels: x*y <= 128 rows, and either
+    >= 32 pixels per image or a divisor of 128 (then 128/(x*y) images fill
+    every row: 2x2 blocks x 32 images on 14x14 maps, 1x1 x 128 on 7x7)."""
+    px = bx * by
+    return px <= 128 and (px >= 32 or (128 % px == 0 and n * px >= 128))
+
+
 def tune_igemm(shape, spec, prec, log):
     """Tensor-core projection: small exhaustive device search over (x, y, z, kernel).
 
@@ -105,7 +113,7 @@ def tune_igemm(shape, spec, prec, log):
     variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
     for bx in [d for d in range(1, q + 1) if q % d == 0]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
-            if bx * by > 128 or bx * by < 32:
+            if not block_ok(bx, by, shape.n):
                 continue
             for z, sb, nzt in variants:
                 tile = TileConfig(bx, by, z, sb, 1, 1, nzt, layout="HWC")
@@ -145,7 +153,7 @@ def tune_direct_nhwc(shape, spec, log):
     best, best_t, tried = None, _m.inf, 0
     for bx in [d for d in range(1, q + 1) if q % d == 0]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
-            if bx * by > 128 or bx * by < 32:
+            if not block_ok(bx, by, shape.n):
                 continue
             for z in [z for z in (64, 128) if spec.k % z == 0]:
                 for sb in (16384, 32768):
