@@ -28,20 +28,25 @@ static IgemmFn igemm_kernel(int bn, int kind) {
     return igemm_kernel_kind<KIND_TF32>(bn);
 }
 
-template <int KIND>
+template <int KIND, bool HALO>
 static PairFn pair_kernel_kind(int bn) {
     switch (bn) {
-        case 64: return &igemm_pair_kernel<64, KIND>;
-        case 128: return &igemm_pair_kernel<128, KIND>;
-        case 256: return &igemm_pair_kernel<256, KIND>;
+        case 64: return &igemm_pair_kernel<64, KIND, HALO>;
+        case 128: return &igemm_pair_kernel<128, KIND, HALO>;
+        case 256: return &igemm_pair_kernel<256, KIND, HALO>;
         default: return nullptr;
     }
 }
 
-static PairFn pair_kernel(int bn, int kind) {
-    if (kind == KIND_3XTF32) return pair_kernel_kind<KIND_3XTF32>(bn);
-    if (kind == KIND_BF16) return pair_kernel_kind<KIND_BF16>(bn);
-    return pair_kernel_kind<KIND_TF32>(bn);
+template <bool HALO>
+static PairFn pair_kernel_h(int bn, int kind) {
+    if (kind == KIND_3XTF32) return pair_kernel_kind<KIND_3XTF32, HALO>(bn);
+    if (kind == KIND_BF16) return pair_kernel_kind<KIND_BF16, HALO>(bn);
+    return pair_kernel_kind<KIND_TF32, HALO>(bn);
+}
+
+static PairFn pair_kernel(int bn, int kind, bool halo) {
+    return halo ? pair_kernel_h<true>(bn, kind) : pair_kernel_h<false>(bn, kind);
 }
 
 static const char *kind_name(int kind) {
@@ -105,20 +110,25 @@ static int pfail(char *reason, size_t rlen, int code, const char *fmt, ...) {
 static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *reason, size_t rlen) {
     if (pair) {
         // persistent pair: one CTA per SM, the whole shared memory is the ring
-        PairFn pfn = pair_kernel(bn, kind);
+        // (halo: two footprint slots first, the filter stages in the rest)
+        PairFn pfn = pair_kernel(bn, kind, pl->halo);
         if (!pfn)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
-        const size_t stage_bytes = (size_t)(128 * 128 + (bn / 2) * 128) * (kind == KIND_3XTF32 ? 2 : 1);
+        const int mult = kind == KIND_3XTF32 ? 2 : 1;
+        const size_t stage_bytes = (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) * mult;
+        const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : 0;
         const size_t budget = 227 * 1024 - 1024 - 512;
-        int stages = (int)std::min<size_t>(8, budget / stage_bytes);
+        if (a_ring + 2 * stage_bytes > budget)
+            return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
+        int stages = (int)std::min<size_t>(8, (budget - a_ring) / stage_bytes);
         if (stages < 2)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair ring does not fit");
         pl->P.stages = stages;
         pl->pair = true;
         pl->pfn = pfn;
         pl->fn = nullptr;
-        pl->smem = stages * stage_bytes + 1024 + 512;
+        pl->smem = a_ring + stages * stage_bytes + 1024 + 512;
         pl->bn = bn;
         pl->kind = kind;
         pl->threads = kind == KIND_3XTF32 ? 384 : 256;
@@ -165,6 +175,47 @@ static int finish_pair_grid(IgemmPlan *pl) {
     return CONVIO_OK;
 }
 
+// Halo staging (tile n_xt = 2, CTA pair n_zt = 2, stride 1): a block is y rows
+// x fpr = x + S - 1 footprint columns (fpr % 8 == 0, fpr * y = 128 MMA rows,
+// x valid outputs per row); the (y + R - 1) x fpr footprint is staged once per
+// channel block and the taps are row offsets into it.  Ragged edges (Q % x,
+// P % y) are zero-filled by TMA and masked in the epilogue.
+static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
+                           size_t rlen, int kind, int p, int q) {
+    if (t->n_yt != 1 || t->n_zt != 2)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE,
+                     "halo-staged tcgen05 tiles take n_xt = 2, n_yt = 1, n_zt = 2 (CTA pair)");
+    if (d->stride != 1)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "halo staging needs stride 1");
+    const int fpr = t->x + d->s - 1;
+    if (fpr % 8 || fpr * t->y != 128)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE,
+                     "halo tile: (x + S - 1) = %d must be a multiple of 8 with (x + S - 1) * y = 128", fpr);
+    if (d->k % t->z)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "z=%d does not divide K=%d", t->z, d->k);
+    if (t->x > q + d->s - 1 || t->y > p + d->r - 1 || fpr > 256 || t->y + d->r - 1 > 256)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "halo tile larger than the output");
+    const int cb = kind == KIND_BF16 ? 64 : 32;
+    IgemmParams &P = pl->P;
+    memset(&P, 0, sizeof(P));
+    pl->halo = true;
+    pl->fpr = fpr;
+    const int fp_rows = (t->y + d->r - 1) * fpr;
+    pl->fp_bytes = fp_rows * 128;
+    pl->a_slot = ((fp_rows + d->s - 1) * 128 + 1023) & ~1023;
+    pl->na = 2;
+    int rc = plan_ring(pl, t->z, kind, t->s_b, true, reason, rlen);
+    if (rc) return rc;
+    P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
+    P.pad = d->pad; P.stride = 1; P.ks = d->r;
+    P.bx = t->x; P.by = t->y; P.imgs = 1;
+    P.tiles_x = (q + t->x - 1) / t->x; P.tiles_y = (p + t->y - 1) / t->y; P.img_groups = d->n;
+    P.cblocks = d->c / cb; P.kblocks = d->r * d->s * P.cblocks;
+    pl->groups = 1;
+    pl->blocks_per_group = P.tiles_x * P.tiles_y * P.img_groups;
+    return finish_pair_grid(pl);
+}
+
 static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
                       size_t rlen, int kind) {
     auto fail = [&](int code, const char *fmt, ...) {
@@ -191,6 +242,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d (one 128-B K block)", d->c, cb);
     if (t->x < 1 || t->y < 1 || t->z < 1 || t->s_b < 1)
         return fail(CONVIO_EINFEASIBLE, "tile fields must be >= 1");
+    if (t->n_xt == 2) return plan_igemm_halo(d, t, pl, reason, rlen, kind, p, q);
     if (q % t->x || p % t->y || d->k % t->z)
         return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
@@ -265,6 +317,11 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     // stride: box spans stride*(pixels) input positions, traversal stride picks every stride-th
     cuuint32_t xb[4] = {cb, (cuuint32_t)(P.bx * P.stride), (cuuint32_t)(P.by * P.stride),
                         (cuuint32_t)P.imgs};
+    if (pl.halo) {   // the block's whole input footprint: y + R - 1 rows of fpr pixels
+        xb[1] = (cuuint32_t)pl.fpr;
+        xb[2] = (cuuint32_t)(P.by + P.ks - 1);
+        xb[3] = 1;
+    }
     cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const int taps = P.batched ? P.n : P.ks * P.ks;
@@ -296,6 +353,10 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.pairs_per_group = (pl.blocks_per_group + 1) / 2;
         PP.nblocks = pl.P.k / pl.bn;
         PP.items = PP.groups * PP.pairs_per_group * PP.nblocks;
+        PP.fpr = pl.fpr;
+        PP.fp_bytes = pl.fp_bytes;
+        PP.a_slot = pl.a_slot;
+        PP.na = pl.na;
         pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
@@ -338,7 +399,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages",
-             kind_name(kind), pl.pair ? " CTA pair (persistent)" : "", pl.pair ? 256 : 128,
+             kind_name(kind), pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.pair ? " CTA pair (persistent)" : ""), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
     return CONVIO_OK;
 }

@@ -14,6 +14,15 @@
 //  * The TMEM accumulator is double-buffered (2 x BN columns): the epilogue
 //    warps drain tile i while the MMA issuer accumulates tile i+1.
 //
+// HALO variant (stride 1, tile n_xt = 2): instead of one tap-shifted A box per
+// (tap, channel block), the block's input footprint is staged once per channel
+// block in its own ring and the R*S taps are descriptor offsets into it (an
+// SW128 K-major operand may start at any 128-B row: the swizzle phase follows
+// the absolute smem address, see scripts/dev/umma_shift_selftest.cu), cutting
+// the A operand's L2 traffic by ~R*S / (1 + halo).  Each footprint row holds
+// fpr pixels of which fpr - S + 1 are valid outputs (the rest are wrap-around
+// rows, computed and never stored).
+//
 // Warp roles (per CTA):  warp 0 = TMA producer, warp 1 = MMA issuer (leader
 // CTA) + TMEM allocator, warps 4..7 = epilogue (TMEM lane quadrants 0..3),
 // warps 8..11 = 3xTF32 converters (KIND_3XTF32 only).
@@ -38,6 +47,15 @@ struct PairParams {
     int pairs_per_group;    // ceil(blocks_per_group / 2)
     int nblocks;            // K / BN
     int items;              // groups * pairs_per_group * nblocks
+    // halo staging (HALO kernels): the (y + R - 1) x fpr input footprint of a
+    // 128-row block is staged ONCE per channel block; tap (r, s) is the view
+    // starting (r * fpr + s) rows into it (rows = y x fpr pixels, x = fpr - S + 1
+    // of each footprint row valid).  fp_bytes = footprint box bytes per CTA,
+    // a_slot = its smem slot (rounded to 1 KB, + S - 1 overrun rows).
+    int fpr;
+    int fp_bytes;
+    int a_slot;
+    int na;                 // footprint slots
 };
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -150,7 +168,42 @@ __device__ __forceinline__ void pair_block_origin(const IgemmParams &P, int grp,
     }
 }
 
-template <int BN, int KIND>
+// lo = v - tf32(v) (rounded to TF32) of n16 16-byte vectors, 128 threads,
+// explicit shared-window addressing; loads batched so their latencies overlap
+__device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n16, int ct) {
+    int i = ct;
+    for (; i + 3 * 128 < n16; i += 4 * 128) {
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = lds128(hi + (uint32_t)(i + j * 128) * 16);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float4 l;
+            l.x = v[j].x - __uint_as_float(__float_as_uint(v[j].x) & 0xffffe000u);
+            l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
+            l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
+            l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
+            sts128_tf32(lo + (uint32_t)(i + j * 128) * 16, l);
+        }
+    }
+    for (; i < n16; i += 128) {
+        const float4 v = lds128(hi + (uint32_t)i * 16);
+        float4 l;
+        l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
+        l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u);
+        l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u);
+        l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u);
+        sts128_tf32(lo + (uint32_t)i * 16, l);
+    }
+}
+
+// K-major SW128 descriptor of an operand starting at any 128-B row of a
+// 1 KB-aligned tile (base offset = the row's phase in the 8-row swizzle atom)
+__device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) {
+    return umma_desc_sw128(addr) | ((uint64_t)((addr >> 7) & 7) << 49);
+}
+
+template <int BN, int KIND, bool HALO>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 ? 384 : 256, 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
@@ -158,20 +211,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
     constexpr int HB = BN / 2;                        // filter rows staged per CTA
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = HB * 128;
-    constexpr int STAGE = (A_BYTES + B_BYTES) * (SPLIT ? 2 : 1);
+    constexpr int MULT = SPLIT ? 2 : 1;               // hi (raw) + lo copies
     constexpr int CB = KIND == KIND_BF16 ? 64 : 32;
     constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
     const IgemmParams &P = PP.g;
+    // stage layout: non-halo [A | B] (+ lo copy);  halo: A footprint slots, then B stages
+    const int STAGE = HALO ? B_BYTES * MULT : (A_BYTES + B_BYTES) * MULT;
+    const int ASLOT = HALO ? PP.a_slot * MULT : 0;
+    const int NA = HALO ? PP.na : 0;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int NS = P.stages;
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + NS * STAGE);
+    uint8_t *aring = smem;                            // halo footprint slots
+    uint8_t *bring = smem + NA * ASLOT;               // stages
+    uint64_t *full = reinterpret_cast<uint64_t *>(bring + NS * STAGE);
     uint64_t *empty = full + NS;
     uint64_t *conv = empty + NS;
     uint64_t *tfull = conv + NS;
     uint64_t *tempty = tfull + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    uint64_t *afull = tempty + 2;                     // halo: footprint slot barriers
+    uint64_t *aempty = afull + 2;
+    uint64_t *aconv = aempty + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(aconv + 2);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -191,6 +253,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 8);
+            mbar_init(afull + a, 1);
+            mbar_init(aempty + a, 1);
+            mbar_init(aconv + a, 8);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
@@ -214,15 +279,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
         pair = rest % PP.pairs_per_group;
         grp = rest / PP.pairs_per_group;
     };
+    const int taps = P.ks * P.ks;
 
     if (warp == 0) {
         if (lane == 0) {
             // ---- TMA producer (both CTAs) -------------------------------------------
             const uint32_t a_rows_bytes = (uint32_t)(P.bx * P.by * P.imgs * 128);
-            const uint32_t cta_bytes = a_rows_bytes + B_BYTES;
-            int s = 0;
-            uint32_t ph = 0;
-            int it = 0;
+            const uint32_t cta_bytes = HALO ? (uint32_t)B_BYTES : a_rows_bytes + B_BYTES;
+            int s = 0, sa = 0;
+            uint32_t ph = 0, pha = 0;
+            int it = 0, ita = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters) {
                 int grp, pair, nb;
                 decode(item, grp, pair, nb);
@@ -231,22 +297,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
                 const int n0 = nb * BN + (int)rank * HB;
                 int tap = 0, cb = 0;
                 for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+                    if (HALO && tap == 0) {
+                        // the block's input footprint for channel block cb, once
+                        if (ita >= NA) mbar_wait(aempty + sa, pha ^ 1);
+                        uint8_t *fa = aring + sa * ASLOT;
+                        const int xc = ox0 - P.pad, yc = oy0 - P.pad;
+                        if constexpr (SPLIT) {
+                            mbar_arrive_expect_tx(afull + sa, (uint32_t)PP.fp_bytes);
+                            tma_load_4d(fa, map_x, cb * CB, xc, yc, img0, afull + sa);
+                        } else {
+                            if (leader) mbar_arrive_expect_tx(afull + sa, 2u * (uint32_t)PP.fp_bytes);
+                            tma_load_4d_pair(fa, map_x, cb * CB, xc, yc, img0, afull + sa);
+                        }
+                        ++ita;
+                        if (++sa == NA) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
                     if (it >= NS) mbar_wait(empty + s, ph ^ 1);
                     const int r = tap / P.ks, sx = tap - r * P.ks;
-                    uint8_t *a = smem + s * STAGE;
-                    uint8_t *b = a + A_BYTES;
+                    uint8_t *a = bring + s * STAGE;
+                    uint8_t *b = HALO ? a : a + A_BYTES;
                     const int xc = ox0 * P.stride + sx - P.pad, yc = oy0 * P.stride + r - P.pad;
                     const int wc = P.batched ? img0 : tap;
                     if constexpr (SPLIT) {   // own barrier: the converters need a local signal
                         mbar_arrive_expect_tx(full + s, cta_bytes);
-                        tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
+                        if (!HALO) tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
                         tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
                     } else {                 // both CTAs' bytes complete on the leader's barrier
                         if (leader) mbar_arrive_expect_tx(full + s, 2 * cta_bytes);
-                        tma_load_4d_pair(a, map_x, cb * CB, xc, yc, img0, full + s);
+                        if (!HALO) tma_load_4d_pair(a, map_x, cb * CB, xc, yc, img0, full + s);
                         tma_load_3d_pair(b, map_w, cb * CB, n0, wc, full + s);
                     }
-                    if (++cb == P.cblocks) {
+                    // halo: channel block outer, taps inner (footprint reused by all taps)
+                    if (HALO) {
+                        if (++tap == taps) {
+                            tap = 0;
+                            ++cb;
+                        }
+                    } else if (++cb == P.cblocks) {
                         cb = 0;
                         ++tap;
                     }
@@ -261,28 +351,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
         if (leader && lane == 0) {
             // ---- MMA issuer (leader CTA, one thread) -----------------------------------
             constexpr uint32_t idesc = idesc_m256<BN, KIND>();
-            int s = 0;
-            uint32_t ph = 0;
+            int s = 0, sa = 0;
+            uint32_t ph = 0, pha = 0;
             int t = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
                 const int acc = t & 1;
                 if (t >= 2) mbar_wait_cluster(tempty + acc, ((t >> 1) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
+                int tap = 0;
+                uint32_t fa = 0;
                 for (int kb = 0; kb < P.kblocks; ++kb) {
+                    if (HALO && tap == 0) {
+                        if constexpr (SPLIT) mbar_wait_cluster(aconv + sa, pha);
+                        else mbar_wait(afull + sa, pha);
+                        fa = smem_u32(aring + sa * ASLOT);
+                    }
                     if constexpr (SPLIT) mbar_wait_cluster(conv + s, ph);
                     else mbar_wait(full + s, ph);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                    const uint32_t a = smem_u32(smem + s * STAGE);
-                    const uint32_t b = a + A_BYTES;
-                    const uint64_t ad = umma_desc_sw128(a), bd = umma_desc_sw128(b);
+                    const uint32_t st = smem_u32(bring + s * STAGE);
+                    uint32_t a, b;
+                    if (HALO) {
+                        const int r = tap / P.ks, sx = tap - r * P.ks;
+                        a = fa + (uint32_t)((r * PP.fpr + sx) * 128);
+                        b = st;
+                    } else {
+                        a = st;
+                        b = st + A_BYTES;
+                    }
+                    const uint64_t ad = HALO ? umma_desc_sw128_row(a) : umma_desc_sw128(a);
+                    const uint64_t bd = umma_desc_sw128(b);
+                    const bool first = kb == 0;
                     if constexpr (SPLIT) {
-                        const uint64_t adl = umma_desc_sw128(a + A_BYTES + B_BYTES);
-                        const uint64_t bdl = umma_desc_sw128(b + A_BYTES + B_BYTES);
+                        const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : a + A_BYTES + B_BYTES;
+                        const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : b + A_BYTES + B_BYTES;
+                        const uint64_t adl = HALO ? umma_desc_sw128_row(alo) : umma_desc_sw128(alo);
+                        const uint64_t bdl = umma_desc_sw128(blo);
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t o = (uint64_t)(kk * 2);
-                            umma_pair<KIND>(d, ad + o, bdl + o, idesc, (kb | kk) != 0);
+                            umma_pair<KIND>(d, ad + o, bdl + o, idesc, !(first && kk == 0));
                             umma_pair<KIND>(d, adl + o, bd + o, idesc, 1);
                             umma_pair<KIND>(d, ad + o, bd + o, idesc, 1);
                         }
@@ -290,9 +399,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk)
                             umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                                            (kb | kk) != 0);
+                                            !(first && kk == 0));
                     }
                     umma_commit_pair(empty + s);
+                    if (HALO && ++tap == taps) {
+                        tap = 0;
+                        umma_commit_pair(aempty + sa);   // footprint consumed by all taps
+                        if (++sa == NA) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
                     if (++s == NS) {
                         s = 0;
                         ph ^= 1;
@@ -317,12 +434,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
             const int blk = pair * 2 + (int)rank;
             int ox0, oy0, img0;
             pair_block_origin(P, grp, blk, ox0, oy0, img0);
-            const int per_img = P.bx * P.by;
-            const int im = m / per_img, pix = m - im * per_img;
-            const int py = pix / P.bx, px = pix - py * P.bx;
-            const int img = img0 + im, oy = oy0 + py, ox = ox0 + px;
-            const bool valid = blk < PP.blocks_per_group && m < per_img * P.imgs && img < P.n &&
-                               oy < P.p && ox < P.q;
+            int img, oy, ox;
+            bool valid;
+            if (HALO) {   // row = (footprint row, column); wrap-around columns are not outputs
+                const int py = m / PP.fpr, px = m - py * PP.fpr;
+                img = img0; oy = oy0 + py; ox = ox0 + px;
+                valid = blk < PP.blocks_per_group && px < P.bx && img < P.n && oy < P.p && ox < P.q;
+            } else {
+                const int per_img = P.bx * P.by;
+                const int im = m / per_img, pix = m - im * per_img;
+                const int py = pix / P.bx, px = pix - py * P.bx;
+                img = img0 + im; oy = oy0 + py; ox = ox0 + px;
+                valid = blk < PP.blocks_per_group && m < per_img * P.imgs && img < P.n && oy < P.p &&
+                        ox < P.q;
+            }
             const int k0 = nb * BN;
             float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
 #pragma unroll 1
@@ -351,32 +476,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
             if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
         }
     } else if (SPLIT && warp >= 8) {
-        // ---- converters: lo = v - tf32(v) of this CTA's stage (3xTF32) -------------
+        // ---- converters: lo = v - tf32(v) of this CTA's staged operands (3xTF32) ----
         const int ct = tid - 256;                    // 0..127
-        constexpr int PER = (A_BYTES + B_BYTES) / 16 / 128;
         const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
-        int s = 0;
-        uint32_t ph = 0;
+        const uint32_t aconv_leader = mapa_shared(smem_u32(aconv), 0);
+        int s = 0, sa = 0;
+        uint32_t ph = 0, pha = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
+            int tap = 0;
             for (int kb = 0; kb < P.kblocks; ++kb) {
-                mbar_wait(full + s, ph);
-                const uint32_t hi_s = smem_u32(smem + s * STAGE) + ct * 16;
-                const uint32_t lo_s = hi_s + A_BYTES + B_BYTES;
-                float4 v[PER];
-#pragma unroll
-                for (int j = 0; j < PER; ++j) v[j] = lds128(hi_s + j * 128 * 16);
-#pragma unroll
-                for (int j = 0; j < PER; ++j) {
-                    float4 l;
-                    l.x = v[j].x - __uint_as_float(__float_as_uint(v[j].x) & 0xffffe000u);
-                    l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
-                    l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
-                    l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
-                    sts128_tf32(lo_s + j * 128 * 16, l);
+                if (HALO && tap == 0) {
+                    mbar_wait(afull + sa, pha);
+                    const uint32_t hi = smem_u32(aring + sa * ASLOT);
+                    convert_lo_range(hi, hi + (uint32_t)PP.a_slot, PP.fp_bytes / 16, ct);
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(aconv_leader + (uint32_t)(sa * 8));
+                    if (++sa == NA) {
+                        sa = 0;
+                        pha ^= 1;
+                    }
                 }
+                mbar_wait(full + s, ph);
+                const uint32_t hi = smem_u32(bring + s * STAGE);
+                if (HALO) convert_lo_range(hi, hi + B_BYTES, B_BYTES / 16, ct);
+                else convert_lo_range(hi, hi + A_BYTES + B_BYTES, (A_BYTES + B_BYTES) / 16, ct);
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(conv_leader + (uint32_t)(s * 8));
+                if (HALO && ++tap == taps) tap = 0;
                 if (++s == NS) {
                     s = 0;
                     ph ^= 1;

@@ -349,8 +349,10 @@ struct IgemmPlan {
     IgemmParams P;
     IgemmFn fn = nullptr;
     bool pair = false;       // persistent CTA-pair kernel (igemm_pair.cuh)
+    bool halo = false;       // footprint staging (pair kernel, stride 1)
     PairFn pfn = nullptr;
     int groups = 1, blocks_per_group = 0;
+    int fpr = 0, fp_bytes = 0, a_slot = 0, na = 0;
     dim3 grid;
     size_t smem = 0;
     int regs = 0;

@@ -71,6 +71,8 @@ VGG16_3X3 = [
 SINGLE_RESNET = [LayerSpec("res2_3x3", 64, 56, 64, 1)]
 
 WORKLOADS = {"resnet50": RESNET50_3X3, "vgg16": VGG16_3X3, "single": SINGLE_RESNET}
+# BASELINE.json batch of each workload (config 4: 256, config 3: 32, configs 1-2: 1)
+DEFAULT_BATCH = {"resnet50": 256, "vgg16": 32, "single": 1}
 
 
 def expand(layers: list[LayerSpec]) -> list[LayerSpec]:

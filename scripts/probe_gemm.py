@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--m", type=int, default=16384)
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--k", type=int, default=1024)
+    ap.add_argument("--one", default="", help="prec:z:nzt -- run one config twice (ncu target)")
     args = ap.parse_args()
     m, n, k = args.m, args.n, args.k
     h = m // 128
@@ -34,10 +35,18 @@ def main():
     flops = 2.0 * m * n * k
     out = C.empty_act(1, n, h, 128, "HWC", device="cuda")
     ws = torch.empty(2 * x.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
+    if args.one:
+        prec, z, nzt = args.one.split(":")
+        wp = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
+        tile = TileConfig(128, 1, int(z), 65536, 1, 1, int(nzt), layout="HWC")
+        for _ in range(2):
+            C.conv_igemm(x, w, padding=0, tile=tile, precision=prec, w_packed=wp, out=out, workspace=ws)
+        torch.cuda.synchronize()
+        return
     for prec in ("tf32", "bf16", "3xtf32"):
         wp = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
         for z, nzt in ((256, 2), (128, 2), (128, 1), (256, 1)):
-            tile = TileConfig(128, 1, z, 32768, 1, 1, nzt, layout="HWC")
+            tile = TileConfig(128, 1, z, 65536, 1, 1, nzt, layout="HWC")
             try:
                 t = timeit(lambda: C.conv_igemm(x, w, padding=0, tile=tile, precision=prec,
                                                 w_packed=wp, out=out, workspace=ws), reps=20)

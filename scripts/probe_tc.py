@@ -67,6 +67,11 @@ def build(spec, kind, n, x, w, wcache):
         if spec.k % z:
             return None
         tile = igemm_tile(spec, z, nzt)
+        if len(rest) > 2 and rest[2].startswith("h"):   # halo-staged footprint, fpr = h<N>
+            if spec.stride != 1:
+                return None
+            fpr = int(rest[2][1:])
+            tile = TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, 2, layout="HWC")
         key = ("ig", prec == "bf16")
         if key not in wcache:
             wcache[key] = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)

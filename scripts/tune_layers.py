@@ -111,6 +111,24 @@ def tune_igemm(shape, spec, prec, log):
     out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
     ws = torch.empty(2 * xh.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
     variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
+    # halo-staged footprint tiles (pair kernel, stride 1): (x + S - 1) * y = 128
+    halo = []
+    if spec.stride == 1:
+        for fpr in (8, 16, 32, 64, 128):
+            x_, y_ = fpr - spec.r + 1, 128 // fpr
+            if 1 <= x_ <= q + spec.r - 1 and y_ <= p + spec.r - 1:
+                halo += [TileConfig(x_, y_, z, 32768, 2, 1, 2, layout="HWC") for z in zs
+                         if x_ % 2 == 0 and z % 2 == 0]
+    for tile in halo:
+        try:
+            t = DT.device_time(lambda: C.conv_igemm(xh, w, padding=spec.pad, tile=tile,
+                                                     precision=prec, w_packed=wq,
+                                                     stride=spec.stride, out=out, workspace=ws))
+        except Exception:  # noqa: BLE001 -- illegal projection
+            continue
+        tried += 1
+        if t < best_t:
+            best, best_t = tile, t
     for bx in [d for d in range(1, q + 1) if q % d == 0]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
             if not block_ok(bx, by, shape.n):

@@ -244,6 +244,30 @@ def test_igemm_cta_pair_matches_oracle_and_single_cta(case):
     assert co.rel_err(y.contiguous().cpu().numpy(), y1.contiguous().cpu().numpy()) <= 1e-5
 
 
+HALO_CASES = [
+    # (n, c, h, w, k, precision, tile) -- n_xt = 2: footprint staged once per channel
+    # block, taps = row offsets into it (stride 1, pair kernel)
+    (2, 64, 56, 56, 64, "3xtf32", TileConfig(14, 8, 64, 32768, 2, 1, 2, layout="HWC")),
+    (2, 64, 56, 56, 128, "tf32", TileConfig(6, 16, 128, 32768, 2, 1, 2, layout="HWC")),
+    (3, 128, 28, 28, 256, "3xtf32", TileConfig(14, 8, 256, 32768, 2, 1, 2, layout="HWC")),  # ragged
+    (2, 128, 14, 14, 128, "bf16", TileConfig(30, 4, 128, 32768, 2, 1, 2, layout="HWC")),   # x > Q
+    (3, 32, 7, 7, 64, "tf32", TileConfig(6, 16, 64, 32768, 2, 1, 2, layout="HWC")),        # 3 blocks
+]
+
+
+@pytest.mark.parametrize("case", HALO_CASES, ids=[str(i) for i in range(len(HALO_CASES))])
+def test_igemm_halo_staging_matches_oracle(case):
+    n, c, h, w, k, prec, tile = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    info = C.query(x.shape, wt.shape, 1, 1, "HWC", tile, f"igemm_{prec}")
+    assert info["rc"] == 0 and "halo" in info["reason"], info
+    y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision=prec, bias=_dev(b))
+    ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= TOL_PREC.get(prec, tol_fp32(c)), err
+
+
 def test_igemm_generic_entry_matches_split_entry():
     x, wt = _inputs(2, 64, 28, 28, 64, 3, 3)
     tile = TileConfig(14, 4, 64, 16384, 1, 1, 1, layout="HWC")

@@ -52,3 +52,37 @@ def test_committed_tables_name_real_layers_and_legal_tiles(workload):
     for name, plan in plans.items():
         assert plan["algorithm"] in runner.FP32_ALGORITHMS
         assert isinstance(plan["tile"], TileConfig)
+
+
+@pytest.mark.parametrize("key,alg,e", [
+    ("direct", "direct", None), ("direct_nhwc", "direct", None), ("winograd2", "winograd", 2),
+    ("winograd4", "winograd", 4), ("igemm_3xtf32", "igemm_3xtf32", None),
+    ("igemm_bf16", "igemm_bf16", None), ("winograd_tc_3xtf32_e4", "winograd_tc_3xtf32", 4),
+    ("winograd_tc_bf16_e2", "winograd_tc_bf16", 2),
+])
+def test_candidate_keys_map_to_algorithms(key, alg, e):
+    assert runner.candidate_algorithm(key) == (alg, e)
+
+
+def test_tensor_core_winograd_and_bf16_plans(tmp_path, monkeypatch):
+    t_wtc = TileConfig(4, 4, 256, 16384, 1, 1, 2, layout="HWC", e=4).to_dict()
+    t_ig = TileConfig(2, 2, 256, 32768, 1, 1, 2, layout="HWC").to_dict()
+    t_nhwc = TileConfig(2, 2, 128, 32768, 1, 1, 1, layout="HWC").to_dict()
+    layers = {"L": {"candidates": {
+        "winograd_tc_3xtf32_e4": {"tuner": {"best": t_wtc, "seconds": 1e-3}},
+        "igemm_3xtf32": {"tuner": {"best": t_ig, "seconds": 2e-3}},
+        "igemm_bf16": {"tuner": {"best": t_ig, "seconds": 0.2e-3}},
+        "winograd_tc_bf16_e4": {"tuner": {"best": t_wtc, "seconds": 0.1e-3}},
+        "direct_nhwc": {"tuner": {"best": t_nhwc, "seconds": 5e-3}},
+    }}}
+    monkeypatch.setattr(runner, "TUNED_DIR", _write(tmp_path, layers))
+    fp32 = runner.load_plans("toy")["L"]
+    assert fp32["algorithm"] == "winograd_tc_3xtf32" and fp32["e"] == 4   # bf16 is never FP32
+    bf16 = runner.load_plans("toy", ("igemm_bf16", "winograd_tc_bf16"))["L"]
+    assert bf16["algorithm"] == "winograd_tc_bf16"
+    cuda = runner.load_plans("toy", runner.CUDA_CORE_ALGORITHMS)["L"]
+    assert cuda["algorithm"] == "direct" and cuda["tile"].layout == "HWC"
+    spec = runner.LayerSpec("L", 64, 14, 256)
+    layer = runner.ConvLayer(spec, None, fp32)
+    assert layer.precision == "3xtf32" and layer.layout == "HWC" and layer.e == 4
+    assert layer.filter_elems() == 36 * 64 * 256
