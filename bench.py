@@ -451,19 +451,47 @@ def main() -> None:
         h2d = sum(h.numel() * 4 for h in hx)
         d2h = sum(h.numel() * 4 for h in hy)
 
+        # copies overlap compute: H2D of every layer's input on one stream, the convs on
+        # the compute stream (each waits for its input), D2H of each output on a third
+        # stream as soon as it is produced -- PCIe runs both directions at once.
+        # WAR hazards across steps (dx / ys reuse) are ordered by events.
+        s_h2d = torch.cuda.Stream(dev)
+        s_d2h = torch.cuda.Stream(dev)
+        ev_in = [torch.cuda.Event() for _ in layers]
+        ev_done = [torch.cuda.Event() for _ in layers]
+        ev_out = [torch.cuda.Event() for _ in layers]
+        ev_drained = [torch.cuda.Event() for _ in layers]
+        first = [True]
+
         def e2e_step():
+            for i in range(len(layers)):
+                if not first[0]:
+                    s_h2d.wait_event(ev_done[i])        # previous conv i has read dx[i]
+                with torch.cuda.stream(s_h2d):
+                    dx[i].copy_(hx[i], non_blocking=True)
+                ev_in[i].record(s_h2d)
             for i, layer in enumerate(layers):
-                dx[i].copy_(hx[i], non_blocking=True)
+                stream.wait_event(ev_in[i])
+                if not first[0]:
+                    stream.wait_event(ev_drained[i])    # previous D2H of ys[i] finished
                 y = layer.forward(dx[i], out=ys[i], stream=stream)
-                hy[i].copy_(y, non_blocking=True)
+                ev_done[i].record(stream)
+                s_d2h.wait_event(ev_done[i])
+                with torch.cuda.stream(s_d2h):
+                    hy[i].copy_(y, non_blocking=True)
+                ev_drained[i].record(s_d2h)
+            first[0] = False
         e2e_step()
         torch.cuda.synchronize(dev)
         barrier()
         a = torch.cuda.Event(enable_timing=True)
         b = torch.cuda.Event(enable_timing=True)
         a.record(stream)
+        s_h2d.wait_stream(stream)
         for _ in range(args.steps):
             e2e_step()
+        stream.wait_stream(s_d2h)
+        stream.wait_stream(s_h2d)
         b.record(stream)
         b.synchronize()
         barrier()
