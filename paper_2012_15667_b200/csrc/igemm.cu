@@ -131,7 +131,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         pl->smem = a_ring + stages * stage_bytes + 1024 + 512;
         pl->bn = bn;
         pl->kind = kind;
-        pl->threads = kind == KIND_3XTF32 ? 384 : 256;
+        pl->threads = kind == KIND_3XTF32 ? (bn >= 256 ? 384 : 512) : 256;
         if (launch_fit_cluster((const void *)pfn, pl->threads, pl->smem, &pl->regs) < 1)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          "tcgen05 pair block (%d threads, %zu B smem) does not fit", pl->threads,
@@ -155,7 +155,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     pl->smem = smem;
     pl->bn = bn;
     pl->kind = kind;
-    pl->threads = kind == KIND_3XTF32 ? 256 : 128;
+    pl->threads = kind == KIND_3XTF32 ? (bn >= 256 ? 256 : 384) : 128;
     if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
                      pl->threads, smem);

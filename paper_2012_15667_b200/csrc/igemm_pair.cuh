@@ -25,7 +25,7 @@
 //
 // Warp roles (per CTA):  warp 0 = TMA producer, warp 1 = MMA issuer (leader
 // CTA) + TMEM allocator, warps 4..7 = epilogue (TMEM lane quadrants 0..3),
-// warps 8..11 = 3xTF32 converters (KIND_3XTF32 only).
+// warps 8.. = 3xTF32 converters (KIND_3XTF32 only; 4 at BN = 256, 8 below).
 //
 // Synchronisation (s = ring stage, a = accumulator buffer):
 //   full[s]   leader: TMA bytes of BOTH CTAs (non-split; .cta_group::2 TMA
@@ -168,14 +168,23 @@ __device__ __forceinline__ void pair_block_origin(const IgemmParams &P, int grp,
     }
 }
 
-// lo = v - tf32(v) (rounded to TF32) of n16 16-byte vectors, 128 threads,
+// 3xTF32 converter warps per CTA: the A block's conversion cost does not shrink
+// with BN while the MMA work does, so narrow tiles get twice the converters
+template <int BN>
+constexpr int pair_conv_warps() { return BN >= 256 ? 4 : 8; }
+
+template <int BN, int KIND>
+constexpr int pair_threads() { return KIND == KIND_3XTF32 ? 256 + 32 * pair_conv_warps<BN>() : 256; }
+
+// lo = v - tf32(v) (rounded to TF32) of n16 16-byte vectors by NT threads,
 // explicit shared-window addressing; loads batched so their latencies overlap
+template <int NT>
 __device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n16, int ct) {
     int i = ct;
-    for (; i + 3 * 128 < n16; i += 4 * 128) {
+    for (; i + 3 * NT < n16; i += 4 * NT) {
         float4 v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = lds128(hi + (uint32_t)(i + j * 128) * 16);
+        for (int j = 0; j < 4; ++j) v[j] = lds128(hi + (uint32_t)(i + j * NT) * 16);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             float4 l;
@@ -183,10 +192,10 @@ __device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n
             l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
             l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
             l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
-            sts128_tf32(lo + (uint32_t)(i + j * 128) * 16, l);
+            sts128_tf32(lo + (uint32_t)(i + j * NT) * 16, l);
         }
     }
-    for (; i < n16; i += 128) {
+    for (; i < n16; i += NT) {
         const float4 v = lds128(hi + (uint32_t)i * 16);
         float4 l;
         l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u);
@@ -198,13 +207,16 @@ __device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n
 }
 
 // K-major SW128 descriptor of an operand starting at any 128-B row of a
-// 1 KB-aligned tile (base offset = the row's phase in the 8-row swizzle atom)
-__device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) {
-    return umma_desc_sw128(addr) | ((uint64_t)((addr >> 7) & 7) << 49);
-}
+// 1 KB-aligned TMA-written tile.  The tensor core applies the 128-B swizzle on
+// absolute smem address bits (as TMA does when writing), so the plain
+// descriptor of the row address is correct and the base-offset field must stay
+// 0 -- measured: scripts/dev/umma_shift_selftest.cu (base_offset = 0 exact for
+// every row shift; base_offset = (addr >> 7) & 7 wrong unless the shift is a
+// multiple of 8 rows).
+__device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return umma_desc_sw128(addr); }
 
 template <int BN, int KIND, bool HALO>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 ? 384 : 256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
     constexpr bool SPLIT = KIND == KIND_3XTF32;
@@ -214,6 +226,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
     constexpr int MULT = SPLIT ? 2 : 1;               // hi (raw) + lo copies
     constexpr int CB = KIND == KIND_BF16 ? 64 : 32;
     constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+    constexpr int NCW = pair_conv_warps<BN>();        // converter warps (3xTF32)
     const IgemmParams &P = PP.g;
     // stage layout: non-halo [A | B] (+ lo copy);  halo: A footprint slots, then B stages
     const int STAGE = HALO ? B_BYTES * MULT : (A_BYTES + B_BYTES) * MULT;
@@ -248,14 +261,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
         for (int s = 0; s < NS; ++s) {
             mbar_init(full + s, 1);
             mbar_init(empty + s, 1);
-            mbar_init(conv + s, 8);
+            mbar_init(conv + s, 2 * NCW);
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 8);
             mbar_init(afull + a, 1);
             mbar_init(aempty + a, 1);
-            mbar_init(aconv + a, 8);
+            mbar_init(aconv + a, 2 * NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
@@ -477,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
         }
     } else if (SPLIT && warp >= 8) {
         // ---- converters: lo = v - tf32(v) of this CTA's staged operands (3xTF32) ----
-        const int ct = tid - 256;                    // 0..127
+        const int ct = tid - 256;                    // 0 .. 32*NCW-1
         const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
         const uint32_t aconv_leader = mapa_shared(smem_u32(aconv), 0);
         int s = 0, sa = 0;
@@ -488,7 +501,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
                 if (HALO && tap == 0) {
                     mbar_wait(afull + sa, pha);
                     const uint32_t hi = smem_u32(aring + sa * ASLOT);
-                    convert_lo_range(hi, hi + (uint32_t)PP.a_slot, PP.fp_bytes / 16, ct);
+                    convert_lo_range<32 * NCW>(hi, hi + (uint32_t)PP.a_slot, PP.fp_bytes / 16, ct);
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(aconv_leader + (uint32_t)(sa * 8));
@@ -499,8 +512,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(KIND == KIND_3XTF32 
                 }
                 mbar_wait(full + s, ph);
                 const uint32_t hi = smem_u32(bring + s * STAGE);
-                if (HALO) convert_lo_range(hi, hi + B_BYTES, B_BYTES / 16, ct);
-                else convert_lo_range(hi, hi + A_BYTES + B_BYTES, (A_BYTES + B_BYTES) / 16, ct);
+                if (HALO) convert_lo_range<32 * NCW>(hi, hi + B_BYTES, B_BYTES / 16, ct);
+                else convert_lo_range<32 * NCW>(hi, hi + A_BYTES + B_BYTES, (A_BYTES + B_BYTES) / 16, ct);
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(conv_leader + (uint32_t)(s * 8));

@@ -142,8 +142,15 @@ __device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32
 // lo = rna_tf32(v - hi) written by 4 converter warps; every k-step issues
 // A_hi*B_lo + A_lo*B_hi + A_hi*B_hi -- FP32-level accuracy on the tensor cores.
 // KIND_BF16: operands are bf16 in HBM (64 channels per 128-B row), kind::f16.
+// 3xTF32 converter warps: the A block's conversion does not shrink with BN
+template <int BN>
+constexpr int conv_warps() { return BN >= 256 ? 4 : 8; }
+
 template <int BN, int KIND>
-__global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
+constexpr int igemm_threads() { return KIND == KIND_3XTF32 ? 128 + 32 * conv_warps<BN>() : 128; }
+
+template <int BN, int KIND>
+__global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
     igemm_tcgen05_kernel(const __grid_constant__ IgemmParams P,
                               const __grid_constant__ CUtensorMap tm_x,
                               const __grid_constant__ CUtensorMap tm_w) {
@@ -182,7 +189,7 @@ __global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
         }
         mbar_init(done, 1);
         if (SPLIT)
-            for (int s = 0; s < NS; ++s) mbar_init(conv + s, 4);   // 4 converter warps
+            for (int s = 0; s < NS; ++s) mbar_init(conv + s, conv_warps<BN>());
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_w));
@@ -265,8 +272,9 @@ __global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
         // The tensor core reads the raw fp32 operand as TF32 by dropping the low
         // 13 mantissa bits, so hi = v & ~0x1fff needs no store: only lo is
         // written (itself rounded to TF32), halving the conversion's smem traffic.
-        const int ct = tid - 128;                    // 0..127
-        constexpr int PER = (A_BYTES + B_BYTES) / 16 / 128;   // float4 per converter thread
+        constexpr int NT = 32 * conv_warps<BN>();
+        const int ct = tid - 128;                    // 0 .. NT-1
+        constexpr int PER = (A_BYTES + B_BYTES) / 16 / NT;    // float4 per converter thread
         int s = 0;
         uint32_t ph = 0;
         for (int kb = 0; kb < P.kblocks; ++kb) {
@@ -277,7 +285,7 @@ __global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
             const uint32_t lo_s = hi_s + A_BYTES + B_BYTES;
             float4 v[PER];
 #pragma unroll
-            for (int j = 0; j < PER; ++j) v[j] = lds128(hi_s + j * 128 * 16);
+            for (int j = 0; j < PER; ++j) v[j] = lds128(hi_s + j * NT * 16);
 #pragma unroll
             for (int j = 0; j < PER; ++j) {
                 float4 l;
@@ -285,7 +293,7 @@ __global__ void __launch_bounds__(KIND == KIND_3XTF32 ? 256 : 128, 1)
                 l.y = v[j].y - __uint_as_float(__float_as_uint(v[j].y) & 0xffffe000u);
                 l.z = v[j].z - __uint_as_float(__float_as_uint(v[j].z) & 0xffffe000u);
                 l.w = v[j].w - __uint_as_float(__float_as_uint(v[j].w) & 0xffffe000u);
-                sts128_tf32(lo_s + j * 128 * 16, l);
+                sts128_tf32(lo_s + j * NT * 16, l);
             }
             // generic-proxy stores -> visible to the tensor core's async proxy
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");

@@ -1,0 +1,8 @@
+set -x
+timeout 600 python -m pytest tests/test_conv_gpu.py -x -q -k "halo or pair or igemm or winograd_tc" > gpurun_out/conv8_tests.log 2>&1
+tail -5 gpurun_out/conv8_tests.log
+timeout 600 python scripts/probe_tc.py --n 256 --layers res2_3x3,res3_3x3,res4_3x3 --kinds igemm_3xtf32:64:1,igemm_3xtf32:64:2,igemm_3xtf32:64:2:h16,igemm_3xtf32:128:1,igemm_3xtf32:128:2,igemm_3xtf32:256:2 > gpurun_out/probe_conv8.log 2>&1
+cat gpurun_out/probe_conv8.log
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:"igemm_tcgen05|igemm_pair" -c 1 -o gpurun_out/ncu_res2_pair64 -f python scripts/probe_tc.py --one igemm_3xtf32:64:2 --layers res2_3x3 --reps 2 > /dev/null 2>&1
+timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/wtc_launches.csv python scripts/probe_tc.py --one winograd_tc_3xtf32:4:64:2 --layers res2_3x3 --reps 2 > gpurun_out/ncu_wtc.log 2>&1
+ls gpurun_out/*.ncu-rep

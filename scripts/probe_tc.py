@@ -158,6 +158,9 @@ def main():
         wcache = {}
         if args.one:
             fn = build(spec, args.one, args.n, x, w, wcache)
+            if fn is None:
+                print("skip", args.one, spec.name)
+                continue
             for _ in range(args.reps):
                 fn()
             torch.cuda.synchronize()

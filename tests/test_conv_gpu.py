@@ -250,8 +250,8 @@ HALO_CASES = [
     (2, 64, 56, 56, 64, "3xtf32", TileConfig(14, 8, 64, 32768, 2, 1, 2, layout="HWC")),
     (2, 64, 56, 56, 128, "tf32", TileConfig(6, 16, 128, 32768, 2, 1, 2, layout="HWC")),
     (3, 128, 28, 28, 256, "3xtf32", TileConfig(14, 8, 256, 32768, 2, 1, 2, layout="HWC")),  # ragged
-    (2, 128, 14, 14, 128, "bf16", TileConfig(30, 4, 128, 32768, 2, 1, 2, layout="HWC")),   # x > Q
-    (3, 32, 7, 7, 64, "tf32", TileConfig(6, 16, 64, 32768, 2, 1, 2, layout="HWC")),        # 3 blocks
+    (2, 128, 14, 14, 128, "bf16", TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC")),   # ragged y
+    (2, 32, 20, 20, 64, "tf32", TileConfig(6, 16, 64, 32768, 2, 1, 2, layout="HWC")),      # ragged x, y
 ]
 
 
