@@ -199,6 +199,23 @@ def load_profile_traffic() -> dict:
     return out
 
 
+def _traffic(tab: dict, workload: str, fam: dict, dom: str):
+    """DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, one capture
+    per layer call, committed under profiles/*_traffic.json) of the dominant family's
+    layers: {layer: bytes}; None if no capture is committed."""
+    alg = dom.split()[0]
+    if alg.startswith("winograd F("):
+        alg = "winograd"
+    out = {}
+    for layer in sorted(fam["layers"]):
+        t = tab.get(f"{workload}:{layer}:{alg}")
+        if isinstance(t, dict):
+            out[layer] = t.get("dram_bytes_per_call")
+        elif t is not None:
+            out[layer] = t
+    return out or None
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -399,7 +416,7 @@ def main() -> None:
             "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec == "bf16" else " / 2 (dense TF32 rate)")
                             if peaks.get("bf16_tflops") else "fallback 1.59 PFLOP/s bf16"),
-            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom.split()[0]}"),
+            "traffic": _traffic(traffic_tab, args.workload, d, dom),
         }
     else:
         peak = ffma_peak_tflops(torch, stream)
@@ -408,7 +425,7 @@ def main() -> None:
             "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4) if peak else None,
             "peak_source": "live FFMA probe (convio_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
-            "traffic": traffic_tab.get(f"{args.workload}:{sorted(d['layers'])[0]}:{dom}"),
+            "traffic": _traffic(traffic_tab, args.workload, d, dom),
         }
     roofline["layers"] = sorted(d["layers"])
     roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)

@@ -155,7 +155,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     pl->smem = smem;
     pl->bn = bn;
     pl->kind = kind;
-    pl->threads = kind == KIND_3XTF32 ? (bn >= 256 ? 256 : 384) : 128;
+    pl->threads = kind == KIND_3XTF32 ? 256 : 128;
     if (launch_fit((const void *)fn, pl->threads, smem, &pl->regs) < 1)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 block (%d threads, %zu B smem) does not fit",
                      pl->threads, smem);

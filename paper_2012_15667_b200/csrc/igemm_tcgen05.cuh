@@ -142,9 +142,11 @@ __device__ __forceinline__ void tmem_ld_32x32b<32>(uint32_t taddr, float (&v)[32
 // lo = rna_tf32(v - hi) written by 4 converter warps; every k-step issues
 // A_hi*B_lo + A_lo*B_hi + A_hi*B_hi -- FP32-level accuracy on the tensor cores.
 // KIND_BF16: operands are bf16 in HBM (64 channels per 128-B row), kind::f16.
-// 3xTF32 converter warps: the A block's conversion does not shrink with BN
+// 3xTF32 converter warps of the single-CTA kernel: 4 keeps 256 threads so two
+// CTAs share an SM at s_b = 16384 (measured: 8 warps cost res2 0.518 -> 0.674 ms
+// by losing that second CTA); the pair kernel uses 8 below BN = 256.
 template <int BN>
-constexpr int conv_warps() { return BN >= 256 ? 4 : 8; }
+constexpr int conv_warps() { return 4; }
 
 template <int BN, int KIND>
 constexpr int igemm_threads() { return KIND == KIND_3XTF32 ? 128 + 32 * conv_warps<BN>() : 128; }
