@@ -103,7 +103,7 @@ static int pfail(char *reason, size_t rlen, int code, const char *fmt, ...) {
 // Ring depth, smem and occupancy shared by the conv and batched plans.  The
 // outputs live in TMEM, so s_b only sizes the TMA ring: ring bytes <= 6*s_b
 // (s_b = 16384 words -> 96 KB, two CTAs per SM; 32768 -> 192 KB, one deep-ring
-// CTA per SM), 2..6 stages.
+// CTA per SM), 2..12 stages.
 // pair = true: the persistent CTA-pair kernel (igemm_pair.cuh), selected by a
 // tile with n_zt == 2 (two CTAs share the z = BN output channels of one MMA);
 // n_zt == 1: one 128-row tile per CTA (igemm_tcgen05.cuh).
@@ -121,7 +121,9 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         const size_t budget = 227 * 1024 - 1024 - 512;
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
-        int stages = (int)std::min<size_t>(8, (budget - a_ring) / stage_bytes);
+        // small stages (narrow BN, no lo copy) need many in flight to cover the
+        // TMA latency (~1 us) at a few hundred MMA cycles per stage
+        int stages = (int)std::min<size_t>(16, (budget - a_ring) / stage_bytes);
         if (stages < 2)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair ring does not fit");
         pl->P.stages = stages;
@@ -144,7 +146,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
                      bn);
     const size_t stage_bytes = (size_t)(128 * 128 + bn * 128) * (kind == KIND_3XTF32 ? 2 : 1);
     const size_t ring_cap = std::min<size_t>((size_t)6 * s_b, 227 * 1024 - 2048);
-    int stages = (int)std::min<size_t>(6, ring_cap / stage_bytes);
+    int stages = (int)std::min<size_t>(12, ring_cap / stage_bytes);
     if (stages < 2) stages = 2;
     while (stages > 2 && stages * stage_bytes + 2048 > 227 * 1024) --stages;
     const size_t smem = stages * stage_bytes + 1024 + 512;

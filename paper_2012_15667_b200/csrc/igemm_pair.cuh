@@ -76,28 +76,18 @@ __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
     return r;
 }
 
+// Arrive on a barrier of the pair (shared::cluster address from mapa) with the
+// default .release.cta semantics -- the form CUTLASS's 2-SM transform pipeline
+// uses (cutlass/arch/barrier.h umma_arrive_2x1SM_sm0).  The .release.cluster
+// form compiles to MEMBAR.ALL.GPU + ERRBAR per arrive, which measured as the
+// 3xTF32 converters' dominant stall (ncu, res2 pair BN=64).
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr)
-                 : "memory");
+    asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];\n" ::"r"(cluster_addr) : "memory");
 }
 
-// wait with cluster-scope acquire (arrivals from the peer CTA)
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) {
-    uint32_t done = 0, polls = 0;
-    while (true) {
-        asm volatile(
-            "{\n"
-            ".reg .pred P1;\n"
-            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%1], %2;\n"
-            "selp.u32 %0, 1, 0, P1;\n"
-            "}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (done) return;
-        if (++polls > (1u << 28)) asm volatile("trap;");
-    }
-}
+// wait on a barrier that the peer CTA also arrives on (default acquire, as the
+// CUTLASS 2-SM consumer waits)
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 
 // TMA load whose completion is signalled on the LEADER CTA's barrier (peer bit cleared)
 __device__ __forceinline__ void tma_load_4d_pair(void *dst, uint64_t map, int c0, int c1, int c2, int c3,

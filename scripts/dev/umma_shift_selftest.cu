@@ -68,6 +68,67 @@ __global__ void k_shift(const __grid_constant__ CUtensorMap tma, const __grid_co
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(64));
 }
 
+// Throughput probe: one thread issues `iters` x 4 MMAs (M=128, N=64, K=8 tf32)
+// reading the A operand at row offset `shift`; returns cycles per MMA.
+template <int NN, bool BF16>
+__global__ void k_rate(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
+                       long long *cycles, int shift, int iters) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *a = sm;
+    uint8_t *b = sm + ROWS * 128;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(b + 256 * 128);
+    uint64_t *done = bar + 1;
+    uint32_t *slot = reinterpret_cast<uint32_t *>(done + 1);
+    const int warp = threadIdx.x >> 5;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        mbar_arrive_expect_tx(bar, ROWS * 128 + N * 128);
+        tma_load_2d(a, reinterpret_cast<uint64_t>(&tma), 0, 0, bar);
+        tma_load_2d(b, reinterpret_cast<uint64_t>(&tmb), 0, 0, bar);
+        mbar_wait(bar, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint64_t ad = umma_desc_sw128(smem_u32(a) + shift * 128);
+        const uint64_t bd = umma_desc_sw128(smem_u32(b));   // rows >= N are stale: timing only
+        constexpr uint32_t idesc = idesc_m128<NN, BF16 ? KIND_BF16 : KIND_TF32>();
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it)
+            for (int kk = 0; kk < 4; ++kk) {
+                if constexpr (BF16) umma_bf16(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
+                else umma_tf32(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
+            }
+        umma_commit(done);
+        mbar_wait(done, 0);
+        *cycles = (clock64() - t0) / (4LL * iters);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+}
+
+template <int NN, bool BF16>
+static void rate(const CUtensorMap &ma, const CUtensorMap &mb, long long *dcyc, int s) {
+    const size_t smem = 1024 + ROWS * 128 + 256 * 128 + 64;
+    cudaFuncSetAttribute(k_rate<NN, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long cyc = 0;
+    k_rate<NN, BF16><<<1, 128, smem>>>(ma, mb, dcyc, s, 4096);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
+    printf("rate: %s M128 N%3d shift=%2d: %lld cycles per MMA (K = 32 B)\n", BF16 ? "bf16" : "tf32", NN, s, cyc);
+}
+
 int main() {
     void *p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -113,5 +174,14 @@ int main() {
             printf("base_offset=%s shift=%2d: max abs err %.3g\n", use_base ? "(start>>7)&7" : "0", s, maxerr);
         }
     }
+    long long *dcyc;
+    cudaMalloc(&dcyc, 8);
+    for (int s : {0, 1, 17}) rate<64, false>(ma, mb, dcyc, s);
+    rate<128, false>(ma, mb, dcyc, 0);
+    rate<256, false>(ma, mb, dcyc, 0);
+    rate<256, false>(ma, mb, dcyc, 17);
+    rate<64, true>(ma, mb, dcyc, 0);
+    rate<128, true>(ma, mb, dcyc, 0);
+    rate<256, true>(ma, mb, dcyc, 0);
     return 0;
 }

@@ -57,6 +57,9 @@ def igemm_tile(spec, z, nzt=1):
     return TileConfig(x, y, z, 32768, 1, 1, nzt, layout="HWC")
 
 
+TILE_OVERRIDE = None   # --tile x,y,z,s_b,n_xt,n_yt,n_zt for the igemm kinds
+
+
 def build(spec, kind, n, x, w, wcache):
     """Return a zero-argument launcher for (algorithm kind string)."""
     alg, *rest = kind.split(":")
@@ -72,6 +75,8 @@ def build(spec, kind, n, x, w, wcache):
                 return None
             fpr = int(rest[2][1:])
             tile = TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, 2, layout="HWC")
+        if TILE_OVERRIDE:
+            tile = TileConfig(*TILE_OVERRIDE, layout="HWC")
         key = ("ig", prec == "bf16")
         if key not in wcache:
             wcache[key] = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
@@ -142,7 +147,11 @@ def main():
     ap.add_argument("--one", default="", help="run one kind a few times (ncu target)")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default="")
+    ap.add_argument("--tile", default="", help="x,y,z,s_b,n_xt,n_yt,n_zt for igemm kinds")
     args = ap.parse_args()
+    global TILE_OVERRIDE
+    if args.tile:
+        TILE_OVERRIDE = [int(v) for v in args.tile.split(",")]
     torch.backends.cudnn.benchmark = True
     specs = R.WORKLOADS[args.workload]
     if args.layers:
