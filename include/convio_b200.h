@@ -149,7 +149,9 @@ int convio_pack_filter_igemm(const convio_conv_desc *desc, const float *w, float
  * tile z in {64,128,256}, x*y <= 128 (ceil(128/(x*y)) images stacked per MMA
  * tile).  tile->n_zt selects the kernel: 1 = one 128-row tile per CTA,
  * 2 = persistent CTA pair (cta_group::2, M = 256, each CTA stages z/2 filter
- * rows, double-buffered TMEM accumulators); n_xt = n_yt = 1.  Inputs are consumed at TF32 precision, accumulation is FP32.
+ * rows, double-buffered TMEM accumulators), 4 = the pair with the 3xTF32 A
+ * operand split into TMEM (z <= 128); n_xt = 2 (with n_zt = 2, stride 1):
+ * halo-staged input footprint; otherwise n_xt = n_yt = 1.  Inputs are consumed at TF32 precision, accumulation is FP32.
  * Replaces the same schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
 int convio_conv_igemm_tf32(const convio_conv_desc *desc, const convio_tile *tile, const float *x,
                            const float *w, int32_t w_is_packed, const float *bias, int32_t relu,

@@ -31,9 +31,9 @@ static IgemmFn igemm_kernel(int bn, int kind) {
 template <int KIND, bool HALO>
 static PairFn pair_kernel_kind(int bn) {
     switch (bn) {
-        case 64: return &igemm_pair_kernel<64, KIND, HALO>;
-        case 128: return &igemm_pair_kernel<128, KIND, HALO>;
-        case 256: return &igemm_pair_kernel<256, KIND, HALO>;
+        case 64: return &igemm_pair_kernel<64, KIND, HALO, false>;
+        case 128: return &igemm_pair_kernel<128, KIND, HALO, false>;
+        case 256: return &igemm_pair_kernel<256, KIND, HALO, false>;
         default: return nullptr;
     }
 }
@@ -45,7 +45,14 @@ static PairFn pair_kernel_h(int bn, int kind) {
     return pair_kernel_kind<KIND_TF32, HALO>(bn);
 }
 
-static PairFn pair_kernel(int bn, int kind, bool halo) {
+// tsa: 3xTF32 with the A operand in tensor memory (BN <= 128, no halo)
+static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
+    if (tsa) {
+        if (kind != KIND_3XTF32 || halo) return nullptr;
+        if (bn == 64) return &igemm_pair_kernel<64, KIND_3XTF32, false, true>;
+        if (bn == 128) return &igemm_pair_kernel<128, KIND_3XTF32, false, true>;
+        return nullptr;
+    }
     return halo ? pair_kernel_h<true>(bn, kind) : pair_kernel_h<false>(bn, kind);
 }
 
@@ -111,14 +118,16 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     if (pair) {
         // persistent pair: one CTA per SM, the whole shared memory is the ring
         // (halo: two footprint slots first, the filter stages in the rest)
-        PairFn pfn = pair_kernel(bn, kind, pl->halo);
+        PairFn pfn = pair_kernel(bn, kind, pl->halo, pl->tsa);
         if (!pfn)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
-                         "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
+                         pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
+                                 : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
         const int mult = kind == KIND_3XTF32 ? 2 : 1;
-        const size_t stage_bytes = (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) * mult;
+        const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
+                                           : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) * mult;
         const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : 0;
-        const size_t budget = 227 * 1024 - 1024 - 512;
+        const size_t budget = 227 * 1024 - 1024 - 1024;
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
         // small stages (narrow BN, no lo copy) need many in flight to cover the
@@ -130,10 +139,10 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         pl->pair = true;
         pl->pfn = pfn;
         pl->fn = nullptr;
-        pl->smem = a_ring + stages * stage_bytes + 1024 + 512;
+        pl->smem = a_ring + stages * stage_bytes + 1024 + 1024;
         pl->bn = bn;
         pl->kind = kind;
-        pl->threads = kind == KIND_3XTF32 ? (bn >= 256 ? 384 : 512) : 256;
+        pl->threads = kind == KIND_3XTF32 ? ((bn >= 256 || pl->tsa) ? 384 : 512) : 256;
         if (launch_fit_cluster((const void *)pfn, pl->threads, pl->smem, &pl->regs) < 1)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          "tcgen05 pair block (%d threads, %zu B smem) does not fit", pl->threads,
@@ -259,10 +268,12 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         return fail(CONVIO_EINFEASIBLE, "TMA box dims > 256");
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
-    if (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2))
+    if (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2 && t->n_zt != 4))
         return fail(CONVIO_EINFEASIBLE,
-                    "tcgen05 tiles take n_xt = n_yt = 1 and n_zt in {1 (one CTA), 2 (CTA pair)}");
-    int rc = plan_ring(pl, t->z, kind, t->s_b, t->n_zt == 2, reason, rlen);
+                    "tcgen05 tiles take n_xt = n_yt = 1 and n_zt in {1 (one CTA), 2 (CTA pair), "
+                    "4 (CTA pair, 3xTF32 A operand in TMEM)}");
+    pl->tsa = t->n_zt == 4;
+    int rc = plan_ring(pl, t->z, kind, t->s_b, t->n_zt >= 2, reason, rlen);
     if (rc) return rc;
     const int imgs = std::max(1, std::min(128 / px, d->n));
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
@@ -401,7 +412,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages",
-             kind_name(kind), pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.pair ? " CTA pair (persistent)" : ""), pl.pair ? 256 : 128,
+             kind_name(kind), pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
     return CONVIO_OK;
 }

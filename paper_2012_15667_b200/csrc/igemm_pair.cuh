@@ -160,11 +160,33 @@ __device__ __forceinline__ void pair_block_origin(const IgemmParams &P, int grp,
 
 // 3xTF32 converter warps per CTA: the A block's conversion cost does not shrink
 // with BN while the MMA work does, so narrow tiles get twice the converters
-template <int BN>
-constexpr int pair_conv_warps() { return BN >= 256 ? 4 : 8; }
+template <int BN, bool TSA = false>
+constexpr int pair_conv_warps() { return (BN >= 256 || TSA) ? 4 : 8; }
 
-template <int BN, int KIND>
-constexpr int pair_threads() { return KIND == KIND_3XTF32 ? 256 + 32 * pair_conv_warps<BN>() : 256; }
+template <int BN, int KIND, bool TSA = false>
+constexpr int pair_threads() { return KIND == KIND_3XTF32 ? 256 + 32 * pair_conv_warps<BN, TSA>() : 256; }
+
+// A operand from tensor memory (TSA): tcgen05.mma [d], [a_tmem], b_desc -- the
+// tensor core then reads only B from shared memory
+__device__ __forceinline__ void umma_pair_ts_tf32(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                                  uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31, %32};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+        "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+        "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
 
 // lo = v - tf32(v) (rounded to TF32) of n16 16-byte vectors by NT threads,
 // explicit shared-window addressing; loads batched so their latencies overlap
@@ -205,8 +227,8 @@ __device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n
 // multiple of 8 rows).
 __device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return umma_desc_sw128(addr); }
 
-template <int BN, int KIND, bool HALO>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND>(), 1)
+template <int BN, int KIND, bool HALO, bool TSA>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND, TSA>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
     constexpr bool SPLIT = KIND == KIND_3XTF32;
@@ -215,11 +237,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr int B_BYTES = HB * 128;
     constexpr int MULT = SPLIT ? 2 : 1;               // hi (raw) + lo copies
     constexpr int CB = KIND == KIND_BF16 ? 64 : 32;
-    constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-    constexpr int NCW = pair_conv_warps<BN>();        // converter warps (3xTF32)
+    // TSA (3xTF32, BN <= 128): A_hi / A_lo live in TMEM columns after the two
+    // accumulators, NTA k-block slots of 64 columns (32 hi + 32 lo)
+    static_assert(!TSA || (SPLIT && !HALO && BN <= 128), "TSA: 3xTF32, no halo, BN <= 128");
+    constexpr uint32_t TMEM_COLS = TSA ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
+    constexpr uint32_t A_COL0 = 2 * BN;
+    constexpr int NTA = TSA ? (512 - 2 * BN) / 64 : 1;
+    constexpr int NCW = pair_conv_warps<BN, TSA>();   // converter warps (3xTF32)
     const IgemmParams &P = PP.g;
-    // stage layout: non-halo [A | B] (+ lo copy);  halo: A footprint slots, then B stages
-    const int STAGE = HALO ? B_BYTES * MULT : (A_BYTES + B_BYTES) * MULT;
+    // stage layout: non-halo [A | B] (+ lo copy); TSA [A | B | B_lo];
+    // halo: A footprint slots, then B stages
+    const int STAGE = HALO ? B_BYTES * MULT : (TSA ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * MULT);
     const int ASLOT = HALO ? PP.a_slot * MULT : 0;
     const int NA = HALO ? PP.na : 0;
 
@@ -236,7 +264,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     uint64_t *afull = tempty + 2;                     // halo: footprint slot barriers
     uint64_t *aempty = afull + 2;
     uint64_t *aconv = aempty + 2;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(aconv + 2);
+    uint64_t *tconv = aconv + 2;                      // TSA: A slot in TMEM converted
+    uint64_t *tfree = tconv + 6;                      // TSA: A slot in TMEM consumed
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfree + 6);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -259,6 +289,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             mbar_init(afull + a, 1);
             mbar_init(aempty + a, 1);
             mbar_init(aconv + a, 2 * NCW);
+        }
+        for (int a = 0; a < NTA && TSA; ++a) {
+            mbar_init(tconv + a, 2 * NCW);
+            mbar_init(tfree + a, 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
         asm volatile("prefetch.tensormap [%0];\n" ::"l"(map_x));
@@ -354,8 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         if (leader && lane == 0) {
             // ---- MMA issuer (leader CTA, one thread) -----------------------------------
             constexpr uint32_t idesc = idesc_m256<BN, KIND>();
-            int s = 0, sa = 0;
-            uint32_t ph = 0, pha = 0;
+            int s = 0, sa = 0, ta = 0;
+            uint32_t ph = 0, pha = 0, pht = 0;
             int t = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
                 const int acc = t & 1;
@@ -365,6 +399,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 int tap = 0;
                 uint32_t fa = 0;
                 for (int kb = 0; kb < P.kblocks; ++kb) {
+                    if constexpr (TSA) {
+                        mbar_wait_cluster(tconv + ta, pht);
+                        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                        const uint32_t b = smem_u32(bring + s * STAGE) + A_BYTES;
+                        const uint64_t bd = umma_desc_sw128(b), bdl = umma_desc_sw128(b + B_BYTES);
+                        const uint32_t ahi = tmem + A_COL0 + (uint32_t)(ta * 64);
+                        const bool first = kb == 0;
+#pragma unroll
+                        for (int kk = 0; kk < 4; ++kk) {
+                            const uint64_t o = (uint64_t)(kk * 2);
+                            const uint32_t ak = ahi + (uint32_t)(kk * 8);
+                            umma_pair_ts_tf32(d, ak, bdl + o, idesc, !(first && kk == 0));
+                            umma_pair_ts_tf32(d, ak + 32, bd + o, idesc, 1);
+                            umma_pair_ts_tf32(d, ak, bd + o, idesc, 1);
+                        }
+                        umma_commit_pair(empty + s);
+                        umma_commit_pair(tfree + ta);
+                        if (++ta == NTA) {
+                            ta = 0;
+                            pht ^= 1;
+                        }
+                        if (++s == NS) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                        continue;
+                    }
                     if (HALO && tap == 0) {
                         if constexpr (SPLIT) mbar_wait_cluster(aconv + sa, pha);
                         else mbar_wait(afull + sa, pha);
@@ -478,7 +539,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
         }
-    } else if (SPLIT && warp >= 8) {
+    } else if (TSA && warp >= 8) {
+        // ---- TSA converters: warp q owns TMEM lanes 32q..32q+31 = A rows; each
+        // thread reads its row's 32 channels from the SW128 stage, writes the
+        // hi (truncated) / lo (rna) halves to TMEM with tcgen05.st, and converts
+        // its share of the B rows to B_lo in shared memory.
+        const int q = warp & 3;
+        const int m = q * 32 + lane;
+        const int ct = tid - 256;                    // 0..127
+        const uint32_t tconv_leader = mapa_shared(smem_u32(tconv), 0);
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + A_COL0;
+        int s = 0, ta = 0, it = 0;
+        uint32_t ph = 0, pht = 0;
+        for (int item = cluster_id; item < PP.items; item += nclusters) {
+            for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+                mbar_wait(full + s, ph);
+                if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
+                const uint32_t st = smem_u32(bring + s * STAGE);
+                const uint32_t row = st + (uint32_t)m * 128;
+                uint32_t hi[32], lo[32];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const float4 v = lds128(row + (uint32_t)((c ^ (m & 7)) << 4));
+                    const float e[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t h = __float_as_uint(e[j]) & 0xffffe000u;
+                        hi[c * 4 + j] = h;
+                        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(lo[c * 4 + j]) : "f"(e[j] - __uint_as_float(h)));
+                    }
+                }
+                const uint32_t ta_col = (uint32_t)(ta * 64);
+                tmem_st_32x32b_x32(lane_base + ta_col, hi);
+                tmem_st_32x32b_x32(lane_base + ta_col + 32, lo);
+                convert_lo_range<128>(st + A_BYTES, st + A_BYTES + B_BYTES, B_BYTES / 16, ct);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tconv_leader + (uint32_t)(ta * 8));
+                if (++ta == NTA) {
+                    ta = 0;
+                    pht ^= 1;
+                }
+                if (++s == NS) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
+        }
+    } else if (SPLIT && !TSA && warp >= 8) {
         // ---- converters: lo = v - tf32(v) of this CTA's staged operands (3xTF32) ----
         const int ct = tid - 256;                    // 0 .. 32*NCW-1
         const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);

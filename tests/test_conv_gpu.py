@@ -223,6 +223,11 @@ PAIR_CASES = [
     (3, 128, 14, 14, 256, 1, "tf32", TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC")),
     (4, 128, 28, 28, 256, 2, "bf16", TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC")),
     (1, 64, 14, 14, 128, 1, "bf16", TileConfig(14, 2, 128, 32768, 1, 1, 2, layout="HWC")),  # 7 blocks
+    # n_zt = 4: 3xTF32 pair with the A operand (hi / lo) in tensor memory
+    (2, 64, 56, 56, 64, 1, "3xtf32", TileConfig(8, 1, 64, 32768, 1, 1, 4, layout="HWC")),
+    (3, 128, 28, 28, 128, 1, "3xtf32", TileConfig(4, 1, 128, 32768, 1, 1, 4, layout="HWC")),
+    (3, 256, 7, 7, 128, 1, "3xtf32", TileConfig(1, 1, 128, 32768, 1, 1, 4, layout="HWC")),
+    (2, 64, 28, 28, 128, 2, "3xtf32", TileConfig(14, 7, 128, 32768, 1, 1, 4, layout="HWC")),
 ]
 TOL_PREC = {"tf32": TOL_TF32, "bf16": TOL_BF16}
 
@@ -238,6 +243,9 @@ def test_igemm_cta_pair_matches_oracle_and_single_cta(case):
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
     assert err <= TOL_PREC.get(prec, tol_fp32(c)), err
     single = TileConfig(tile.x, tile.y, tile.z, tile.s_b, 1, 1, 1, layout="HWC")
+    if tile.n_zt == 4:
+        assert "A in TMEM" in C.query(x.shape, wt.shape, stride, 1, "HWC", tile,
+                                      f"igemm_{prec}")["reason"]
     y1 = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=single,
                       precision=prec, bias=_dev(b))
     # same products, same per-output summation order: identical up to MMA-internal order
