@@ -347,7 +347,7 @@ def main() -> None:
                 if layer.algorithm == "winograd":
                     f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
                     name = f"winograd F({layer.e},3)"
-                elif layer.algorithm.startswith("winograd_tc"):
+                elif layer.algorithm.startswith("winograd_tc") or layer.algorithm == "winograd_nhwc":
                     f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
                     name = f"{layer.algorithm} F({layer.e},3)"
                 else:

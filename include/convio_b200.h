@@ -61,11 +61,13 @@ extern "C" {
 #define CONVIO_ALG_WINOGRAD_TC_TF32 5   /* Winograd, element-wise GEMMs on tcgen05 (TF32) */
 #define CONVIO_ALG_WINOGRAD_TC_3XTF32 6 /* ... 3xTF32 (FP32-level GEMM accuracy) */
 #define CONVIO_ALG_WINOGRAD_TC_BF16 7   /* ... BF16 transformed operands */
+#define CONVIO_ALG_WINOGRAD_NHWC 8      /* same pipeline, element-wise GEMMs as a batched FP32 FFMA GEMM */
 
 /* Operand precision of the tcgen05 contractions (FP32 accumulate always). */
 #define CONVIO_PREC_TF32 0
 #define CONVIO_PREC_3XTF32 1
 #define CONVIO_PREC_BF16 2
+#define CONVIO_PREC_FP32 3   /* convio_winograd_bgemm only: FP32 FFMA GEMMs on the CUDA cores */
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {
@@ -191,7 +193,10 @@ int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e,
  * M[xi][t][k] = sum_c V[xi][t][c] U[xi][k][c] on tcgen05 in one launch, and
  * the input/output transforms as HBM-streaming kernels; the batch is chunked
  * so each chunk's V and M stay in L2.  NHWC, stride 1, C % 32 (% 64 for
- * BF16) == 0; tile->z in {64,128,256} is the GEMM's N tile, tile->s_b sizes
+ * BF16) == 0; precision CONVIO_PREC_FP32 runs the element-wise GEMMs on the
+ * CUDA cores (the channels-last FFMA kernel in batched mode, z in {64, 128},
+ * U laid out [xi][c][k] as convio_winograd_filter_transform writes it);
+ * tile->z in {64,128,256} is the GEMM's N tile, tile->s_b sizes
  * the TMA ring, tile->n_zt in {1, 2} picks the single-CTA / CTA-pair GEMM
  * kernel, tile->e must equal e (tile == NULL: defaults).
  * Replaces plan_winograd_dataflow + simulate (dataflow.py:253-338). */

@@ -97,7 +97,8 @@ ALGORITHMS = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
               "igemm_tf32": N.ALG_IGEMM_TF32, "igemm_3xtf32": N.ALG_IGEMM_3XTF32,
               "igemm_bf16": N.ALG_IGEMM_BF16, "winograd_tc_tf32": N.ALG_WINOGRAD_TC_TF32,
               "winograd_tc_3xtf32": N.ALG_WINOGRAD_TC_3XTF32,
-              "winograd_tc_bf16": N.ALG_WINOGRAD_TC_BF16}
+              "winograd_tc_bf16": N.ALG_WINOGRAD_TC_BF16, "winograd_nhwc": N.ALG_WINOGRAD_NHWC,
+              "winograd_tc_fp32": N.ALG_WINOGRAD_NHWC}
 
 
 def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CHW",
@@ -338,13 +339,15 @@ def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int =
 def winograd_filter_transform_tc(w: torch.Tensor, e: int, precision: str = "3xtf32",
                                  stream=None) -> torch.Tensor:
     """``U[xi][k][c] = (G g G^T)[xi]`` (K-major B operand of the tensor-core
-    Winograd GEMMs; bf16 for ``precision="bf16"``)."""
+    Winograd GEMMs; bf16 for ``precision="bf16"``); ``precision="fp32"`` (the
+    FFMA GEMM) gives ``U[xi][c][k]``."""
     _check_tensor(w, "w")
     prec = _precision(precision)
     w = w.contiguous()
     k, c, r, s = w.shape
     m = e + r - 1
-    u = torch.empty((m * m, k, c), device=w.device,
+    shape = (m * m, c, k) if prec == N.PREC_FP32 else (m * m, k, c)
+    u = torch.empty(shape, device=w.device,
                     dtype=torch.bfloat16 if prec == N.PREC_BF16 else torch.float32)
     desc = N.make_desc(1, c, 8, 8, k, r, s, 1, 1, 2)
     N.check(N.lib().convio_winograd_filter_transform_tc(ctypes.byref(desc), e, prec, _ptr(w),
@@ -363,7 +366,8 @@ def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int 
     (``convio_winograd_bgemm``).  Channels-last input, stride 1.  ``u`` from
     :func:`winograd_filter_transform_tc` (same precision) skips the filter
     transform.  Ragged outputs (P, Q not multiples of e) are handled by
-    zero-padded tiles.  Tolerances: 3xtf32 as the FP32 Winograd (F(2,3) 1e-4,
+    zero-padded tiles.  ``precision="fp32"`` runs the element-wise GEMMs on
+    the CUDA cores (FP32 FFMA, the paper-faithful arithmetic) instead.  Tolerances: 3xtf32 as the FP32 Winograd (F(2,3) 1e-4,
     F(4,3) 1e-3), tf32 5e-3, bf16 3e-2.
     """
     _check_tensor(x, "x")
@@ -378,6 +382,8 @@ def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int 
         out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
     if tile is not None:
         ct = N.make_tile(tile, 2)
+    elif prec == N.PREC_FP32:   # library default for the FFMA GEMM
+        ct = N.Tile(e, e, 128 if desc.k % 128 == 0 else 64, 32768, 1, 1, 1, 2, e)
     else:   # library default: widest N tile dividing K, CTA-pair kernel
         z = 256 if desc.k % 256 == 0 else (128 if desc.k % 128 == 0 else 64)
         ct = N.Tile(e, e, z, 16384, 1, 1, 2, 2, e)

@@ -647,6 +647,7 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
     if (algorithm == CONVIO_ALG_IGEMM_BF16) return igemm_query(desc, tile, out, 2);
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_query(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32, out);
+    if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_query(desc, tile, CONVIO_PREC_FP32, out);
     set_error("unknown algorithm %d", algorithm);
     return CONVIO_EINVAL;
 }
@@ -662,6 +663,7 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
         return igemm_workspace_bytes(desc, algorithm - CONVIO_ALG_IGEMM_TF32);
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_workspace_bytes(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32);
+    if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_workspace_bytes(desc, tile, CONVIO_PREC_FP32);
     return -1;
 }
 

@@ -87,6 +87,66 @@ static int plan_nhwc(const convio_conv_desc *d, const convio_tile *t, NhwcPlan *
     return CONVIO_OK;
 }
 
+// M[xi][t][k] = sum_c V[xi][t][c] * U[xi][c][k] on the FFMA kernel: the
+// Winograd element-wise GEMMs of the channels-last FP32 Winograd path
+// (winograd_tc.cu, precision CONVIO_PREC_FP32).  One launch for all xi.
+int direct_nhwc_batched_run(int bn, int s_b, int xi, int t_count, int c, int k, const float *v,
+                            const float *u, float *m, cudaStream_t stream) {
+    if (bn != 64 && bn != 128) {
+        set_error("FFMA batched GEMM needs z in {64, 128}, got %d", bn);
+        return CONVIO_EINFEASIBLE;
+    }
+    if (c % 32 || k % bn) {
+        set_error("FFMA batched GEMM needs C %% 32 == 0 and z | K (C=%d, K=%d, z=%d)", c, k, bn);
+        return CONVIO_EINFEASIBLE;
+    }
+    NhwcPlan pl;
+    NhwcParams &P = pl.P;
+    memset(&P, 0, sizeof(P));
+    NhwcFn fn = bn == 128 ? &direct_nhwc_f32_kernel<128> : &direct_nhwc_f32_kernel<64>;
+    const size_t stage = 128 * 128 + 32 * (size_t)bn * 4;
+    const size_t ring = std::min<size_t>((size_t)8 * s_b, 227 * 1024 - 2048);
+    const int stages = std::max(2, (int)std::min<size_t>(6, ring / stage));
+    const size_t smem = stages * stage + 1024 + 256;
+    P.n = xi; P.c = c; P.h = 1; P.w = t_count; P.k = k; P.p = 1; P.q = t_count;
+    P.pad = 0; P.stride = 1; P.ks = 1;
+    P.bx = 128; P.by = 1; P.imgs = 1;
+    P.tiles_x = (t_count + 127) / 128; P.tiles_y = 1; P.img_groups = xi;
+    P.cblocks = c / 32; P.kblocks = P.cblocks;
+    P.stages = stages;
+    P.batched = 1;
+    int regs = 0;
+    if (launch_fit((const void *)fn, 288, smem, &regs) < 1) {
+        set_error("FFMA batched GEMM block does not fit");
+        return CONVIO_EINFEASIBLE;
+    }
+    const dim3 grid(k / bn, P.tiles_x * xi, 1);
+    if (grid.y > 65535) {
+        set_error("grid exceeds launch limits");
+        return CONVIO_EINFEASIBLE;
+    }
+    CUtensorMap tx, tw;
+    cuuint64_t xd[4] = {(cuuint64_t)c, (cuuint64_t)t_count, 1, (cuuint64_t)xi};
+    cuuint64_t xs[3] = {(cuuint64_t)c * 4, (cuuint64_t)t_count * c * 4, (cuuint64_t)t_count * c * 4};
+    cuuint32_t xb[4] = {32, 128, 1, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    cuuint64_t wd[3] = {(cuuint64_t)k, (cuuint64_t)c, (cuuint64_t)xi};
+    cuuint64_t ws[2] = {(cuuint64_t)k * 4, (cuuint64_t)c * k * 4};
+    cuuint32_t wb[3] = {(cuuint32_t)bn, 32, 1};
+    if (!encode_tensor_map_tiled_ex(&tx, 4, const_cast<float *>(v), xd, xs, xb, es, true) ||
+        !encode_tensor_map_tiled_ex(&tw, 3, const_cast<float *>(u), wd, ws, wb, es, false)) {
+        set_error("TMA descriptors cannot describe the Winograd operands");
+        return CONVIO_EINFEASIBLE;
+    }
+    P.bias = nullptr;
+    P.y = m;
+    P.relu = 0;
+    fn<<<grid, 288, smem, stream>>>(P, tx, tw);
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
+}
+
 int direct_nhwc_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out) {
     NhwcPlan pl;
     int rc = plan_nhwc(d, t, &pl, out->reason, sizeof(out->reason));

@@ -33,6 +33,7 @@ struct NhwcParams {
     int kblocks, cblocks;
     int stages;
     int relu;
+    int batched;      // Winograd element-wise GEMMs: "image" = xi, pixels = tiles, filter = U[xi][C][K]
 };
 
 __device__ __forceinline__ float4 lds128_f(uint32_t addr) {
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(288, 1)
                 mbar_arrive_expect_tx(full + s, bytes);
                 tma_load_4d(a, map_x, cb * 32, ox0 * P.stride + sx - P.pad, oy0 * P.stride + r - P.pad,
                             img0, full + s);
-                tma_load_3d(a + A_BYTES, map_w, k0, tap, cb * 32, full + s);
+                if (P.batched) tma_load_3d(a + A_BYTES, map_w, k0, cb * 32, img0, full + s);
+                else tma_load_3d(a + A_BYTES, map_w, k0, tap, cb * 32, full + s);
                 if (++cb == P.cblocks) {
                     cb = 0;
                     ++tap;
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(288, 1)
         const int im = m / per_img, pix = m - im * per_img;
         const int py = pix / P.bx, px = pix - py * P.bx;
         const int img = img0 + im, oy = oy0 + py, ox = ox0 + px;
-        if (m >= per_img * P.imgs || img >= P.n) continue;
+        if (m >= per_img * P.imgs || img >= P.n || oy >= P.p || ox >= P.q) continue;
         float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0 + ng * 4;
 #pragma unroll
         for (int h = 0; h < H; ++h) {

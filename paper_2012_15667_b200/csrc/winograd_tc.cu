@@ -147,8 +147,10 @@ __global__ void __launch_bounds__(256) winograd_input_tc_kernel(const float *__r
     }
 }
 
-// Step 2: U[xi][k][c] = (G g G^T)[xi], one thread per (k, c), c fastest.
-template <int E, typename T>
+// Step 2: U[xi][k][c] = (G g G^T)[xi] (K-major B operand of the tensor-core
+// GEMM) or, CK = true, U[xi][c][k] (the FFMA GEMM's [channel][n] rows); one
+// thread per (k, c), c fastest.
+template <int E, typename T, bool CK = false>
 __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__restrict__ u, int k,
                                           int c) {
     constexpr int M = WinoTf<E>::M;
@@ -169,7 +171,10 @@ __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__rest
             float o[M];
             WinoTf<E>::g(t[a], o);
 #pragma unroll
-            for (int b = 0; b < M; ++b) store_elem(u + (int64_t)(a * M + b) * pairs + i, o[b]);
+            for (int b = 0; b < M; ++b) {
+                const int64_t j = CK ? (i % c) * (int64_t)k + i / c : i;
+                store_elem(u + (int64_t)(a * M + b) * pairs + j, o[b]);
+            }
         }
     }
 }
@@ -223,14 +228,22 @@ __global__ void __launch_bounds__(256) winograd_output_tc_kernel(const float *__
     }
 }
 
+// KIND_FFMA: the element-wise GEMMs on the CUDA cores (direct_nhwc_f32_kernel
+// in batched mode) -- the paper-faithful FP32 path in the same pipeline
+constexpr int KIND_FFMA = 3;
+
 static int kind_of_prec(int32_t precision) {
     switch (precision) {
         case CONVIO_PREC_TF32: return KIND_TF32;
         case CONVIO_PREC_3XTF32: return KIND_3XTF32;
         case CONVIO_PREC_BF16: return KIND_BF16;
+        case CONVIO_PREC_FP32: return KIND_FFMA;
         default: return -1;
     }
 }
+
+int direct_nhwc_batched_run(int bn, int s_b, int xi, int t_count, int c, int k, const float *v,
+                            const float *u, float *m, cudaStream_t stream);
 
 static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 
@@ -273,10 +286,14 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
     int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));
     int s_b = t ? t->s_b : 16384;
-    const bool pair = t ? t->n_zt == 2 : true;
-    if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2)))
+    const bool pair = kind != KIND_FFMA && (t ? t->n_zt == 2 : true);
+    if (kind == KIND_FFMA && !t) bn = d->k % 128 == 0 ? 128 : 64;
+    if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2) ||
+              (kind == KIND_FFMA && t->n_zt != 1)))
         return fail(CONVIO_EINFEASIBLE,
-                    "tcgen05 Winograd tiles take n_xt = n_yt = 1 and n_zt in {1, 2 (CTA pair)}");
+                    "Winograd tiles take n_xt = n_yt = 1 and n_zt in {1, 2 (tcgen05 CTA pair)}");
+    if (kind == KIND_FFMA && bn != 64 && bn != 128)
+        return fail(CONVIO_EINFEASIBLE, "FFMA Winograd GEMM needs z in {64, 128}, got %d", bn);
     if (t && t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
     if (t && t->e != e) return fail(CONVIO_EINVAL, "tile e=%d differs from e=%d", t->e, e);
     if (bn != 64 && bn != 128 && bn != 256)
@@ -307,7 +324,10 @@ static int launch_filter_tc(const WinoTcPlan &pl, const float *w, void *u, cudaS
     const int64_t pairs = (int64_t)pl.g.k * pl.g.c;
     const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
     const bool bf = pl.kind == KIND_BF16;
-    if (pl.e == 2) {
+    if (pl.kind == KIND_FFMA) {   // U[xi][c][k]: the FFMA GEMM reads [channel][n] rows
+        if (pl.e == 2) winograd_filter_tc_kernel<2, float, true><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+        else winograd_filter_tc_kernel<4, float, true><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+    } else if (pl.e == 2) {
         if (bf) winograd_filter_tc_kernel<2, __nv_bfloat16><<<blocks, 256, 0, st>>>(w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c);
         else winograd_filter_tc_kernel<2, float><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
     } else {
@@ -331,23 +351,28 @@ int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t preci
     if (rc) return rc;
     IgemmPlan gp;
     const int tc = pl.chunk_imgs * pl.g.tiles_y * pl.g.tiles_x;
-    rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, d->c, d->k, &gp, out->reason,
-                            sizeof(out->reason));
-    if (rc) return rc;
+    if (pl.kind != KIND_FFMA) {
+        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, d->c, d->k, &gp,
+                                out->reason, sizeof(out->reason));
+        if (rc) return rc;
+        out->grid_x = gp.grid.x; out->grid_y = gp.grid.y; out->grid_z = gp.grid.z;
+        out->block_threads = gp.threads;
+        out->smem_bytes = (int)gp.smem;
+        out->regs_per_thread = gp.regs;
+        out->stages = gp.P.stages;
+    } else {
+        out->grid_x = d->k / pl.bn; out->grid_y = ((tc + 127) / 128) * pl.m * pl.m; out->grid_z = 1;
+        out->block_threads = 288;
+    }
     out->legal = 1;
-    out->grid_x = gp.grid.x; out->grid_y = gp.grid.y; out->grid_z = gp.grid.z;
-    out->block_threads = gp.threads;
-    out->smem_bytes = (int)gp.smem;
-    out->regs_per_thread = gp.regs;
     out->channel_chunk = pl.kind == KIND_BF16 ? 64 : 32;
-    out->stages = gp.P.stages;
     out->p = pl.g.p; out->q = pl.g.q;
     const int64_t tiles = (int64_t)d->n * pl.g.tiles_y * pl.g.tiles_x;
     out->flops = 2LL * pl.m * pl.m * tiles * d->k * d->c;   // element-wise GEMM flops
     out->workspace_bytes = (int64_t)(pl.u_bytes + pl.v_bytes + pl.m_bytes);
     snprintf(out->reason, sizeof(out->reason),
              "tcgen05 Winograd F(%d,3) %s: %d GEMMs of T=%d (chunk %d img) x K=%d x C=%d, N=%d",
-             pl.e, pl.kind == KIND_BF16 ? "bf16" : (pl.kind == KIND_3XTF32 ? "3xtf32" : "tf32"),
+             pl.e, pl.kind == KIND_FFMA ? "fp32 FFMA" : pl.kind == KIND_BF16 ? "bf16" : (pl.kind == KIND_3XTF32 ? "3xtf32" : "tf32"),
              pl.m * pl.m, tc, pl.chunk_imgs, d->k, d->c, pl.bn);
     return CONVIO_OK;
 }
@@ -433,10 +458,16 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         }
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
-        IgemmPlan gp;
-        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, g.c, g.k, &gp, why, sizeof(why));
-        if (rc) return rc;
-        rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);
+        if (pl.kind == KIND_FFMA) {
+            rc = direct_nhwc_batched_run(pl.bn, pl.s_b, pl.m * pl.m, tc, g.c, g.k, (const float *)v,
+                                         (const float *)u, mm, st);
+        } else {
+            IgemmPlan gp;
+            rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, g.c, g.k, &gp, why,
+                                    sizeof(why));
+            if (rc) return rc;
+            rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);
+        }
         if (rc) return rc;
         if (pl.e == 2)
             winograd_output_tc_kernel<2><<<gout, 256, 0, st>>>(mm, bias, y, g, relu);

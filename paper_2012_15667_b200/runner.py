@@ -83,8 +83,8 @@ def expand(layers: list[LayerSpec]) -> list[LayerSpec]:
 # Algorithms whose results meet the FP32 tolerance (1e-5 normwise vs the float64
 # oracle; Winograd F(e,3) is looser by construction, 1e-4 / 1e-3) -- the
 # headline plan picks among these; "igemm_tf32" is the reduced-precision variant.
-FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32")
-CUDA_CORE_ALGORITHMS = ("direct", "winograd")
+FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32", "winograd_nhwc")
+CUDA_CORE_ALGORITHMS = ("direct", "winograd", "winograd_nhwc")
 
 
 def candidate_algorithm(key: str) -> tuple[str, int | None]:
@@ -94,6 +94,8 @@ def candidate_algorithm(key: str) -> tuple[str, int | None]:
     if key.startswith("winograd_tc_"):
         prec, _, e = key[len("winograd_tc_"):].partition("_e")
         return f"winograd_tc_{prec}", int(e)
+    if key.startswith("winograd_nhwc_e"):   # FP32 FFMA element-wise GEMMs, channels-last
+        return "winograd_nhwc", int(key[len("winograd_nhwc_e"):])
     if key.startswith("winograd"):
         return "winograd", int(key[len("winograd"):])
     if key == "direct_nhwc":   # the channels-last FFMA direct kernel (an HWC "direct" tile)
@@ -150,6 +152,8 @@ class ConvLayer:
     @property
     def precision(self) -> str | None:
         """Operand precision of a tensor-core plan (tf32 / 3xtf32 / bf16), else None."""
+        if self.algorithm == "winograd_nhwc":
+            return "fp32"
         for prefix in ("igemm_", "winograd_tc_"):
             if self.algorithm.startswith(prefix):
                 return self.algorithm[len(prefix):]
@@ -180,7 +184,7 @@ class ConvLayer:
         desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0,
                            2 if prec else 0)
         sp = C._stream_ptr(stream)
-        if self.algorithm.startswith("winograd_tc"):
+        if self.algorithm.startswith("winograd_tc") or self.algorithm == "winograd_nhwc":
             rc = N.lib().convio_winograd_filter_transform_tc(ctypes.byref(desc), self.e,
                                                              N.PRECISIONS[prec], C._ptr(w),
                                                              C._ptr(self._ws), sp)
@@ -201,7 +205,7 @@ class ConvLayer:
     def run(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """The conv kernel alone, on the prepared filter."""
         s = self.spec
-        if self.algorithm.startswith("winograd_tc"):
+        if self.algorithm.startswith("winograd_tc") or self.algorithm == "winograd_nhwc":
             if self._run_ws is None or self._run_ws.device != x.device:
                 info = C.query(tuple(x.shape), tuple(self.weight.shape), 1, s.pad, "HWC",
                                self.tile, self.algorithm)

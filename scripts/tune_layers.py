@@ -208,11 +208,12 @@ def tune_winograd_tc(shape, spec, prec, e, log):
     u = C.winograd_filter_transform_tc(w, e, prec)
     out = C.empty_act(shape.n, spec.k, shape.h_out, shape.w_out, "HWC", device="cuda")
     best, best_t, tried = None, _m.inf, 0
-    for z in [z for z in (64, 128, 256) if spec.k % z == 0]:
-        for nzt in (1, 2):
+    zs = (64, 128) if prec == "fp32" else (64, 128, 256)
+    for z in [z for z in zs if spec.k % z == 0]:
+        for nzt in ((1,) if prec == "fp32" else (1, 2)):
             tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
             info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
-                           f"winograd_tc_{prec}")
+                           "winograd_nhwc" if prec == "fp32" else f"winograd_tc_{prec}")
             if info["rc"]:
                 continue
             ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
@@ -240,7 +241,7 @@ def main():
     ap.add_argument("--exhaustive-cap", type=int, default=0)
     ap.add_argument("--algs", default="direct,direct_nhwc,winograd2,winograd4,igemm_3xtf32,igemm_tf32,"
                     "igemm_bf16,winograd_tc_3xtf32_e2,winograd_tc_3xtf32_e4,"
-                    "winograd_tc_tf32_e4,winograd_tc_bf16_e4")
+                    "winograd_tc_tf32_e4,winograd_tc_bf16_e4,winograd_nhwc_e2,winograd_nhwc_e4")
     ap.add_argument("--layers", default="")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
@@ -280,6 +281,9 @@ def main():
                 if spec.stride == 1 and spec.r == 3:
                     prec, _, e = alg[len("winograd_tc_"):].partition("_e")
                     cands[alg] = tune_winograd_tc(shape, spec, prec, int(e), log)
+            elif alg.startswith("winograd_nhwc_e"):
+                if spec.stride == 1 and spec.r == 3:
+                    cands[alg] = tune_winograd_tc(shape, spec, "fp32", int(alg[-1]), log)
             elif alg.startswith("winograd") and spec.stride == 1 and spec.r == 3:
                 e = int(alg[len("winograd"):])
                 cands[alg] = tune_one(shape, hw, "winograd", WinogradParams(e, 3), args.budget,

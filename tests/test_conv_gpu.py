@@ -304,6 +304,11 @@ WTC_CASES = [
     (2, 128, 28, 28, 256, 4, "bf16", 256),
     (3, 64, 13, 13, 64, 2, "bf16", 64),
     (2, 128, 14, 14, 256, 4, "3xtf32", 256),
+    # precision "fp32": the element-wise GEMMs on the CUDA cores (FFMA, batched)
+    (2, 64, 56, 56, 64, 4, "fp32", 64),
+    (2, 64, 28, 28, 128, 2, "fp32", 128),
+    (4, 256, 7, 7, 128, 4, "fp32", 128),       # ragged, several T blocks per xi
+    (10, 64, 56, 56, 64, 2, "fp32", 64),       # two L2 chunks
 ]
 # Reduced-precision Winograd: the operand rounding error is amplified by the
 # transforms (F(4,3)'s B^T / G entries up to 5 and 1/6..1/24), so the stated
@@ -317,7 +322,8 @@ def test_winograd_tc_matches_oracle(case):
     n, c, h, w, k, e, prec, z = case
     x, wt = _inputs(n, c, h, w, k, 3, 3)
     b = np.linspace(-0.25, 0.25, k).astype(np.float32)
-    tile = TileConfig(e, e, z, 16384, 1, 1, 2 if n % 2 else 1, layout="HWC", e=e)
+    nzt = 1 if prec == "fp32" else (2 if n % 2 else 1)
+    tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision=prec,
                            bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
