@@ -226,7 +226,7 @@ def tune_winograd_tc(shape, spec, prec, e, log):
             tried += 1
             if t < best_t:
                 best, best_t = tile, t
-    log(f"    winograd_tc_{prec}_e{e}: {tried} tiles, best {best} {best_t}")
+    log(f"    {'winograd_nhwc' if prec == 'fp32' else 'winograd_tc_' + prec}_e{e}: {tried} tiles, best {best} {best_t}")
     return {"tuner": {"best": best.to_dict() if best else None,
                       "seconds": best_t if best else None, "measurements": tried},
             "space": "exhaustive tcgen05 projection"}
