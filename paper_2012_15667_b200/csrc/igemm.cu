@@ -45,6 +45,14 @@ static PairFn pair_kernel_h(int bn, int kind) {
     return pair_kernel_kind<KIND_TF32, HALO>(bn);
 }
 
+// fold: halo + S taps per MMA, N = 3 K (K = 64 -> N = 192)
+static PairFn pair_kernel_fold(int n, int kind) {
+    if (n != 192) return nullptr;
+    if (kind == KIND_3XTF32) return &igemm_pair_kernel<192, KIND_3XTF32, true, false, true>;
+    if (kind == KIND_BF16) return &igemm_pair_kernel<192, KIND_BF16, true, false, true>;
+    return &igemm_pair_kernel<192, KIND_TF32, true, false, true>;
+}
+
 // tsa: 3xTF32 with the A operand in tensor memory (BN <= 128, no halo)
 static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
     if (tsa) {
@@ -118,7 +126,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     if (pair) {
         // persistent pair: one CTA per SM, the whole shared memory is the ring
         // (halo: two footprint slots first, the filter stages in the rest)
-        PairFn pfn = pair_kernel(bn, kind, pl->halo, pl->tsa);
+        PairFn pfn = pl->fold ? pair_kernel_fold(bn, kind) : pair_kernel(bn, kind, pl->halo, pl->tsa);
         if (!pfn)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
@@ -176,7 +184,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
 // persistent grid: one CTA pair per TPC (fewer if there are fewer work items)
 static int finish_pair_grid(IgemmPlan *pl) {
     const int pairs = (pl->blocks_per_group + 1) / 2;
-    const int64_t items = (int64_t)pl->groups * pairs * (pl->P.k / pl->bn);
+    const int64_t items = (int64_t)pl->groups * pairs * (pl->fold ? 1 : pl->P.k / pl->bn);
     if (items >= ((int64_t)1 << 31)) {
         set_error("too many work items");
         return CONVIO_EINFEASIBLE;
@@ -210,18 +218,20 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
     pl->halo = true;
+    // fold the S horizontal taps into one MMA when N = S * z fits (z = K, 3x3)
+    pl->fold = t->z == d->k && d->s == 3 && d->s * t->z == 192;
     pl->fpr = fpr;
     const int fp_rows = (t->y + d->r - 1) * fpr;
     pl->fp_bytes = fp_rows * 128;
     pl->a_slot = ((fp_rows + d->s - 1) * 128 + 1023) & ~1023;
     pl->na = 2;
-    int rc = plan_ring(pl, t->z, kind, t->s_b, true, reason, rlen);
+    int rc = plan_ring(pl, pl->fold ? d->s * t->z : t->z, kind, t->s_b, true, reason, rlen);
     if (rc) return rc;
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
     P.pad = d->pad; P.stride = 1; P.ks = d->r;
     P.bx = t->x; P.by = t->y; P.imgs = 1;
     P.tiles_x = (q + t->x - 1) / t->x; P.tiles_y = (p + t->y - 1) / t->y; P.img_groups = d->n;
-    P.cblocks = d->c / cb; P.kblocks = d->r * d->s * P.cblocks;
+    P.cblocks = d->c / cb; P.kblocks = (pl->fold ? d->r : d->r * d->s) * P.cblocks;
     pl->groups = 1;
     pl->blocks_per_group = P.tiles_x * P.tiles_y * P.img_groups;
     return finish_pair_grid(pl);
@@ -341,6 +351,16 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps};
     cuuint64_t ws[2] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.k * P.c * es_b};
     cuuint32_t wb[3] = {cb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1};
+    if (pl.fold) {   // packed filter as [R*S*K rows][C]: a kernel row's S*K rows are contiguous
+        cuuint64_t fd[2] = {(cuuint64_t)P.c, (cuuint64_t)taps * P.k};
+        cuuint64_t fs[1] = {(cuuint64_t)P.c * es_b};
+        cuuint32_t fb[2] = {cb, (cuuint32_t)(pl.bn / 2)};
+        if (bf)
+            return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
+                   encode_tensor_map_bf16_sw128(tw, 2, const_cast<void *>(wq), fd, fs, fb, es);
+        return encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true) &&
+               encode_tensor_map_tiled_ex(tw, 2, const_cast<void *>(wq), fd, fs, fb, es, true);
+    }
     if (bf)
         return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
                encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), wd, ws, wb, es);
@@ -364,7 +384,7 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.groups = pl.groups;
         PP.blocks_per_group = pl.blocks_per_group;
         PP.pairs_per_group = (pl.blocks_per_group + 1) / 2;
-        PP.nblocks = pl.P.k / pl.bn;
+        PP.nblocks = pl.fold ? 1 : pl.P.k / pl.bn;
         PP.items = PP.groups * PP.pairs_per_group * PP.nblocks;
         PP.fpr = pl.fpr;
         PP.fp_bytes = pl.fp_bytes;
@@ -412,7 +432,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages",
-             kind_name(kind), pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
+             kind_name(kind), pl.fold ? " CTA pair (persistent, halo footprint, 3 taps per MMA)" : pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
     return CONVIO_OK;
 }

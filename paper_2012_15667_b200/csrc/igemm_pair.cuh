@@ -107,6 +107,14 @@ __device__ __forceinline__ void tma_load_3d_pair(void *dst, uint64_t map, int c0
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, uint64_t map, int c0, int c1, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
+
 template <int BN, int KIND>
 __device__ __forceinline__ constexpr uint32_t idesc_m256() {
     return (1u << 4) | ((KIND == KIND_BF16 ? 1u : 2u) << 7) | ((KIND == KIND_BF16 ? 1u : 2u) << 10) |
@@ -227,7 +235,13 @@ __device__ __forceinline__ void convert_lo_range(uint32_t hi, uint32_t lo, int n
 // multiple of 8 rows).
 __device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return umma_desc_sw128(addr); }
 
-template <int BN, int KIND, bool HALO, bool TSA>
+// FOLD (halo tiles with S * K <= 256, K = z): the S horizontal taps of a kernel
+// row share one MMA of N = S * K -- B = [W(r,0); W(r,1); W(r,2)] rows, A = the
+// footprint view of row r -- and the epilogue adds the S column groups shifted
+// by s rows (warp shuffles: the s-shift stays inside a footprint row).  R MMAs
+// of N = 192 per channel block instead of R*S of N = 64 (48 cycles each on the
+// tensor core: 67 % of its rate at N = 64).
+template <int BN, int KIND, bool HALO, bool TSA, bool FOLD = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND, TSA>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
@@ -240,7 +254,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     // TSA (3xTF32, BN <= 128): A_hi / A_lo live in TMEM columns after the two
     // accumulators, NTA k-block slots of 64 columns (32 hi + 32 lo)
     static_assert(!TSA || (SPLIT && !HALO && BN <= 128), "TSA: 3xTF32, no halo, BN <= 128");
-    constexpr uint32_t TMEM_COLS = TSA ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
+    // (power-of-two allocation; FOLD's 2 x 192 columns take 512)
+    constexpr uint32_t TMEM_COLS = (TSA || 2 * BN > 256) ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
     constexpr uint32_t A_COL0 = 2 * BN;
     constexpr int NTA = TSA ? (512 - 2 * BN) / 64 : 1;
     constexpr int NCW = pair_conv_warps<BN, TSA>();   // converter warps (3xTF32)
@@ -316,7 +331,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         pair = rest % PP.pairs_per_group;
         grp = rest / PP.pairs_per_group;
     };
-    const int taps = P.ks * P.ks;
+    const int taps = FOLD ? P.ks : P.ks * P.ks;       // k-groups per channel block
+    constexpr int KOUT = FOLD ? BN / 3 : BN;          // output channels per work item
+    static_assert(!FOLD || (HALO && BN % 3 == 0), "FOLD: halo tiles, N = 3 * K");
 
     if (warp == 0) {
         if (lane == 0) {
@@ -334,6 +351,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 const int n0 = nb * BN + (int)rank * HB;
                 int tap = 0, cb = 0;
                 for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+                    // FOLD: the filter rows of kernel row `tap` (S taps x K channels) of
+                    // the packed [R*S*K][C] view; this CTA stages its HB of them
+                    const int frow = tap * P.ks * P.k + (int)rank * HB;
                     if (HALO && tap == 0) {
                         // the block's input footprint for channel block cb, once
                         if (ita >= NA) mbar_wait(aempty + sa, pha ^ 1);
@@ -361,11 +381,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     if constexpr (SPLIT) {   // own barrier: the converters need a local signal
                         mbar_arrive_expect_tx(full + s, cta_bytes);
                         if (!HALO) tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
-                        tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
+                        if (FOLD) tma_load_2d(b, map_w, cb * CB, frow, full + s);
+                        else tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
                     } else {                 // both CTAs' bytes complete on the leader's barrier
                         if (leader) mbar_arrive_expect_tx(full + s, 2 * cta_bytes);
                         if (!HALO) tma_load_4d_pair(a, map_x, cb * CB, xc, yc, img0, full + s);
-                        tma_load_3d_pair(b, map_w, cb * CB, n0, wc, full + s);
+                        if (FOLD) tma_load_2d_pair(b, map_w, cb * CB, frow, full + s);
+                        else tma_load_3d_pair(b, map_w, cb * CB, n0, wc, full + s);
                     }
                     // halo: channel block outer, taps inner (footprint reused by all taps)
                     if (HALO) {
@@ -437,7 +459,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const uint32_t st = smem_u32(bring + s * STAGE);
                     uint32_t a, b;
                     if (HALO) {
-                        const int r = tap / P.ks, sx = tap - r * P.ks;
+                        const int r = FOLD ? tap : tap / P.ks, sx = FOLD ? 0 : tap - r * P.ks;
                         a = fa + (uint32_t)((r * PP.fpr + sx) * 128);
                         b = st;
                     } else {
@@ -512,12 +534,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 valid = blk < PP.blocks_per_group && m < per_img * P.imgs && img < P.n && oy < P.p &&
                         ox < P.q;
             }
-            const int k0 = nb * BN;
+            const int k0 = nb * KOUT;
             float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = 0; c0 < KOUT; c0 += 32) {
                 float v[32];
                 tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                if constexpr (FOLD) {
+                    // y[p] = E[p][0:K] + E[p+1][K:2K] + E[p+2][2K:3K]: rows p+1, p+2 are
+                    // lanes +1, +2 of this warp (valid columns never cross a footprint row)
+#pragma unroll
+                    for (int sft = 1; sft < 3; ++sft) {
+                        float u[32];
+                        tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) +
+                                               (uint32_t)(acc * BN + sft * KOUT + c0), u);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += __shfl_down_sync(0xffffffffu, u[j], sft);
+                    }
+                }
                 if (valid) {
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {

@@ -70,7 +70,7 @@ __global__ void k_shift(const __grid_constant__ CUtensorMap tma, const __grid_co
 
 // Throughput probe: one thread issues `iters` x 4 MMAs (M=128, N=64, K=8 tf32)
 // reading the A operand at row offset `shift`; returns cycles per MMA.
-template <int NN, bool BF16>
+template <int NN, bool BF16, int ND = 1>
 __global__ void k_rate(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb,
                        long long *cycles, int shift, int iters) {
     extern __shared__ __align__(1024) uint8_t raw[];
@@ -106,8 +106,11 @@ __global__ void k_rate(const __grid_constant__ CUtensorMap tma, const __grid_con
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it)
             for (int kk = 0; kk < 4; ++kk) {
-                if constexpr (BF16) umma_bf16(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
-                else umma_tf32(tmem, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
+                // ND independent accumulators (D columns kk % ND * NN): does the tensor
+                // core overlap MMAs that do not chain on one accumulator?
+                const uint32_t dcol = tmem + (uint32_t)((kk % ND) * NN);
+                if constexpr (BF16) umma_bf16(dcol, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
+                else umma_tf32(dcol, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc, 1);
             }
         umma_commit(done);
         mbar_wait(done, 0);
@@ -118,15 +121,16 @@ __global__ void k_rate(const __grid_constant__ CUtensorMap tma, const __grid_con
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
 }
 
-template <int NN, bool BF16>
+template <int NN, bool BF16, int ND = 1>
 static void rate(const CUtensorMap &ma, const CUtensorMap &mb, long long *dcyc, int s) {
     const size_t smem = 1024 + ROWS * 128 + 256 * 128 + 64;
-    cudaFuncSetAttribute(k_rate<NN, BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_rate<NN, BF16, ND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     long long cyc = 0;
-    k_rate<NN, BF16><<<1, 128, smem>>>(ma, mb, dcyc, s, 4096);
+    k_rate<NN, BF16, ND><<<1, 128, smem>>>(ma, mb, dcyc, s, 4096);
     cudaDeviceSynchronize();
     cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
-    printf("rate: %s M128 N%3d shift=%2d: %lld cycles per MMA (K = 32 B)\n", BF16 ? "bf16" : "tf32", NN, s, cyc);
+    printf("rate: %s M128 N%3d shift=%2d accumulators=%d: %lld cycles per MMA (K = 32 B)\n",
+           BF16 ? "bf16" : "tf32", NN, s, ND, cyc);
 }
 
 int main() {
@@ -183,5 +187,8 @@ int main() {
     rate<64, true>(ma, mb, dcyc, 0);
     rate<128, true>(ma, mb, dcyc, 0);
     rate<256, true>(ma, mb, dcyc, 0);
+    rate<64, false, 2>(ma, mb, dcyc, 0);
+    rate<64, false, 4>(ma, mb, dcyc, 0);
+    rate<128, false, 2>(ma, mb, dcyc, 0);
     return 0;
 }

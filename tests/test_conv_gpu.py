@@ -260,6 +260,9 @@ HALO_CASES = [
     (3, 128, 28, 28, 256, "3xtf32", TileConfig(14, 8, 256, 32768, 2, 1, 2, layout="HWC")),  # ragged
     (2, 128, 14, 14, 128, "bf16", TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC")),   # ragged y
     (2, 32, 20, 20, 64, "tf32", TileConfig(6, 16, 64, 32768, 2, 1, 2, layout="HWC")),      # ragged x, y
+    # z = K = 64: the 3 horizontal taps folded into one MMA of N = 192
+    (2, 64, 56, 56, 64, "bf16", TileConfig(14, 8, 64, 32768, 2, 1, 2, layout="HWC")),
+    (3, 64, 28, 28, 64, "tf32", TileConfig(30, 4, 64, 32768, 2, 1, 2, layout="HWC")),
 ]
 
 
@@ -270,6 +273,7 @@ def test_igemm_halo_staging_matches_oracle(case):
     b = np.linspace(-0.25, 0.25, k).astype(np.float32)
     info = C.query(x.shape, wt.shape, 1, 1, "HWC", tile, f"igemm_{prec}")
     assert info["rc"] == 0 and "halo" in info["reason"], info
+    assert ("3 taps per MMA" in info["reason"]) == (tile.z == k == 64), info
     y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision=prec, bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
