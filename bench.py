@@ -242,7 +242,7 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, shard_range,
+        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, shard_range, tuned_table,
         gather_outputs, CUDA_CORE_ALGORITHMS)
     from paper_2012_15667_b200.device import winograd_gemm_flops
 
@@ -369,7 +369,7 @@ def main() -> None:
                 })
             return rows, fam
 
-    plans = load_plans(args.workload)
+    plans = load_plans(args.workload, n=n_local)
     arm = Arm(plans)
     flush = arm.work_bytes < 4 * L2_BYTES
     scratch = torch.empty(2 * L2_BYTES // 4, device=dev) if flush else None
@@ -436,7 +436,7 @@ def main() -> None:
         for vname, allowed in (("fp32_cuda_cores", CUDA_CORE_ALGORITHMS),
                                ("tf32_tcgen05", ("igemm_tf32", "winograd_tc_tf32")),
                                ("bf16_tcgen05", ("igemm_bf16", "winograd_tc_bf16"))):
-            vplans = load_plans(args.workload, allowed)
+            vplans = load_plans(args.workload, allowed, n=n_local)
             if not vplans:
                 continue
             varm = Arm(vplans)
@@ -556,6 +556,7 @@ def main() -> None:
                 "l2": ("flushed between steps" if flush else
                        f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
                 "tuned_plans": bool(plans),
+                "tuned_table": os.path.basename(tuned_table(args.workload, n_local)),
                 "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
                          "(FFMA), 3xTF32 tcgen05 implicit GEMM or 3xTF32 tcgen05 Winograd "
                          "(FP32-level GEMM accuracy)",

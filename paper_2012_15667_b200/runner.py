@@ -103,12 +103,25 @@ def candidate_algorithm(key: str) -> tuple[str, int | None]:
     return key, None
 
 
-def load_plans(workload: str, allowed=FP32_ALGORITHMS) -> dict:
+def tuned_table(workload: str, n: int | None = None) -> str:
+    """Path of the tuned table for ``workload``: the per-batch table
+    ``b200_<workload>_n<n>.json`` tuned at the local batch of a sharded run
+    (strong scaling gives each rank N/G images) when one exists, else the table
+    tuned at the workload's full batch."""
+    if n is not None:
+        path = os.path.join(TUNED_DIR, f"b200_{workload}_n{n}.json")
+        if os.path.exists(path):
+            return path
+    return os.path.join(TUNED_DIR, f"b200_{workload}.json")
+
+
+def load_plans(workload: str, allowed=FP32_ALGORITHMS, n: int | None = None) -> dict:
     """Tuned per-layer plans ``{name: {"algorithm", "tile", "e"}}`` (empty if untuned).
 
-    Each layer takes the fastest tuned candidate whose algorithm is in ``allowed``.
+    Each layer takes the fastest tuned candidate whose algorithm is in ``allowed``;
+    ``n`` (local batch) selects a per-batch table when one was tuned.
     """
-    path = os.path.join(TUNED_DIR, f"b200_{workload}.json")
+    path = tuned_table(workload, n)
     if not os.path.exists(path):
         return {}
     with open(path) as fh:

@@ -248,7 +248,10 @@ def main():
     warnings.simplefilter("ignore")
     torch.cuda.init()
     hw = b200_hw_model()
-    out_path = args.out or os.path.join(TUNED_DIR, f"b200_{args.workload}.json")
+    full_batch = {"resnet50": 256, "vgg16": 32, "single": 1}.get(args.workload)
+    out_path = args.out or os.path.join(
+        TUNED_DIR, f"b200_{args.workload}.json" if args.n == full_batch
+        else f"b200_{args.workload}_n{args.n}.json")
     result = {"workload": args.workload, "n_tune": args.n, "budget": args.budget,
               "hw_model": {"s": hw.s, "s_sm": hw.s_sm, "n_p": hw.n_p},
               "device": torch.cuda.get_device_name(), "layers": {}}

@@ -86,3 +86,18 @@ def test_tensor_core_winograd_and_bf16_plans(tmp_path, monkeypatch):
     layer = runner.ConvLayer(spec, None, fp32)
     assert layer.precision == "3xtf32" and layer.layout == "HWC" and layer.e == 4
     assert layer.filter_elems() == 36 * 64 * 256
+
+
+def test_per_batch_table_preferred_for_the_local_batch(tmp_path, monkeypatch):
+    d = tmp_path / "tuned"
+    d.mkdir()
+    t1 = TileConfig(2, 2, 256, 32768, 1, 1, 2, layout="HWC").to_dict()
+    t2 = TileConfig(1, 1, 128, 32768, 1, 1, 1, layout="HWC").to_dict()
+    (d / "b200_toy.json").write_text(json.dumps({"n_tune": 256, "layers": {"L": {"candidates": {
+        "igemm_3xtf32": {"tuner": {"best": t1, "seconds": 1e-3}}}}}}))
+    (d / "b200_toy_n32.json").write_text(json.dumps({"n_tune": 32, "layers": {"L": {"candidates": {
+        "igemm_3xtf32": {"tuner": {"best": t2, "seconds": 1e-4}}}}}}))
+    monkeypatch.setattr(runner, "TUNED_DIR", str(d))
+    assert runner.load_plans("toy")["L"]["tile"].z == 256
+    assert runner.load_plans("toy", n=32)["L"]["tile"].z == 128
+    assert runner.load_plans("toy", n=64)["L"]["tile"].z == 256   # no n64 table: full-batch one
