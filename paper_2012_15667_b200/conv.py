@@ -383,10 +383,10 @@ def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int 
     if tile is not None:
         ct = N.make_tile(tile, 2)
     elif prec == N.PREC_FP32:   # library default for the FFMA GEMM
-        ct = N.Tile(e, e, 128 if desc.k % 128 == 0 else 64, 32768, 1, 1, 1, 2, e)
+        ct = N.Tile(e, e, 128 if desc.k % 128 == 0 else 64, 8192, 1, 1, 1, 2, e)
     else:   # library default: widest N tile dividing K, CTA-pair kernel
         z = 256 if desc.k % 256 == 0 else (128 if desc.k % 128 == 0 else 64)
-        ct = N.Tile(e, e, z, 16384, 1, 1, 2, 2, e)
+        ct = N.Tile(e, e, z, 8192, 1, 1, 2, 2, e)
     alg = N.ALG_WINOGRAD_TC_TF32 + prec
     need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), ctypes.byref(ct), alg))
     if need < 0:

@@ -247,9 +247,10 @@ int direct_nhwc_batched_run(int bn, int s_b, int xi, int t_count, int c, int k, 
 
 static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 
-// L2 budget for one chunk's transformed tiles (V + M): about half the 126 MB
-// L2, leaving room for the input/output streams and the filter.
-static constexpr size_t kChunkL2Bytes = 56ull << 20;
+// L2 budget for one chunk's transformed tiles (V + M) = 4 KB x tile.s_b (the
+// tile's fast-memory size, here the L2 share of the chunk): s_b = 8192 (the
+// default) -> 32 MB, a quarter of the 126 MB L2 (two 63 MB partitions).
+static size_t chunk_l2_bytes(int s_b) { return (size_t)4096 * (size_t)std::max(s_b, 256); }
 
 struct WinoTcPlan {
     WinoTcGeom g;
@@ -285,7 +286,7 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     const int cb = kind == KIND_BF16 ? 64 : 32;
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
     int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));
-    int s_b = t ? t->s_b : 16384;
+    int s_b = t ? t->s_b : 8192;
     const bool pair = kind != KIND_FFMA && (t ? t->n_zt == 2 : true);
     if (kind == KIND_FFMA && !t) bn = d->k % 128 == 0 ? 128 : 64;
     if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2) ||
@@ -307,7 +308,7 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     g.tiles_y = (p + e - 1) / e; g.tiles_x = (q + e - 1) / e;
     const size_t tpi = (size_t)g.tiles_y * g.tiles_x;
     const size_t per_img = tpi * m * m * ((size_t)d->c * es + (size_t)d->k * 4);
-    int chunk = (int)std::max<size_t>(1, kChunkL2Bytes / per_img);
+    int chunk = (int)std::max<size_t>(1, chunk_l2_bytes(s_b) / per_img);
     chunk = std::min(chunk, d->n);
     // keep the GEMM's T axis within the TMA box-coordinate / grid limits
     while (chunk > 1 && (size_t)chunk * tpi > (size_t)1 << 24) chunk /= 2;
@@ -459,7 +460,7 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
         if (pl.kind == KIND_FFMA) {
-            rc = direct_nhwc_batched_run(pl.bn, pl.s_b, pl.m * pl.m, tc, g.c, g.k, (const float *)v,
+            rc = direct_nhwc_batched_run(pl.bn, 32768, pl.m * pl.m, tc, g.c, g.k, (const float *)v,
                                          (const float *)u, mm, st);
         } else {
             IgemmPlan gp;

@@ -209,23 +209,24 @@ def tune_winograd_tc(shape, spec, prec, e, log):
     out = C.empty_act(shape.n, spec.k, shape.h_out, shape.w_out, "HWC", device="cuda")
     best, best_t, tried = None, _m.inf, 0
     zs = (64, 128) if prec == "fp32" else (64, 128, 256)
-    for z in [z for z in zs if spec.k % z == 0]:
-        for nzt in ((1,) if prec == "fp32" else (1, 2)):
-            tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
-            info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
-                           "winograd_nhwc" if prec == "fp32" else f"winograd_tc_{prec}")
-            if info["rc"]:
-                continue
-            ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
-            try:
-                t = DT.device_time(lambda: C.conv_winograd_tc(xh, w, e=e, padding=spec.pad, tile=tile,
-                                                               precision=prec, u=u, out=out,
-                                                               workspace=ws))
-            except Exception:  # noqa: BLE001
-                continue
-            tried += 1
-            if t < best_t:
-                best, best_t = tile, t
+    for z, nzt, sb in [(z, nzt, sb) for z in zs if spec.k % z == 0
+                   for nzt in ((1,) if prec == "fp32" else (1, 2))
+                   for sb in (2048, 4096, 8192, 16384)]:   # L2 chunk = 4 KB x s_b
+        tile = TileConfig(e, e, z, sb, 1, 1, nzt, layout="HWC", e=e)
+        info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
+                       "winograd_nhwc" if prec == "fp32" else f"winograd_tc_{prec}")
+        if info["rc"]:
+            continue
+        ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
+        try:
+            t = DT.device_time(lambda: C.conv_winograd_tc(xh, w, e=e, padding=spec.pad, tile=tile,
+                                                           precision=prec, u=u, out=out,
+                                                           workspace=ws))
+        except Exception:  # noqa: BLE001
+            continue
+        tried += 1
+        if t < best_t:
+            best, best_t = tile, t
     log(f"    {'winograd_nhwc' if prec == 'fp32' else 'winograd_tc_' + prec}_e{e}: {tried} tiles, best {best} {best_t}")
     return {"tuner": {"best": best.to_dict() if best else None,
                       "seconds": best_t if best else None, "measurements": tried},
