@@ -296,6 +296,15 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (pl->pair) return finish_pair_grid(pl);
     pl->grid = dim3(d->k / pl->bn, P.tiles_x * P.tiles_y * P.img_groups, 1);
     if (pl->grid.y > 65535) return fail(CONVIO_EINFEASIBLE, "grid exceeds launch limits");
+    // split-K when the output tiles cannot fill the GPU (small batches, e.g. a
+    // rank's shard of a sharded batch): up to two CTAs per SM, >= 4 k-blocks each;
+    // partial tiles are added with fp32 atomics into the zeroed output (no ReLU)
+    const int64_t ctas = (int64_t)pl->grid.x * pl->grid.y;
+    const int target = 2 * device_sms();
+    P.splits = 1;
+    if (ctas < target && P.kblocks >= 8)
+        P.splits = (int)std::max<int64_t>(1, std::min<int64_t>({8, (target + ctas - 1) / ctas, P.kblocks / 4}));
+    pl->grid.z = P.splits;
     return CONVIO_OK;
 }
 
@@ -318,6 +327,7 @@ int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count
     P.tiles_x = (t_count + 127) / 128; P.tiles_y = 1; P.img_groups = xi;
     P.cblocks = c / cb; P.kblocks = P.cblocks;
     P.batched = 1;
+    P.splits = 1;
     pl->groups = xi;
     pl->blocks_per_group = P.tiles_x;
     if (pl->pair) return finish_pair_grid(pl);
@@ -395,6 +405,12 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         CONVIO_CUDA_TRY(cudaGetLastError());
         return CONVIO_OK;
     }
+    if (pl.P.splits > 1 && relu) {   // ReLU does not commute with the split sum
+        pl.P.splits = 1;
+        pl.grid.z = 1;
+    }
+    if (pl.P.splits > 1)
+        CONVIO_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)pl.P.n * pl.P.p * pl.P.q * pl.P.k * sizeof(float), stream));
     pl.fn<<<pl.grid, pl.threads, pl.smem, stream>>>(pl.P, tx, tw);
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
@@ -431,9 +447,11 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
-    snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages",
+    out->grid_z = pl.grid.z;
+    snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages%s",
              kind_name(kind), pl.fold ? " CTA pair (persistent, halo footprint, 3 taps per MMA)" : pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
-             pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages);
+             pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages,
+             pl.P.splits > 1 ? ", split-K" : "");
     return CONVIO_OK;
 }
 

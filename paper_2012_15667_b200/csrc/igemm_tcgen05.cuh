@@ -41,6 +41,7 @@ struct IgemmParams {
     int stages;
     int relu;
     int batched;               // 1: Winograd element-wise GEMMs (see header)
+    int splits;                // split-K factor (blockIdx.z = split; > 1 only without ReLU)
 };
 
 // operand kinds of the tcgen05 contraction
@@ -207,11 +208,16 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
+    // split-K (small grids): this CTA reduces k-blocks [kb_lo, kb_hi) and adds its
+    // partial tile into the zeroed output
+    const int kb_lo = (int)(((int64_t)P.kblocks * blockIdx.z) / P.splits);
+    const int kb_hi = (int)(((int64_t)P.kblocks * (blockIdx.z + 1)) / P.splits);
+    const int nkb = kb_hi - kb_lo;
     if (tid == 0) {
         // ---- TMA producer ---------------------------------------------------------
-        int s = 0, tap = 0, cb = 0;
+        int s = 0, tap = kb_lo / P.cblocks, cb = kb_lo - tap * P.cblocks;
         uint32_t ph = 0;
-        for (int kb = 0; kb < P.kblocks; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
             if (kb >= NS) mbar_wait(empty + s, ph ^ 1);
             const int r = tap / P.ks, sx = tap - r * P.ks;
             uint8_t *a = smem + s * STAGE;
@@ -235,7 +241,7 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
         constexpr uint32_t idesc = idesc_m128<BN, KIND>();
         int s = 0;
         uint32_t ph = 0;
-        for (int kb = 0; kb < P.kblocks; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(SPLIT ? conv + s : full + s, ph);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t a = smem_u32(smem + s * STAGE);
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
         constexpr int PER = (A_BYTES + B_BYTES) / 16 / NT;    // float4 per converter thread
         int s = 0;
         uint32_t ph = 0;
-        for (int kb = 0; kb < P.kblocks; ++kb) {
+        for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(full + s, ph);
             // explicit shared-window addressing (LDS/STS, not generic LD/ST);
             // all loads first so their latencies overlap
@@ -323,6 +329,7 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
     const int img = img0 + im, oy = oy0 + py, ox = ox0 + px;
     const bool valid = m < per_img * P.imgs && img < P.n && oy < P.p && ox < P.q;
     float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
+    const bool add_bias = P.bias && blockIdx.z == 0;
 #pragma unroll
     for (int c0 = 0; c0 < BN; c0 += 32) {
         float v[32];
@@ -331,10 +338,14 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
                 float4 o;
-                o.x = v[j] + (P.bias ? __ldg(P.bias + k0 + c0 + j) : 0.0f);
-                o.y = v[j + 1] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 1) : 0.0f);
-                o.z = v[j + 2] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 2) : 0.0f);
-                o.w = v[j + 3] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 3) : 0.0f);
+                o.x = v[j] + (add_bias ? __ldg(P.bias + k0 + c0 + j) : 0.0f);
+                o.y = v[j + 1] + (add_bias ? __ldg(P.bias + k0 + c0 + j + 1) : 0.0f);
+                o.z = v[j + 2] + (add_bias ? __ldg(P.bias + k0 + c0 + j + 2) : 0.0f);
+                o.w = v[j + 3] + (add_bias ? __ldg(P.bias + k0 + c0 + j + 3) : 0.0f);
+                if (P.splits > 1) {   // partial sums of the K range: fp32 vector atomics
+                    atomicAdd(reinterpret_cast<float4 *>(dst + c0 + j), o);
+                    continue;
+                }
                 if (P.relu) {
                     o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
                     o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);

@@ -406,3 +406,21 @@ def test_direct_nhwc_illegal_tiles():
     with pytest.raises(InfeasibleTileError):
         C.conv_direct(_dev(x, "HWC"), _dev(wt), padding=1,
                       tile=TileConfig(14, 7, 64, 32768, 1, 1, 1, layout="HWC"))
+
+
+@pytest.mark.parametrize("prec", ["3xtf32", "tf32"])
+def test_igemm_split_k_on_small_grids(prec):
+    # 2 images of a 7x7x512 layer: 4 output tiles -> the library splits K over CTAs
+    x, wt = _inputs(2, 512, 7, 7, 512, 3, 3)
+    b = np.linspace(-0.25, 0.25, 512).astype(np.float32)
+    tile = TileConfig(7, 7, 128, 32768, 1, 1, 1, layout="HWC")
+    info = C.query(x.shape, wt.shape, 1, 1, "HWC", tile, f"igemm_{prec}")
+    assert info["rc"] == 0 and "split-K" in info["reason"] and info["grid_z"] > 1, info
+    ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
+    tol = TOL_PREC.get(prec, tol_fp32(512))
+    y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision=prec, bias=_dev(b))
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= tol
+    # ReLU does not commute with the split sum: the library runs it unsplit
+    yr = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision=prec, bias=_dev(b),
+                      relu=True)
+    assert co.rel_err(yr.contiguous().cpu().numpy(), np.maximum(ref, 0)) <= tol
