@@ -248,8 +248,9 @@ def test_igemm_cta_pair_matches_oracle_and_single_cta(case):
                                       f"igemm_{prec}")["reason"]
     y1 = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=single,
                       precision=prec, bias=_dev(b))
-    # same products, same per-output summation order: identical up to MMA-internal order
-    assert co.rel_err(y.contiguous().cpu().numpy(), y1.contiguous().cpu().numpy()) <= 1e-5
+    # same products; the summation order differs by MMA-internal order and, on small
+    # grids, by the single-CTA kernel's split-K partial sums
+    assert co.rel_err(y.contiguous().cpu().numpy(), y1.contiguous().cpu().numpy()) <= 2 * tol_fp32(c)
 
 
 HALO_CASES = [
