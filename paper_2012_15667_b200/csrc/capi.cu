@@ -631,7 +631,8 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
             int p, q;
             int rc = check_desc(desc, &p, &q);
             if (rc) {
-                snprintf(out->reason, sizeof(out->reason), "%s", t_err);
+                strncpy(out->reason, t_err, sizeof(out->reason) - 1);
+                out->reason[sizeof(out->reason) - 1] = '\0';
                 return rc;
             }
             return direct_nhwc_query(desc, tile, out);
