@@ -204,8 +204,6 @@ def _traffic(tab: dict, workload: str, fam: dict, dom: str):
     per layer call, committed under profiles/*_traffic.json) of the dominant family's
     layers: {layer: bytes}; None if no capture is committed."""
     alg = dom.split()[0]
-    if alg.startswith("winograd F("):
-        alg = "winograd"
     out = {}
     for layer in sorted(fam["layers"]):
         t = tab.get(f"{workload}:{layer}:{alg}")
@@ -214,6 +212,17 @@ def _traffic(tab: dict, workload: str, fam: dict, dom: str):
         elif t is not None:
             out[layer] = t
     return out or None
+
+
+def _traffic_mean(by_layer: dict | None, fam: dict):
+    """One figure for `roofline.traffic`: DRAM bytes per launch averaged over the
+    dominant family's launches (each layer weighted by its launch count)."""
+    if not by_layer:
+        return None
+    cnt = fam.get("layer_launches", {})
+    num = sum(v * cnt.get(k, 1) for k, v in by_layer.items() if v is not None)
+    den = sum(cnt.get(k, 1) for k, v in by_layer.items() if v is not None)
+    return int(num / den) if den else None
 
 
 def main() -> None:
@@ -228,6 +237,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -294,18 +304,61 @@ def main() -> None:
                        for s, lay in zip(specs, self.layers)]
             self.work_bytes = sum(x.numel() * 4 for x in self.xs) + sum(y.numel() * 4 for y in self.ys)
 
-        def step(self, events=None):
+        def step(self, events=None, st=None):
+            st = st or stream
             launches = 0
             for i, layer in enumerate(self.layers):
-                layer.prepare(dev, stream)
+                layer.prepare(dev, st)
                 launches += 1
                 if events is not None:
-                    events[i][0].record(stream)
-                layer.run(self.xs[i], out=self.ys[i], stream=stream)
+                    events[i][0].record(st)
+                layer.run(self.xs[i], out=self.ys[i], stream=st)
                 if events is not None:
-                    events[i][1].record(stream)
+                    events[i][1].record(st)
                 launches += layer.launches
             return launches
+
+        def capture(self):
+            """One step (filter prep + all convs) captured as a CUDA graph: the
+            launches are replayed by the driver, no per-call host work."""
+            side = torch.cuda.Stream(dev)
+            side.wait_stream(stream)
+            with torch.cuda.stream(side):
+                self.step(st=side)
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self.step(st=side)
+            torch.cuda.synchronize(dev)
+            return g
+
+        def timed_graph(self, steps, graph, flush_buf=None):
+            """K device-timed graph replays (barrier + sync both sides)."""
+            barrier()
+            torch.cuda.synchronize(dev)
+            total = 0.0
+            if flush_buf is not None:
+                for k in range(steps):
+                    flush_buf.fill_(float(k))
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    graph.replay()
+                    b.record(stream)
+                    b.synchronize()
+                    total += a.elapsed_time(b)
+            else:
+                a = torch.cuda.Event(enable_timing=True)
+                b = torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                for _ in range(steps):
+                    graph.replay()
+                b.record(stream)
+                torch.cuda.synchronize(dev)
+                total = a.elapsed_time(b)
+            barrier()
+            torch.cuda.synchronize(dev)
+            return total
 
         def timed(self, steps, flush_buf=None):
             """K device-timed steps (barrier + sync both sides); per-layer events."""
@@ -353,7 +406,9 @@ def main() -> None:
                 else:
                     f_alg = f_dir
                     name = layer.algorithm
-                agg = fam.setdefault(name, {"ms": 0.0, "flops": 0.0, "launches": 0, "layers": set()})
+                agg = fam.setdefault(name, {"ms": 0.0, "flops": 0.0, "launches": 0, "layers": set(),
+                                            "layer_launches": {}})
+                agg["layer_launches"][s.name] = agg["layer_launches"].get(s.name, 0) + steps
                 agg["ms"] += sum(ts)
                 agg["flops"] += f_alg * steps
                 agg["launches"] += steps
@@ -381,7 +436,17 @@ def main() -> None:
     clocks = ClockSampler(local_rank)
     clocks.start()
     time.sleep(0.3)
-    total_ms, ev, launches = arm.timed(args.steps, scratch)
+    # eager pass: per-layer CUDA events (the roofline / per_layer breakdown)
+    eager_ms, ev, launches = arm.timed(args.steps, scratch)
+    total_ms = eager_ms
+    graph_used = False
+    if not args.no_graph:
+        # the timed value: the same step replayed as a CUDA graph (no host work per call)
+        g = arm.capture()
+        g.replay()
+        torch.cuda.synchronize(dev)
+        total_ms = arm.timed_graph(args.steps, g, scratch)
+        graph_used = True
     clk = clocks.stop()
     t_max_ms = max_over_ranks(total_ms)
     value = flops_all * args.steps / (t_max_ms / 1e3) / 1e9
@@ -416,7 +481,8 @@ def main() -> None:
             "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec == "bf16" else " / 2 (dense TF32 rate)")
                             if peaks.get("bf16_tflops") else "fallback 1.59 PFLOP/s bf16"),
-            "traffic": _traffic(traffic_tab, args.workload, d, dom),
+            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom), d),
+            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom),
         }
     else:
         peak = ffma_peak_tflops(torch, stream)
@@ -425,7 +491,8 @@ def main() -> None:
             "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4) if peak else None,
             "peak_source": "live FFMA probe (convio_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
-            "traffic": _traffic(traffic_tab, args.workload, d, dom),
+            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom), d),
+            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom),
         }
     roofline["layers"] = sorted(d["layers"])
     roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)
@@ -443,6 +510,12 @@ def main() -> None:
             for _ in range(2):
                 varm.step()
             vt, vev, _ = varm.timed(args.steps, scratch)
+            if not args.no_graph:   # same timing basis as the headline: graph replay
+                vg = varm.capture()
+                vg.replay()
+                torch.cuda.synchronize(dev)
+                vt = varm.timed_graph(args.steps, vg, scratch)
+                del vg
             vt = max_over_ranks(vt)
             rows, _ = varm.breakdown(vev, args.steps)
             variants[vname] = {
@@ -556,6 +629,9 @@ def main() -> None:
                 "l2": ("flushed between steps" if flush else
                        f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
                 "tuned_plans": bool(plans),
+                "step": ("filter prep + all convs replayed as one CUDA graph; per_layer / roofline "
+                         f"from an eager pass with per-layer events ({eager_ms / args.steps:.4f} ms/step)"
+                         if graph_used else "eager launches"),
                 "tuned_table": os.path.basename(tuned_table(args.workload, n_local)),
                 "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
                          "(FFMA), 3xTF32 tcgen05 implicit GEMM or 3xTF32 tcgen05 Winograd "

@@ -121,18 +121,33 @@ int launch_fit_cluster(const void *fn, int threads, size_t smem, int *regs) {
         *regs = 0;
         return 1;
     }
+    // cached per (fn, threads, smem): no runtime attribute calls once warm, so a
+    // conv call can be captured into a CUDA graph
+    static std::mutex mu;
+    static std::unordered_map<FitKey, FitVal, FitKeyHash> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    FitKey key{fn, threads, smem};
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *regs = it->second.regs;
+        return it->second.blocks;
+    }
+    int fit = 1;
     cudaFuncAttributes fa;
     if (cudaFuncGetAttributes(&fa, fn) != cudaSuccess) {
         cudaGetLastError();
-        return 0;
+        fa.numRegs = 0;
+        fit = 0;
     }
     *regs = fa.numRegs;
-    if ((int)smem > dev.max_smem_optin || fa.numRegs * threads > 65536) return 0;
-    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+    if ((int)smem > dev.max_smem_optin || fa.numRegs * threads > 65536) fit = 0;
+    // opt in to the device maximum once per kernel (any later config of it then fits)
+    if (fit && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dev.max_smem_optin) != cudaSuccess) {
         cudaGetLastError();
-        return 0;
+        fit = 0;
     }
-    return 1;
+    cache.emplace(key, FitVal{fit, *regs});
+    return fit;
 }
 
 int launch_fit(const void *fn, int threads, size_t smem, int *regs) {
