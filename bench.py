@@ -199,7 +199,7 @@ def load_profile_traffic() -> dict:
     return out
 
 
-def _traffic(tab: dict, workload: str, fam: dict, dom: str):
+def _traffic(tab: dict, workload: str, fam: dict, dom: str, n: int | None = None):
     """DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, one capture
     per layer call, committed under profiles/*_traffic.json) of the dominant family's
     layers: {layer: bytes}; None if no capture is committed."""
@@ -208,6 +208,8 @@ def _traffic(tab: dict, workload: str, fam: dict, dom: str):
     for layer in sorted(fam["layers"]):
         t = tab.get(f"{workload}:{layer}:{alg}")
         if isinstance(t, dict):
+            if n is not None and t.get("n") not in (None, n):
+                continue   # captured at another batch
             out[layer] = t.get("dram_bytes_per_call")
         elif t is not None:
             out[layer] = t
@@ -481,8 +483,8 @@ def main() -> None:
             "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
             "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec == "bf16" else " / 2 (dense TF32 rate)")
                             if peaks.get("bf16_tflops") else "fallback 1.59 PFLOP/s bf16"),
-            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom), d),
-            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom),
+            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom, n_local), d),
+            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom, n_local),
         }
     else:
         peak = ffma_peak_tflops(torch, stream)
@@ -491,8 +493,8 @@ def main() -> None:
             "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4) if peak else None,
             "peak_source": "live FFMA probe (convio_ffma_peak); MEASURED_PEAKS.json has no FP32 entry",
-            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom), d),
-            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom),
+            "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom, n_local), d),
+            "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom, n_local),
         }
     roofline["layers"] = sorted(d["layers"])
     roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)
