@@ -1,0 +1,99 @@
+"""Seeded randomized parity sweep of the tensor-core and channels-last kernels against
+the C oracle (fp64 accumulation): random batch / channels / map size / stride and a
+random legal tile of each kernel family (single CTA, CTA pair, A-in-TMEM pair, halo,
+halo + fold, split-K small grids, FFMA channels-last, tensor-core and FFMA Winograd).
+Every case goes through the C-ABI; tolerances as tests/test_conv_gpu.py.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import conv_oracle as co
+from paper_2012_15667_b200 import TileConfig
+from paper_2012_15667_b200 import conv as C
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"3xtf32": 2e-5, "tf32": 5e-3, "bf16": 3e-2, "fp32": 1e-5}
+TOL_WINO = {("3xtf32", 2): 1e-4, ("3xtf32", 4): 1e-3, ("fp32", 2): 1e-4, ("fp32", 4): 1e-3,
+            ("tf32", 2): 5e-3, ("tf32", 4): 2e-2, ("bf16", 2): 5e-2, ("bf16", 4): 1.5e-1}
+
+
+def _scale(c):
+    return max(1.0, (c * 9 / 576) ** 0.5)
+
+
+def _divisors(v):
+    return [d for d in range(1, v + 1) if v % d == 0]
+
+
+def _case(seed):
+    r = np.random.default_rng(seed)
+    kind = ["igemm", "igemm_pair", "igemm_tsa", "halo", "fold", "nhwc", "wino_tc", "wino_fp32"][seed % 8]
+    prec = {"nhwc": "fp32", "wino_fp32": "fp32", "igemm_tsa": "3xtf32"}.get(
+        kind, ["3xtf32", "tf32", "bf16"][r.integers(3)])
+    stride = 2 if kind in ("igemm", "igemm_pair", "igemm_tsa", "nhwc") and r.random() < 0.3 else 1
+    cmul = 64 if prec == "bf16" else 32
+    c = int(cmul * r.integers(1, 5))
+    k = 64 if kind == "fold" else int(64 * r.integers(1, 5))
+    h = int(r.choice([14, 20, 28, 30] if kind in ("halo", "fold") else [7, 12, 14, 20, 28, 30]))
+    n = int(r.integers(1, 5))
+    return kind, prec, n, c, h, k, stride, r
+
+
+def _tile(kind, prec, p, q, k, r):
+    if kind in ("halo", "fold"):
+        fprs = [f for f in (8, 16, 32) if f - 2 <= q + 2 and 128 // f <= p + 2]
+        fpr = int(r.choice(fprs))
+        return TileConfig(fpr - 2, 128 // fpr, 64 if kind == "fold" else k, 32768, 2, 1, 2, layout="HWC")
+    zs = [z for z in (64, 128, 256) if k % z == 0]
+    if kind == "igemm_tsa":
+        zs = [z for z in zs if z <= 128]
+    if kind == "nhwc":
+        zs = [z for z in zs if z <= 128]
+    z = int(r.choice(zs))
+    xs = [d for d in _divisors(q) if d <= 128]
+    x = int(r.choice(xs))
+    ys = [d for d in _divisors(p) if d * x <= 128]
+    y = int(r.choice(ys))
+    nzt = {"igemm": 1, "igemm_pair": 2, "igemm_tsa": 4, "nhwc": 1}[kind]
+    # s_b above the resident set x*y*z + footprint + 9z (the rule the device
+    # projection shares with the paper's model); it only sizes the TMA ring here
+    return TileConfig(x, y, z, 65536, 1, 1, nzt, layout="HWC")
+
+
+@pytest.mark.parametrize("seed", list(range(96)))
+def test_randomized_parity(seed):
+    kind, prec, n, c, h, k, stride, r = _case(seed)
+    g = np.random.default_rng(1000 + seed)
+    x = g.uniform(-1, 1, (n, c, h, h)).astype(np.float32)
+    w = (g.uniform(-1, 1, (k, c, 3, 3)) / np.sqrt(c * 9)).astype(np.float32)
+    b = g.uniform(-0.5, 0.5, k).astype(np.float32)
+    relu = bool(r.random() < 0.3)
+    xd = C.to_layout(torch.from_numpy(x).cuda(), "HWC")
+    wd = torch.from_numpy(w).cuda()
+    bd = torch.from_numpy(b).cuda()
+    if kind.startswith("wino"):
+        e = int(r.choice([2, 4]))
+        z = int(r.choice([zz for zz in ((64, 128) if kind == "wino_fp32" else (64, 128, 256))
+                          if k % zz == 0]))
+        nzt = 1 if kind == "wino_fp32" else int(r.choice([1, 2]))
+        tile = TileConfig(e, e, z, int(r.choice([2048, 8192, 16384])), 1, 1, nzt, layout="HWC", e=e)
+        y = C.conv_winograd_tc(xd, wd, e=e, padding=1, tile=tile, precision=prec, bias=bd, relu=relu)
+        tol = TOL_WINO[(prec, e)] * (_scale(c) if prec in ("3xtf32", "fp32") else 1.0)
+        stride = 1
+    else:
+        p = (h + 2 - 3) // stride + 1
+        tile = _tile(kind, prec, p, p, k, r)
+        if kind == "nhwc":
+            y = C.conv_direct(xd, wd, stride=stride, padding=1, tile=tile, bias=bd, relu=relu)
+        else:
+            y = C.conv_igemm(xd, wd, padding=1, stride=stride, tile=tile, precision=prec, bias=bd,
+                             relu=relu)
+        tol = TOL[prec] * (_scale(c) if prec in ("3xtf32", "fp32") else 1.0)
+    ref = co.c_direct_conv(x, w, stride, 1).astype(np.float64) + b[None, :, None, None]
+    if relu:
+        ref = np.maximum(ref, 0)
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= tol, (kind, prec, n, c, h, k, stride, tile, relu, err, tol)
