@@ -192,3 +192,69 @@ int main() {
     rate<128, false, 2>(ma, mb, dcyc, 0);
     return 0;
 }
+
+// ---- CTA-pair (cta_group::2) MMA rate: M = 256 over two CTAs, N = NN --------------
+#include "../../paper_2012_15667_b200/csrc/igemm_pair.cuh"
+
+template <int NN>
+__global__ void __cluster_dims__(2, 1, 1) k_rate_pair(long long *cycles, int iters) {
+    extern __shared__ __align__(1024) uint8_t raw[];
+    uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *a = sm;                       // 128 x 128 B (stale data: timing only)
+    uint8_t *b = sm + 128 * 128;           // NN/2 x 128 B
+    uint64_t *done = reinterpret_cast<uint64_t *>(b + 128 * 128);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(done + 1);
+    const int warp = threadIdx.x >> 5;
+    const uint32_t rank = cluster_ctarank();
+    if (threadIdx.x == 0) {
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(slot)), "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync_all();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (rank == 0 && threadIdx.x == 0) {
+        const uint64_t ad = umma_desc_sw128(smem_u32(a)), bd = umma_desc_sw128(smem_u32(b));
+        constexpr uint32_t idesc = idesc_m256<NN, KIND_TF32>();
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it)
+            for (int kk = 0; kk < 4; ++kk) umma_pair<KIND_TF32>(tmem, ad + kk * 2, bd + kk * 2, idesc, 1);
+        umma_commit_pair(done);
+        mbar_wait(done, 0);
+        *cycles = (clock64() - t0) / (4LL * iters);
+    } else if (rank == 1 && threadIdx.x == 0) {
+        mbar_wait(done, 0);
+    }
+    __syncwarp();
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    cluster_sync_all();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+}
+
+template <int NN>
+static void rate_pair(long long *dcyc) {
+    const size_t smem = 1024 + 2 * 128 * 128 + 64;
+    cudaFuncSetAttribute(k_rate_pair<NN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    long long cyc = 0;
+    k_rate_pair<NN><<<2, 128, smem>>>(dcyc, 4096);
+    cudaError_t e = cudaDeviceSynchronize();
+    cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
+    printf("rate: tf32 pair M256 N%3d: %lld cycles per MMA (K = 32 B) %s\n", NN, cyc,
+           e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int pair_rates() {
+    long long *dcyc;
+    cudaMalloc(&dcyc, 8);
+    rate_pair<64>(dcyc);
+    rate_pair<128>(dcyc);
+    rate_pair<192>(dcyc);
+    rate_pair<256>(dcyc);
+    return 0;
+}
+static int pair_rates_done = (pair_rates(), 0);
