@@ -46,7 +46,8 @@ def _tile(kind, prec, p, q, k, r):
     if kind in ("halo", "fold"):
         fprs = [f for f in (8, 16, 32) if f - 2 <= q + 2 and 128 // f <= p + 2]
         fpr = int(r.choice(fprs))
-        return TileConfig(fpr - 2, 128 // fpr, 64 if kind == "fold" else k, 32768, 2, 1, 2, layout="HWC")
+        z = 64 if kind == "fold" else int(r.choice([z for z in (64, 128, 256) if k % z == 0]))
+        return TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, 2, layout="HWC")
     zs = [z for z in (64, 128, 256) if k % z == 0]
     if kind == "igemm_tsa":
         zs = [z for z in zs if z <= 128]
