@@ -135,7 +135,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
                                            : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) * mult;
         const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : 0;
-        const size_t budget = 227 * 1024 - 1024 - 1024;
+        const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
         // small stages (narrow BN, no lo copy) need many in flight to cover the
@@ -147,7 +147,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         pl->pair = true;
         pl->pfn = pfn;
         pl->fn = nullptr;
-        pl->smem = a_ring + stages * stage_bytes + 1024 + 1024;
+        pl->smem = a_ring + stages * stage_bytes + 1024 + 1024 + kPairEpiBytes;
         pl->bn = bn;
         pl->kind = kind;
         pl->threads = kind == KIND_3XTF32 ? ((bn >= 256 || pl->tsa) ? 384 : 512) : 256;

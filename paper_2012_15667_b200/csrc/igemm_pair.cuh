@@ -40,6 +40,9 @@
 
 namespace convio {
 
+// epilogue transpose buffer after the ring + barriers: 4 warps x 32 rows x 36 floats
+constexpr size_t kPairEpiBytes = 4 * 32 * 36 * sizeof(float);
+
 struct PairParams {
     IgemmParams g;          // geometry as in the single-CTA kernel
     int groups;             // 1 (conv) or xi (batched Winograd GEMMs)
@@ -509,6 +512,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int q = warp - 4;                       // TMEM lane quadrant
         const int m = q * 32 + lane;                  // pixel row of this CTA's A block
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+        float *stg = reinterpret_cast<float *>(bring + NS * STAGE + 1024) + q * (32 * 36);
         int t = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
             int grp, pair, nb;
@@ -536,6 +540,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             }
             const int k0 = nb * KOUT;
             float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
+            // coalesced stores: each warp transposes its 32 rows x 32 columns through
+            // shared memory so 8 lanes write one row's 128 contiguous bytes (a
+            // lane-per-row STG.128 touches 32 lines per instruction and made the
+            // epilogue, not the MMA, the limit of short-K tiles: Winograd GEMMs)
+            const int cc = 4 * (lane & 7);
+            float *drow[8];
+            bool vrow[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int row = i * 4 + (lane >> 3);
+                drow[i] = reinterpret_cast<float *>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), row));
+                vrow[i] = __shfl_sync(0xffffffffu, (int)valid, row) != 0;
+            }
 #pragma unroll 1
             for (int c0 = 0; c0 < KOUT; c0 += 32) {
                 float v[32];
@@ -552,21 +570,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         for (int j = 0; j < 32; ++j) v[j] += __shfl_down_sync(0xffffffffu, u[j], sft);
                     }
                 }
-                if (valid) {
 #pragma unroll
-                    for (int j = 0; j < 32; j += 4) {
-                        float4 o;
-                        o.x = v[j] + (P.bias ? __ldg(P.bias + k0 + c0 + j) : 0.0f);
-                        o.y = v[j + 1] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 1) : 0.0f);
-                        o.z = v[j + 2] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 2) : 0.0f);
-                        o.w = v[j + 3] + (P.bias ? __ldg(P.bias + k0 + c0 + j + 3) : 0.0f);
-                        if (P.relu) {
-                            o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
-                            o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-                        }
-                        *reinterpret_cast<float4 *>(dst + c0 + j) = o;
+                for (int j = 0; j < 32; j += 4)
+                    *reinterpret_cast<float4 *>(stg + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                __syncwarp();
+                const float4 bv = P.bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int row = i * 4 + (lane >> 3);
+                    float4 o = *reinterpret_cast<const float4 *>(stg + row * 36 + cc);
+                    o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
+                    if (P.relu) {
+                        o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
+                        o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
                     }
+                    if (vrow[i]) *reinterpret_cast<float4 *>(drow[i] + c0 + cc) = o;
                 }
+                __syncwarp();
             }
             // accumulator buffer drained: tell the leader's MMA issuer
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");

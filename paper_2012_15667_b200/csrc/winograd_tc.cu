@@ -95,25 +95,57 @@ struct WinoTcGeom {
     int img0, imgs;      // chunk
 };
 
-// Step 1: one thread per (tile, channel); channels fastest so every load and
-// every V store is a coalesced 128-B warp access.
+// per-component application of a 1-D transform to 4 channels at once
+template <int N, int NO, typename F>
+__device__ __forceinline__ void apply4(const float4 (&d)[N], float4 (&o)[NO], F f) {
+    float a[N], r[NO];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) a[i] = reinterpret_cast<const float *>(&d[i])[q];
+        f(a, r);
+#pragma unroll
+        for (int i = 0; i < NO; ++i) reinterpret_cast<float *>(&o[i])[q] = r[i];
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void store4(T *p, float4 v) {
+    if constexpr (sizeof(T) == 2) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t *>(&lo);
+        u.y = *reinterpret_cast<uint32_t *>(&hi);
+        *reinterpret_cast<uint2 *>(p) = u;
+    } else {
+        *reinterpret_cast<float4 *>(p) = v;
+    }
+}
+
+// Step 1: one thread per (tile, 4 channels); channels fastest so every LDG.128
+// and every V store is a coalesced warp access (C % 32 == 0 by the plan); each
+// channel sees the scalar B^T d B of the one-channel form.
+// (The first version -- one thread per channel, 64-bit index math -- was
+// instruction-issue bound at ~990 instructions per warp-element.)
 template <int E, typename T>
-__global__ void __launch_bounds__(256) winograd_input_tc_kernel(const float *__restrict__ x,
+__global__ void __launch_bounds__(128) winograd_input_tc_kernel(const float *__restrict__ x,
                                                                 T *__restrict__ v, WinoTcGeom g) {
     constexpr int M = WinoTf<E>::M;
-    const int64_t tpi = (int64_t)g.tiles_y * g.tiles_x;
-    const int64_t t_count = tpi * g.imgs;
-    const int64_t total = t_count * g.c;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int c = (int)(i % g.c);
-        const int64_t t = i / g.c;
-        const int img = (int)(t / tpi);
-        const int rem = (int)(t - img * tpi);
+    const int c4n = g.c >> 2;
+    const int tpi = g.tiles_y * g.tiles_x;
+    const int t_count = tpi * g.imgs;
+    const int total = t_count * c4n;
+    const int64_t xi_stride = (int64_t)t_count * g.c;
+    const int row4 = g.w * c4n;   // float4 per input row
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int t = i / c4n;
+        const int c4 = i - t * c4n;
+        const int img = t / tpi;
+        const int rem = t - img * tpi;
         const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
         const int iy0 = ty * E - g.pad, ix0 = tx * E - g.pad;
-        const float *xb = x + ((int64_t)(g.img0 + img) * g.h * g.w) * g.c + c;
-        float d[M][M];
+        const float4 *xb = reinterpret_cast<const float4 *>(x + (int64_t)(g.img0 + img) * g.h * g.w * g.c) + c4;
+        float4 d[M][M];
 #pragma unroll
         for (int a = 0; a < M; ++a) {
             const int iy = iy0 + a;
@@ -121,28 +153,27 @@ __global__ void __launch_bounds__(256) winograd_input_tc_kernel(const float *__r
 #pragma unroll
             for (int b = 0; b < M; ++b) {
                 const int ix = ix0 + b;
-                d[a][b] = (rok && ix >= 0 && ix < g.w) ? __ldg(xb + ((int64_t)iy * g.w + ix) * g.c) : 0.0f;
+                d[a][b] = (rok && ix >= 0 && ix < g.w) ? __ldg(xb + iy * row4 + ix * c4n)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        // columns: tmp[a][j] = (B^T d)[a][j]
-        float tmp[M][M];
+        float4 tmp[M][M];   // tmp[a][j] = (B^T d)[a][j]
 #pragma unroll
         for (int j = 0; j < M; ++j) {
-            float col[M], o[M];
+            float4 col[M], o[M];
 #pragma unroll
             for (int a = 0; a < M; ++a) col[a] = d[a][j];
-            WinoTf<E>::bt(col, o);
+            apply4<M, M>(col, o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
 #pragma unroll
             for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
         }
-        const int64_t xi_stride = t_count * g.c;
-        T *vp = v + t * g.c + c;
+        T *vp = v + (int64_t)t * g.c + 4 * c4;
 #pragma unroll
         for (int a = 0; a < M; ++a) {
-            float o[M];
-            WinoTf<E>::bt(tmp[a], o);   // rows: (B^T d B)[a][b]
+            float4 o[M];
+            apply4<M, M>(tmp[a], o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
 #pragma unroll
-            for (int b = 0; b < M; ++b) store_elem(vp + (a * M + b) * xi_stride, o[b]);
+            for (int b = 0; b < M; ++b) store4(vp + (a * M + b) * xi_stride, o[b]);
         }
     }
 }
@@ -182,46 +213,51 @@ __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__rest
 // Step 4: one thread per (tile, output channel), k fastest (coalesced M
 // loads and NHWC stores); bias + ReLU fused; ragged tiles masked.
 template <int E>
-__global__ void __launch_bounds__(256) winograd_output_tc_kernel(const float *__restrict__ mm,
+__global__ void __launch_bounds__(128) winograd_output_tc_kernel(const float *__restrict__ mm,
                                                                  const float *__restrict__ bias,
                                                                  float *__restrict__ y, WinoTcGeom g,
                                                                  int relu) {
+    // one thread per (tile, 4 output channels), LDG.128 / STG.128, 32-bit index math
     constexpr int M = WinoTf<E>::M;
-    const int64_t tpi = (int64_t)g.tiles_y * g.tiles_x;
-    const int64_t t_count = tpi * g.imgs;
-    const int64_t total = t_count * g.k;
-    const int64_t xi_stride = t_count * g.k;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int k = (int)(i % g.k);
-        const int64_t t = i / g.k;
-        const int img = (int)(t / tpi);
-        const int rem = (int)(t - img * tpi);
+    const int k4n = g.k >> 2;
+    const int tpi = g.tiles_y * g.tiles_x;
+    const int t_count = tpi * g.imgs;
+    const int total = t_count * k4n;
+    const int64_t xi_stride = (int64_t)t_count * g.k;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const int t = i / k4n;
+        const int k4 = i - t * k4n;
+        const int img = t / tpi;
+        const int rem = t - img * tpi;
         const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
-        const float *mp = mm + t * g.k + k;
-        float tmp[E][M];
+        const float *mp = mm + (int64_t)t * g.k + 4 * k4;
+        float4 tmp[E][M];
 #pragma unroll
         for (int b = 0; b < M; ++b) {
-            float col[M], o[E];
+            float4 col[M], o[E];
 #pragma unroll
-            for (int a = 0; a < M; ++a) col[a] = __ldg(mp + (a * M + b) * xi_stride);
-            WinoTf<E>::at(col, o);
+            for (int a = 0; a < M; ++a) col[a] = __ldg(reinterpret_cast<const float4 *>(mp + (a * M + b) * xi_stride));
+            apply4<M, E>(col, o, [](const float (&in)[M], float (&out)[E]) { WinoTf<E>::at(in, out); });
 #pragma unroll
             for (int a = 0; a < E; ++a) tmp[a][b] = o[a];
         }
-        const float bv = bias ? __ldg(bias + k) : 0.0f;
-        float *yb = y + ((int64_t)(g.img0 + img) * g.p * g.q) * g.k + k;
+        const float4 bv = bias ? __ldg(reinterpret_cast<const float4 *>(bias) + k4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 *yb = reinterpret_cast<float4 *>(y + (int64_t)(g.img0 + img) * g.p * g.q * g.k) + k4;
 #pragma unroll
         for (int a = 0; a < E; ++a) {
-            float o[E];
-            WinoTf<E>::at(tmp[a], o);
+            float4 o[E];
+            apply4<M, E>(tmp[a], o, [](const float (&in)[M], float (&out)[E]) { WinoTf<E>::at(in, out); });
             const int oy = ty * E + a;
 #pragma unroll
             for (int b = 0; b < E; ++b) {
                 const int ox = tx * E + b;
                 if (oy < g.p && ox < g.q) {
-                    float r = o[b] + bv;
-                    yb[((int64_t)oy * g.q + ox) * g.k] = relu ? fmaxf(r, 0.0f) : r;
+                    float4 rv = make_float4(o[b].x + bv.x, o[b].y + bv.y, o[b].z + bv.z, o[b].w + bv.w);
+                    if (relu) {
+                        rv.x = fmaxf(rv.x, 0.f); rv.y = fmaxf(rv.y, 0.f);
+                        rv.z = fmaxf(rv.z, 0.f); rv.w = fmaxf(rv.w, 0.f);
+                    }
+                    yb[(oy * g.q + ox) * k4n] = rv;
                 }
             }
         }
@@ -340,8 +376,8 @@ static int launch_filter_tc(const WinoTcPlan &pl, const float *w, void *u, cudaS
     return CONVIO_OK;
 }
 
-static int grid_for(int64_t work) {
-    return (int)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 16));
+static int grid_for(int64_t work, int threads = 256) {
+    return (int)std::max<int64_t>(1, std::min<int64_t>((work + threads - 1) / threads, 148 * 16));
 }
 
 int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t precision,
@@ -449,13 +485,13 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         g.img0 = img0;
         g.imgs = std::min(pl.chunk_imgs, desc->n - img0);
         const int tc = g.imgs * tpi;
-        const int gin = grid_for((int64_t)tc * g.c), gout = grid_for((int64_t)tc * g.k);
+        const int gin = grid_for((int64_t)tc * (g.c / 4), 128), gout = grid_for((int64_t)tc * (g.k / 4), 128);
         if (pl.e == 2) {
-            if (bf) winograd_input_tc_kernel<2, __nv_bfloat16><<<gin, 256, 0, st>>>(x, (__nv_bfloat16 *)v, g);
-            else winograd_input_tc_kernel<2, float><<<gin, 256, 0, st>>>(x, (float *)v, g);
+            if (bf) winograd_input_tc_kernel<2, __nv_bfloat16><<<gin, 128, 0, st>>>(x, (__nv_bfloat16 *)v, g);
+            else winograd_input_tc_kernel<2, float><<<gin, 128, 0, st>>>(x, (float *)v, g);
         } else {
-            if (bf) winograd_input_tc_kernel<4, __nv_bfloat16><<<gin, 256, 0, st>>>(x, (__nv_bfloat16 *)v, g);
-            else winograd_input_tc_kernel<4, float><<<gin, 256, 0, st>>>(x, (float *)v, g);
+            if (bf) winograd_input_tc_kernel<4, __nv_bfloat16><<<gin, 128, 0, st>>>(x, (__nv_bfloat16 *)v, g);
+            else winograd_input_tc_kernel<4, float><<<gin, 128, 0, st>>>(x, (float *)v, g);
         }
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
@@ -471,9 +507,9 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         }
         if (rc) return rc;
         if (pl.e == 2)
-            winograd_output_tc_kernel<2><<<gout, 256, 0, st>>>(mm, bias, y, g, relu);
+            winograd_output_tc_kernel<2><<<gout, 128, 0, st>>>(mm, bias, y, g, relu);
         else
-            winograd_output_tc_kernel<4><<<gout, 256, 0, st>>>(mm, bias, y, g, relu);
+            winograd_output_tc_kernel<4><<<gout, 128, 0, st>>>(mm, bias, y, g, relu);
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
     }
