@@ -191,14 +191,15 @@ int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e,
 /* Winograd F(e x e, 3 x 3), e in {2, 4}, with step 3 (the element-wise
  * products summed over channels, dag.py:384-401) as (e+2)^2 batched GEMMs
  * M[xi][t][k] = sum_c V[xi][t][c] U[xi][k][c] on tcgen05 in one launch, and
- * the input/output transforms as HBM-streaming kernels; the batch is chunked
- * so each chunk's V and M stay in L2.  NHWC, stride 1, C % 32 (% 64 for
+ * the input/output transforms as HBM-streaming kernels; the batch is run in
+ * chunks of V + M <= 16 KB x tile->s_b bytes.  NHWC, stride 1, C % 32 (% 64 for
  * BF16) == 0; precision CONVIO_PREC_FP32 runs the element-wise GEMMs on the
  * CUDA cores (the channels-last FFMA kernel in batched mode, z in {64, 128},
  * U laid out [xi][c][k] as convio_winograd_filter_transform writes it);
  * tile->z in {64,128,256} is the GEMM's N tile, tile->s_b sizes
- * the TMA ring, tile->n_zt in {1, 2} picks the single-CTA / CTA-pair GEMM
- * kernel, tile->e must equal e (tile == NULL: defaults).
+ * the chunk, tile->n_zt in {1, 2, 4} picks the single-CTA / CTA-pair /
+ * CTA-pair-with-A-in-TMEM (3xTF32, z <= 128) GEMM kernel, tile->e must equal
+ * e (tile == NULL: defaults).
  * Replaces plan_winograd_dataflow + simulate (dataflow.py:253-338). */
 int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,
                           int32_t precision, const float *x, const void *w, int32_t w_is_transformed,

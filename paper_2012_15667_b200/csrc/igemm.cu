@@ -310,7 +310,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
 
 // M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c]: V is an "image" per xi of
 // 1 x T pixels, U the filter of tap xi.
-int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count, int c, int k,
+int plan_igemm_batched(int kind, int bn, int s_b, bool pair, bool tsa, int xi, int t_count, int c, int k,
                        IgemmPlan *pl, char *reason, size_t rlen) {
     const int cb = kind == KIND_BF16 ? 64 : 32;
     if (c % cb)
@@ -319,6 +319,7 @@ int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "K=%d is not a multiple of z=%d", k, bn);
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
+    pl->tsa = pair && tsa;
     int rc = plan_ring(pl, bn, kind, s_b, pair, reason, rlen);
     if (rc) return rc;
     P.n = xi; P.c = c; P.h = 1; P.w = t_count; P.k = k; P.p = 1; P.q = t_count;

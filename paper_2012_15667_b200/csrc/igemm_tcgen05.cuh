@@ -385,7 +385,7 @@ struct IgemmPlan {
 };
 
 // M[xi][t][k] = sum_c V[xi][t][c] * U[xi][k][c] (Winograd step 3) in one launch
-int plan_igemm_batched(int kind, int bn, int s_b, bool pair, int xi, int t_count, int c, int k,
+int plan_igemm_batched(int kind, int bn, int s_b, bool pair, bool tsa, int xi, int t_count, int c, int k,
                        IgemmPlan *pl, char *reason, size_t rlen);
 int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
                  cudaStream_t stream);

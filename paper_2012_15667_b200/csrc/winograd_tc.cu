@@ -213,7 +213,7 @@ __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__rest
 // Step 4: one thread per (tile, output channel), k fastest (coalesced M
 // loads and NHWC stores); bias + ReLU fused; ragged tiles masked.
 template <int E>
-__global__ void __launch_bounds__(128) winograd_output_tc_kernel(const float *__restrict__ mm,
+__global__ void __launch_bounds__(128, 4) winograd_output_tc_kernel(const float *__restrict__ mm,
                                                                  const float *__restrict__ bias,
                                                                  float *__restrict__ y, WinoTcGeom g,
                                                                  int relu) {
@@ -283,15 +283,19 @@ int direct_nhwc_batched_run(int bn, int s_b, int xi, int t_count, int c, int k, 
 
 static inline size_t al256(size_t b) { return (b + 255) & ~size_t(255); }
 
-// L2 budget for one chunk's transformed tiles (V + M) = 4 KB x tile.s_b (the
-// tile's fast-memory size, here the L2 share of the chunk): s_b = 8192 (the
-// default) -> 32 MB, a quarter of the 126 MB L2 (two 63 MB partitions).
-static size_t chunk_l2_bytes(int s_b) { return (size_t)4096 * (size_t)std::max(s_b, 256); }
+// Budget for one chunk's transformed tiles (V + M) = 16 KB x tile.s_b: s_b =
+// 2048 -> 32 MB (L2-resident chunks), 8192 (the default) -> 128 MB, 32768 ->
+// 512 MB (the whole ResNet-50 batch at once).  Measured (scripts/
+// probe_wtc_chunk.py, 3xTF32 F(4,3), batch 256): the L2-resident chunks lose --
+// every chunk pays three launch ramps and wave tails, and the dirty V / M lines
+// are written back to HBM anyway -- res3 0.311 ms at 64 MB vs 0.206 ms unchunked,
+// res4 0.237 vs 0.161, res5 0.180 vs 0.120; the tuner picks s_b per layer.
+static size_t chunk_l2_bytes(int s_b) { return (size_t)16384 * (size_t)std::max(s_b, 64); }
 
 struct WinoTcPlan {
     WinoTcGeom g;
     int e, m, kind, bn, s_b;
-    bool pair;
+    bool pair, tsa;   // CTA pair (n_zt 2 or 4); 3xTF32 A operand in TMEM (n_zt 4)
     int chunk_imgs;
     size_t u_bytes, v_bytes, m_bytes;   // per chunk for V and M
 };
@@ -323,12 +327,16 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
     int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));
     int s_b = t ? t->s_b : 8192;
-    const bool pair = kind != KIND_FFMA && (t ? t->n_zt == 2 : true);
+    const bool pair = kind != KIND_FFMA && (t ? (t->n_zt == 2 || t->n_zt == 4) : true);
+    const bool tsa = t && t->n_zt == 4;
+    if (tsa && (kind != KIND_3XTF32 || (t->z != 64 && t->z != 128)))
+        return fail(CONVIO_EINFEASIBLE, "A-in-TMEM (n_zt = 4) Winograd GEMMs need 3xTF32 and z <= 128");
     if (kind == KIND_FFMA && !t) bn = d->k % 128 == 0 ? 128 : 64;
-    if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2) ||
+    if (t && (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2 && t->n_zt != 4) ||
               (kind == KIND_FFMA && t->n_zt != 1)))
         return fail(CONVIO_EINFEASIBLE,
-                    "Winograd tiles take n_xt = n_yt = 1 and n_zt in {1, 2 (tcgen05 CTA pair)}");
+                    "Winograd tiles take n_xt = n_yt = 1 and n_zt in {1, 2 (tcgen05 CTA pair), "
+                    "4 (pair, A in TMEM)}");
     if (kind == KIND_FFMA && bn != 64 && bn != 128)
         return fail(CONVIO_EINFEASIBLE, "FFMA Winograd GEMM needs z in {64, 128}, got %d", bn);
     if (t && t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
@@ -350,6 +358,7 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     while (chunk > 1 && (size_t)chunk * tpi > (size_t)1 << 24) chunk /= 2;
     if ((size_t)chunk * tpi >= ((size_t)1 << 31)) return fail(CONVIO_EINFEASIBLE, "too many tiles");
     pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b; pl->pair = pair;
+    pl->tsa = tsa;
     pl->chunk_imgs = chunk;
     pl->u_bytes = al256((size_t)m * m * d->k * d->c * es);
     pl->v_bytes = al256((size_t)m * m * chunk * tpi * d->c * es);
@@ -389,7 +398,7 @@ int wino_tc_query(const convio_conv_desc *d, const convio_tile *t, int32_t preci
     IgemmPlan gp;
     const int tc = pl.chunk_imgs * pl.g.tiles_y * pl.g.tiles_x;
     if (pl.kind != KIND_FFMA) {
-        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, d->c, d->k, &gp,
+        rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.tsa, pl.m * pl.m, tc, d->c, d->k, &gp,
                                 out->reason, sizeof(out->reason));
         if (rc) return rc;
         out->grid_x = gp.grid.x; out->grid_y = gp.grid.y; out->grid_z = gp.grid.z;
@@ -500,7 +509,7 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
                                          (const float *)u, mm, st);
         } else {
             IgemmPlan gp;
-            rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.m * pl.m, tc, g.c, g.k, &gp, why,
+            rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.tsa, pl.m * pl.m, tc, g.c, g.k, &gp, why,
                                     sizeof(why));
             if (rc) return rc;
             rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);

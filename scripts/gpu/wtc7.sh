@@ -1,0 +1,15 @@
+timeout 300 python scripts/probe_wtc_chunk.py --layer res3_3x3 --z 128 --nzt 4 --e 4 --sweep 8192,16384,32768 2>&1 | grep res3
+timeout 300 python scripts/probe_wtc_chunk.py --layer res5_3x3 --z 256 --nzt 2 --e 4 --sweep 16384,32768 2>&1 | grep res5
+timeout 300 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file gpurun_out/wtc7_launches.csv python scripts/probe_wtc_chunk.py --layer res3_3x3 --z 128 --nzt 4 --e 4 --one 16384 > /dev/null 2>&1
+python - <<'PY'
+import csv
+rows=list(csv.reader(open('gpurun_out/wtc7_launches.csv')))
+h=next(i for i,r in enumerate(rows) if 'Kernel Name' in r); H=rows[h]
+ki,ni,vi,ii=H.index('Kernel Name'),H.index('Metric Name'),H.index('Metric Value'),H.index('ID')
+d={}
+for r in rows[h+1:]:
+    if len(r)<=vi: continue
+    d.setdefault(int(r[ii]),{'k':r[ki][:40]})[r[ni]]=r[vi]
+for i in sorted(d)[-3:]:
+    print(i,d[i])
+PY

@@ -210,8 +210,9 @@ def tune_winograd_tc(shape, spec, prec, e, log):
     best, best_t, tried = None, _m.inf, 0
     zs = (64, 128) if prec == "fp32" else (64, 128, 256)
     for z, nzt, sb in [(z, nzt, sb) for z in zs if spec.k % z == 0
-                   for nzt in ((1,) if prec == "fp32" else (1, 2))
-                   for sb in (2048, 4096, 8192, 16384)]:   # L2 chunk = 4 KB x s_b
+                   for nzt in ((1,) if prec == "fp32" else
+                               (1, 2, 4) if prec == "3xtf32" and z <= 128 else (1, 2))
+                   for sb in (2048, 8192, 16384, 32768)]:   # chunk (V + M) = 16 KB x s_b
         tile = TileConfig(e, e, z, sb, 1, 1, nzt, layout="HWC", e=e)
         info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
                        "winograd_nhwc" if prec == "fp32" else f"winograd_tc_{prec}")

@@ -321,7 +321,7 @@ WTC_CASES = [
     (2, 64, 56, 56, 64, 4, "fp32", 64),
     (2, 64, 28, 28, 128, 2, "fp32", 128),
     (4, 256, 7, 7, 128, 4, "fp32", 128),       # ragged, several T blocks per xi
-    (10, 64, 56, 56, 64, 2, "fp32", 64),       # two L2 chunks
+    (10, 64, 56, 56, 64, 2, "fp32", 64),       # two chunks at s_b = 2048 (32 MB)
 ]
 # Reduced-precision Winograd: the operand rounding error is amplified by the
 # transforms (F(4,3)'s B^T / G entries up to 5 and 1/6..1/24), so the stated
@@ -336,12 +336,28 @@ def test_winograd_tc_matches_oracle(case):
     x, wt = _inputs(n, c, h, w, k, 3, 3)
     b = np.linspace(-0.25, 0.25, k).astype(np.float32)
     nzt = 1 if prec == "fp32" else (2 if n % 2 else 1)
-    tile = TileConfig(e, e, z, 16384, 1, 1, nzt, layout="HWC", e=e)
+    tile = TileConfig(e, e, z, 2048 if n >= 10 else 16384, 1, 1, nzt, layout="HWC", e=e)
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision=prec,
                            bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
     assert C.infer_layout(y) == "HWC"
     tol = TOL_WTC.get((prec, e), TOL_WINO[e] * max(1.0, (c / 64) ** 0.5))
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= tol, (err, tol)
+
+
+@pytest.mark.parametrize("case", [(3, 128, 28, 28, 128, 4, 128), (2, 64, 56, 56, 64, 2, 64),
+                                  (4, 256, 7, 7, 128, 4, 128), (5, 64, 14, 14, 192, 4, 64)])
+def test_winograd_tc_a_operand_in_tmem(case):
+    """n_zt = 4: the 3xTF32 batched GEMMs on the CTA pair with A (the V tiles) in TMEM."""
+    n, c, h, w, k, e, z = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    tile = TileConfig(e, e, z, 16384, 1, 1, 4, layout="HWC", e=e)
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xtf32",
+                           bias=_dev(b), relu=True)
+    ref = np.maximum(co.direct_conv(x, wt, 1, 1) + b[None, :, None, None], 0)
+    tol = TOL_WINO[e] * max(1.0, (c / 64) ** 0.5)
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
     assert err <= tol, (err, tol)
 
@@ -368,13 +384,13 @@ def test_winograd_tc_filter_transform_matches_oracle():
         assert np.max(np.abs(u - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
 
 
-def test_winograd_tc_chunks_the_batch_through_l2():
-    # enough images that V + M exceed one L2 chunk: several chunks, same answer
+def test_winograd_tc_chunks_the_batch():
+    # s_b = 2048: chunks of V + M <= 32 MB (9 images here): three chunks, same answer
     x, wt = _inputs(24, 64, 56, 56, 64, 3, 3)
-    info = C.query(x.shape, wt.shape, 1, 1, "HWC", TileConfig(4, 4, 64, 16384, 1, 1, 1,
-                   layout="HWC", e=4), algorithm="winograd_tc_3xtf32")
-    assert info["rc"] == 0 and "chunk" in info["reason"]
-    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, precision="3xtf32")
+    tile = TileConfig(4, 4, 64, 2048, 1, 1, 2, layout="HWC", e=4)
+    info = C.query(x.shape, wt.shape, 1, 1, "HWC", tile, algorithm="winograd_tc_3xtf32")
+    assert info["rc"] == 0 and "chunk 9 img" in info["reason"], info["reason"]
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, precision="3xtf32", tile=tile)
     assert C.last_launch_count() > 4   # filter + 3 launches per chunk, > 1 chunk
     ref = co.direct_conv(x[:2], wt, 1, 1)
     assert co.rel_err(y[:2].contiguous().cpu().numpy(), ref) <= TOL_WINO[4]

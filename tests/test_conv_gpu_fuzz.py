@@ -79,7 +79,7 @@ def test_randomized_parity(seed):
         e = int(r.choice([2, 4]))
         z = int(r.choice([zz for zz in ((64, 128) if kind == "wino_fp32" else (64, 128, 256))
                           if k % zz == 0]))
-        nzt = 1 if kind == "wino_fp32" else int(r.choice([1, 2]))
+        nzt = 1 if kind == "wino_fp32" else int(r.choice([1, 2] + ([4] if prec == "3xtf32" and z <= 128 else [])))
         tile = TileConfig(e, e, z, int(r.choice([2048, 8192, 16384])), 1, 1, nzt, layout="HWC", e=e)
         y = C.conv_winograd_tc(xd, wd, e=e, padding=1, tile=tile, precision=prec, bias=bd, relu=relu)
         tol = TOL_WINO[(prec, e)] * (_scale(c) if prec in ("3xtf32", "fp32") else 1.0)
