@@ -503,6 +503,9 @@ def main() -> None:
     variants = {}
     if not args.no_variants:
         for vname, allowed in (("fp32_cuda_cores", CUDA_CORE_ALGORITHMS),
+                               # the direct (DC) dataflows only: every layer within the
+                               # 1.5 x Q_DRAM gate (Winograd's V / M planes exceed it)
+                               ("fp32_direct_only", ("direct", "igemm_3xtf32")),
                                ("tf32_tcgen05", ("igemm_tf32", "winograd_tc_tf32")),
                                ("bf16_tcgen05", ("igemm_bf16", "winograd_tc_bf16"))):
             vplans = load_plans(args.workload, allowed, n=n_local)
@@ -525,7 +528,8 @@ def main() -> None:
                 "ms_per_step": round(vt / args.steps, 4),
                 "tolerance": {"tf32_tcgen05": "5e-3 direct, 5e-3..2e-2 Winograd (TF32 operands)",
                               "bf16_tcgen05": "3e-2 direct, 5e-2..1.5e-1 Winograd (BF16 operands)"}.get(
-                                  vname, "1e-5 direct / 1e-4..1e-3 Winograd"),
+                                  vname, "1e-5" if vname == "fp32_direct_only"
+                                  else "1e-5 direct / 1e-4..1e-3 Winograd"),
                 "per_layer": [{k: r[k] for k in ("layer", "algorithm", "ms", "gflops")} for r in rows],
             }
             del varm
