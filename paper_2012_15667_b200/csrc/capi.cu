@@ -10,6 +10,8 @@
 #include <map>
 #include <array>
 
+#include <stdlib.h>
+
 #include "direct_fp32.cuh"
 #include "winograd_fp32.cuh"
 
@@ -112,6 +114,14 @@ int kernel_regs(const void *fn) {
 }
 
 int device_sms() { return dev_info().ok ? dev_info().sms : 148; }
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *v = getenv("CONVIO_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
 
 // Cluster kernels (CTA pairs): one block per SM by construction; check the
 // block's registers and shared memory against the SM and opt in to the smem.

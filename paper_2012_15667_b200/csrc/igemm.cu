@@ -71,6 +71,7 @@ static const char *kind_name(int kind) {
 // KCRS -> [R*S][K][C] (fp32 or bf16, round-to-nearest-even)
 template <typename T>
 __global__ void pack_filter_igemm_kernel(const float *w, T *wq, int k, int c, int rs) {
+    pdl_wait();
     const int64_t total = (int64_t)k * c * rs;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -88,6 +89,7 @@ __global__ void pack_filter_igemm_kernel(const float *w, T *wq, int k, int c, in
 // fp32 -> bf16 (RNE), 8 elements per thread-step when aligned
 __global__ void convert_bf16_kernel(const float *__restrict__ src, __nv_bfloat16 *__restrict__ dst,
                                     int64_t n) {
+    pdl_wait();
     const int64_t n8 = n / 8;
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n8; i += step) {
@@ -401,7 +403,7 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.fp_bytes = pl.fp_bytes;
         PP.a_slot = pl.a_slot;
         PP.na = pl.na;
-        pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
+        CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
         return CONVIO_OK;
@@ -412,7 +414,10 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
     }
     if (pl.P.splits > 1)
         CONVIO_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)pl.P.n * pl.P.p * pl.P.q * pl.P.k * sizeof(float), stream));
-    pl.fn<<<pl.grid, pl.threads, pl.smem, stream>>>(pl.P, tx, tw);
+    if (pl.P.splits > 1)   // after a memset node: a plain stream dependency
+        pl.fn<<<pl.grid, pl.threads, pl.smem, stream>>>(pl.P, tx, tw);
+    else
+        CONVIO_CUDA_TRY(launch_pdl(pl.fn, pl.grid, dim3(pl.threads), pl.smem, stream, pl.P, tx, tw));
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
@@ -420,7 +425,8 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
 
 int launch_convert_bf16(const float *src, void *dst, int64_t n, cudaStream_t stream) {
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n / 8 + 255) / 256, 148 * 16));
-    convert_bf16_kernel<<<blocks, 256, 0, stream>>>(src, (__nv_bfloat16 *)dst, n);
+    CONVIO_CUDA_TRY(launch_pdl(convert_bf16_kernel, dim3(blocks), dim3(256), 0, stream, src,
+                               (__nv_bfloat16 *)dst, n));
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
@@ -461,13 +467,12 @@ int launch_pack_filter_igemm(const convio_conv_desc *desc, const float *w, void 
     const int64_t total = (int64_t)desc->k * desc->c * desc->r * desc->s;
     const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4096);
     if (bf16)
-        pack_filter_igemm_kernel<__nv_bfloat16><<<blocks, 256, 0, stream>>>(
-            w, (__nv_bfloat16 *)wq, desc->k, desc->c, desc->r * desc->s);
+        CONVIO_CUDA_TRY(launch_pdl(pack_filter_igemm_kernel<__nv_bfloat16>, dim3(blocks), dim3(256), 0,
+                                   stream, w, (__nv_bfloat16 *)wq, desc->k, desc->c, desc->r * desc->s));
     else
-        pack_filter_igemm_kernel<float><<<blocks, 256, 0, stream>>>(w, (float *)wq, desc->k, desc->c,
-                                                                    desc->r * desc->s);
+        CONVIO_CUDA_TRY(launch_pdl(pack_filter_igemm_kernel<float>, dim3(blocks), dim3(256), 0, stream,
+                                   w, (float *)wq, desc->k, desc->c, desc->r * desc->s));
     note_launch();
-    CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;
 }
 

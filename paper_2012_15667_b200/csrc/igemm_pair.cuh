@@ -326,6 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     cluster_sync_all();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();   // the prologue above overlapped the previous kernel's tail
 
     // work item -> (group, pair, n-block); n fastest
     auto decode = [&](int item, int &grp, int &pair, int &nb) {

@@ -207,6 +207,7 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
+    pdl_wait();
 
     // split-K (small grids): this CTA reduces k-blocks [kb_lo, kb_hi) and adds its
     // partial tile into the zeroed output

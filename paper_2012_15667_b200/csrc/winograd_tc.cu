@@ -130,6 +130,7 @@ __device__ __forceinline__ void store4(T *p, float4 v) {
 template <int E, typename T>
 __global__ void __launch_bounds__(128) winograd_input_tc_kernel(const float *__restrict__ x,
                                                                 T *__restrict__ v, WinoTcGeom g) {
+    pdl_wait();
     constexpr int M = WinoTf<E>::M;
     const int c4n = g.c >> 2;
     const int tpi = g.tiles_y * g.tiles_x;
@@ -184,6 +185,7 @@ __global__ void __launch_bounds__(128) winograd_input_tc_kernel(const float *__r
 template <int E, typename T, bool CK = false>
 __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__restrict__ u, int k,
                                           int c) {
+    pdl_wait();
     constexpr int M = WinoTf<E>::M;
     const int64_t pairs = (int64_t)k * c;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < pairs;
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(128, 4) winograd_output_tc_kernel(const float 
                                                                  float *__restrict__ y, WinoTcGeom g,
                                                                  int relu) {
     // one thread per (tile, 4 output channels), LDG.128 / STG.128, 32-bit index math
+    pdl_wait();
     constexpr int M = WinoTf<E>::M;
     const int k4n = g.k >> 2;
     const int tpi = g.tiles_y * g.tiles_x;
@@ -357,6 +360,12 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     // keep the GEMM's T axis within the TMA box-coordinate / grid limits
     while (chunk > 1 && (size_t)chunk * tpi > (size_t)1 << 24) chunk /= 2;
     if ((size_t)chunk * tpi >= ((size_t)1 << 31)) return fail(CONVIO_EINFEASIBLE, "too many tiles");
+    // the transform kernels index a chunk's tiles x channels and an image's
+    // pixels x channels in 32-bit arithmetic
+    if ((size_t)chunk * tpi * (size_t)std::max(d->c, d->k) >= ((size_t)1 << 31) ||
+        (size_t)std::max<int64_t>((int64_t)d->h * d->w, (int64_t)p * q) * (size_t)std::max(d->c, d->k) >=
+            ((size_t)1 << 31))
+        return fail(CONVIO_EINFEASIBLE, "chunk or image too large for 32-bit transform indexing");
     pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b; pl->pair = pair;
     pl->tsa = tsa;
     pl->chunk_imgs = chunk;
@@ -371,14 +380,14 @@ static int launch_filter_tc(const WinoTcPlan &pl, const float *w, void *u, cudaS
     const int blocks = (int)std::min<int64_t>((pairs + 255) / 256, 148 * 8);
     const bool bf = pl.kind == KIND_BF16;
     if (pl.kind == KIND_FFMA) {   // U[xi][c][k]: the FFMA GEMM reads [channel][n] rows
-        if (pl.e == 2) winograd_filter_tc_kernel<2, float, true><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
-        else winograd_filter_tc_kernel<4, float, true><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+        if (pl.e == 2) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<2, float, true>, dim3(blocks), dim3(256), 0, st, w, (float *)u, pl.g.k, pl.g.c));
+        else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<4, float, true>, dim3(blocks), dim3(256), 0, st, w, (float *)u, pl.g.k, pl.g.c));
     } else if (pl.e == 2) {
-        if (bf) winograd_filter_tc_kernel<2, __nv_bfloat16><<<blocks, 256, 0, st>>>(w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c);
-        else winograd_filter_tc_kernel<2, float><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+        if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<2, __nv_bfloat16>, dim3(blocks), dim3(256), 0, st, w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c));
+        else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<2, float>, dim3(blocks), dim3(256), 0, st, w, (float *)u, pl.g.k, pl.g.c));
     } else {
-        if (bf) winograd_filter_tc_kernel<4, __nv_bfloat16><<<blocks, 256, 0, st>>>(w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c);
-        else winograd_filter_tc_kernel<4, float><<<blocks, 256, 0, st>>>(w, (float *)u, pl.g.k, pl.g.c);
+        if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<4, __nv_bfloat16>, dim3(blocks), dim3(256), 0, st, w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c));
+        else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<4, float>, dim3(blocks), dim3(256), 0, st, w, (float *)u, pl.g.k, pl.g.c));
     }
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
@@ -496,11 +505,11 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         const int tc = g.imgs * tpi;
         const int gin = grid_for((int64_t)tc * (g.c / 4), 128), gout = grid_for((int64_t)tc * (g.k / 4), 128);
         if (pl.e == 2) {
-            if (bf) winograd_input_tc_kernel<2, __nv_bfloat16><<<gin, 128, 0, st>>>(x, (__nv_bfloat16 *)v, g);
-            else winograd_input_tc_kernel<2, float><<<gin, 128, 0, st>>>(x, (float *)v, g);
+            if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<2, __nv_bfloat16>, dim3(gin), dim3(128), 0, st, x, (__nv_bfloat16 *)v, g));
+            else CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<2, float>, dim3(gin), dim3(128), 0, st, x, (float *)v, g));
         } else {
-            if (bf) winograd_input_tc_kernel<4, __nv_bfloat16><<<gin, 128, 0, st>>>(x, (__nv_bfloat16 *)v, g);
-            else winograd_input_tc_kernel<4, float><<<gin, 128, 0, st>>>(x, (float *)v, g);
+            if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<4, __nv_bfloat16>, dim3(gin), dim3(128), 0, st, x, (__nv_bfloat16 *)v, g));
+            else CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<4, float>, dim3(gin), dim3(128), 0, st, x, (float *)v, g));
         }
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
@@ -516,9 +525,9 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         }
         if (rc) return rc;
         if (pl.e == 2)
-            winograd_output_tc_kernel<2><<<gout, 128, 0, st>>>(mm, bias, y, g, relu);
+            CONVIO_CUDA_TRY(launch_pdl(winograd_output_tc_kernel<2>, dim3(gout), dim3(128), 0, st, (const float *)mm, bias, y, g, relu));
         else
-            winograd_output_tc_kernel<4><<<gout, 128, 0, st>>>(mm, bias, y, g, relu);
+            CONVIO_CUDA_TRY(launch_pdl(winograd_output_tc_kernel<4>, dim3(gout), dim3(128), 0, st, (const float *)mm, bias, y, g, relu));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
     }

@@ -1,0 +1,6 @@
+timeout 900 python -m pytest tests/ -m gpu -q -x 2>&1 | grep -E "^E  |FAILED|passed|failed" | head
+for pdl in 0 1; do
+  CONVIO_PDL=$pdl timeout 300 python bench.py --no-variants --no-e2e --no-cpu 2>/dev/null | tail -1 > gpurun_out/pdl_$pdl.json
+  CONVIO_PDL=$pdl timeout 300 python bench.py --batch 32 --no-variants --no-e2e --no-cpu 2>/dev/null | tail -1 > gpurun_out/pdl32_$pdl.json
+  python -c "import json;a=json.load(open('gpurun_out/pdl_$pdl.json'));b=json.load(open('gpurun_out/pdl32_$pdl.json'));print('PDL=$pdl', a['value'], a['ms_per_step'], b['value'], b['ms_per_step'])"
+done
