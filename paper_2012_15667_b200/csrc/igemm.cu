@@ -183,10 +183,29 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     return CONVIO_OK;
 }
 
-// persistent grid: one CTA pair per TPC (fewer if there are fewer work items)
+// persistent grid: one CTA pair per TPC (fewer if there are fewer work items).
+// Split-K (non-halo conv tiles): when the last wave of work items would leave
+// pairs idle -- e.g. ResNet-50 res5 stride 2, 98 items on 74 pairs: 2 rounds for
+// 1.32 rounds of work -- each item's K loop is split so items * splits fills
+// the rounds evenly; partial tiles are added with fp32 vector atomics into the
+// zeroed output (bias by the first split; never with ReLU, see igemm_launch).
 static int finish_pair_grid(IgemmPlan *pl) {
     const int pairs = (pl->blocks_per_group + 1) / 2;
-    const int64_t items = (int64_t)pl->groups * pairs * (pl->fold ? 1 : pl->P.k / pl->bn);
+    const int64_t base = (int64_t)pl->groups * pairs * (pl->fold ? 1 : pl->P.k / pl->bn);
+    const int64_t nclus = std::max(1, device_sms() / 2);
+    pl->P.splits = 1;
+    if (!pl->halo && !pl->P.batched && base < 8 * nclus) {
+        auto eff = [&](int64_t it) { return (double)it / (double)(((it + nclus - 1) / nclus) * nclus); };
+        double best = eff(base);
+        for (int sp = 2; sp <= 4; ++sp) {
+            if (pl->P.kblocks / sp < 16) break;
+            if (eff(base * sp) > best * 1.2) {   // atomics + memset cost ~10-15 %
+                best = eff(base * sp);
+                pl->P.splits = sp;
+            }
+        }
+    }
+    const int64_t items = base * pl->P.splits;
     if (items >= ((int64_t)1 << 31)) {
         set_error("too many work items");
         return CONVIO_EINFEASIBLE;
@@ -398,12 +417,20 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.blocks_per_group = pl.blocks_per_group;
         PP.pairs_per_group = (pl.blocks_per_group + 1) / 2;
         PP.nblocks = pl.fold ? 1 : pl.P.k / pl.bn;
-        PP.items = PP.groups * PP.pairs_per_group * PP.nblocks;
+        PP.base_items = PP.groups * PP.pairs_per_group * PP.nblocks;
+        if (PP.g.splits < 1 || relu) PP.g.splits = 1;   // ReLU does not commute with the split sum
+        PP.items = PP.base_items * PP.g.splits;
+        if (PP.g.splits > 1)
+            CONVIO_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)PP.g.n * PP.g.p * PP.g.q * PP.g.k * sizeof(float),
+                                            stream));
         PP.fpr = pl.fpr;
         PP.fp_bytes = pl.fp_bytes;
         PP.a_slot = pl.a_slot;
         PP.na = pl.na;
-        CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw));
+        if (PP.g.splits > 1)   // after a memset node: a plain stream dependency
+            pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
+        else
+            CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
         return CONVIO_OK;

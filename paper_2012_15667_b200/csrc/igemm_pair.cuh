@@ -49,7 +49,8 @@ struct PairParams {
     int blocks_per_group;   // pixel blocks per group
     int pairs_per_group;    // ceil(blocks_per_group / 2)
     int nblocks;            // K / BN
-    int items;              // groups * pairs_per_group * nblocks
+    int items;              // base_items * splits
+    int base_items;         // groups * pairs_per_group * nblocks (one K range each)
     // halo staging (HALO kernels): the (y + R - 1) x fpr input footprint of a
     // 128-row block is staged ONCE per channel block; tap (r, s) is the view
     // starting (r * fpr + s) rows into it (rows = y x fpr pixels, x = fpr - S + 1
@@ -329,7 +330,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     pdl_wait();   // the prologue above overlapped the previous kernel's tail
 
     // work item -> (group, pair, n-block); n fastest
+    // split-K (P.splits > 1, non-halo): item = split * base_items + tile item; the
+    // split reduces k-blocks [kb_lo, kb_hi) and the epilogue adds its partial tile
+    auto krange = [&](int item, int &kb_lo, int &kb_hi) {
+        if constexpr (HALO) {   // halo tiles never split (compile-time: no cost)
+            kb_lo = 0;
+            kb_hi = P.kblocks;
+            return 0;
+        }
+        const int spl = item / PP.base_items;
+        kb_lo = (int)(((int64_t)P.kblocks * spl) / P.splits);
+        kb_hi = (int)(((int64_t)P.kblocks * (spl + 1)) / P.splits);
+        return spl;
+    };
     auto decode = [&](int item, int &grp, int &pair, int &nb) {
+        if constexpr (!HALO) item %= PP.base_items;
         nb = item % PP.nblocks;
         const int rest = item / PP.nblocks;
         pair = rest % PP.pairs_per_group;
@@ -353,8 +368,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 int ox0, oy0, img0;
                 pair_block_origin(P, grp, pair * 2 + (int)rank, ox0, oy0, img0);
                 const int n0 = nb * BN + (int)rank * HB;
-                int tap = 0, cb = 0;
-                for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+                int kb_lo, kb_hi;
+                krange(item, kb_lo, kb_hi);
+                int tap = HALO ? 0 : kb_lo / P.cblocks, cb = HALO ? 0 : kb_lo - tap * P.cblocks;
+                for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                     // FOLD: the filter rows of kernel row `tap` (S taps x K channels) of
                     // the packed [R*S*K][C] view; this CTA stages its HB of them
                     const int frow = tap * P.ks * P.k + (int)rank * HB;
@@ -424,14 +441,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 int tap = 0;
                 uint32_t fa = 0;
-                for (int kb = 0; kb < P.kblocks; ++kb) {
+                int kb_lo, kb_hi;
+                krange(item, kb_lo, kb_hi);
+                for (int kb = kb_lo; kb < kb_hi; ++kb) {
                     if constexpr (TSA) {
                         mbar_wait_cluster(tconv + ta, pht);
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                         const uint32_t b = smem_u32(bring + s * STAGE) + A_BYTES;
                         const uint64_t bd = umma_desc_sw128(b), bdl = umma_desc_sw128(b + B_BYTES);
                         const uint32_t ahi = tmem + A_COL0 + (uint32_t)(ta * 64);
-                        const bool first = kb == 0;
+                        const bool first = kb == kb_lo;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t o = (uint64_t)(kk * 2);
@@ -472,7 +491,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     }
                     const uint64_t ad = HALO ? umma_desc_sw128_row(a) : umma_desc_sw128(a);
                     const uint64_t bd = umma_desc_sw128(b);
-                    const bool first = kb == 0;
+                    const bool first = kb == kb_lo;
                     if constexpr (SPLIT) {
                         const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : a + A_BYTES + B_BYTES;
                         const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : b + A_BYTES + B_BYTES;
@@ -518,6 +537,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
             int grp, pair, nb;
             decode(item, grp, pair, nb);
+            int kb_lo, kb_hi;
+            const bool lead_split = krange(item, kb_lo, kb_hi) == 0;
             const int acc = t & 1;
             mbar_wait(tfull + acc, (t >> 1) & 1);
             __syncwarp();
@@ -575,7 +596,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int j = 0; j < 32; j += 4)
                     *reinterpret_cast<float4 *>(stg + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 __syncwarp();
-                const float4 bv = P.bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
+                const float4 bv = P.bias && lead_split
+                                      ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
@@ -586,7 +608,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
                         o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
                     }
-                    if (vrow[i]) *reinterpret_cast<float4 *>(drow[i] + c0 + cc) = o;
+                    if (vrow[i]) {
+                        if (!HALO && P.splits > 1)   // partial sum of a K range: fp32 vector atomics
+                            atomicAdd(reinterpret_cast<float4 *>(drow[i] + c0 + cc), o);
+                        else
+                            *reinterpret_cast<float4 *>(drow[i] + c0 + cc) = o;
+                    }
                 }
                 __syncwarp();
             }
@@ -608,7 +635,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         int s = 0, ta = 0, it = 0;
         uint32_t ph = 0, pht = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
-            for (int kb = 0; kb < P.kblocks; ++kb, ++it) {
+            int kb_lo, kb_hi;
+            krange(item, kb_lo, kb_hi);
+            for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                 mbar_wait(full + s, ph);
                 if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
                 const uint32_t st = smem_u32(bring + s * STAGE);
@@ -653,7 +682,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         uint32_t ph = 0, pha = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
             int tap = 0;
-            for (int kb = 0; kb < P.kblocks; ++kb) {
+            int kb_lo, kb_hi;
+            krange(item, kb_lo, kb_hi);
+            for (int kb = kb_lo; kb < kb_hi; ++kb) {
                 if (HALO && tap == 0) {
                     mbar_wait(afull + sa, pha);
                     const uint32_t hi = smem_u32(aring + sa * ASLOT);

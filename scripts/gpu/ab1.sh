@@ -1,0 +1,6 @@
+P="timeout 300 python scripts/probe_tc.py --n 256 --layers res2_3x3 --kinds igemm_3xtf32:64:2:h32"
+for v in head new head new; do
+  cp paper_2012_15667_b200/lib/exp/lib$v.so paper_2012_15667_b200/lib/libconvio_b200.so
+  echo "$v $($P 2>&1 | grep res2)"
+done
+cp paper_2012_15667_b200/lib/exp/libnew.so paper_2012_15667_b200/lib/libconvio_b200.so

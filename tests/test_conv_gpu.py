@@ -449,3 +449,27 @@ def test_igemm_split_k_on_small_grids(prec):
     yr = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, tile=tile, precision=prec, bias=_dev(b),
                       relu=True)
     assert co.rel_err(yr.contiguous().cpu().numpy(), np.maximum(ref, 0)) <= tol
+
+
+@pytest.mark.parametrize("case", [
+    # (n, c, h, k, stride, tile, precision): CTA-pair tiles whose work items leave the
+    # last round of pairs idle -> the library splits each item's K loop
+    (16, 512, 14, 256, 2, TileConfig(1, 1, 256, 32768, 1, 1, 2, layout="HWC"), "3xtf32"),
+    (16, 256, 28, 256, 2, TileConfig(1, 2, 256, 32768, 1, 1, 2, layout="HWC"), "tf32"),
+    (8, 512, 7, 128, 1, TileConfig(7, 7, 128, 32768, 1, 1, 4, layout="HWC"), "3xtf32"),
+    (4, 512, 7, 256, 1, TileConfig(7, 7, 256, 32768, 1, 1, 2, layout="HWC"), "bf16"),
+])
+def test_igemm_pair_split_k(case):
+    n, c, h, k, stride, tile, prec = case
+    x, wt = _inputs(n, c, h, h, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    info = C.query(x.shape, wt.shape, stride, 1, "HWC", tile, f"igemm_{prec}")
+    assert info["rc"] == 0 and "split-K" in info["reason"], info["reason"]
+    ref = co.direct_conv(x, wt, stride, 1) + b[None, :, None, None]
+    tol = TOL_PREC.get(prec, tol_3xtf32(c))
+    y = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile, precision=prec,
+                     bias=_dev(b))
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= tol
+    yr = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile, precision=prec,
+                      bias=_dev(b), relu=True)   # unsplit: ReLU does not commute with the split sum
+    assert co.rel_err(yr.contiguous().cpu().numpy(), np.maximum(ref, 0)) <= tol
