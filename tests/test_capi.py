@@ -123,3 +123,40 @@ def test_no_cpu_fallback_for_conv():
         C.conv_direct(x, w, padding=1)
     with pytest.raises(ValueError, match="CUDA"):
         C.conv_winograd(x, w, e=2, padding=1)
+
+
+def test_tensor_core_projections_plan_pairs_split_k_and_chunks():
+    """Host-side planning of the tcgen05 kernels (no launch): the CTA-pair tile
+    kinds, the pair split-K decision (148 SMs without a device) and the
+    tensor-core Winograd chunking."""
+    hwc = "HWC"
+    # ResNet-50 res5 stride 2 at batch 256: 98 pair items on 74 pairs -> split K
+    s2 = query((256, 512, 14, 14), (512, 512, 3, 3), 2, 1, hwc,
+               TileConfig(1, 1, 256, 32768, 1, 1, 2, layout=hwc), "igemm_3xtf32")
+    assert s2["rc"] == 0 and "CTA pair" in s2["reason"] and "split-K" in s2["reason"]
+    # res4 stride 2: 196 items, 88 % rounds efficiency -> not worth the atomics
+    s4 = query((256, 256, 28, 28), (256, 256, 3, 3), 2, 1, hwc,
+               TileConfig(1, 2, 256, 32768, 1, 1, 2, layout=hwc), "igemm_3xtf32")
+    assert s4["rc"] == 0 and "split-K" not in s4["reason"]
+    # halo + fold tiles never split
+    fold = query((4, 64, 56, 56), (64, 64, 3, 3), 1, 1, hwc,
+                 TileConfig(30, 4, 64, 32768, 2, 1, 2, layout=hwc), "igemm_3xtf32")
+    assert fold["rc"] == 0 and "3 taps per MMA" in fold["reason"] and "split-K" not in fold["reason"]
+    tsa = query((64, 128, 28, 28), (128, 128, 3, 3), 1, 1, hwc,
+                TileConfig(4, 1, 128, 32768, 1, 1, 4, layout=hwc), "igemm_3xtf32")
+    assert tsa["rc"] == 0 and "A in TMEM" in tsa["reason"]
+    bad = query((64, 128, 28, 28), (256, 128, 3, 3), 1, 1, hwc,
+                TileConfig(4, 1, 256, 32768, 1, 1, 4, layout=hwc), "igemm_3xtf32")
+    assert bad["rc"] == 3
+    # Winograd chunk budget 16 KB x s_b: 9 images of 56x56x64 F(4,3) at s_b 2048,
+    # the whole batch at s_b 32768
+    w2 = query((24, 64, 56, 56), (64, 64, 3, 3), 1, 1, hwc,
+               TileConfig(4, 4, 64, 2048, 1, 1, 2, layout=hwc, e=4), "winograd_tc_3xtf32")
+    assert w2["rc"] == 0 and "chunk 9 img" in w2["reason"]
+    w32 = query((24, 64, 56, 56), (64, 64, 3, 3), 1, 1, hwc,
+                TileConfig(4, 4, 64, 32768, 1, 1, 4, layout=hwc, e=4), "winograd_tc_3xtf32")
+    assert w32["rc"] == 0 and "chunk 24 img" in w32["reason"]
+    # A in TMEM needs 3xTF32 and z <= 128
+    wbad = query((24, 64, 56, 56), (256, 64, 3, 3), 1, 1, hwc,
+                 TileConfig(4, 4, 256, 32768, 1, 1, 4, layout=hwc, e=4), "winograd_tc_3xtf32")
+    assert wbad["rc"] == 3
