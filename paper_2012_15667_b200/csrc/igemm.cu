@@ -134,9 +134,12 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
                          pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
                                  : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
         const int mult = kind == KIND_3XTF32 ? 2 : 1;
+        // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
+        const bool loslot = kind == KIND_3XTF32 && !pl->halo && !pl->tsa && bn == 256;
         const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
-                                           : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) * mult;
-        const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : 0;
+                                           : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) *
+                                                 (loslot ? 1 : mult);
+        const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : (loslot ? 2 * stage_bytes : 0);
         const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");

@@ -264,9 +264,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr int NTA = TSA ? (512 - 2 * BN) / 64 : 1;
     constexpr int NCW = pair_conv_warps<BN, TSA>();   // converter warps (3xTF32)
     const IgemmParams &P = PP.g;
-    // stage layout: non-halo [A | B] (+ lo copy); TSA [A | B | B_lo];
-    // halo: A footprint slots, then B stages
-    const int STAGE = HALO ? B_BYTES * MULT : (TSA ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * MULT);
+    // stage layout: non-halo [A | B]; TSA [A | B | B_lo]; halo: A footprint slots,
+    // then B stages [B | B_lo].  Non-halo 3xTF32 (LOSLOT): the lo copies live in
+    // NL = 2 slots after the TMA ring, decoupled from it, so the ring holds more
+    // k-blocks in flight (N = 256: 4 TMA stages instead of 3 whole [hi | lo]
+    // stages) -- the MMA issuer of the short-K Winograd GEMMs was waiting on
+    // converters that were waiting on TMA data.
+    // (N = 256 only: measured 1-2 % faster there, 7-8 % slower at N = 128, where
+    // two lo slots let the converters run only two k-blocks ahead of the MMAs)
+    constexpr bool LOSLOT = SPLIT && !HALO && !TSA && BN == 256;
+    constexpr int NL = 2;
+    constexpr int LO_SLOT = A_BYTES + B_BYTES;
+    const int STAGE = HALO ? B_BYTES * MULT : (TSA ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (LOSLOT ? 1 : MULT));
     const int ASLOT = HALO ? PP.a_slot * MULT : 0;
     const int NA = HALO ? PP.na : 0;
 
@@ -275,7 +284,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     const int NS = P.stages;
     uint8_t *aring = smem;                            // halo footprint slots
     uint8_t *bring = smem + NA * ASLOT;               // stages
-    uint64_t *full = reinterpret_cast<uint64_t *>(bring + NS * STAGE);
+    uint8_t *loring = bring + NS * STAGE;             // LOSLOT: lo copies
+    uint8_t *ring_end = loring + (LOSLOT ? NL * LO_SLOT : 0);
+    uint64_t *full = reinterpret_cast<uint64_t *>(ring_end);
     uint64_t *empty = full + NS;
     uint64_t *conv = empty + NS;
     uint64_t *tfull = conv + NS;
@@ -285,7 +296,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     uint64_t *aconv = aempty + 2;
     uint64_t *tconv = aconv + 2;                      // TSA: A slot in TMEM converted
     uint64_t *tfree = tconv + 6;                      // TSA: A slot in TMEM consumed
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tfree + 6);
+    uint64_t *lofree = tfree + 6;                     // LOSLOT: lo slot consumed by the MMAs
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofree + NL);
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
@@ -309,6 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             mbar_init(aempty + a, 1);
             mbar_init(aconv + a, 2 * NCW);
         }
+        for (int l = 0; l < NL && LOSLOT; ++l) mbar_init(lofree + l, 1);
         for (int a = 0; a < NTA && TSA; ++a) {
             mbar_init(tconv + a, 2 * NCW);
             mbar_init(tfree + a, 1);
@@ -431,7 +444,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         if (leader && lane == 0) {
             // ---- MMA issuer (leader CTA, one thread) -----------------------------------
             constexpr uint32_t idesc = idesc_m256<BN, KIND>();
-            int s = 0, sa = 0, ta = 0;
+            int s = 0, sa = 0, ta = 0, l = 0;
             uint32_t ph = 0, pha = 0, pht = 0;
             int t = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
@@ -493,8 +506,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const uint64_t bd = umma_desc_sw128(b);
                     const bool first = kb == kb_lo;
                     if constexpr (SPLIT) {
-                        const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : a + A_BYTES + B_BYTES;
-                        const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : b + A_BYTES + B_BYTES;
+                        const uint32_t lo = smem_u32(loring + l * LO_SLOT);
+                        const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : (LOSLOT ? lo : a + A_BYTES + B_BYTES);
+                        const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : (LOSLOT ? lo + A_BYTES : b + A_BYTES + B_BYTES);
                         const uint64_t adl = HALO ? umma_desc_sw128_row(alo) : umma_desc_sw128(alo);
                         const uint64_t bdl = umma_desc_sw128(blo);
 #pragma unroll
@@ -511,6 +525,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                                             !(first && kk == 0));
                     }
                     umma_commit_pair(empty + s);
+                    if constexpr (LOSLOT) {
+                        umma_commit_pair(lofree + l);   // lo slot consumed
+                        if (++l == NL) l = 0;
+                    }
                     if (HALO && ++tap == taps) {
                         tap = 0;
                         umma_commit_pair(aempty + sa);   // footprint consumed by all taps
@@ -532,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int q = warp - 4;                       // TMEM lane quadrant
         const int m = q * 32 + lane;                  // pixel row of this CTA's A block
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
-        float *stg = reinterpret_cast<float *>(bring + NS * STAGE + 1024) + q * (32 * 36);
+        float *stg = reinterpret_cast<float *>(ring_end + 1024) + q * (32 * 36);
         int t = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
             int grp, pair, nb;
@@ -678,8 +696,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int ct = tid - 256;                    // 0 .. 32*NCW-1
         const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
         const uint32_t aconv_leader = mapa_shared(smem_u32(aconv), 0);
-        int s = 0, sa = 0;
-        uint32_t ph = 0, pha = 0;
+        int s = 0, sa = 0, l = 0, itl = 0;
+        uint32_t ph = 0, pha = 0, phl = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
             int tap = 0;
             int kb_lo, kb_hi;
@@ -699,8 +717,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 }
                 mbar_wait(full + s, ph);
                 const uint32_t hi = smem_u32(bring + s * STAGE);
-                if (HALO) convert_lo_range<32 * NCW>(hi, hi + B_BYTES, B_BYTES / 16, ct);
-                else convert_lo_range<32 * NCW>(hi, hi + A_BYTES + B_BYTES, (A_BYTES + B_BYTES) / 16, ct);
+                if constexpr (HALO) {
+                    convert_lo_range<32 * NCW>(hi, hi + B_BYTES, B_BYTES / 16, ct);
+                } else if constexpr (!LOSLOT) {
+                    convert_lo_range<32 * NCW>(hi, hi + A_BYTES + B_BYTES, (A_BYTES + B_BYTES) / 16, ct);
+                } else {
+                    if (itl >= NL) mbar_wait(lofree + l, phl ^ 1);   // slot's previous MMAs done
+                    convert_lo_range<32 * NCW>(hi, smem_u32(loring + l * LO_SLOT), (A_BYTES + B_BYTES) / 16, ct);
+                    ++itl;
+                    if (++l == NL) {
+                        l = 0;
+                        phl ^= 1;
+                    }
+                }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(conv_leader + (uint32_t)(s * 8));

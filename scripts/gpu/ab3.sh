@@ -1,0 +1,10 @@
+timeout 900 python -m pytest tests/test_conv_gpu.py tests/test_conv_gpu_fuzz.py tests/test_graph_replay_gpu.py -q -x 2>&1 | grep -E "^E  |FAILED|passed|failed" | head -5
+P="timeout 300 python scripts/probe_tc.py --n 256 --layers res3_3x3_s2,res4_3x3_s2,res5_3x3_s2 --kinds igemm_3xtf32:128:2,igemm_3xtf32:256:2"
+for v in head new; do
+  cp paper_2012_15667_b200/lib/exp/lib$v.so paper_2012_15667_b200/lib/libconvio_b200.so
+  $P 2>&1 | grep res | sed "s/^/$v /"
+  timeout 300 python scripts/probe_wtc_chunk.py --layer res4_3x3 --z 256 --nzt 2 --e 4 --sweep 32768 2>&1 | grep res4 | sed "s/^/$v /"
+  timeout 300 python scripts/probe_wtc_chunk.py --layer res5_3x3 --z 256 --nzt 2 --e 4 --sweep 32768 2>&1 | grep res5 | sed "s/^/$v /"
+  timeout 300 python scripts/probe_wtc_chunk.py --layer res3_3x3 --z 128 --nzt 2 --e 4 --sweep 32768 2>&1 | grep res3 | sed "s/^/$v /"
+done
+cp paper_2012_15667_b200/lib/exp/libnew.so paper_2012_15667_b200/lib/libconvio_b200.so
