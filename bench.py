@@ -264,6 +264,9 @@ def main() -> None:
     # rank, so the max-over-ranks / barrier path is the same code at N=1 and N=8
     if world > 1 or "MASTER_ADDR" in os.environ:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL's version banner goes to stdout; the contract is one JSON line there
+        if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+            os.environ["NCCL_DEBUG"] = "WARN"
         dist.init_process_group("nccl", device_id=dev)
     distributed = dist.is_available() and dist.is_initialized()
 
