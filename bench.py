@@ -501,6 +501,19 @@ def main() -> None:
         }
     roofline["layers"] = sorted(d["layers"])
     roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)
+    # the same family against HBM: the committed ncu DRAM bytes of its layer calls
+    # over their device time (the unfused Winograd pipeline moves V and M through
+    # HBM, so bandwidth, not the tensor pipe, is its ceiling)
+    by_layer = roofline.get("traffic_by_layer") or {}
+    cnt = d.get("layer_launches", {})
+    if by_layer and d["ms"] and all(by_layer.get(k) for k in d["layers"]):
+        moved = sum(by_layer[k] * cnt.get(k, 1) for k in d["layers"])   # over all timed steps
+        gbs = moved / (d["ms"] / 1e3) / 1e9
+        hbm = peaks.get("hbm_gbs")
+        roofline["hbm_view"] = {"achieved": round(gbs, 1), "peak": hbm, "unit": "GB/s",
+                                "frac": round(gbs / hbm, 4) if hbm else None,
+                                "bytes_per_step": int(moved / max(1, args.steps)),
+                                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy read+write)"}
 
     # ---- variants: paper-faithful FP32 CUDA cores only, and reduced-precision TF32 ----
     variants = {}
