@@ -34,6 +34,10 @@ int direct_instance_count();
 int winograd_default_tile(const convio_conv_desc *d, int e, convio_tile *out);
 int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out, int kind);
 bool nhwc_tile(const convio_conv_desc *d, const convio_tile *t);
+bool smallc_tile(const convio_conv_desc *d, const convio_tile *t);
+int direct_smallc_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
+int direct_smallc_run(const convio_conv_desc *d, const convio_tile *t, const float *x, const float *wp,
+                      const float *bias, int relu, float *y, cudaStream_t stream);
 int direct_nhwc_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_info *out);
 int direct_nhwc_run(const convio_conv_desc *d, const convio_tile *t, const float *x, const float *wp,
                     const float *bias, int relu, float *y, cudaStream_t stream);
@@ -652,6 +656,16 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
     }
     memset(out, 0, sizeof(*out));
     if (algorithm == CONVIO_ALG_DIRECT) {
+        if (smallc_tile(desc, tile)) {   // C <= 4 input layers (direct_smallc.cu)
+            int p, q;
+            int rc = check_desc(desc, &p, &q);
+            if (rc) {
+                strncpy(out->reason, t_err, sizeof(out->reason) - 1);
+                out->reason[sizeof(out->reason) - 1] = '\0';
+                return rc;
+            }
+            return direct_smallc_query(desc, tile, out);
+        }
         if (nhwc_tile(desc, tile)) {
             int p, q;
             int rc = check_desc(desc, &p, &q);
@@ -729,7 +743,7 @@ int convio_conv_direct_f32(const convio_conv_desc *desc, const convio_tile *tile
     DirectPlan pl;
     char why[160];
     bool generic = false;
-    if (nhwc_tile(desc, tile)) {   // channels-last stacked-pixel kernel (direct_nhwc.cuh)
+    if (smallc_tile(desc, tile) || nhwc_tile(desc, tile)) {   // channels-last kernels
         const float *wpk = w;
         if (!w_is_packed) {
             const size_t need = 4ULL * desc->k * desc->c * desc->r * desc->s;
@@ -741,6 +755,7 @@ int convio_conv_direct_f32(const convio_conv_desc *desc, const convio_tile *tile
             if (rc) return rc;
             wpk = (const float *)workspace;
         }
+        if (smallc_tile(desc, tile)) return direct_smallc_run(desc, tile, x, wpk, bias, relu, y, st);
         return direct_nhwc_run(desc, tile, x, wpk, bias, relu, y, st);
     }
     if (!tile) {

@@ -162,8 +162,9 @@ def tune_direct_nhwc(shape, spec, log):
     import math as _m
     from paper_2012_15667_b200.dataflow import TileConfig
     from paper_2012_15667_b200 import conv as C
-    if spec.c % 32 or spec.stride > 2:
-        return {"error": "needs C % 32 == 0 and stride <= 2"}
+    small_c = spec.c <= 4 and spec.r == 3 and spec.k % 32 == 0   # K8 (direct_smallc.cu)
+    if (spec.c % 32 and not small_c) or spec.stride > 2:
+        return {"error": "needs C % 32 == 0 (or C <= 4) and stride <= 2"}
     q, p = shape.w_out, shape.h_out
     x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
     xh = C.to_layout(x, "HWC")
@@ -171,7 +172,15 @@ def tune_direct_nhwc(shape, spec, log):
     wp = C.pack_filter_direct(w)
     out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
     best, best_t, tried = None, _m.inf, 0
-    for bx in [d for d in range(1, q + 1) if q % d == 0]:
+    if small_c:   # one tile shape: 16 x 16 pixels x 32 channels, the whole C staged
+        tile = TileConfig(16, 16, 32, 32768, 1, 1, 1, layout="HWC")
+        try:
+            best_t = DT.device_time(lambda: C.conv_direct(xh, w, stride=spec.stride, padding=spec.pad,
+                                                           tile=tile, w_packed=wp, out=out))
+            best, tried = tile, 1
+        except Exception:  # noqa: BLE001 -- illegal projection
+            pass
+    for bx in [d for d in range(1, q + 1) if q % d == 0 and not small_c]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
             if not block_ok(bx, by, shape.n):
                 continue

@@ -473,3 +473,30 @@ def test_igemm_pair_split_k(case):
     yr = C.conv_igemm(_dev(x, "HWC"), _dev(wt), padding=1, stride=stride, tile=tile, precision=prec,
                       bias=_dev(b), relu=True)   # unsplit: ReLU does not commute with the split sum
     assert co.rel_err(yr.contiguous().cpu().numpy(), np.maximum(ref, 0)) <= tol
+
+
+@pytest.mark.parametrize("case", [
+    # (n, c, h, w, k, stride): K8, the channels-last small-C kernel (C <= 4)
+    (2, 3, 224, 224, 64, 1),    # VGG-16 conv1_1 shape (2 images)
+    (3, 3, 30, 30, 64, 1),      # ragged 16 x 16 blocks
+    (2, 2, 20, 17, 32, 1),
+    (2, 4, 33, 30, 96, 2),
+    (1, 3, 18, 18, 256, 1),   # 8 output-channel chunks per block
+    (1, 2, 16, 16, 32, 2),
+])
+def test_direct_small_c_matches_oracle(case):
+    n, c, h, w, k, stride = case
+    x, wt = _inputs(n, c, h, w, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    tile = TileConfig(16, 16, 32, 32768, 1, 1, 1, layout="HWC")
+    info = C.query(x.shape, wt.shape, stride, 1, "HWC", tile, "direct")
+    assert info["rc"] == 0 and "small-C" in info["reason"], info["reason"]
+    y = C.conv_direct(_dev(x, "HWC"), _dev(wt), stride=stride, padding=1, tile=tile, bias=_dev(b),
+                      relu=True)
+    assert C.infer_layout(y) == "HWC"
+    ref = np.maximum(co.direct_conv(x, wt, stride, 1) + b[None, :, None, None], 0)
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= 1e-5
+    wp = C.pack_filter_direct(_dev(wt))
+    y2 = C.conv_direct(_dev(x, "HWC"), _dev(wt), stride=stride, padding=1, tile=tile, bias=_dev(b),
+                       relu=True, w_packed=wp)
+    assert torch.equal(y, y2)
