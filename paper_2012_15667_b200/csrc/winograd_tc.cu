@@ -128,7 +128,7 @@ __device__ __forceinline__ void store4(T *p, float4 v) {
 // (The first version -- one thread per channel, 64-bit index math -- was
 // instruction-issue bound at ~990 instructions per warp-element.)
 template <int E, typename T>
-__global__ void __launch_bounds__(128) winograd_input_tc_kernel(const float *__restrict__ x,
+__global__ void __launch_bounds__(128, 3) winograd_input_tc_kernel(const float *__restrict__ x,
                                                                 T *__restrict__ v, WinoTcGeom g) {
     pdl_wait();
     constexpr int M = WinoTf<E>::M;
