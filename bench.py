@@ -264,10 +264,20 @@ def main() -> None:
     # rank, so the max-over-ranks / barrier path is the same code at N=1 and N=8
     if world > 1 or "MASTER_ADDR" in os.environ:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        # NCCL's version banner goes to stdout; the contract is one JSON line there
+        # NCCL prints its version banner on stdout when the communicator is created;
+        # the contract is one JSON line there, so communicator setup writes to stderr
         if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
             os.environ["NCCL_DEBUG"] = "WARN"
-        dist.init_process_group("nccl", device_id=dev)
+        sys.stdout.flush()
+        saved_fd = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=dev)
+            dist.barrier()
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved_fd, 1)
+            os.close(saved_fd)
     distributed = dist.is_available() and dist.is_initialized()
 
     def barrier():
