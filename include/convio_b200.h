@@ -62,12 +62,16 @@ extern "C" {
 #define CONVIO_ALG_WINOGRAD_TC_3XTF32 6 /* ... 3xTF32 (FP32-level GEMM accuracy) */
 #define CONVIO_ALG_WINOGRAD_TC_BF16 7   /* ... BF16 transformed operands */
 #define CONVIO_ALG_WINOGRAD_NHWC 8      /* same pipeline, element-wise GEMMs as a batched FP32 FFMA GEMM */
+#define CONVIO_ALG_WINOGRAD_TC_3XF16 9  /* ... scaled fp16 hi / lo planes, 3 f16 MMAs (FP32-level) */
 
 /* Operand precision of the tcgen05 contractions (FP32 accumulate always). */
 #define CONVIO_PREC_TF32 0
 #define CONVIO_PREC_3XTF32 1
 #define CONVIO_PREC_BF16 2
 #define CONVIO_PREC_FP32 3   /* convio_winograd_bgemm only: FP32 FFMA GEMMs on the CUDA cores */
+#define CONVIO_PREC_3XF16 4  /* convio_winograd_bgemm only: operands split by the transforms into
+                                power-of-two-scaled fp16 hi / lo planes (22-bit, like 3xTF32),
+                                3 MMAs at the f16 rate; C % 64 == 0, CTA pair tiles */
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {

@@ -21,8 +21,10 @@ ALG_DIRECT, ALG_WINOGRAD, ALG_IGEMM_TF32, ALG_IGEMM_3XTF32 = 0, 1, 2, 3
 ALG_IGEMM_BF16 = 4
 ALG_WINOGRAD_TC_TF32, ALG_WINOGRAD_TC_3XTF32, ALG_WINOGRAD_TC_BF16 = 5, 6, 7
 ALG_WINOGRAD_NHWC = 8
-PREC_TF32, PREC_3XTF32, PREC_BF16, PREC_FP32 = 0, 1, 2, 3
-PRECISIONS = {"tf32": PREC_TF32, "3xtf32": PREC_3XTF32, "bf16": PREC_BF16, "fp32": PREC_FP32}
+ALG_WINOGRAD_TC_3XF16 = 9
+PREC_TF32, PREC_3XTF32, PREC_BF16, PREC_FP32, PREC_3XF16 = 0, 1, 2, 3, 4
+PRECISIONS = {"tf32": PREC_TF32, "3xtf32": PREC_3XTF32, "bf16": PREC_BF16, "fp32": PREC_FP32,
+              "3xf16": PREC_3XF16}
 
 
 class ConvDesc(ctypes.Structure):

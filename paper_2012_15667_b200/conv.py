@@ -98,7 +98,7 @@ ALGORITHMS = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
               "igemm_bf16": N.ALG_IGEMM_BF16, "winograd_tc_tf32": N.ALG_WINOGRAD_TC_TF32,
               "winograd_tc_3xtf32": N.ALG_WINOGRAD_TC_3XTF32,
               "winograd_tc_bf16": N.ALG_WINOGRAD_TC_BF16, "winograd_nhwc": N.ALG_WINOGRAD_NHWC,
-              "winograd_tc_fp32": N.ALG_WINOGRAD_NHWC}
+              "winograd_tc_fp32": N.ALG_WINOGRAD_NHWC, "winograd_tc_3xf16": N.ALG_WINOGRAD_TC_3XF16}
 
 
 def query(x_shape, w_shape, stride: int = 1, padding: int = 0, layout: str = "CHW",
@@ -347,6 +347,8 @@ def winograd_filter_transform_tc(w: torch.Tensor, e: int, precision: str = "3xtf
     k, c, r, s = w.shape
     m = e + r - 1
     shape = (m * m, c, k) if prec == N.PREC_FP32 else (m * m, k, c)
+    if prec == N.PREC_3XF16:   # packed: fp32 U, fp16 hi / lo planes, per-row exponents
+        shape = (m * m, k, 2 * c + 1)
     u = torch.empty(shape, device=w.device,
                     dtype=torch.bfloat16 if prec == N.PREC_BF16 else torch.float32)
     desc = N.make_desc(1, c, 8, 8, k, r, s, 1, 1, 2)
@@ -387,7 +389,7 @@ def conv_winograd_tc(x: torch.Tensor, w: torch.Tensor, e: int = 4, padding: int 
     else:   # library default: widest N tile dividing K, CTA-pair kernel
         z = 256 if desc.k % 256 == 0 else (128 if desc.k % 128 == 0 else 64)
         ct = N.Tile(e, e, z, 8192, 1, 1, 2, 2, e)
-    alg = N.ALG_WINOGRAD_TC_TF32 + prec
+    alg = N.ALG_WINOGRAD_TC_3XF16 if prec == N.PREC_3XF16 else N.ALG_WINOGRAD_TC_TF32 + prec
     need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), ctypes.byref(ct), alg))
     if need < 0:
         rc, _ = N.query(desc, ct, alg)

@@ -688,6 +688,7 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_query(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32, out);
     if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_query(desc, tile, CONVIO_PREC_FP32, out);
+    if (algorithm == CONVIO_ALG_WINOGRAD_TC_3XF16) return wino_tc_query(desc, tile, CONVIO_PREC_3XF16, out);
     set_error("unknown algorithm %d", algorithm);
     return CONVIO_EINVAL;
 }
@@ -704,6 +705,8 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_workspace_bytes(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32);
     if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_workspace_bytes(desc, tile, CONVIO_PREC_FP32);
+    if (algorithm == CONVIO_ALG_WINOGRAD_TC_3XF16)
+        return wino_tc_workspace_bytes(desc, tile, CONVIO_PREC_3XF16);
     return -1;
 }
 

@@ -61,6 +61,10 @@ static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
         if (bn == 128) return &igemm_pair_kernel<128, KIND_3XTF32, false, true>;
         return nullptr;
     }
+    if (kind == KIND_3XF16) {   // scaled fp16 hi / lo planes (batched Winograd GEMMs)
+        if (halo) return nullptr;
+        return pair_kernel_kind<KIND_3XF16, false>(bn);
+    }
     return halo ? pair_kernel_h<true>(bn, kind) : pair_kernel_h<false>(bn, kind);
 }
 
@@ -133,7 +137,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
                                  : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
-        const int mult = kind == KIND_3XTF32 ? 2 : 1;
+        const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16) ? 2 : 1;
         // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
         const bool loslot = kind == KIND_3XTF32 && !pl->halo && !pl->tsa && bn == 256;
         const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
@@ -336,7 +340,9 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
 // 1 x T pixels, U the filter of tap xi.
 int plan_igemm_batched(int kind, int bn, int s_b, bool pair, bool tsa, int xi, int t_count, int c, int k,
                        IgemmPlan *pl, char *reason, size_t rlen) {
-    const int cb = kind == KIND_BF16 ? 64 : 32;
+    const int cb = (kind == KIND_BF16 || kind == KIND_3XF16) ? 64 : 32;
+    if (kind == KIND_3XF16 && (!pair || tsa))
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "3xF16 GEMMs run on the CTA pair (n_zt = 2)");
     if (c % cb)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", c, cb);
     if (k % bn)
@@ -366,10 +372,13 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
                             CUtensorMap *tw) {
     const IgemmParams &P = pl.P;
     if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15)) return false;
-    const bool bf = pl.kind == KIND_BF16;
+    // 2-byte operands (bf16, or the 3xF16 fp16 planes: TMA copies bytes, the type
+    // only sets the element size)
+    const bool bf = pl.kind == KIND_BF16 || pl.kind == KIND_3XF16;
+    const int planes = pl.kind == KIND_3XF16 ? 2 : 1;   // hi, lo planes along images / taps
     const cuuint64_t es_b = bf ? 2 : 4;
     const cuuint32_t cb = bf ? 64 : 32;
-    cuuint64_t xd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.n};
+    cuuint64_t xd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.n * planes};
     cuuint64_t xs[3] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.w * P.c * es_b,
                         (cuuint64_t)P.h * P.w * P.c * es_b};
     // stride: box spans stride*(pixels) input positions, traversal stride picks every stride-th
@@ -383,7 +392,7 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const int taps = P.batched ? P.n : P.ks * P.ks;
-    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps};
+    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps * planes};
     cuuint64_t ws[2] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.k * P.c * es_b};
     cuuint32_t wb[3] = {cb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1};
     if (pl.fold) {   // packed filter as [R*S*K rows][C]: a kernel row's S*K rows are contiguous

@@ -121,14 +121,16 @@ __device__ __forceinline__ void tma_load_2d_pair(void *dst, uint64_t map, int c0
 
 template <int BN, int KIND>
 __device__ __forceinline__ constexpr uint32_t idesc_m256() {
-    return (1u << 4) | ((KIND == KIND_BF16 ? 1u : 2u) << 7) | ((KIND == KIND_BF16 ? 1u : 2u) << 10) |
+    // A/B format: 0 F16 (kind::f16), 1 BF16 (kind::f16), 2 TF32 (kind::tf32)
+    constexpr uint32_t F = KIND == KIND_BF16 ? 1u : (KIND == KIND_3XF16 ? 0u : 2u);
+    return (1u << 4) | (F << 7) | (F << 10) |
            ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
 }
 
 template <int KIND>
 __device__ __forceinline__ void umma_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
                                           uint32_t accumulate) {
-    if constexpr (KIND == KIND_BF16) {
+    if constexpr (KIND == KIND_BF16 || KIND == KIND_3XF16) {
         asm volatile(
             "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
             "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
@@ -250,11 +252,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
     constexpr bool SPLIT = KIND == KIND_3XTF32;
+    // KIND_3XF16 (batched Winograd GEMMs): operands pre-split by the transforms into
+    // scaled fp16 hi / lo planes (the lo plane xi-count images / taps further on);
+    // TMA brings all four, the MMA issues hi*lo + lo*hi + hi*hi like 3xTF32 -- no
+    // converters -- and the epilogue undoes the power-of-two row / column scales
+    constexpr bool F16X3 = KIND == KIND_3XF16;
+    static_assert(!F16X3 || (!HALO && !TSA && !FOLD), "3xF16: plain pair tiles");
     constexpr int HB = BN / 2;                        // filter rows staged per CTA
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = HB * 128;
-    constexpr int MULT = SPLIT ? 2 : 1;               // hi (raw) + lo copies
-    constexpr int CB = KIND == KIND_BF16 ? 64 : 32;
+    constexpr int MULT = (SPLIT || F16X3) ? 2 : 1;    // hi (raw) + lo copies
+    constexpr int CB = (KIND == KIND_BF16 || F16X3) ? 64 : 32;
     // TSA (3xTF32, BN <= 128): A_hi / A_lo live in TMEM columns after the two
     // accumulators, NTA k-block slots of 64 columns (32 hi + 32 lo)
     static_assert(!TSA || (SPLIT && !HALO && BN <= 128), "TSA: 3xTF32, no halo, BN <= 128");
@@ -418,10 +426,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         if (FOLD) tma_load_2d(b, map_w, cb * CB, frow, full + s);
                         else tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
                     } else {                 // both CTAs' bytes complete on the leader's barrier
-                        if (leader) mbar_arrive_expect_tx(full + s, 2 * cta_bytes);
+                        if (leader) mbar_arrive_expect_tx(full + s, 2 * MULT * cta_bytes);
                         if (!HALO) tma_load_4d_pair(a, map_x, cb * CB, xc, yc, img0, full + s);
                         if (FOLD) tma_load_2d_pair(b, map_w, cb * CB, frow, full + s);
                         else tma_load_3d_pair(b, map_w, cb * CB, n0, wc, full + s);
+                        if constexpr (F16X3) {   // lo planes: P.n (= xi) images / taps further on
+                            tma_load_4d_pair(a + A_BYTES + B_BYTES, map_x, cb * CB, xc, yc, img0 + P.n, full + s);
+                            tma_load_3d_pair(b + A_BYTES + B_BYTES, map_w, cb * CB, n0, wc + P.n, full + s);
+                        }
                     }
                     // halo: channel block outer, taps inner (footprint reused by all taps)
                     if (HALO) {
@@ -490,7 +502,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         fa = smem_u32(aring + sa * ASLOT);
                     }
                     if constexpr (SPLIT) mbar_wait_cluster(conv + s, ph);
-                    else mbar_wait(full + s, ph);
+                    else mbar_wait(full + s, ph);   // F16X3: all four planes by TMA
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     const uint32_t st = smem_u32(bring + s * STAGE);
                     uint32_t a, b;
@@ -505,7 +517,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const uint64_t ad = HALO ? umma_desc_sw128_row(a) : umma_desc_sw128(a);
                     const uint64_t bd = umma_desc_sw128(b);
                     const bool first = kb == kb_lo;
-                    if constexpr (SPLIT) {
+                    if constexpr (SPLIT || F16X3) {
                         const uint32_t lo = smem_u32(loring + l * LO_SLOT);
                         const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : (LOSLOT ? lo : a + A_BYTES + B_BYTES);
                         const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : (LOSLOT ? lo + A_BYTES : b + A_BYTES + B_BYTES);
@@ -587,12 +599,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             const int cc = 4 * (lane & 7);
             float *drow[8];
             bool vrow[8];
+            int rexp[8];   // F16X3: the rows' operand scale exponents
+            const int my_re = (F16X3 && valid) ? __ldg(P.row_exp + (int64_t)img * P.q + ox) : 0;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 const int row = i * 4 + (lane >> 3);
                 drow[i] = reinterpret_cast<float *>(
                     __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), row));
                 vrow[i] = __shfl_sync(0xffffffffu, (int)valid, row) != 0;
+                rexp[i] = F16X3 ? __shfl_sync(0xffffffffu, my_re, row) : 0;
             }
 #pragma unroll 1
             for (int c0 = 0; c0 < KOUT; c0 += 32) {
@@ -614,6 +629,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int j = 0; j < 32; j += 4)
                     *reinterpret_cast<float4 *>(stg + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 __syncwarp();
+                int4 cexp = make_int4(0, 0, 0, 0);
+                if constexpr (F16X3)
+                    cexp = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + k0 + c0 + cc));
                 const float4 bv = P.bias && lead_split
                                       ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -621,6 +639,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int i = 0; i < 8; ++i) {
                     const int row = i * 4 + (lane >> 3);
                     float4 o = *reinterpret_cast<const float4 *>(stg + row * 36 + cc);
+                    if constexpr (F16X3) {   // exact: powers of two
+                        o.x *= pow2f(-(rexp[i] + cexp.x));
+                        o.y *= pow2f(-(rexp[i] + cexp.y));
+                        o.z *= pow2f(-(rexp[i] + cexp.z));
+                        o.w *= pow2f(-(rexp[i] + cexp.w));
+                    }
                     o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
                     if (P.relu) {
                         o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);

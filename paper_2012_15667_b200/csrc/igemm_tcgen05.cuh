@@ -42,10 +42,21 @@ struct IgemmParams {
     int relu;
     int batched;               // 1: Winograd element-wise GEMMs (see header)
     int splits;                // split-K factor (blockIdx.z = split; > 1 only without ReLU)
+    // KIND_3XF16 (batched only): power-of-two exponents the operands were scaled by;
+    // the epilogue multiplies D[t][k] by 2^-(row_exp[g][t] + col_exp[g][k])
+    const int *row_exp;
+    const int *col_exp;
 };
 
 // operand kinds of the tcgen05 contraction
-enum IgemmKind : int { KIND_TF32 = 0, KIND_3XTF32 = 1, KIND_BF16 = 2 };
+enum IgemmKind : int { KIND_TF32 = 0, KIND_3XTF32 = 1, KIND_BF16 = 2, KIND_3XF16 = 4 };
+
+// 2^e as a float for e in [-126, 127] (exponent bits; a multiply by it is exact
+// wherever the product stays normal) -- ldexpf costs ~20 instructions
+__device__ __forceinline__ float pow2f(int e) {
+    e = max(-126, min(127, e));
+    return __int_as_float((e + 127) << 23);
+}
 
 // ---- tcgen05 / UMMA primitives ----------------------------------------------------
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t smem_addr) {

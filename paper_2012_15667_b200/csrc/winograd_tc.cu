@@ -17,6 +17,7 @@
 // in the 126 MB L2 between the three launches, large ones (measured faster)
 // run the whole batch in three launches.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdarg.h>
 #include <algorithm>
 
@@ -179,6 +180,161 @@ __global__ void __launch_bounds__(128, 3) winograd_input_tc_kernel(const float *
     }
 }
 
+// Power-of-two scale exponent for a row whose largest magnitude is `mx`: the
+// scaled row lies in (-2^15, 2^15), so its fp16 hi parts are normal down to
+// 2^-24 of the row maximum and nothing overflows.
+__device__ __forceinline__ int f16_row_exp(float mx) {
+    if (!(mx >= 1.17549435e-38f)) return 0;   // zero / subnormal rows: unscaled
+    const int ex = ((__float_as_int(mx) >> 23) & 0xff) - 126;   // mx = f * 2^ex, f in [0.5, 1)
+    return 15 - ex;
+}
+
+__device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __half &lo) {
+    const float s = v * scale;
+    hi = __float2half_rn(s);
+    lo = __float2half_rn(s - __half2float(hi));
+}
+
+// Step 1, 3xF16 form: V = B^T d B as above, then per (xi, tile) row a power-of-two
+// scale over all C channels (the row's threads are consecutive: c4 fastest) and
+// fp16 hi / lo planes V16[plane][xi][t][c] + row_exp[xi][t] for the GEMM epilogue.
+// The loop is block-uniform (C / 4 threads of a tile never straddle a block: 128
+// is a multiple of C / 4 for C in {64, 128, 256, 512}).
+template <int E>
+__global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *__restrict__ x,
+                                                                   __half *__restrict__ v,
+                                                                   int *__restrict__ row_exp,
+                                                                   WinoTcGeom g) {
+    pdl_wait();
+    constexpr int M = WinoTf<E>::M;
+    __shared__ float red[4][M * M];
+    const int c4n = g.c >> 2;
+    const int tpi = g.tiles_y * g.tiles_x;
+    const int t_count = tpi * g.imgs;
+    const int total = t_count * c4n;
+    const int64_t xi_stride = (int64_t)t_count * g.c;
+    const int row4 = g.w * c4n;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = blockIdx.x * blockDim.x; base < total; base += gridDim.x * blockDim.x) {
+        const int i = base + threadIdx.x;
+        const bool active = i < total;
+        const int ii = active ? i : total - 1;
+        const int t = ii / c4n;
+        const int c4 = ii - t * c4n;
+        const int img = t / tpi;
+        const int rem = t - img * tpi;
+        const int ty = rem / g.tiles_x, tx = rem - ty * g.tiles_x;
+        const int iy0 = ty * E - g.pad, ix0 = tx * E - g.pad;
+        const float4 *xb = reinterpret_cast<const float4 *>(x + (int64_t)(g.img0 + img) * g.h * g.w * g.c) + c4;
+        float4 d[M][M];
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            const int iy = iy0 + a;
+            const bool rok = active && iy >= 0 && iy < g.h;
+#pragma unroll
+            for (int b = 0; b < M; ++b) {
+                const int ix = ix0 + b;
+                d[a][b] = (rok && ix >= 0 && ix < g.w) ? __ldg(xb + iy * row4 + ix * c4n)
+                                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
+        float4 tmp[M][M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            float4 col[M], o[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) col[a] = d[a][j];
+            apply4<M, M>(col, o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
+#pragma unroll
+            for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
+        }
+        // pass 1: row maxima over the tile's channels
+        float mx[M * M];
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            float4 o[M];
+            apply4<M, M>(tmp[a], o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
+#pragma unroll
+            for (int b = 0; b < M; ++b)
+                mx[a * M + b] = fmaxf(fmaxf(fabsf(o[b].x), fabsf(o[b].y)), fmaxf(fabsf(o[b].z), fabsf(o[b].w)));
+        }
+        const int grp = c4n < 32 ? c4n : 32;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            if (off < grp) {
+#pragma unroll
+                for (int q = 0; q < M * M; ++q) mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], off));
+            }
+        }
+        if (c4n > 32) {   // the tile spans c4n / 32 warps of this block
+            if (lane == 0) {
+#pragma unroll
+                for (int q = 0; q < M * M; ++q) red[warp][q] = mx[q];
+            }
+            __syncthreads();
+            const int w0 = warp & ~(c4n / 32 - 1);
+#pragma unroll
+            for (int q = 0; q < M * M; ++q) {
+                float m = red[w0][q];
+                for (int w = 1; w < c4n / 32; ++w) m = fmaxf(m, red[w0 + w][q]);
+                mx[q] = m;
+            }
+            __syncthreads();
+        }
+        // pass 2: scaled hi / lo planes
+        if (active) {
+            __half *vp = v + (int64_t)t * g.c + 4 * c4;
+            const int64_t plane = (int64_t)M * M * xi_stride;
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                float4 o[M];
+                apply4<M, M>(tmp[a], o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    const int e = f16_row_exp(mx[a * M + b]);
+                    const float sc = pow2f(e);
+                    __half h[4], l[4];
+                    split_f16(o[b].x, sc, h[0], l[0]);
+                    split_f16(o[b].y, sc, h[1], l[1]);
+                    split_f16(o[b].z, sc, h[2], l[2]);
+                    split_f16(o[b].w, sc, h[3], l[3]);
+                    __half *dst = vp + (a * M + b) * xi_stride;
+                    *reinterpret_cast<uint2 *>(dst) = *reinterpret_cast<const uint2 *>(h);
+                    *reinterpret_cast<uint2 *>(dst + plane) = *reinterpret_cast<const uint2 *>(l);
+                    if (c4 == 0) row_exp[(int64_t)(a * M + b) * t_count + t] = e;
+                }
+            }
+        }
+    }
+}
+
+// 3xF16 kernel operand: U (fp32, [xi][k][c]) -> power-of-two scale per (xi, k) row
+// over c, fp16 hi / lo planes U16[plane][xi][k][c] and col_exp[xi][k].  One warp
+// per row.
+__global__ void __launch_bounds__(256) winograd_u_split_f16x3_kernel(const float *__restrict__ u,
+                                                                     __half *__restrict__ u16,
+                                                                     int *__restrict__ col_exp,
+                                                                     int rows, int c) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int64_t plane = (int64_t)rows * c;
+    for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += (gridDim.x * blockDim.x) >> 5) {
+        const float *ur = u + (int64_t)r * c;
+        float mx = 0.0f;
+        for (int j = lane; j < c; j += 32) mx = fmaxf(mx, fabsf(ur[j]));
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const int e = f16_row_exp(mx);
+        const float sc = pow2f(e);
+        for (int j = lane; j < c; j += 32) {
+            __half h, l;
+            split_f16(ur[j], sc, h, l);
+            u16[(int64_t)r * c + j] = h;
+            u16[plane + (int64_t)r * c + j] = l;
+        }
+        if (lane == 0) col_exp[r] = e;
+    }
+}
+
 // Step 2: U[xi][k][c] = (G g G^T)[xi] (K-major B operand of the tensor-core
 // GEMM) or, CK = true, U[xi][c][k] (the FFMA GEMM's [channel][n] rows); one
 // thread per (k, c), c fastest.
@@ -277,6 +433,7 @@ static int kind_of_prec(int32_t precision) {
         case CONVIO_PREC_3XTF32: return KIND_3XTF32;
         case CONVIO_PREC_BF16: return KIND_BF16;
         case CONVIO_PREC_FP32: return KIND_FFMA;
+        case CONVIO_PREC_3XF16: return KIND_3XF16;
         default: return -1;
     }
 }
@@ -326,12 +483,16 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
         return fail(CONVIO_EINFEASIBLE, "tensor-core Winograd needs the HWC (NHWC) layout");
     const int p = d->h + 2 * d->pad - 2, q = d->w + 2 * d->pad - 2;
     if (p < 1 || q < 1) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
-    const int cb = kind == KIND_BF16 ? 64 : 32;
+    const int cb = (kind == KIND_BF16 || kind == KIND_3XF16) ? 64 : 32;
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
     int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));
     int s_b = t ? t->s_b : 8192;
     const bool pair = kind != KIND_FFMA && (t ? (t->n_zt == 2 || t->n_zt == 4) : true);
     const bool tsa = t && t->n_zt == 4;
+    if (kind == KIND_3XF16 && (!pair || tsa))
+        return fail(CONVIO_EINFEASIBLE, "3xF16 Winograd GEMMs run on the CTA pair (n_zt = 2)");
+    if (kind == KIND_3XF16 && (d->c > 512 || (d->c & (d->c - 1))))
+        return fail(CONVIO_EINFEASIBLE, "3xF16 input transform: C a power of two in [64, 512]");
     if (tsa && (kind != KIND_3XTF32 || (t->z != 64 && t->z != 128)))
         return fail(CONVIO_EINFEASIBLE, "A-in-TMEM (n_zt = 4) Winograd GEMMs need 3xTF32 and z <= 128");
     if (kind == KIND_FFMA && !t) bn = d->k % 128 == 0 ? 128 : 64;
@@ -369,8 +530,10 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
     pl->e = e; pl->m = m; pl->kind = kind; pl->bn = bn; pl->s_b = s_b; pl->pair = pair;
     pl->tsa = tsa;
     pl->chunk_imgs = chunk;
-    pl->u_bytes = al256((size_t)m * m * d->k * d->c * es);
-    pl->v_bytes = al256((size_t)m * m * chunk * tpi * d->c * es);
+    // 3xF16: U = [fp32 U | fp16 hi plane | fp16 lo plane | col_exp], V = [hi | lo | row_exp]
+    const bool f16 = kind == KIND_3XF16;
+    pl->u_bytes = al256((size_t)m * m * d->k * d->c * es * (f16 ? 2 : 1) + (f16 ? (size_t)m * m * d->k * 4 : 0));
+    pl->v_bytes = al256((size_t)m * m * chunk * tpi * d->c * es + (f16 ? (size_t)m * m * chunk * tpi * 4 : 0));
     pl->m_bytes = al256((size_t)m * m * chunk * tpi * d->k * 4);
     return CONVIO_OK;
 }
@@ -388,6 +551,14 @@ static int launch_filter_tc(const WinoTcPlan &pl, const float *w, void *u, cudaS
     } else {
         if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<4, __nv_bfloat16>, dim3(blocks), dim3(256), 0, st, w, (__nv_bfloat16 *)u, pl.g.k, pl.g.c));
         else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_kernel<4, float>, dim3(blocks), dim3(256), 0, st, w, (float *)u, pl.g.k, pl.g.c));
+    }
+    if (pl.kind == KIND_3XF16) {   // fp32 U -> scaled fp16 hi / lo planes + col_exp
+        note_launch();
+        const int rows = pl.m * pl.m * pl.g.k;
+        const size_t ub = (size_t)rows * pl.g.c * 4;
+        CONVIO_CUDA_TRY(launch_pdl(winograd_u_split_f16x3_kernel, dim3((unsigned)std::min(rows / 8 + 1, 148 * 16)),
+                                   dim3(256), 0, st, (const float *)u, (__half *)((uint8_t *)u + ub),
+                                   (int *)((uint8_t *)u + 2 * ub), rows, pl.g.c));
     }
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
@@ -504,7 +675,15 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
         g.imgs = std::min(pl.chunk_imgs, desc->n - img0);
         const int tc = g.imgs * tpi;
         const int gin = grid_for((int64_t)tc * (g.c / 4), 128), gout = grid_for((int64_t)tc * (g.k / 4), 128);
-        if (pl.e == 2) {
+        const size_t vb = (size_t)pl.m * pl.m * tc * g.c * 4;   // 3xF16: hi + lo planes
+        if (pl.kind == KIND_3XF16) {
+            if (pl.e == 2)
+                CONVIO_CUDA_TRY(launch_pdl(winograd_input_f16x3_kernel<2>, dim3(gin), dim3(128), 0, st, x,
+                                           (__half *)v, (int *)((uint8_t *)v + vb), g));
+            else
+                CONVIO_CUDA_TRY(launch_pdl(winograd_input_f16x3_kernel<4>, dim3(gin), dim3(128), 0, st, x,
+                                           (__half *)v, (int *)((uint8_t *)v + vb), g));
+        } else if (pl.e == 2) {
             if (bf) CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<2, __nv_bfloat16>, dim3(gin), dim3(128), 0, st, x, (__nv_bfloat16 *)v, g));
             else CONVIO_CUDA_TRY(launch_pdl(winograd_input_tc_kernel<2, float>, dim3(gin), dim3(128), 0, st, x, (float *)v, g));
         } else {
@@ -521,7 +700,14 @@ int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile,
             rc = plan_igemm_batched(pl.kind, pl.bn, pl.s_b, pl.pair, pl.tsa, pl.m * pl.m, tc, g.c, g.k, &gp, why,
                                     sizeof(why));
             if (rc) return rc;
-            rc = igemm_launch(gp, v, u, nullptr, 0, mm, st);
+            const void *ua = u;
+            if (pl.kind == KIND_3XF16) {
+                const size_t ub = (size_t)pl.m * pl.m * g.k * g.c * 4;
+                ua = (const uint8_t *)u + ub;
+                gp.P.row_exp = (const int *)((const uint8_t *)v + vb);
+                gp.P.col_exp = (const int *)((const uint8_t *)u + 2 * ub);
+            }
+            rc = igemm_launch(gp, v, ua, nullptr, 0, mm, st);
         }
         if (rc) return rc;
         if (pl.e == 2)

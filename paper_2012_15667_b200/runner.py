@@ -83,7 +83,8 @@ def expand(layers: list[LayerSpec]) -> list[LayerSpec]:
 # Algorithms whose results meet the FP32 tolerance (1e-5 normwise vs the float64
 # oracle; Winograd F(e,3) is looser by construction, 1e-4 / 1e-3) -- the
 # headline plan picks among these; "igemm_tf32" is the reduced-precision variant.
-FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32", "winograd_nhwc")
+FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32", "winograd_nhwc",
+                   "winograd_tc_3xf16")
 CUDA_CORE_ALGORITHMS = ("direct", "winograd", "winograd_nhwc")
 
 
@@ -181,6 +182,8 @@ class ConvLayer:
         s = self.spec
         if self.algorithm.startswith("winograd"):
             m = self.e + s.r - 1
+            if self.algorithm == "winograd_tc_3xf16":   # fp32 U + fp16 hi / lo planes + exponents
+                return m * m * s.k * (2 * s.c + 1)
             return m * m * s.c * s.k
         return s.k * s.c * s.r * s.r
 

@@ -160,3 +160,16 @@ def test_tensor_core_projections_plan_pairs_split_k_and_chunks():
     wbad = query((24, 64, 56, 56), (256, 64, 3, 3), 1, 1, hwc,
                  TileConfig(4, 4, 256, 32768, 1, 1, 4, layout=hwc, e=4), "winograd_tc_3xtf32")
     assert wbad["rc"] == 3
+
+
+def test_winograd_3xf16_projection():
+    hwc = "HWC"
+    ok = query((8, 128, 28, 28), (128, 128, 3, 3), 1, 1, hwc,
+               TileConfig(4, 4, 128, 32768, 1, 1, 2, layout=hwc, e=4), "winograd_tc_3xf16")
+    assert ok["rc"] == 0
+    single = query((8, 128, 28, 28), (128, 128, 3, 3), 1, 1, hwc,
+                   TileConfig(4, 4, 128, 32768, 1, 1, 1, layout=hwc, e=4), "winograd_tc_3xf16")
+    assert single["rc"] == 3 and "pair" in single["reason"]
+    odd = query((8, 96, 28, 28), (128, 96, 3, 3), 1, 1, hwc,
+                TileConfig(4, 4, 128, 32768, 1, 1, 2, layout=hwc, e=4), "winograd_tc_3xf16")
+    assert odd["rc"] == 3

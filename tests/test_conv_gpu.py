@@ -500,3 +500,25 @@ def test_direct_small_c_matches_oracle(case):
     y2 = C.conv_direct(_dev(x, "HWC"), _dev(wt), stride=stride, padding=1, tile=tile, bias=_dev(b),
                        relu=True, w_packed=wp)
     assert torch.equal(y, y2)
+
+
+@pytest.mark.parametrize("case", [
+    # (n, c, h, k, e, z): scaled-fp16 3-product Winograd GEMMs (CONVIO_PREC_3XF16)
+    (2, 64, 28, 64, 4, 64), (3, 128, 14, 256, 4, 256), (2, 256, 7, 128, 2, 128),
+    (2, 512, 7, 512, 4, 256), (4, 128, 28, 128, 4, 128),
+])
+def test_winograd_tc_3xf16_matches_oracle(case):
+    n, c, h, k, e, z = case
+    x, wt = _inputs(n, c, h, h, k, 3, 3)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    tile = TileConfig(e, e, z, 32768, 1, 1, 2, layout="HWC", e=e)
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16",
+                           bias=_dev(b))
+    ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
+    tol = TOL_WINO[e] * max(1.0, (c / 64) ** 0.5)   # the FP32 Winograd tolerance
+    assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= tol
+    # rows of very different magnitude: the per-row power-of-two scales keep them exact
+    xs = x * np.float32(2.0 ** 20)
+    ys = C.conv_winograd_tc(_dev(xs, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16")
+    refs = co.direct_conv(xs, wt, 1, 1)
+    assert co.rel_err(ys.contiguous().cpu().numpy(), refs) <= tol
