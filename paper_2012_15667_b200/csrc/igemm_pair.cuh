@@ -609,7 +609,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 vrow[i] = __shfl_sync(0xffffffffu, (int)valid, row) != 0;
                 rexp[i] = F16X3 ? __shfl_sync(0xffffffffu, my_re, row) : 0;
             }
-#pragma unroll 1
+            // F16X3: every chunk's column exponents up front (a per-chunk load left its
+            // latency on the critical path of the epilogue, which then paced the MMAs)
+            constexpr int NCH = F16X3 ? KOUT / 32 : 1;
+            int4 cexp_all[NCH];
+            if constexpr (F16X3) {
+#pragma unroll
+                for (int j = 0; j < NCH; ++j)
+                    cexp_all[j] = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + k0 + j * 32 + cc));
+            }
+            constexpr int EPI_UNROLL = F16X3 ? NCH : 1;
+#pragma unroll EPI_UNROLL
             for (int c0 = 0; c0 < KOUT; c0 += 32) {
                 float v[32];
                 tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
@@ -629,9 +639,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int j = 0; j < 32; j += 4)
                     *reinterpret_cast<float4 *>(stg + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                 __syncwarp();
-                int4 cexp = make_int4(0, 0, 0, 0);
-                if constexpr (F16X3)
-                    cexp = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + k0 + c0 + cc));
+                const int4 cexp = cexp_all[F16X3 ? c0 / 32 : 0];
                 const float4 bv = P.bias && lead_split
                                       ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
                                          : make_float4(0.f, 0.f, 0.f, 0.f);
