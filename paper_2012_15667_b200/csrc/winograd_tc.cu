@@ -33,6 +33,7 @@ struct WinoTf;
 template <>
 struct WinoTf<2> {   // F(2x2, 3x3), m = 4
     static constexpr int M = 4;
+    static constexpr float GMAX = 4.0f;     // (max row abs-sum of B^T = 2)^2
     template <typename T>
     __device__ __forceinline__ static void bt(const T (&d)[4], T (&o)[4]) {
         o[0] = d[0] - d[2];
@@ -55,6 +56,7 @@ struct WinoTf<2> {   // F(2x2, 3x3), m = 4
 template <>
 struct WinoTf<4> {   // F(4x4, 3x3), m = 6
     static constexpr int M = 6;
+    static constexpr float GMAX = 100.0f;   // (max row abs-sum of B^T = 10)^2
     template <typename T>
     __device__ __forceinline__ static void bt(const T (&d)[6], T (&o)[6]) {
         o[0] = fmaf(4.0f, d[0], fmaf(-5.0f, d[2], d[4]));
@@ -195,19 +197,20 @@ __device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __ha
     lo = __float2half_rn(s - __half2float(hi));
 }
 
-// Step 1, 3xF16 form: V = B^T d B as above, then per (xi, tile) row a power-of-two
-// scale over all C channels (the row's threads are consecutive: c4 fastest) and
-// fp16 hi / lo planes V16[plane][xi][t][c] + row_exp[xi][t] for the GEMM epilogue.
+// Step 1, 3xF16 form: V = B^T d B as above, then per tile a power-of-two scale
+// from the footprint's largest |d| over all C channels (the tile's threads are
+// consecutive: c4 fastest) and fp16 hi / lo planes V16[plane][xi][t][c] +
+// row_exp[xi][t] for the GEMM epilogue.
 // The loop is block-uniform (C / 4 threads of a tile never straddle a block: 128
 // is a multiple of C / 4 for C in {64, 128, 256, 512}).
 template <int E>
-__global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *__restrict__ x,
+__global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const float *__restrict__ x,
                                                                    __half *__restrict__ v,
                                                                    int *__restrict__ row_exp,
                                                                    WinoTcGeom g) {
     pdl_wait();
     constexpr int M = WinoTf<E>::M;
-    __shared__ float red[4][M * M];
+    __shared__ float red[4][1];
     const int c4n = g.c >> 2;
     const int tpi = g.tiles_y * g.tiles_x;
     const int t_count = tpi * g.imgs;
@@ -238,6 +241,29 @@ __global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *
                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
+        // one scale per tile: |V| <= Gmax * max|d| over the tile's footprint and channels
+        // (Gmax = the largest (row abs-sum of B^T)^2), so every xi row of the tile fits
+        // (-2^15, 2^15); fp16 being floating point, rows below the bound keep their 11 bits
+        float fm = 0.0f;
+#pragma unroll
+        for (int a = 0; a < M; ++a)
+#pragma unroll
+            for (int b = 0; b < M; ++b)
+                fm = fmaxf(fm, fmaxf(fmaxf(fabsf(d[a][b].x), fabsf(d[a][b].y)),
+                                     fmaxf(fabsf(d[a][b].z), fabsf(d[a][b].w))));
+        const int grp = c4n < 32 ? c4n : 32;
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1)
+            if (off < grp) fm = fmaxf(fm, __shfl_xor_sync(0xffffffffu, fm, off));
+        if (c4n > 32) {   // the tile spans c4n / 32 warps of this block
+            if (lane == 0) red[warp][0] = fm;
+            __syncthreads();
+            const int w0 = warp & ~(c4n / 32 - 1);
+            for (int w = 0; w < c4n / 32; ++w) fm = fmaxf(fm, red[w0 + w][0]);
+            __syncthreads();
+        }
+        const int e = f16_row_exp(fm * WinoTf<E>::GMAX);
+        const float sc = pow2f(e);
         float4 tmp[M][M];
 #pragma unroll
         for (int j = 0; j < M; ++j) {
@@ -247,39 +273,6 @@ __global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *
             apply4<M, M>(col, o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
 #pragma unroll
             for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
-        }
-        // pass 1: row maxima over the tile's channels
-        float mx[M * M];
-#pragma unroll
-        for (int a = 0; a < M; ++a) {
-            float4 o[M];
-            apply4<M, M>(tmp[a], o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
-#pragma unroll
-            for (int b = 0; b < M; ++b)
-                mx[a * M + b] = fmaxf(fmaxf(fabsf(o[b].x), fabsf(o[b].y)), fmaxf(fabsf(o[b].z), fabsf(o[b].w)));
-        }
-        const int grp = c4n < 32 ? c4n : 32;
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            if (off < grp) {
-#pragma unroll
-                for (int q = 0; q < M * M; ++q) mx[q] = fmaxf(mx[q], __shfl_xor_sync(0xffffffffu, mx[q], off));
-            }
-        }
-        if (c4n > 32) {   // the tile spans c4n / 32 warps of this block
-            if (lane == 0) {
-#pragma unroll
-                for (int q = 0; q < M * M; ++q) red[warp][q] = mx[q];
-            }
-            __syncthreads();
-            const int w0 = warp & ~(c4n / 32 - 1);
-#pragma unroll
-            for (int q = 0; q < M * M; ++q) {
-                float m = red[w0][q];
-                for (int w = 1; w < c4n / 32; ++w) m = fmaxf(m, red[w0 + w][q]);
-                mx[q] = m;
-            }
-            __syncthreads();
         }
         // pass 2: scaled hi / lo planes
         if (active) {
@@ -291,8 +284,6 @@ __global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *
                 apply4<M, M>(tmp[a], o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
 #pragma unroll
                 for (int b = 0; b < M; ++b) {
-                    const int e = f16_row_exp(mx[a * M + b]);
-                    const float sc = pow2f(e);
                     __half h[4], l[4];
                     split_f16(o[b].x, sc, h[0], l[0]);
                     split_f16(o[b].y, sc, h[1], l[1]);

@@ -252,7 +252,8 @@ def main():
     ap.add_argument("--exhaustive-cap", type=int, default=0)
     ap.add_argument("--algs", default="direct,direct_nhwc,winograd2,winograd4,igemm_3xtf32,igemm_tf32,"
                     "igemm_bf16,winograd_tc_3xtf32_e2,winograd_tc_3xtf32_e4,"
-                    "winograd_tc_tf32_e4,winograd_tc_bf16_e4,winograd_nhwc_e2,winograd_nhwc_e4")
+                    "winograd_tc_tf32_e4,winograd_tc_bf16_e4,winograd_nhwc_e2,winograd_nhwc_e4,"
+                    "winograd_tc_3xf16_e4")
     ap.add_argument("--layers", default="")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
