@@ -34,6 +34,7 @@ template <>
 struct WinoTf<2> {   // F(2x2, 3x3), m = 4
     static constexpr int M = 4;
     static constexpr float GMAX = 4.0f;     // (max row abs-sum of B^T = 2)^2
+    static constexpr float GROW = 2.0f;     // max row abs-sum of B^T
     template <typename T>
     __device__ __forceinline__ static void bt(const T (&d)[4], T (&o)[4]) {
         o[0] = d[0] - d[2];
@@ -57,6 +58,7 @@ template <>
 struct WinoTf<4> {   // F(4x4, 3x3), m = 6
     static constexpr int M = 6;
     static constexpr float GMAX = 100.0f;   // (max row abs-sum of B^T = 10)^2
+    static constexpr float GROW = 10.0f;    // max row abs-sum of B^T
     template <typename T>
     __device__ __forceinline__ static void bt(const T (&d)[6], T (&o)[6]) {
         o[0] = fmaf(4.0f, d[0], fmaf(-5.0f, d[2], d[4]));
@@ -204,7 +206,7 @@ __device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __ha
 // The loop is block-uniform (C / 4 threads of a tile never straddle a block: 128
 // is a multiple of C / 4 for C in {64, 128, 256, 512}).
 template <int E>
-__global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const float *__restrict__ x,
+__global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *__restrict__ x,
                                                                    __half *__restrict__ v,
                                                                    int *__restrict__ row_exp,
                                                                    WinoTcGeom g) {
@@ -241,16 +243,27 @@ __global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const floa
                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
-        // one scale per tile: |V| <= Gmax * max|d| over the tile's footprint and channels
-        // (Gmax = the largest (row abs-sum of B^T)^2), so every xi row of the tile fits
-        // (-2^15, 2^15); fp16 being floating point, rows below the bound keep their 11 bits
+        float4 tmp[M][M];
+#pragma unroll
+        for (int j = 0; j < M; ++j) {
+            float4 col[M], o[M];
+#pragma unroll
+            for (int a = 0; a < M; ++a) col[a] = d[a][j];
+            apply4<M, M>(col, o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
+#pragma unroll
+            for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
+        }
+        // one scale per tile: |V| <= GROW * max|B^T d| over the tile's (B^T d) values and
+        // channels (GROW = the largest row abs-sum of B^T), so every xi row of the tile fits
+        // (-2^15, 2^15); fp16 being floating point, rows below the bound keep their 11 bits.
+        // (Taken from B^T d, not d, so the footprint registers are dead across the barrier.)
         float fm = 0.0f;
 #pragma unroll
         for (int a = 0; a < M; ++a)
 #pragma unroll
             for (int b = 0; b < M; ++b)
-                fm = fmaxf(fm, fmaxf(fmaxf(fabsf(d[a][b].x), fabsf(d[a][b].y)),
-                                     fmaxf(fabsf(d[a][b].z), fabsf(d[a][b].w))));
+                fm = fmaxf(fm, fmaxf(fmaxf(fabsf(tmp[a][b].x), fabsf(tmp[a][b].y)),
+                                     fmaxf(fabsf(tmp[a][b].z), fabsf(tmp[a][b].w))));
         const int grp = c4n < 32 ? c4n : 32;
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1)
@@ -262,18 +275,8 @@ __global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const floa
             for (int w = 0; w < c4n / 32; ++w) fm = fmaxf(fm, red[w0 + w][0]);
             __syncthreads();
         }
-        const int e = f16_row_exp(fm * WinoTf<E>::GMAX);
+        const int e = f16_row_exp(fm * WinoTf<E>::GROW);
         const float sc = pow2f(e);
-        float4 tmp[M][M];
-#pragma unroll
-        for (int j = 0; j < M; ++j) {
-            float4 col[M], o[M];
-#pragma unroll
-            for (int a = 0; a < M; ++a) col[a] = d[a][j];
-            apply4<M, M>(col, o, [](const float (&in)[M], float (&out)[M]) { WinoTf<E>::bt(in, out); });
-#pragma unroll
-            for (int a = 0; a < M; ++a) tmp[a][j] = o[a];
-        }
         // pass 2: scaled hi / lo planes
         if (active) {
             __half *vp = v + (int64_t)t * g.c + 4 * c4;
@@ -289,9 +292,19 @@ __global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const floa
                     split_f16(o[b].y, sc, h[1], l[1]);
                     split_f16(o[b].z, sc, h[2], l[2]);
                     split_f16(o[b].w, sc, h[3], l[3]);
+                    // lane pairs (c4, c4 + 1) trade halves so each lane stores 16 B of one
+                    // plane: even lanes the 8 channels' hi, odd lanes their lo
                     __half *dst = vp + (a * M + b) * xi_stride;
-                    *reinterpret_cast<uint2 *>(dst) = *reinterpret_cast<const uint2 *>(h);
-                    *reinterpret_cast<uint2 *>(dst + plane) = *reinterpret_cast<const uint2 *>(l);
+                    const uint2 hv = *reinterpret_cast<const uint2 *>(h);
+                    const uint2 lv = *reinterpret_cast<const uint2 *>(l);
+                    const bool odd = c4 & 1;
+                    const uint2 send = odd ? hv : lv;
+                    const unsigned am = __activemask();
+                    const uint32_t gx = __shfl_xor_sync(am, send.x, 1), gy = __shfl_xor_sync(am, send.y, 1);
+                    if (!odd)
+                        *reinterpret_cast<uint4 *>(dst) = make_uint4(hv.x, hv.y, gx, gy);
+                    else
+                        *reinterpret_cast<uint4 *>(dst - 4 + plane) = make_uint4(gx, gy, lv.x, lv.y);
                     if (c4 == 0) row_exp[(int64_t)(a * M + b) * t_count + t] = e;
                 }
             }

@@ -1,0 +1,5 @@
+for v in fu u2; do
+  cp paper_2012_15667_b200/lib/exp/lib$v.so paper_2012_15667_b200/lib/libconvio_b200.so
+  timeout 600 python scripts/f16_check.py 2>&1 | grep -E "3xf16" | sed "s/^/$v /"
+done
+cp paper_2012_15667_b200/lib/exp/libfu.so paper_2012_15667_b200/lib/libconvio_b200.so
