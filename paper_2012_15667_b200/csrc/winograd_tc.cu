@@ -206,7 +206,7 @@ __device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __ha
 // The loop is block-uniform (C / 4 threads of a tile never straddle a block: 128
 // is a multiple of C / 4 for C in {64, 128, 256, 512}).
 template <int E>
-__global__ void __launch_bounds__(128) winograd_input_f16x3_kernel(const float *__restrict__ x,
+__global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const float *__restrict__ x,
                                                                    __half *__restrict__ v,
                                                                    int *__restrict__ row_exp,
                                                                    WinoTcGeom g) {
