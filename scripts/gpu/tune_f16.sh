@@ -1,5 +1,6 @@
 mkdir -p gpurun_out
-
+timeout 600 python -m pytest tests/test_conv_gpu.py -q -x -k "3xf16" 2>&1 | grep -E "passed|failed" | head -2
+ 
 for n in 256 128 64 32; do
   timeout 900 python scripts/tune_layers.py --workload resnet50 --n $n --algs winograd_tc_3xtf32_e4,winograd_tc_3xf16_e4 > gpurun_out/tune_f16_n$n.log 2>&1
 done
