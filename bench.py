@@ -482,10 +482,12 @@ def main() -> None:
         # tensor pipe: dense TF32 = 1/2 of the measured bf16 rate; 3xTF32 issues 3 MMAs per
         # algorithmic flop; BF16 runs at the bf16 rate
         prec = dom.split()[0].rsplit("_", 1)[-1]
-        mma_per_flop = 3 if prec == "3xtf32" else 1
+        # 3xTF32 / 3xF16 issue 3 MMAs per algorithmic flop; f16 and bf16 run at the
+        # bf16 rate, TF32 at half of it
+        mma_per_flop = 3 if prec in ("3xtf32", "3xf16") else 1
         bf16 = peaks.get("bf16_tflops") or 1590.0
-        peak = bf16 if prec == "bf16" else bf16 / 2
-        kind = "kind::f16 (bf16)" if prec == "bf16" else "kind::tf32"
+        peak = bf16 if prec in ("bf16", "3xf16") else bf16 / 2
+        kind = {"bf16": "kind::f16 (bf16)", "3xf16": "kind::f16 (scaled fp16 hi/lo)"}.get(prec, "kind::tf32")
         what = ("implicit GEMM" if dom.startswith("igemm") else
                 "Winograd pipeline: input transform + batched GEMM + output transform, "
                 "flops = element-wise GEMM flops")
@@ -494,7 +496,7 @@ def main() -> None:
             "achieved": round(achieved * mma_per_flop, 3), "peak": round(peak, 3), "unit": "TFLOP/s",
             "frac": round(achieved * mma_per_flop / peak, 4),
             "achieved_algorithmic": round(achieved, 3), "mma_flops_per_algorithmic_flop": mma_per_flop,
-            "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec == "bf16" else " / 2 (dense TF32 rate)")
+            "peak_source": ("MEASURED_PEAKS.json bf16_tflops" + ("" if prec in ("bf16", "3xf16") else " / 2 (dense TF32 rate)")
                             if peaks.get("bf16_tflops") else "fallback 1.59 PFLOP/s bf16"),
             "traffic": _traffic_mean(_traffic(traffic_tab, args.workload, d, dom, n_local), d),
             "traffic_by_layer": _traffic(traffic_tab, args.workload, d, dom, n_local),

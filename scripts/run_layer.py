@@ -58,7 +58,7 @@ def parse(paths, workload, out):
         per = {}
         names = {}
         for r in rows[hdr + 1:]:
-            if len(r) < len(h) or "pack_filter" in r[ki] or "filter_tc" in r[ki] or "filter_transform" in r[ki]:
+            if len(r) < len(h) or "pack_filter" in r[ki] or "filter_tc" in r[ki] or "filter_transform" in r[ki] or "u_split" in r[ki]:
                 continue
             per.setdefault(int(r[ii]), {})[r[ni]] = float(r[vi].replace(",", ""))
             names[int(r[ii])] = r[ki].split("(")[0]
