@@ -3,6 +3,11 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload resnet50|vgg16|single]
     python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
     python bench.py --impl reference      # the CPU path (oracle port, all host threads)
+    python bench.py --gpus 2 --dry-run    # CPU/gloo rehearsal of the rank / shard / max-over-ranks logic
+
+``--gpus N`` without a torchrun environment (no WORLD_SIZE) re-executes itself
+under ``torch.distributed.run --nproc-per-node N`` (127.0.0.1), and every arm
+checks that the launched world size equals ``--gpus``.
 
 Workload (default): BASELINE config 4 -- the 16 ResNet-50 3x3 convolutions at
 global batch 256, batch-sharded over the ranks (strong scaling: 256/N images
@@ -227,6 +232,89 @@ def _traffic_mean(by_layer: dict | None, fam: dict):
     return int(num / den) if den else None
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def reexec_under_torchrun(n: int) -> None:
+    """``--gpus N`` outside torchrun: one rank per GPU via torch.distributed.run."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
+def run_dry(args, rank: int, world: int) -> None:
+    """``--dry-run``: the multi-rank host logic of the GPU arm on CPU (gloo).
+
+    Same shard ranges, replicated-by-seed filters, barrier + max-over-ranks
+    timing and whole-job value as the GPU arm; the per-rank "step" is the C
+    oracle over the rank's images (test infrastructure standing in for the
+    kernels, which need a B200).  Prints one JSON line on rank 0.
+    """
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    from oracle import conv_oracle
+    from paper_2012_15667_b200.runner import WORKLOADS, expand, shard_range
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo")
+    distributed = dist.is_available() and dist.is_initialized()
+    n_total = args.batch or world
+    lo, hi = shard_range(n_total, rank, world)
+    specs = expand(WORKLOADS[args.workload])[:2]
+    rng = np.random.default_rng(1000)
+    ws = [(rng.uniform(-1, 1, (s.k, s.c, s.r, s.r)) / np.sqrt(s.c * s.r * s.r)).astype(np.float32)
+          for s in specs]
+    xs = [np.random.default_rng(7919 * (i + 1)).uniform(-1, 1, (n_total, s.c, s.hw, s.hw))
+          .astype(np.float32)[lo:hi] for i, s in enumerate(specs)]
+    threads = max(1, (os.cpu_count() or 1) // world)
+
+    def step():
+        for s, x, w in zip(specs, xs, ws):
+            if len(x):
+                conv_oracle.c_direct_conv(x, w, s.stride, s.pad, threads=threads)
+
+    def reduce(v: float, op) -> float:
+        if not distributed:
+            return v
+        t = torch.tensor([v], dtype=torch.float64)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    if distributed:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    el = time.perf_counter() - t0
+    if distributed:
+        dist.barrier()
+    t_max = reduce(el, dist.ReduceOp.MAX if distributed else None)
+    flops_all = reduce(float(sum(s.flops(hi - lo) for s in specs)), dist.ReduceOp.SUM if distributed else None)
+    images = reduce(float(hi - lo), dist.ReduceOp.SUM if distributed else None)
+    if rank == 0:
+        print(json.dumps({
+            "impl": "dry-run", "metric": METRIC, "value": round(flops_all * args.steps / t_max / 1e9, 3),
+            "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * t_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOAD_NAME[args.workload] + " (first 2 layers, CPU oracle)",
+                       "global_batch": n_total, "images_over_ranks": int(images),
+                       "parallelism": f"batch-sharded x{world} (gloo, no data-path collective)"},
+        }), flush=True)
+    if distributed:
+        dist.destroy_process_group()
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -240,12 +328,22 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU (gloo) rehearsal of the multi-rank logic; no GPU needed")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        reexec_under_torchrun(args.gpus)   # does not return
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} rank(s) "
+                         "(WORLD_SIZE); run `python bench.py --gpus N` or torchrun --nproc-per-node N")
+    if args.dry_run:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return

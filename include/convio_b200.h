@@ -49,6 +49,13 @@ extern "C" {
 #define CONVIO_EINFEASIBLE 3
 #define CONVIO_EINTERNAL 4
 
+/* Reference exception class of the last rc-3 failure (convio_last_error_kind):
+ * the Python binding raises exactly this class, never guessing from the text. */
+#define CONVIO_EKIND_NONE 0
+#define CONVIO_EKIND_SCHEDULE 1    /* dataflow.ScheduleError (pkg/src/convio/dataflow.py:30) */
+#define CONVIO_EKIND_INFEASIBLE 2  /* dataflow.InfeasibleTileError (pkg/src/convio/dataflow.py:26) */
+#define CONVIO_EKIND_GEOMETRY 3    /* model.GeometryError (pkg/src/convio/model.py:14) */
+
 #define CONVIO_LAYOUT_CHW 0
 #define CONVIO_LAYOUT_CWH 1
 #define CONVIO_LAYOUT_HWC 2
@@ -107,6 +114,8 @@ typedef struct convio_launch_info {
 
 int convio_version(void);
 const char *convio_last_error(void);
+/* CONVIO_EKIND_* of the last failure on this thread (valid with convio_last_error). */
+int convio_last_error_kind(void);
 
 /* Legality + launch shape of (desc, tile, algorithm); never launches. */
 int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t algorithm,

@@ -33,7 +33,45 @@ int oracle_set_threads(int n) {
 #endif
 }
 
-/* x: [n, c, h, w] fp32; wt: [k, c, kh, kw] fp32; y: [n, k, p, q] fp64 */
+/* x: [n, c, h, w] fp32; wt: [k, c, kh, kw] fp32; y: [n, k, p, q] fp64
+ *
+ * Register-blocked: a task owns OB output channels x one output row; for each
+ * XB-wide column block the OB x XB accumulators stay in registers while the
+ * (c, ky, kx) terms stream in that fixed order, every output's sum still
+ * left-deep in the DAG order.  The input is copied once, zero-padded, so the
+ * padding taps are real "+ 0 * w" terms as in the DAG over the padded input
+ * (fp64 products of fp32 values are exact, so the result is bit-identical to
+ * a scalar (c, ky, kx) loop and independent of the blocking and thread count).
+ */
+#define OB 6
+#define XB 8
+typedef double v4d __attribute__((vector_size(32)));
+
+/* one XB-wide block of OB output rows; S = stride (1 and 2 compile-time) */
+static inline __attribute__((always_inline)) void dc_block(const float *xc0, const double *wk, int c, int taps,
+                                                          int kw, size_t plane, int wp, int S,
+                                                          v4d acc[OB][XB / 4]) {
+    for (int o = 0; o < OB; ++o)
+        for (int j = 0; j < XB / 4; ++j) acc[o][j] = (v4d){0.0, 0.0, 0.0, 0.0};
+    for (int ci = 0; ci < c; ++ci) {
+        const float *xc = xc0 + (size_t)ci * plane;
+        const double *wc = wk + (size_t)ci * taps * OB;
+        for (int t = 0; t < taps; ++t) {
+            const int ky = t / kw, kx = t - ky * kw;
+            const float *xr = xc + (size_t)ky * wp + kx;
+            v4d xv[XB / 4];
+            for (int j = 0; j < XB / 4; ++j)
+                xv[j] = (v4d){(double)xr[(4 * j) * S], (double)xr[(4 * j + 1) * S], (double)xr[(4 * j + 2) * S],
+                              (double)xr[(4 * j + 3) * S]};
+            for (int o = 0; o < OB; ++o) {
+                const double wv = wc[t * OB + o];
+                const v4d wb = {wv, wv, wv, wv};
+                for (int j = 0; j < XB / 4; ++j) acc[o][j] += xv[j] * wb;
+            }
+        }
+    }
+}
+
 int oracle_direct_conv_f32in(const float *x, const float *wt, double *y,
                              int n, int c, int h, int w, int k, int kh, int kw,
                              int stride, int pad, int reserved) {
@@ -43,41 +81,60 @@ int oracle_direct_conv_f32in(const float *x, const float *wt, double *y,
     const int hp = h + 2 * pad, wp = w + 2 * pad;
     if (kh > hp || kw > wp) return 3;
     const int p = (hp - kh) / stride + 1, q = (wp - kw) / stride + 1;
-    const long pairs = (long)n * k;
-#pragma omp parallel for schedule(dynamic, 1)
-    for (long bk = 0; bk < pairs; ++bk) {
-        const int b = (int)(bk / k), oc = (int)(bk % k);
-        double *acc = y + bk * (long)p * q;
-        memset(acc, 0, sizeof(double) * (size_t)p * q);
-        const float *xb = x + (long)b * c * h * w;
-        const float *wk = wt + (long)oc * c * kh * kw;
-        for (int ci = 0; ci < c; ++ci) {
-            const float *xc = xb + (long)ci * h * w;
-            for (int ky = 0; ky < kh; ++ky) {
-                for (int kx = 0; kx < kw; ++kx) {
-                    const double wv = (double)wk[(ci * kh + ky) * kw + kx];
-                    /* valid output columns for this tap: 0 <= ox*stride + kx - pad < w */
-                    int ox_lo = 0, ox_hi = q;
-                    while (ox_lo < q && ox_lo * stride + kx - pad < 0) ++ox_lo;
-                    while (ox_hi > ox_lo && (ox_hi - 1) * stride + kx - pad >= w) --ox_hi;
-                    for (int oy = 0; oy < p; ++oy) {
-                        const int iy = oy * stride + ky - pad;
-                        if (iy < 0 || iy >= h) continue;        /* zero padding */
-                        const float *xr = xc + (long)iy * w + kx - pad;
-                        double *ar = acc + (long)oy * q;
-                        if (stride == 1) {
-                            for (int ox = ox_lo; ox < ox_hi; ++ox) ar[ox] += (double)xr[ox] * wv;
-                        } else {
-                            for (int ox = ox_lo; ox < ox_hi; ++ox)
-                                ar[ox] += (double)xr[ox * stride] * wv;
-                        }
-                    }
-                }
+    if (n == 0) return 0;
+    /* zero-padded copy; XB*stride floats of slack past the end for the last
+       column block's don't-care reads */
+    const size_t plane = (size_t)hp * wp;
+    float *xp = (float *)calloc((size_t)n * c * plane + (size_t)XB * stride + 64, sizeof(float));
+    if (!xp) return 4;
+#pragma omp parallel for schedule(static)
+    for (long bc = 0; bc < (long)n * c; ++bc)
+        for (int iy = 0; iy < h; ++iy)
+            memcpy(xp + bc * plane + (size_t)(iy + pad) * wp + pad, x + (bc * h + iy) * (long)w,
+                   sizeof(float) * (size_t)w);
+    const int kbl = (k + OB - 1) / OB;
+    const long tasks = (long)n * kbl * p;
+    const int taps = kh * kw;
+    /* filters as fp64 [k block][c][tap][OB] (missing channels of a ragged block: 0) */
+    double *wk = (double *)calloc((size_t)kbl * c * taps * OB, sizeof(double));
+    if (!wk) {
+        free(xp);
+        return 4;
+    }
+#pragma omp parallel for schedule(static)
+    for (int oc = 0; oc < k; ++oc)
+        for (int ci = 0; ci < c; ++ci)
+            for (int t = 0; t < taps; ++t)
+                wk[(((size_t)(oc / OB) * c + ci) * taps + t) * OB + oc % OB] =
+                    (double)wt[((size_t)oc * c + ci) * taps + t];
+#pragma omp parallel for schedule(dynamic, 4)
+    for (long tk = 0; tk < tasks; ++tk) {
+        const int oy = (int)(tk % p);
+        const int kb = (int)((tk / p) % kbl);
+        const int b = (int)(tk / ((long)p * kbl));
+        const int oc0 = kb * OB;
+        const int nob = k - oc0 < OB ? k - oc0 : OB;
+        const float *xb = xp + (size_t)b * c * plane + (size_t)oy * stride * wp;
+        for (int ox0 = 0; ox0 < q; ox0 += XB) {
+            v4d acc[OB][XB / 4];
+            const float *xc0 = xb + (size_t)ox0 * stride;
+            const double *wb = wk + (size_t)kb * c * taps * OB;
+            if (stride == 1) dc_block(xc0, wb, c, taps, kw, plane, wp, 1, acc);
+            else if (stride == 2) dc_block(xc0, wb, c, taps, kw, plane, wp, 2, acc);
+            else dc_block(xc0, wb, c, taps, kw, plane, wp, stride, acc);
+            const int nx = q - ox0 < XB ? q - ox0 : XB;
+            for (int o = 0; o < nob; ++o) {
+                double *yr = y + (((size_t)b * k + oc0 + o) * p + oy) * q + ox0;
+                for (int j = 0; j < nx; ++j) yr[j] = acc[o][j / 4][j % 4];
             }
         }
     }
+    free(wk);
+    free(xp);
     return 0;
 }
+#undef OB
+#undef XB
 
 /* matrices row-major: at [e x m], g [m x r], bt [m x m] */
 int oracle_winograd_conv_f32in(const float *x, const float *wt, double *y,

@@ -76,6 +76,7 @@ def lib() -> ctypes.CDLL:
         sigs = {
             "convio_version": ([], ctypes.c_int),
             "convio_last_error": ([], ctypes.c_char_p),
+            "convio_last_error_kind": ([], ctypes.c_int),
             "convio_last_launch_count": ([], ctypes.c_int),
             "convio_query": ([D, T, I32, LI], ctypes.c_int),
             "convio_workspace_bytes": ([D, T, I32], I64),
@@ -105,7 +106,7 @@ def lib() -> ctypes.CDLL:
 
 
 EXPORTED = (
-    "convio_version", "convio_last_error", "convio_last_launch_count", "convio_query",
+    "convio_version", "convio_last_error", "convio_last_error_kind", "convio_last_launch_count", "convio_query",
     "convio_workspace_bytes", "convio_pack_filter_direct", "convio_conv_direct_f32",
     "convio_winograd_filter_transform", "convio_conv_winograd_f32", "convio_winograd_matrices",
     "convio_ffma_peak", "convio_default_tile", "convio_pack_filter_igemm", "convio_conv_igemm_tf32",
@@ -119,20 +120,26 @@ def last_error() -> str:
     return msg.decode(errors="replace") if msg else ""
 
 
+EKIND_NONE, EKIND_SCHEDULE, EKIND_INFEASIBLE, EKIND_GEOMETRY = 0, 1, 2, 3
+_KIND_CLASS = {EKIND_SCHEDULE: ScheduleError, EKIND_GEOMETRY: GeometryError}
+
+
 def check(rc: int, what: str = "") -> None:
-    """Map a C-ABI return code onto the reference's exception classes."""
+    """Map a C-ABI return code onto the reference's exception classes.
+
+    rc 3 carries its class explicitly (``convio_last_error_kind``): the
+    reference's ``ScheduleError`` / ``GeometryError``, else
+    ``InfeasibleTileError`` -- so ``measure()``'s
+    ``except (ScheduleError, InfeasibleTileError)`` keeps its meaning
+    whatever the message text says.
+    """
     if rc == 0:
         return
     msg = last_error() or what
     if rc == 2:
         raise ValueError(msg)
     if rc == 3:
-        low = msg.lower()
-        if "resident" in low or "does not divide" in low or "not divisible" in low:
-            raise ScheduleError(msg)
-        if "larger than" in low or "unit stride" in low or "square" in low:
-            raise GeometryError(msg)
-        raise InfeasibleTileError(msg)
+        raise _KIND_CLASS.get(lib().convio_last_error_kind(), InfeasibleTileError)(msg)
     raise DeviceError(f"{what}: {msg} (rc={rc})")
 
 
@@ -156,6 +163,7 @@ def query(desc: ConvDesc, tile: Tile | None, algorithm: int) -> tuple[int, dict]
     rc = lib().convio_query(ctypes.byref(desc), ctypes.byref(tile) if tile else None,
                             algorithm, ctypes.byref(info))
     d = info.to_dict()
+    d["kind"] = lib().convio_last_error_kind() if rc != 0 else EKIND_NONE
     if rc != 0 and not d["reason"]:
         d["reason"] = last_error()
     return rc, d

@@ -18,6 +18,7 @@
 namespace convio {
 
 static thread_local char t_err[512];
+static thread_local int t_kind = CONVIO_EKIND_NONE;
 static thread_local int t_launches = 0;
 
 void set_error(const char *fmt, ...) {
@@ -26,7 +27,18 @@ void set_error(const char *fmt, ...) {
     vsnprintf(t_err, sizeof(t_err), fmt, ap);
     va_end(ap);
 }
-void clear_error() { t_err[0] = 0; }
+void clear_error() {
+    t_err[0] = 0;
+    t_kind = CONVIO_EKIND_NONE;
+}
+int schedule_error() {
+    t_kind = CONVIO_EKIND_SCHEDULE;
+    return CONVIO_EINFEASIBLE;
+}
+int geometry_error() {
+    t_kind = CONVIO_EKIND_GEOMETRY;
+    return CONVIO_EINFEASIBLE;
+}
 void note_launch() { ++t_launches; }
 void reset_launches() { t_launches = 0; }
 
@@ -219,7 +231,7 @@ static int check_desc(const convio_conv_desc *d, int *p, int *q) {
     const int hp = d->h + 2 * d->pad, wp = d->w + 2 * d->pad;
     if (d->r > hp || d->s > wp) {
         set_error("kernel %dx%d larger than padded input %dx%d", d->s, d->r, wp, hp);
-        return CONVIO_EINFEASIBLE;
+        return geometry_error();
     }
     *p = (hp - d->r) / d->stride + 1;
     *q = (wp - d->s) / d->stride + 1;
@@ -308,14 +320,14 @@ static int plan_direct(const convio_conv_desc *d, const convio_tile *t, DirectPl
     if (t->x % t->n_xt || t->y % t->n_yt || t->z % t->n_zt)
         return fail(CONVIO_EINFEASIBLE, "thread counts must divide the tile dims");
     if (q % t->x || p % t->y || d->k % t->z)
-        return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
+        return fail(schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
     const int tile_w = d->stride * (t->x - 1) + d->s;
     const int tile_h = d->stride * (t->y - 1) + d->r;
     const int64_t vol = (int64_t)t->x * t->y * t->z;
     const int64_t resident = vol + (int64_t)tile_w * tile_h + (int64_t)d->r * d->s * t->z;
     if (resident > t->s_b)
-        return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
+        return fail(schedule_error(), "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     const int threads = t->n_xt * t->n_yt * t->n_zt;
     if (threads > 1024) return fail(CONVIO_EINFEASIBLE, "%d threads per block > 1024", threads);
@@ -627,6 +639,11 @@ extern "C" {
 int convio_version(void) { return 100; }
 
 const char *convio_last_error(void) { return t_err; }
+
+int convio_last_error_kind(void) {
+    // rc 3 without an explicit kind is an infeasible tile / capacity limit
+    return t_kind != CONVIO_EKIND_NONE ? t_kind : (t_err[0] ? CONVIO_EKIND_INFEASIBLE : CONVIO_EKIND_NONE);
+}
 
 int convio_last_launch_count(void) { return t_launches; }
 

@@ -12,7 +12,14 @@ namespace convio {
 
 // ---- error plumbing (thread-local message, codes from convio_b200.h) -------
 void set_error(const char *fmt, ...);
-void clear_error();
+void clear_error();   // also resets the error kind to CONVIO_EKIND_NONE
+// rc CONVIO_EINFEASIBLE with the reference exception class recorded explicitly
+// (convio_last_error_kind): the reference's ScheduleError (dataflow.py:30,
+// raised by the planners for a tile that does not divide the output or a
+// resident set above s_b, dataflow.py:222-233,263-279) and GeometryError
+// (model.py:14: kernel larger than the padded input, non-unit Winograd stride)
+int schedule_error();
+int geometry_error();
 void note_launch();
 void reset_launches();
 

@@ -42,19 +42,19 @@ static int plan_nhwc(const convio_conv_desc *d, const convio_tile *t, NhwcPlan *
         return code;
     };
     const int hp = d->h + 2 * d->pad, wp = d->w + 2 * d->pad;
-    if (d->r > hp || d->s > wp) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
+    if (d->r > hp || d->s > wp) return fail(geometry_error(), "kernel larger than padded input");
     const int p = (hp - d->r) / d->stride + 1, q = (wp - d->s) / d->stride + 1;
     if (d->r != d->s) return fail(CONVIO_EINFEASIBLE, "square kernels only");
     if (d->stride > 2) return fail(CONVIO_EINFEASIBLE, "channels-last direct kernel: stride 1 or 2");
     if (d->c % 32) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of 32 (one 128-B stage row)", d->c);
     if (d->k % 4) return fail(CONVIO_EINFEASIBLE, "K must be a multiple of 4");
     if (q % t->x || p % t->y || d->k % t->z)
-        return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
+        return fail(schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
     const int tile_w = d->stride * (t->x - 1) + d->s, tile_h = d->stride * (t->y - 1) + d->r;
     const int64_t resident = (int64_t)t->x * t->y * t->z + (int64_t)tile_w * tile_h + (int64_t)d->r * d->s * t->z;
     if (resident > t->s_b)
-        return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
+        return fail(schedule_error(), "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     const int px = t->x * t->y;
     if (px > 128) return fail(CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the 128-row register tile", px);

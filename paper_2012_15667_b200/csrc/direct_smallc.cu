@@ -182,14 +182,14 @@ static int smallc_plan(const convio_conv_desc *d, const convio_tile *t, SmallCPa
         return fail(CONVIO_EINFEASIBLE, "small-C kernel: stride 1 or 2");
     if (d->k % SC_BK) return fail(CONVIO_EINFEASIBLE, "small-C kernel: K=%d not a multiple of 32", d->k);
     const int hp = d->h + 2 * d->pad, wp = d->w + 2 * d->pad;
-    if (hp < 3 || wp < 3) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
+    if (hp < 3 || wp < 3) return fail(geometry_error(), "kernel larger than padded input");
     const int p = (hp - 3) / d->stride + 1, q = (wp - 3) / d->stride + 1;
     // the model's legality rule on the block (reference dataflow.py:228-233):
     // resident x*y*z outputs + footprint + kw*z filter words <= s_b
     const int fw = SC_BX * d->stride + 2, fh = SC_BY * d->stride + 2;
     const int64_t resident = (int64_t)SC_BX * SC_BY * SC_BK + (int64_t)fw * fh + 3 * SC_BK;
     if (resident > t->s_b)
-        return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
+        return fail(schedule_error(), "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     *fn = d->stride == 1 ? smallc_fn<1>(d->c) : smallc_fn<2>(d->c);
     if (!*fn) return fail(CONVIO_EINFEASIBLE, "small-C kernel: C=%d > 4", d->c);

@@ -279,7 +279,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         d->stride < 1 || d->pad < 0)
         return fail(CONVIO_EINVAL, "descriptor fields must be >= 1 (pad >= 0)");
     const int hp = d->h + 2 * d->pad, wp = d->w + 2 * d->pad;
-    if (d->r > hp || d->s > wp) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
+    if (d->r > hp || d->s > wp) return fail(geometry_error(), "kernel larger than padded input");
     const int p = (hp - d->r) / d->stride + 1, q = (wp - d->s) / d->stride + 1;
     if (d->layout != CONVIO_LAYOUT_HWC)
         return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM needs the HWC (NHWC) layout");
@@ -293,12 +293,12 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         return fail(CONVIO_EINFEASIBLE, "tile fields must be >= 1");
     if (t->n_xt == 2) return plan_igemm_halo(d, t, pl, reason, rlen, kind, p, q);
     if (q % t->x || p % t->y || d->k % t->z)
-        return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
+        return fail(schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
     const int tile_w = d->stride * (t->x - 1) + d->s, tile_h = d->stride * (t->y - 1) + d->r;
     const int64_t resident = (int64_t)t->x * t->y * t->z + (int64_t)tile_w * tile_h + (int64_t)d->r * d->s * t->z;
     if (resident > t->s_b)
-        return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
+        return fail(schedule_error(), "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     const int px = t->x * t->y;
     if (px > 128) return fail(CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the M=128 MMA tile", px);

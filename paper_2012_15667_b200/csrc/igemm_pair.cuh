@@ -647,11 +647,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int i = 0; i < 8; ++i) {
                     const int row = i * 4 + (lane >> 3);
                     float4 o = *reinterpret_cast<const float4 *>(stg + row * 36 + cc);
-                    if constexpr (F16X3) {   // exact: powers of two
-                        o.x *= pow2f(-(rexp[i] + cexp.x));
-                        o.y *= pow2f(-(rexp[i] + cexp.y));
-                        o.z *= pow2f(-(rexp[i] + cexp.z));
-                        o.w *= pow2f(-(rexp[i] + cexp.w));
+                    if constexpr (F16X3) {
+                        // exact powers of two, applied as two multiplies: each exponent is
+                        // within pow2f's range but their sum need not be (operands near
+                        // 2^-60 give row + column exponents past 126)
+                        const float rs = pow2f(-rexp[i]);
+                        o.x = (o.x * rs) * pow2f(-cexp.x);
+                        o.y = (o.y * rs) * pow2f(-cexp.y);
+                        o.z = (o.z * rs) * pow2f(-cexp.z);
+                        o.w = (o.w * rs) * pow2f(-cexp.w);
                     }
                     o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
                     if (P.relu) {

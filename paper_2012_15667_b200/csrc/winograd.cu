@@ -106,7 +106,7 @@ static int wino_check_desc(const convio_conv_desc *d, int e, int *p, int *q, cha
     }
     if (d->stride != 1) {
         snprintf(reason, rlen, "Winograd requires unit stride");
-        return CONVIO_EINFEASIBLE;
+        return geometry_error();
     }
     if (d->r != 3 || d->s != 3) {
         snprintf(reason, rlen, "Winograd kernels are compiled for 3x3 filters, got %dx%d", d->s, d->r);
@@ -119,7 +119,7 @@ static int wino_check_desc(const convio_conv_desc *d, int e, int *p, int *q, cha
     const int hp = d->h + 2 * d->pad, wp = d->w + 2 * d->pad;
     if (hp < 3 || wp < 3) {
         snprintf(reason, rlen, "kernel larger than padded input");
-        return CONVIO_EINFEASIBLE;
+        return geometry_error();
     }
     *p = hp - 2;
     *q = wp - 2;
@@ -150,17 +150,17 @@ static int plan_winograd(const convio_conv_desc *d, const convio_tile *t, int e,
     if (t->x % t->n_xt || t->y % t->n_yt || t->z % t->n_zt)
         return fail(CONVIO_EINFEASIBLE, "thread counts must divide the tile dims");
     if (q % t->x || p % t->y || d->k % t->z)
-        return fail(CONVIO_EINFEASIBLE, "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
+        return fail(schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
                     t->z, q, p, d->k);
     if (t->x % e || t->y % e)
-        return fail(CONVIO_EINFEASIBLE, "tile dims %dx%d not divisible by e=%d", t->x, t->y, e);
+        return fail(schedule_error(), "tile dims %dx%d not divisible by e=%d", t->x, t->y, e);
     const int m = e + 2, mm = m * m;
     const int npos = (t->x / e) * (t->y / e);
     // the model's shared-kernel-transform schedule must fit s_b
     // (pkg/src/convio/dataflow.py:268-280 with shared_kernel_transform=True)
     const int64_t resident = 2LL * mm * npos * t->z + (int64_t)npos * mm + 9LL * t->z;
     if (resident > t->s_b)
-        return fail(CONVIO_EINFEASIBLE, "stage 0 resident set %lld words exceeds s_b=%d",
+        return fail(schedule_error(), "stage 0 resident set %lld words exceeds s_b=%d",
                     (long long)resident, t->s_b);
     const int threads = t->n_xt * t->n_yt * t->n_zt;
     if (threads > 1024) return fail(CONVIO_EINFEASIBLE, "%d threads per block > 1024", threads);

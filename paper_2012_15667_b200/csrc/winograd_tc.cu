@@ -187,10 +187,13 @@ __global__ void __launch_bounds__(128, 3) winograd_input_tc_kernel(const float *
 // Power-of-two scale exponent for a row whose largest magnitude is `mx`: the
 // scaled row lies in (-2^15, 2^15), so its fp16 hi parts are normal down to
 // 2^-24 of the row maximum and nothing overflows.
+// The exponent is clamped to pow2f's range [-126, 127] here, so the exponent the
+// epilogue undoes is always the one that was applied (rows near 2^-126 keep
+// fewer fp16 bits; they stay exact powers-of-two scalings).
 __device__ __forceinline__ int f16_row_exp(float mx) {
     if (!(mx >= 1.17549435e-38f)) return 0;   // zero / subnormal rows: unscaled
     const int ex = ((__float_as_int(mx) >> 23) & 0xff) - 126;   // mx = f * 2^ex, f in [0.5, 1)
-    return 15 - ex;
+    return min(127, max(-126, 15 - ex));
 }
 
 __device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __half &lo) {
@@ -277,8 +280,9 @@ __global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const floa
         }
         const int e = f16_row_exp(fm * WinoTf<E>::GROW);
         const float sc = pow2f(e);
-        // pass 2: scaled hi / lo planes
-        if (active) {
+        // pass 2: scaled hi / lo planes (all lanes: the lane-pair exchange below is
+        // a full-warp shuffle; inactive lanes skip only the stores)
+        {
             __half *vp = v + (int64_t)t * g.c + 4 * c4;
             const int64_t plane = (int64_t)M * M * xi_stride;
 #pragma unroll
@@ -297,10 +301,13 @@ __global__ void __launch_bounds__(128, 3) winograd_input_f16x3_kernel(const floa
                     __half *dst = vp + (a * M + b) * xi_stride;
                     const uint2 hv = *reinterpret_cast<const uint2 *>(h);
                     const uint2 lv = *reinterpret_cast<const uint2 *>(l);
+                    // every lane of the warp runs the exchange (inactive lanes trade
+                    // don't-care halves) so the full-mask shuffle is well defined
                     const bool odd = c4 & 1;
                     const uint2 send = odd ? hv : lv;
-                    const unsigned am = __activemask();
-                    const uint32_t gx = __shfl_xor_sync(am, send.x, 1), gy = __shfl_xor_sync(am, send.y, 1);
+                    const uint32_t gx = __shfl_xor_sync(0xffffffffu, send.x, 1),
+                                   gy = __shfl_xor_sync(0xffffffffu, send.y, 1);
+                    if (!active) continue;
                     if (!odd)
                         *reinterpret_cast<uint4 *>(dst) = make_uint4(hv.x, hv.y, gx, gy);
                     else
@@ -482,11 +489,11 @@ static int plan_wino_tc(const convio_conv_desc *d, const convio_tile *t, int e, 
         return fail(CONVIO_EINVAL, "descriptor fields must be >= 1 (pad >= 0)");
     if (d->r != 3 || d->s != 3) return fail(CONVIO_EINFEASIBLE, "Winograd needs a 3x3 kernel");
     if (d->stride != 1)
-        return fail(CONVIO_EINFEASIBLE, "Winograd requires stride 1 (reference WinogradParams.check_shape)");
+        return fail(geometry_error(), "Winograd requires stride 1 (reference WinogradParams.check_shape)");
     if (d->layout != CONVIO_LAYOUT_HWC)
         return fail(CONVIO_EINFEASIBLE, "tensor-core Winograd needs the HWC (NHWC) layout");
     const int p = d->h + 2 * d->pad - 2, q = d->w + 2 * d->pad - 2;
-    if (p < 1 || q < 1) return fail(CONVIO_EINFEASIBLE, "kernel larger than padded input");
+    if (p < 1 || q < 1) return fail(geometry_error(), "kernel larger than padded input");
     const int cb = (kind == KIND_BF16 || kind == KIND_3XF16) ? 64 : 32;
     if (d->c % cb) return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d", d->c, cb);
     int bn = t ? t->z : (d->k % 256 == 0 ? 256 : (d->k % 128 == 0 ? 128 : 64));

@@ -15,21 +15,8 @@ from paper_2012_15667_b200 import conv as C
 
 pytestmark = pytest.mark.gpu
 
-TOL_DIRECT = 1e-5
-TOL_WINO = {2: 1e-4, 4: 1e-3}
-
-
-def tol_fp32(c, r=3, s=3):
-    """FP32 tolerance: 1e-5 at the config-1 reduction length (C*R*S = 576), growing
-    like sqrt(C*R*S) -- the random-walk growth of fp32 accumulation error."""
-    return TOL_DIRECT * max(1.0, ((c * r * s) / 576) ** 0.5)
-
-
-def tol_3xtf32(c, r=3, s=3):
-    """3xTF32 (hi*lo + lo*hi + hi*hi, FP32 accumulate) drops the lo*lo term and rounds
-    lo to TF32, ~2^-21 relative per product like an fp32 rounding; stated tolerance
-    2x the FP32 one (measured: 3.4e-5 at C*R*S = 4608 where FP32 is 2.8e-5)."""
-    return 2 * tol_fp32(c, r, s)
+from tolerances import (TOL_DIRECT, TOL_WINO, TOL_TF32, TOL_BF16, TOL_WTC, tol_fp32,  # noqa: E402
+                        tol_3xtf32)
 
 
 def _inputs(n, c, h, w, k, r, s, seed=0):
@@ -133,8 +120,6 @@ def test_winograd_filter_transform_matches_oracle():
         assert np.max(np.abs(u - ref)) <= 1e-6 * max(1.0, np.max(np.abs(ref)))
 
 
-TOL_TF32 = 5e-3
-
 IGEMM_CASES = [
     (2, 64, 56, 56, 64, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
     (2, 64, 56, 56, 128, TileConfig(14, 8, 128, 32768, 1, 1, 1, layout="HWC")),
@@ -193,7 +178,6 @@ def test_direct_fp32_error_at_long_reductions(c):
 
 
 # ---- BF16 tcgen05 implicit GEMM (kind::f16) -------------------------------------
-TOL_BF16 = 3e-2
 
 BF16_CASES = [
     (2, 64, 56, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 1, layout="HWC")),
@@ -327,7 +311,6 @@ WTC_CASES = [
 # transforms (F(4,3)'s B^T / G entries up to 5 and 1/6..1/24), so the stated
 # tolerances are looser than the direct conv's at the same precision:
 #   tf32: F(2,3) 5e-3, F(4,3) 2e-2;  bf16: F(2,3) 5e-2, F(4,3) 1.5e-1.
-TOL_WTC = {("tf32", 2): 5e-3, ("tf32", 4): 2e-2, ("bf16", 2): 5e-2, ("bf16", 4): 1.5e-1}
 
 
 @pytest.mark.parametrize("case", WTC_CASES, ids=[str(i) for i in range(len(WTC_CASES))])
@@ -522,3 +505,20 @@ def test_winograd_tc_3xf16_matches_oracle(case):
     ys = C.conv_winograd_tc(_dev(xs, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16")
     refs = co.direct_conv(xs, wt, 1, 1)
     assert co.rel_err(ys.contiguous().cpu().numpy(), refs) <= tol
+
+
+@pytest.mark.parametrize("sx,sw", [(-60, -60), (-70, -50), (60, 60), (-70, 60)],
+                         ids=["x2^-60,w2^-60", "x2^-70,w2^-50", "x2^60,w2^60", "x2^-70,w2^60"])
+@pytest.mark.parametrize("e", [4, 2])
+def test_winograd_tc_3xf16_extreme_operand_scales(sx, sw, e):
+    """Row (input tile) and column (filter) scale exponents whose sum passes pow2f's
+    range: the epilogue unscales with two exact multiplies, so only the relative
+    error of the split remains (outputs near 2^-120 .. 2^120 are normal floats)."""
+    x, wt = _inputs(2, 64, 14, 14, 128, 3, 3)
+    x = x * np.float32(2.0 ** sx)
+    wt = wt * np.float32(2.0 ** sw)
+    tile = TileConfig(e, e, 128, 32768, 1, 1, 2, layout="HWC", e=e)
+    y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16")
+    ref = co.direct_conv(x, wt, 1, 1)
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert np.isfinite(err) and err <= TOL_WINO[e], err

@@ -83,3 +83,34 @@ def test_two_rank_shard_conv_gather_equals_single_process():
     assert err < 1e-6                      # gathered shards == full-batch conv
     assert tmax == 2.0                     # max over ranks
     assert wsum == pytest.approx(wsum_expect)   # identical replicated filters
+
+
+def _bench(*argv, env=None):
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), *argv], capture_output=True,
+                       text=True, timeout=300, env=e, cwd=root)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    return r.returncode, (json.loads(lines[-1]) if lines else None), r.stderr
+
+
+def test_bench_gpus_2_relaunches_two_ranks():
+    """``bench.py --gpus 2`` re-executes under torchrun: two gloo ranks shard the
+    batch, time with barrier + max over ranks, and rank 0 reports n_gpus 2."""
+    rc, line, err = _bench("--gpus", "2", "--dry-run", "--steps", "1", "--warmup", "3", "--batch", "3")
+    assert rc == 0, err[-2000:]
+    assert line["n_gpus"] == 2
+    assert line["config"]["images_over_ranks"] == 3       # 2 + 1 images: the whole batch
+    assert line["value"] > 0 and line["ms_per_step"] > 0
+
+
+def test_bench_rejects_world_size_mismatch():
+    rc, line, err = _bench("--gpus", "2", "--dry-run", env={"WORLD_SIZE": "1"})
+    assert rc != 0 and line is None
+    assert "--gpus 2" in err
