@@ -17,11 +17,17 @@ in the DAG builders:
   divisible by ``e`` are computed on the padded domain
   (``dag.py:291-299``) and cropped.
 
-Everything is float64.  Parity status: the reference pins no conv value
-(no golden vector exists), so this oracle is **pinned by construction and by
-cross-check**: the direct path against ``torch.nn.functional.conv2d`` in
-float64, the Winograd path against the direct path (~1e-12), and the C
-restatement (``conv_oracle.c``) against both (``tests/test_oracle.py``).
+Everything is float64.  Parity status: **pinned to the reference's own code**.
+The reference ships no conv value, but its direct-convolution DAG fixes every
+arithmetic step, so ``tests/golden/make_dag_golden.py`` evaluates the
+REFERENCE's ``build_direct_conv_dag`` vertex by vertex on seeded inputs (11
+shapes: strides 1-3, 1x1 / 3x3 / 5x5 / 3x2 kernels, batch 2) and
+``tests/test_dag_parity.py`` requires :func:`direct_conv` and the C
+restatement to reproduce those values bit for bit; the Winograd tiling
+(:func:`tile_patches`) is checked against the patch leaves of the reference's
+``build_winograd_dag``.  Cross-checks: the direct path against
+``torch.nn.functional.conv2d`` in float64, the Winograd path against the
+direct path (~1e-12), the C restatement against both (``tests/test_oracle.py``).
 """
 
 from __future__ import annotations
@@ -66,6 +72,18 @@ def direct_conv(x: np.ndarray, w: np.ndarray, stride: int = 1, padding: int = 0)
     return acc
 
 
+def tile_patches(xp: np.ndarray, e: int, m: int, ty: int, tx: int) -> np.ndarray:
+    """The m x m input patch of every e x e output tile, ``[n, c, ty, tx, m, m]``:
+    tile (ty, tx) reads ``xp[b, c, ty*e + dy, tx*e + dx]`` for ``dy, dx < m``
+    (``dag.py:358-363``; pinned to the reference DAG by tests/test_dag_parity.py)."""
+    n, c_in = xp.shape[:2]
+    patches = np.empty((n, c_in, ty, tx, m, m), dtype=xp.dtype)
+    for i in range(ty):
+        for j in range(tx):
+            patches[:, :, i, j] = xp[:, :, i * e:i * e + m, j * e:j * e + m]
+    return patches
+
+
 def winograd_conv(x: np.ndarray, w: np.ndarray, e: int, padding: int = 0) -> np.ndarray:
     """fp64 Winograd F(e x e, r x r) following the four DAG steps (``dag.py:358-401``)."""
     xp = pad_input(x, padding)
@@ -82,10 +100,7 @@ def winograd_conv(x: np.ndarray, w: np.ndarray, e: int, padding: int = 0) -> np.
     mats = winograd_mats.matrices_float(e, r)
     at, g, bt = mats["AT"], mats["G"], mats["BT"]
     # step 1: input transform per (b, c, tile) and kernel transform per (oc, c)
-    patches = np.empty((n, c_in, ty, tx, m, m))
-    for i in range(ty):
-        for j in range(tx):
-            patches[:, :, i, j] = xp[:, :, i * e:i * e + m, j * e:j * e + m]
+    patches = tile_patches(xp, e, m, ty, tx)
     v = np.einsum("ij,bcyxjk,lk->bcyxil", bt, patches, bt)
     u = np.einsum("ij,ocjk,lk->ocil", g, w, g)
     # steps 2+3: element-wise products summed left-deep over channels
