@@ -1,8 +1,8 @@
 """GPU parity: the sm_100a kernels vs the float64 CPU oracle (``oracle/``).
 
-Tolerances (norm-wise max error ``||y - y_ref||_inf / ||y_ref||_inf``,
-SURVEY.md §8(d)): direct FP32 <= 1e-5, Winograd F(2,3) FP32 <= 1e-4,
-F(4,3) FP32 <= 1e-3.  Every call goes through the C-ABI.
+Tolerances (norm-wise max error ``||y - y_ref||_inf / ||y_ref||_inf``):
+tests/tolerances.py, each within ~10x of the error measured on a B200.
+Every call goes through the C-ABI.
 """
 
 import numpy as np
@@ -15,8 +15,8 @@ from paper_2012_15667_b200 import conv as C
 
 pytestmark = pytest.mark.gpu
 
-from tolerances import (TOL_DIRECT, TOL_WINO, TOL_TF32, TOL_BF16, TOL_WTC, tol_fp32,  # noqa: E402
-                        tol_3xtf32)
+from tolerances import (TOL_DIRECT, TOL_TF32, TOL_BF16, TOL_WTC, tol_fp32,  # noqa: E402
+                        tol_3xtf32, tol_wino)
 
 
 def _inputs(n, c, h, w, k, r, s, seed=0):
@@ -103,9 +103,9 @@ def test_winograd_matches_oracle(case):
     x, wt = _inputs(n, c, h, w, k, 3, 3)
     y = C.conv_winograd(_dev(x), _dev(wt), e=e, padding=1, tile=tile)
     ref = co.direct_conv(x, wt, 1, 1)
-    assert co.rel_err(y.cpu().numpy(), ref) <= TOL_WINO[e]
+    assert co.rel_err(y.cpu().numpy(), ref) <= tol_wino(e, c)
     # and against the Winograd oracle itself (same transform matrices)
-    assert co.rel_err(y.cpu().numpy(), co.winograd_conv(x, wt, e, 1)) <= TOL_WINO[e]
+    assert co.rel_err(y.cpu().numpy(), co.winograd_conv(x, wt, e, 1)) <= tol_wino(e, c)
 
 
 def test_winograd_filter_transform_matches_oracle():
@@ -324,7 +324,7 @@ def test_winograd_tc_matches_oracle(case):
                            bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
     assert C.infer_layout(y) == "HWC"
-    tol = TOL_WTC.get((prec, e), TOL_WINO[e] * max(1.0, (c / 64) ** 0.5))
+    tol = TOL_WTC.get((prec, e), tol_wino(e, c))
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
     assert err <= tol, (err, tol)
 
@@ -340,7 +340,7 @@ def test_winograd_tc_a_operand_in_tmem(case):
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xtf32",
                            bias=_dev(b), relu=True)
     ref = np.maximum(co.direct_conv(x, wt, 1, 1) + b[None, :, None, None], 0)
-    tol = TOL_WINO[e] * max(1.0, (c / 64) ** 0.5)
+    tol = tol_wino(e, c)
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
     assert err <= tol, (err, tol)
 
@@ -353,7 +353,7 @@ def test_winograd_tc_pretransformed_filter_and_relu():
     y2 = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, relu=True, u=u)
     assert torch.equal(y1, y2)
     ref = np.maximum(co.direct_conv(x, wt, 1, 1), 0)
-    assert co.rel_err(y1.contiguous().cpu().numpy(), ref) <= TOL_WINO[4]
+    assert co.rel_err(y1.contiguous().cpu().numpy(), ref) <= tol_wino(4, 64)
 
 
 def test_winograd_tc_filter_transform_matches_oracle():
@@ -376,9 +376,9 @@ def test_winograd_tc_chunks_the_batch():
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=4, precision="3xtf32", tile=tile)
     assert C.last_launch_count() > 4   # filter + 3 launches per chunk, > 1 chunk
     ref = co.direct_conv(x[:2], wt, 1, 1)
-    assert co.rel_err(y[:2].contiguous().cpu().numpy(), ref) <= TOL_WINO[4]
+    assert co.rel_err(y[:2].contiguous().cpu().numpy(), ref) <= tol_wino(4, 64)
     ref_last = co.direct_conv(x[-2:], wt, 1, 1)
-    assert co.rel_err(y[-2:].contiguous().cpu().numpy(), ref_last) <= TOL_WINO[4]
+    assert co.rel_err(y[-2:].contiguous().cpu().numpy(), ref_last) <= tol_wino(4, 64)
 
 
 # ---- channels-last FP32 direct kernel (stacked pixels, TMA ring) -----------------
@@ -498,7 +498,7 @@ def test_winograd_tc_3xf16_matches_oracle(case):
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16",
                            bias=_dev(b))
     ref = co.direct_conv(x, wt, 1, 1) + b[None, :, None, None]
-    tol = TOL_WINO[e] * max(1.0, (c / 64) ** 0.5)   # the FP32 Winograd tolerance
+    tol = tol_wino(e, c)   # the FP32 Winograd tolerance
     assert co.rel_err(y.contiguous().cpu().numpy(), ref) <= tol
     # rows of very different magnitude: the per-row power-of-two scales keep them exact
     xs = x * np.float32(2.0 ** 20)
@@ -521,4 +521,4 @@ def test_winograd_tc_3xf16_extreme_operand_scales(sx, sw, e):
     y = C.conv_winograd_tc(_dev(x, "HWC"), _dev(wt), e=e, padding=1, tile=tile, precision="3xf16")
     ref = co.direct_conv(x, wt, 1, 1)
     err = co.rel_err(y.contiguous().cpu().numpy(), ref)
-    assert np.isfinite(err) and err <= TOL_WINO[e], err
+    assert np.isfinite(err) and err <= tol_wino(e, 64), err

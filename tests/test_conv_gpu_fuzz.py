@@ -2,7 +2,7 @@
 the C oracle (fp64 accumulation): random batch / channels / map size / stride and a
 random legal tile of each kernel family (single CTA, CTA pair, A-in-TMEM pair, halo,
 halo + fold, split-K small grids, FFMA channels-last, tensor-core and FFMA Winograd).
-Every case goes through the C-ABI; tolerances as tests/test_conv_gpu.py.
+Every case goes through the C-ABI; tolerances from tests/tolerances.py.
 """
 
 import numpy as np
@@ -15,13 +15,15 @@ from paper_2012_15667_b200 import conv as C
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"3xtf32": 2e-5, "tf32": 5e-3, "bf16": 3e-2, "fp32": 1e-5}
-TOL_WINO = {("3xtf32", 2): 1e-4, ("3xtf32", 4): 1e-3, ("fp32", 2): 1e-4, ("fp32", 4): 1e-3,
-            ("tf32", 2): 5e-3, ("tf32", 4): 2e-2, ("bf16", 2): 5e-2, ("bf16", 4): 1.5e-1}
+from tolerances import TOL_BF16, TOL_TF32, TOL_WTC, tol_3xtf32, tol_fp32, tol_wino  # noqa: E402
 
 
-def _scale(c):
-    return max(1.0, (c * 9 / 576) ** 0.5)
+def _tol_direct(prec, c):
+    return {"3xtf32": tol_3xtf32(c), "fp32": tol_fp32(c), "tf32": TOL_TF32, "bf16": TOL_BF16}[prec]
+
+
+def _tol_wino(prec, e, c):
+    return tol_wino(e, c) if prec in ("3xtf32", "fp32") else TOL_WTC[(prec, e)]
 
 
 def _divisors(v):
@@ -82,7 +84,7 @@ def test_randomized_parity(seed):
         nzt = 1 if kind == "wino_fp32" else int(r.choice([1, 2] + ([4] if prec == "3xtf32" and z <= 128 else [])))
         tile = TileConfig(e, e, z, int(r.choice([2048, 8192, 16384])), 1, 1, nzt, layout="HWC", e=e)
         y = C.conv_winograd_tc(xd, wd, e=e, padding=1, tile=tile, precision=prec, bias=bd, relu=relu)
-        tol = TOL_WINO[(prec, e)] * (_scale(c) if prec in ("3xtf32", "fp32") else 1.0)
+        tol = _tol_wino(prec, e, c)
         stride = 1
     else:
         p = (h + 2 - 3) // stride + 1
@@ -92,7 +94,7 @@ def test_randomized_parity(seed):
         else:
             y = C.conv_igemm(xd, wd, padding=1, stride=stride, tile=tile, precision=prec, bias=bd,
                              relu=relu)
-        tol = TOL[prec] * (_scale(c) if prec in ("3xtf32", "fp32") else 1.0)
+        tol = _tol_direct(prec, c)
     ref = co.c_direct_conv(x, w, stride, 1).astype(np.float64) + b[None, :, None, None]
     if relu:
         ref = np.maximum(ref, 0)

@@ -19,7 +19,7 @@ from paper_2012_15667_b200.cli import main as cli_main
 from paper_2012_15667_b200.dataflow import execute
 from paper_2012_15667_b200.device import b200_hw_model
 
-from tolerances import tol_fp32, TOL_WINO
+from tolerances import tol_fp32, tol_wino
 
 pytestmark = pytest.mark.gpu
 
@@ -46,11 +46,11 @@ def test_execute_winograd_schedule_matches_oracle():
     shape = ConvShape.from_output(28, 28, 32, 16, 3, 3)
     p = WinogradParams(2, 3)
     hw = b200_hw_model()
-    tile = TileConfig(28, 4, 32, 32768, 7, 2, 4, e=2)
+    tile = TileConfig(28, 4, 32, 32768, 7, 4, 4, e=2)     # a compiled micro-tile (smoke's)
     sched = plan_winograd_dataflow(shape, p, hw, tile, shared_kernel_transform=True)
     x, w = _xw(shape, 3)
     y = execute(sched, shape, torch.from_numpy(x).cuda(), torch.from_numpy(w).cuda(), hw=hw, winograd=p)
-    assert co.rel_err(y.cpu().numpy(), co.direct_conv(x, w, 1, 0)) <= TOL_WINO[2]
+    assert co.rel_err(y.cpu().numpy(), co.direct_conv(x, w, 1, 0)) <= tol_wino(2, 16)
 
 
 def test_measure_device_backend_times_legal_and_rejects_illegal():
@@ -81,7 +81,10 @@ def test_tune_device_backend_over_legal_projection():
 
 
 def test_cli_simulate_tune_report_device_modes(capsys, tmp_path):
-    base = ["--alg", "direct", "--cin", "32", "--out", "14x14x32", "--ker", "3x3", "--pad", "1"]
+    # the B200 machine model (device.b200_hw_model): s words over n_p = 296 blocks
+    hw = b200_hw_model()
+    base = ["--alg", "direct", "--cin", "32", "--out", "14x14x32", "--ker", "3x3", "--pad", "1",
+            "--s", str(hw.s), "--ssm", str(hw.s_sm), "--np", str(hw.n_p)]
     assert cli_main(["simulate", *base, "--tile", "14x14x32", "--sb", "16384", "--device"]) == 0
     out = json.loads(capsys.readouterr().out)
     assert out["device"]["legal"] and out["device"]["seconds"] > 0 and out["device"]["gflops"] > 0

@@ -14,7 +14,7 @@ from paper_2012_15667_b200 import runner as R
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"igemm_3xtf32": 2e-5, "winograd_tc_3xtf32": 1e-3}
+from tolerances import tol_for  # noqa: E402
 
 
 def test_tuned_resnet50_plans_replay_in_a_cuda_graph():
@@ -50,5 +50,5 @@ def test_tuned_resnet50_plans_replay_in_a_cuda_graph():
         xc = x[:2].contiguous().cpu().numpy()   # logical NCHW whatever the physical layout
         ref = co.direct_conv(xc, layer.weight.cpu().numpy(), s.stride, s.pad)
         err = co.rel_err(y[:2].contiguous().cpu().numpy(), ref)
-        tol = TOL.get(layer.algorithm, 1e-3) * max(1.0, (s.c * 9 / 576) ** 0.5)
+        tol = tol_for(layer.algorithm, s.c, layer.e)
         assert err <= tol, (s.name, layer.algorithm, err, tol)
