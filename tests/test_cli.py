@@ -39,8 +39,28 @@ def test_usage_and_infeasible_exit_codes(capsys):
     code, _, err = run(capsys, "tune", "--alg", "direct", "--out", "4x4x4", "--ker", "3x3",
                        "--cin", "8", "--s", "512", "--ssm", "256", "--ns", "8", "--budget", "4")
     assert code == 2 and "budget" in err
-    code, _, err = run(capsys, "pebble", "--fixture", "product2", "--s", "3")
-    assert code == 2 and "out of scope" in err
+    code, _, err = run(capsys, "pebble", "--fixture", "nope", "--s", "3")
+    assert code == 2 and "available" in err
+    code, _, err = run(capsys, "dag-stats", "--alg", "direct", "--out", "64x64x64", "--ker", "3x3",
+                       "--cin", "64", "--cap", "1000")
+    assert code == 3 and "vertices" in err
+
+
+def test_dag_stats_and_pebble(capsys, tmp_path):
+    export = tmp_path / "dc.dag"
+    code, out, _ = run(capsys, "dag-stats", "--alg", "direct", "--out", "2x2x1", "--ker", "3x3",
+                       "--cin", "2", "--export", str(export))
+    payload = json.loads(out)
+    assert code == 0 and payload["match"] == "yes" and payload["internal_plus_output"] == 140
+    assert payload["steps"] == [1, 2] and export.exists()
+    code, out, _ = run(capsys, "dag-stats", "--alg", "winograd", "--e", "2", "--out", "2x2x1",
+                       "--ker", "3x3", "--cin", "1")
+    assert code == 0 and json.loads(out)["match"] == "yes"
+    code, out, _ = run(capsys, "pebble", "--fixture", "product2", "--s", "3")
+    payload = json.loads(out)
+    assert code == 0 and payload["q_min"] == 3 and payload["holds"] is True
+    code, out, _ = run(capsys, "pebble", "--dag", str(export), "--s", "3")
+    assert code == 3        # 2x2x1 output of a 2-channel 3x3 conv: too big for the exact oracle
 
 
 def test_simulate_and_trace(capsys, tmp_path):
