@@ -83,9 +83,11 @@ def test_tune_device_backend_over_legal_projection():
 def test_cli_simulate_tune_report_device_modes(capsys, tmp_path):
     # the B200 machine model (device.b200_hw_model): s words over n_p = 296 blocks
     hw = b200_hw_model()
-    base = ["--alg", "direct", "--cin", "32", "--out", "14x14x32", "--ker", "3x3", "--pad", "1",
+    base = ["--alg", "direct", "--cin", "32", "--out", "28x28x32", "--ker", "3x3", "--pad", "1",
             "--s", str(hw.s), "--ssm", str(hw.s_sm), "--np", str(hw.n_p)]
-    assert cli_main(["simulate", *base, "--tile", "14x14x32", "--sb", "16384", "--device"]) == 0
+    # a compiled K1 micro-tile (4 x 1 x 8 outputs per thread), as in smoke()
+    assert cli_main(["simulate", *base, "--tile", "28x4x32", "--threads", "7x4x4", "--sb", "16384",
+                     "--device"]) == 0
     out = json.loads(capsys.readouterr().out)
     assert out["device"]["legal"] and out["device"]["seconds"] > 0 and out["device"]["gflops"] > 0
     ds = tmp_path / "ds.json"
