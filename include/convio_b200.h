@@ -70,15 +70,19 @@ extern "C" {
 #define CONVIO_ALG_WINOGRAD_TC_BF16 7   /* ... BF16 transformed operands */
 #define CONVIO_ALG_WINOGRAD_NHWC 8      /* same pipeline, element-wise GEMMs as a batched FP32 FFMA GEMM */
 #define CONVIO_ALG_WINOGRAD_TC_3XF16 9  /* ... scaled fp16 hi / lo planes, 3 f16 MMAs (FP32-level) */
+#define CONVIO_ALG_IGEMM_3XF16 10       /* tcgen05 implicit GEMM, 3xF16 split (FP32-level, f16 rate) */
 
 /* Operand precision of the tcgen05 contractions (FP32 accumulate always). */
 #define CONVIO_PREC_TF32 0
 #define CONVIO_PREC_3XTF32 1
 #define CONVIO_PREC_BF16 2
 #define CONVIO_PREC_FP32 3   /* convio_winograd_bgemm only: FP32 FFMA GEMMs on the CUDA cores */
-#define CONVIO_PREC_3XF16 4  /* convio_winograd_bgemm only: operands split by the transforms into
-                                power-of-two-scaled fp16 hi / lo planes (22-bit, like 3xTF32),
-                                3 MMAs at the f16 rate; C % 64 == 0, CTA pair tiles */
+#define CONVIO_PREC_3XF16 4  /* operands split into power-of-two-scaled fp16 hi / lo planes
+                                (22-bit, like 3xTF32), 3 MMAs at the f16 rate; C % 64 == 0,
+                                CTA pair tiles.  convio_winograd_bgemm: split by the transforms
+                                (one scale per tile row / filter row); convio_conv_igemm: the
+                                activations split in shared memory with one scale per tensor
+                                (an |x| max pass first), the filter per output channel */
 
 /* One convolution layer (valid geometry after zero padding `pad`). */
 typedef struct convio_conv_desc {
@@ -179,14 +183,26 @@ int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *ti
                              const float *w, int32_t w_is_packed, const float *bias, int32_t relu,
                              float *y, void *workspace, size_t workspace_bytes, void *stream);
 
-/* Generic form of the two calls above plus BF16 (CONVIO_PREC_*).  For BF16
- * the fp32 activations are converted to bf16 NHWC in the workspace first
+/* Generic form of the two calls above plus BF16 and 3xF16 (CONVIO_PREC_*).  For
+ * BF16 the fp32 activations are converted to bf16 NHWC in the workspace first
  * (C % 64 == 0), filters packed to bf16 [R*S][K][C] unless `w_is_packed`
- * (then w holds convio_pack_filter_igemm_bf16 output).  Replaces the same
- * schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
+ * (then w holds convio_pack_filter_igemm_bf16 output).  For 3xF16 (CTA pair
+ * tiles, C % 64 == 0) the workspace (256-byte aligned) holds the |x| maxima and,
+ * unless `w_is_packed` (convio_pack_filter_igemm_f16x3 output), the packed
+ * filter; the activations stay fp32 in HBM and are split on chip.  Replaces the
+ * same schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
 int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
                       const float *x, const void *w, int32_t w_is_packed, const float *bias,
                       int32_t relu, float *y, void *workspace, size_t workspace_bytes, void *stream);
+
+/* KCRS fp32 -> the 3xF16 filter operand of convio_conv_igemm (CONVIO_PREC_3XF16):
+ * fp16 hi / lo planes [2][R*S][K][C] scaled by 2^e[k] per output channel, then
+ * e[K] (int32) at byte offset align256(4*K*C*R*S); w_packed 256-byte aligned and
+ * convio_pack_filter_igemm_f16x3_bytes(desc) long.  Replaces the filter side of
+ * the same schedule (dataflow.py:219-250). */
+int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w, void *w_packed,
+                                   void *stream);
+int64_t convio_pack_filter_igemm_f16x3_bytes(const convio_conv_desc *desc);
 
 /* KCRS fp32 -> [R*S][K][C] bf16 (round to nearest even). */
 int convio_pack_filter_igemm_bf16(const convio_conv_desc *desc, const float *w, void *w_packed,

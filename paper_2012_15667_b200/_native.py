@@ -15,13 +15,15 @@ from .dataflow import LAYOUTS, InfeasibleTileError, ScheduleError
 from .model import GeometryError
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib")
-LIB_PATH = os.path.join(LIB_DIR, "libconvio_b200.so")
+# CONVIO_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("CONVIO_LIB") or os.path.join(LIB_DIR, "libconvio_b200.so")
 
 ALG_DIRECT, ALG_WINOGRAD, ALG_IGEMM_TF32, ALG_IGEMM_3XTF32 = 0, 1, 2, 3
 ALG_IGEMM_BF16 = 4
 ALG_WINOGRAD_TC_TF32, ALG_WINOGRAD_TC_3XTF32, ALG_WINOGRAD_TC_BF16 = 5, 6, 7
 ALG_WINOGRAD_NHWC = 8
 ALG_WINOGRAD_TC_3XF16 = 9
+ALG_IGEMM_3XF16 = 10
 PREC_TF32, PREC_3XTF32, PREC_BF16, PREC_FP32, PREC_3XF16 = 0, 1, 2, 3, 4
 PRECISIONS = {"tf32": PREC_TF32, "3xtf32": PREC_3XTF32, "bf16": PREC_BF16, "fp32": PREC_FP32,
               "3xf16": PREC_3XF16}
@@ -96,6 +98,8 @@ def lib() -> ctypes.CDLL:
             "convio_winograd_filter_transform_tc": ([D, I32, I32, P, P, P], ctypes.c_int),
             "convio_winograd_bgemm": ([D, T, I32, I32, P, P, I32, P, I32, P, P, SZ, P],
                                       ctypes.c_int),
+            "convio_pack_filter_igemm_f16x3": ([D, P, P, P], ctypes.c_int),
+            "convio_pack_filter_igemm_f16x3_bytes": ([D], I64),
         }
         for name, (args, res) in sigs.items():
             fn = getattr(L, name)
@@ -112,6 +116,7 @@ EXPORTED = (
     "convio_ffma_peak", "convio_default_tile", "convio_pack_filter_igemm", "convio_conv_igemm_tf32",
     "convio_conv_igemm_3xtf32", "convio_conv_igemm", "convio_pack_filter_igemm_bf16",
     "convio_convert_bf16", "convio_winograd_filter_transform_tc", "convio_winograd_bgemm",
+    "convio_pack_filter_igemm_f16x3", "convio_pack_filter_igemm_f16x3_bytes",
 )
 
 

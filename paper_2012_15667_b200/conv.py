@@ -25,7 +25,7 @@ from .dataflow import LAYOUTS, TileConfig
 
 __all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "conv_igemm", "conv_winograd_tc",
            "winograd_filter_transform", "winograd_filter_transform_tc",
-           "pack_filter_direct", "pack_filter_igemm", "pack_filter_igemm_bf16",
+           "pack_filter_direct", "pack_filter_igemm", "pack_filter_igemm_bf16", "pack_filter_igemm_f16x3",
            "infer_layout", "to_layout", "empty_act", "query", "last_launch_count"]
 
 
@@ -95,7 +95,8 @@ def _out_hw(h, w, r, s, stride, padding):
 
 ALGORITHMS = {"direct": N.ALG_DIRECT, "winograd": N.ALG_WINOGRAD,
               "igemm_tf32": N.ALG_IGEMM_TF32, "igemm_3xtf32": N.ALG_IGEMM_3XTF32,
-              "igemm_bf16": N.ALG_IGEMM_BF16, "winograd_tc_tf32": N.ALG_WINOGRAD_TC_TF32,
+              "igemm_bf16": N.ALG_IGEMM_BF16, "igemm_3xf16": N.ALG_IGEMM_3XF16,
+              "winograd_tc_tf32": N.ALG_WINOGRAD_TC_TF32,
               "winograd_tc_3xtf32": N.ALG_WINOGRAD_TC_3XTF32,
               "winograd_tc_bf16": N.ALG_WINOGRAD_TC_BF16, "winograd_nhwc": N.ALG_WINOGRAD_NHWC,
               "winograd_tc_fp32": N.ALG_WINOGRAD_NHWC, "winograd_tc_3xf16": N.ALG_WINOGRAD_TC_3XF16}
@@ -286,6 +287,25 @@ def pack_filter_igemm_bf16(w: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+def pack_filter_igemm_f16x3(w: torch.Tensor, stream=None) -> torch.Tensor:
+    """KCRS fp32 filter -> the 3xF16 implicit-GEMM operand (uint8 buffer: fp16
+    hi / lo planes ``[2][R*S][K][C]`` scaled by ``2^e[k]`` per output channel,
+    then ``e[K]``), for ``conv_igemm(..., precision="3xf16", w_packed=...)``."""
+    _check_tensor(w, "w")
+    k, c, r, s_ = w.shape
+    desc = N.make_desc(1, c, r, s_, k, r, s_, 1, 0, 2)
+    nbytes = int(N.lib().convio_pack_filter_igemm_f16x3_bytes(ctypes.byref(desc)))
+    out = torch.empty(nbytes, device=w.device, dtype=torch.uint8)
+    N.check(N.lib().convio_pack_filter_igemm_f16x3(ctypes.byref(desc), _ptr(w.contiguous()), _ptr(out),
+                                                   _stream_ptr(stream)), "pack_filter_igemm_f16x3")
+    return out
+
+
+# conv_igemm precisions -> the C-ABI algorithm ids (workspace size / query)
+_IGEMM_ALG = {"tf32": N.ALG_IGEMM_TF32, "3xtf32": N.ALG_IGEMM_3XTF32, "bf16": N.ALG_IGEMM_BF16,
+              "3xf16": N.ALG_IGEMM_3XF16}
+
+
 def _precision(precision: str) -> int:
     try:
         return N.PRECISIONS[precision]
@@ -300,11 +320,14 @@ def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int =
                w_packed: torch.Tensor | None = None,
                workspace: torch.Tensor | None = None) -> torch.Tensor:
     """Direct conv as a tcgen05 implicit GEMM at ``precision`` ("tf32",
-    "3xtf32" or "bf16"; FP32 accumulation in TMEM).  Channels-last input,
-    ``C % 32 == 0`` (``% 64`` for bf16).  For bf16 the activations are
-    converted to bf16 in the workspace by the library; ``w_packed`` must come
-    from :func:`pack_filter_igemm_bf16` (bf16) or :func:`pack_filter_igemm`.
-    Tolerances: 3xtf32 1e-5, tf32 5e-3, bf16 3e-2.
+    "3xtf32", "3xf16" or "bf16"; FP32 accumulation in TMEM).  Channels-last
+    input, ``C % 32 == 0`` (``% 64`` for bf16 / 3xf16).  For bf16 the
+    activations are converted to bf16 in the workspace by the library; 3xf16
+    (CTA-pair tiles) splits them on chip into power-of-two-scaled fp16 hi / lo
+    planes (FP32-level accuracy at the f16 tensor rate).  ``w_packed`` must come
+    from :func:`pack_filter_igemm_bf16` (bf16), :func:`pack_filter_igemm_f16x3`
+    (3xf16) or :func:`pack_filter_igemm`.
+    Tolerances (tests/tolerances.py): 3xtf32 / 3xf16 FP32-level, tf32 5e-3, bf16 2e-2.
     ``tile.n_zt`` selects the kernel: 1 = one 128-pixel tile per CTA, 2 = the
     persistent CTA pair (``tcgen05.mma.cta_group::2``, M = 256, z/2 filter
     rows staged per CTA, double-buffered TMEM accumulators).
@@ -321,10 +344,11 @@ def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int =
     p, q = _out_hw(desc.h, desc.w, desc.r, desc.s, stride, padding)
     if out is None:
         out = empty_act(desc.n, desc.k, p, q, layout, device=x.device)
-    need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), None,
-                                              N.ALG_IGEMM_TF32 + prec))
+    need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), None, _IGEMM_ALG[precision]))
     wsrc, is_packed = (w_packed, 1) if w_packed is not None else (w.contiguous(), 0)
-    if w_packed is not None and prec != N.PREC_BF16:
+    if w_packed is not None and prec == N.PREC_3XF16:
+        need = 256 * ((4 * 296 + 255) // 256)   # the |x| maxima only
+    elif w_packed is not None and prec != N.PREC_BF16:
         need = 0
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):
         workspace = torch.empty(need, device=x.device, dtype=torch.uint8)

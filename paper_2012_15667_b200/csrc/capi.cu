@@ -702,6 +702,7 @@ int convio_query(const convio_conv_desc *desc, const convio_tile *tile, int32_t 
     if (algorithm == CONVIO_ALG_IGEMM_TF32) return igemm_query(desc, tile, out, 0);
     if (algorithm == CONVIO_ALG_IGEMM_3XTF32) return igemm_query(desc, tile, out, 1);
     if (algorithm == CONVIO_ALG_IGEMM_BF16) return igemm_query(desc, tile, out, 2);
+    if (algorithm == CONVIO_ALG_IGEMM_3XF16) return igemm_query(desc, tile, out, 5);   // KIND_3XF16C
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_query(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32, out);
     if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_query(desc, tile, CONVIO_PREC_FP32, out);
@@ -719,6 +720,7 @@ int64_t convio_workspace_bytes(const convio_conv_desc *desc, const convio_tile *
     if (algorithm == CONVIO_ALG_IGEMM_TF32 || algorithm == CONVIO_ALG_IGEMM_3XTF32 ||
         algorithm == CONVIO_ALG_IGEMM_BF16)
         return igemm_workspace_bytes(desc, algorithm - CONVIO_ALG_IGEMM_TF32);
+    if (algorithm == CONVIO_ALG_IGEMM_3XF16) return igemm_workspace_bytes(desc, 5);   // KIND_3XF16C
     if (algorithm >= CONVIO_ALG_WINOGRAD_TC_TF32 && algorithm <= CONVIO_ALG_WINOGRAD_TC_BF16)
         return wino_tc_workspace_bytes(desc, tile, algorithm - CONVIO_ALG_WINOGRAD_TC_TF32);
     if (algorithm == CONVIO_ALG_WINOGRAD_NHWC) return wino_tc_workspace_bytes(desc, tile, CONVIO_PREC_FP32);

@@ -48,6 +48,7 @@ static PairFn pair_kernel_h(int bn, int kind) {
 // fold: halo + S taps per MMA, N = 3 K (K = 64 -> N = 192)
 static PairFn pair_kernel_fold(int n, int kind) {
     if (n != 192) return nullptr;
+    if (kind == KIND_3XF16C) return &igemm_pair_kernel<192, KIND_3XF16C, true, false, true>;
     if (kind == KIND_3XTF32) return &igemm_pair_kernel<192, KIND_3XTF32, true, false, true>;
     if (kind == KIND_BF16) return &igemm_pair_kernel<192, KIND_BF16, true, false, true>;
     return &igemm_pair_kernel<192, KIND_TF32, true, false, true>;
@@ -65,11 +66,84 @@ static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
         if (halo) return nullptr;
         return pair_kernel_kind<KIND_3XF16, false>(bn);
     }
+    if (kind == KIND_3XF16C)    // direct conv, activations split in shared memory
+        return halo ? pair_kernel_kind<KIND_3XF16C, true>(bn) : pair_kernel_kind<KIND_3XF16C, false>(bn);
     return halo ? pair_kernel_h<true>(bn, kind) : pair_kernel_h<false>(bn, kind);
 }
 
 static const char *kind_name(int kind) {
-    return kind == KIND_3XTF32 ? "3xtf32" : (kind == KIND_BF16 ? "bf16" : "tf32");
+    return kind == KIND_3XTF32 ? "3xtf32" : (kind == KIND_BF16 ? "bf16" : (kind == KIND_3XF16C ? "3xf16" : "tf32"));
+}
+
+// channels per k-block: one 128-B operand row (32 fp32, 64 bf16 / fp16)
+static int kblock_channels(int kind) {
+    return (kind == KIND_BF16 || kind == KIND_3XF16 || kind == KIND_3XF16C) ? 64 : 32;
+}
+
+// 3xF16C filter operand: KCRS -> fp16 hi / lo planes [2][R*S][K][C] with one
+// power-of-two scale per output channel k over its C*R*S weights (col_exp[k],
+// undone by the GEMM epilogue).  One warp per output channel.
+__global__ void __launch_bounds__(256) pack_filter_f16x3_kernel(const float *__restrict__ w,
+                                                                __half *__restrict__ wq,
+                                                                int *__restrict__ col_exp, int k, int c,
+                                                                int rs) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    const int crs = c * rs;
+    const int64_t plane = (int64_t)rs * k * c;
+    for (int kk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; kk < k; kk += (gridDim.x * blockDim.x) >> 5) {
+        const float *wr = w + (int64_t)kk * crs;
+        float mx = 0.0f;
+        for (int j = lane; j < crs; j += 32) mx = fmaxf(mx, fabsf(wr[j]));
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const int e = f16_row_exp(mx);
+        const float sc = pow2f(e);
+        for (int j = lane; j < crs; j += 32) {   // j = cc * rs + tap (KCRS)
+            const int cc = j / rs, tap = j - cc * rs;
+            const float v = wr[j] * sc;
+            const __half hi = __float2half_rn(v);
+            const __half lo = __float2half_rn(v - __half2float(hi));
+            const int64_t o = ((int64_t)tap * k + kk) * c + cc;
+            wq[o] = hi;
+            wq[plane + o] = lo;
+        }
+        if (lane == 0) col_exp[kk] = e;
+    }
+}
+
+// 3xF16C activation scale: per-block max |x| (float bits) into partials[blockIdx.x];
+// the GEMM reduces the nred partials into one exponent (f16c_act_exp)
+constexpr int kAbsmaxBlocks = 296;
+__global__ void __launch_bounds__(256) absmax_partials_kernel(const float *__restrict__ x, int64_t n,
+                                                              int *__restrict__ partials) {
+    pdl_wait();
+    __shared__ float red[8];
+    float m = 0.0f;
+    const int64_t n4 = n >> 2;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    const float4 *x4 = reinterpret_cast<const float4 *>(x);
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; i + 3 * step < n4; i += 4 * step) {
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = __ldg(x4 + i + j * step);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
+    }
+    for (; i < n4; i += step) {
+        const float4 v = __ldg(x4 + i);
+        m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+    }
+    for (int64_t j = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += step)
+        m = fmaxf(m, fabsf(x[j]));
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmaxf(m, red[w]);
+        partials[blockIdx.x] = __float_as_int(m);
+    }
 }
 
 // KCRS -> [R*S][K][C] (fp32 or bf16, round-to-nearest-even)
@@ -137,7 +211,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
                                  : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
-        const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16) ? 2 : 1;
+        const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16 || kind == KIND_3XF16C) ? 2 : 1;
         // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
         const bool loslot = kind == KIND_3XTF32 && !pl->halo && !pl->tsa && bn == 256;
         const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
@@ -150,6 +224,8 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         // small stages (narrow BN, no lo copy) need many in flight to cover the
         // TMA latency (~1 us) at a few hundred MMA cycles per stage
         int stages = (int)std::min<size_t>(16, (budget - a_ring) / stage_bytes);
+        if (const char *cap = getenv("CONVIO_DEV_MAX_STAGES"))   // dev knob: ring-depth sensitivity
+            stages = std::max(2, std::min(stages, atoi(cap)));
         if (stages < 2)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair ring does not fit");
         pl->P.stages = stages;
@@ -159,13 +235,15 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         pl->smem = a_ring + stages * stage_bytes + 1024 + 1024 + kPairEpiBytes;
         pl->bn = bn;
         pl->kind = kind;
-        pl->threads = kind == KIND_3XTF32 ? ((bn >= 256 || pl->tsa) ? 384 : 512) : 256;
+        pl->threads = kind == KIND_3XF16C ? 512 : (kind == KIND_3XTF32 ? ((bn >= 256 || pl->tsa) ? 384 : 512) : 256);
         if (launch_fit_cluster((const void *)pfn, pl->threads, pl->smem, &pl->regs) < 1)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
                          "tcgen05 pair block (%d threads, %zu B smem) does not fit", pl->threads,
                          pl->smem);
         return CONVIO_OK;
     }
+    if (kind == KIND_3XF16C)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "3xF16 implicit GEMMs run on the CTA pair (n_zt = 2)");
     IgemmFn fn = igemm_kernel(bn, kind);
     if (!fn)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 tiles need z in {64, 128, 256}, got %d",
@@ -242,7 +320,7 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "z=%d does not divide K=%d", t->z, d->k);
     if (t->x > q + d->s - 1 || t->y > p + d->r - 1 || fpr > 256 || t->y + d->r - 1 > 256)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "halo tile larger than the output");
-    const int cb = kind == KIND_BF16 ? 64 : 32;
+    const int cb = kblock_channels(kind);
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
     pl->halo = true;
@@ -286,7 +364,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (t->layout != d->layout) return fail(CONVIO_EINVAL, "tile layout differs from tensor layout");
     if (d->stride > 2) return fail(CONVIO_EINFEASIBLE, "tcgen05 implicit GEMM supports stride 1 and 2");
     if (d->r != d->s) return fail(CONVIO_EINFEASIBLE, "square kernels only");
-    const int cb = kind == KIND_BF16 ? 64 : 32;
+    const int cb = kblock_channels(kind);
     if (d->c % cb)
         return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d (one 128-B K block)", d->c, cb);
     if (t->x < 1 || t->y < 1 || t->z < 1 || t->s_b < 1)
@@ -374,10 +452,15 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     if ((reinterpret_cast<uintptr_t>(x) & 15) || (reinterpret_cast<uintptr_t>(wq) & 15)) return false;
     // 2-byte operands (bf16, or the 3xF16 fp16 planes: TMA copies bytes, the type
     // only sets the element size)
+    // 3xF16C: fp32 activations (32-channel boxes, split in smem), fp16 filter planes
     const bool bf = pl.kind == KIND_BF16 || pl.kind == KIND_3XF16;
+    const bool wbf = bf || pl.kind == KIND_3XF16C;
     const int planes = pl.kind == KIND_3XF16 ? 2 : 1;   // hi, lo planes along images / taps
+    const int wplanes = (pl.kind == KIND_3XF16 || pl.kind == KIND_3XF16C) ? 2 : 1;
     const cuuint64_t es_b = bf ? 2 : 4;
+    const cuuint64_t wes_b = wbf ? 2 : 4;
     const cuuint32_t cb = bf ? 64 : 32;
+    const cuuint32_t wcb = wbf ? 64 : 32;
     cuuint64_t xd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.w, (cuuint64_t)P.h, (cuuint64_t)P.n * planes};
     cuuint64_t xs[3] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.w * P.c * es_b,
                         (cuuint64_t)P.h * P.w * P.c * es_b};
@@ -392,24 +475,21 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const int taps = P.batched ? P.n : P.ks * P.ks;
-    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps * planes};
-    cuuint64_t ws[2] = {(cuuint64_t)P.c * es_b, (cuuint64_t)P.k * P.c * es_b};
-    cuuint32_t wb[3] = {cb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1};
+    cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps * wplanes};
+    cuuint64_t ws[2] = {(cuuint64_t)P.c * wes_b, (cuuint64_t)P.k * P.c * wes_b};
+    cuuint32_t wb[3] = {wcb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1};
+    const bool xok = bf ? encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes)
+                        : encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true);
+    if (!xok) return false;
     if (pl.fold) {   // packed filter as [R*S*K rows][C]: a kernel row's S*K rows are contiguous
-        cuuint64_t fd[2] = {(cuuint64_t)P.c, (cuuint64_t)taps * P.k};
-        cuuint64_t fs[1] = {(cuuint64_t)P.c * es_b};
-        cuuint32_t fb[2] = {cb, (cuuint32_t)(pl.bn / 2)};
-        if (bf)
-            return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
-                   encode_tensor_map_bf16_sw128(tw, 2, const_cast<void *>(wq), fd, fs, fb, es);
-        return encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true) &&
-               encode_tensor_map_tiled_ex(tw, 2, const_cast<void *>(wq), fd, fs, fb, es, true);
+        cuuint64_t fd[2] = {(cuuint64_t)P.c, (cuuint64_t)taps * P.k * wplanes};
+        cuuint64_t fs[1] = {(cuuint64_t)P.c * wes_b};
+        cuuint32_t fb[2] = {wcb, (cuuint32_t)(pl.bn / 2)};
+        if (wbf) return encode_tensor_map_bf16_sw128(tw, 2, const_cast<void *>(wq), fd, fs, fb, es);
+        return encode_tensor_map_tiled_ex(tw, 2, const_cast<void *>(wq), fd, fs, fb, es, true);
     }
-    if (bf)
-        return encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes) &&
-               encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), wd, ws, wb, es);
-    return encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true) &&
-           encode_tensor_map_tiled_ex(tw, 3, const_cast<void *>(wq), wd, ws, wb, es, true);
+    if (wbf) return encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), wd, ws, wb, es);
+    return encode_tensor_map_tiled_ex(tw, 3, const_cast<void *>(wq), wd, ws, wb, es, true);
 }
 
 int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
@@ -473,7 +553,15 @@ int launch_convert_bf16(const float *src, void *dst, int64_t n, cudaStream_t str
 
 static inline size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+// 3xF16C packed filter: [fp16 hi plane | fp16 lo plane] (align256) then col_exp[K]
+static size_t f16c_filter_bytes(const convio_conv_desc *d) {
+    return align256((size_t)4 * d->k * d->c * d->r * d->s) + align256((size_t)4 * d->k);
+}
+// 3xF16C workspace: [absmax partials (align256) | packed filter]
+static size_t f16c_partials_bytes() { return align256((size_t)4 * kAbsmaxBlocks); }
+
 int64_t igemm_workspace_bytes(const convio_conv_desc *d, int kind) {
+    if (kind == KIND_3XF16C) return (int64_t)(f16c_partials_bytes() + f16c_filter_bytes(d));
     const int64_t wbytes = (int64_t)d->k * d->c * d->r * d->s * (kind == KIND_BF16 ? 2 : 4);
     if (kind != KIND_BF16) return wbytes;
     return (int64_t)align256(wbytes) + 2LL * d->n * d->c * d->h * d->w;
@@ -488,7 +576,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->block_threads = pl.threads;
     out->smem_bytes = (int)pl.smem;
     out->regs_per_thread = pl.regs;
-    out->channel_chunk = kind == KIND_BF16 ? 64 : 32;
+    out->channel_chunk = kblock_channels(kind);
     out->stages = pl.P.stages;
     out->p = pl.P.p; out->q = pl.P.q;
     out->flops = 2LL * d->n * d->k * pl.P.p * pl.P.q * (int64_t)d->c * d->r * d->s;
@@ -498,6 +586,24 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
              kind_name(kind), pl.fold ? " CTA pair (persistent, halo footprint, 3 taps per MMA)" : pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages,
              pl.P.splits > 1 ? ", split-K" : "");
+    return CONVIO_OK;
+}
+
+int launch_pack_filter_f16x3(const convio_conv_desc *desc, const float *w, void *packed, cudaStream_t stream) {
+    const int blocks = std::max(1, std::min((desc->k + 7) / 8, 148 * 8));
+    __half *planes = (__half *)packed;
+    int *col_exp = (int *)((uint8_t *)packed + align256((size_t)4 * desc->k * desc->c * desc->r * desc->s));
+    CONVIO_CUDA_TRY(launch_pdl(pack_filter_f16x3_kernel, dim3(blocks), dim3(256), 0, stream, w, planes, col_exp,
+                               desc->k, desc->c, desc->r * desc->s));
+    note_launch();
+    return CONVIO_OK;
+}
+
+int launch_absmax_partials(const float *x, int64_t n, int *partials, int *nred, cudaStream_t stream) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(kAbsmaxBlocks, (n / 4 + 2047) / 2048));
+    CONVIO_CUDA_TRY(launch_pdl(absmax_partials_kernel, dim3(blocks), dim3(256), 0, stream, x, n, partials));
+    note_launch();
+    *nred = blocks;
     return CONVIO_OK;
 }
 
@@ -524,6 +630,7 @@ static int prec_kind(int32_t precision) {
         case CONVIO_PREC_TF32: return KIND_TF32;
         case CONVIO_PREC_3XTF32: return KIND_3XTF32;
         case CONVIO_PREC_BF16: return KIND_BF16;
+        case CONVIO_PREC_3XF16: return KIND_3XF16C;
         default: return -1;
     }
 }
@@ -547,6 +654,25 @@ int convio_pack_filter_igemm_bf16(const convio_conv_desc *desc, const float *w, 
         return CONVIO_EINVAL;
     }
     return launch_pack_filter_igemm(desc, w, wq, 1, (cudaStream_t)stream);
+}
+
+int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w, void *w_packed,
+                                   void *stream) {
+    clear_error();
+    if (!desc || !w || !w_packed) {
+        set_error("null argument");
+        return CONVIO_EINVAL;
+    }
+    if (reinterpret_cast<uintptr_t>(w_packed) & 255) {
+        set_error("convio_pack_filter_igemm_f16x3 needs a 256-byte aligned buffer");
+        return CONVIO_EINVAL;
+    }
+    return launch_pack_filter_f16x3(desc, w, w_packed, (cudaStream_t)stream);
+}
+
+int64_t convio_pack_filter_igemm_f16x3_bytes(const convio_conv_desc *desc) {
+    if (!desc) return -1;
+    return (int64_t)f16c_filter_bytes(desc);
 }
 
 int convio_convert_bf16(const float *src, void *dst, int64_t n, void *stream) {
@@ -582,6 +708,33 @@ int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int
     int rc = plan_igemm(desc, tile, &pl, why, sizeof(why), kind);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream;
+    if (kind == KIND_3XF16C) {
+        // workspace [absmax partials | packed fp16 filter planes + col_exp]; a packed
+        // filter (convio_pack_filter_igemm_f16x3) leaves only the partials here
+        const size_t need_here = w_is_packed ? f16c_partials_bytes() : (size_t)igemm_workspace_bytes(desc, kind);
+        if (!workspace || workspace_bytes < need_here || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
+            set_error("workspace of %zu bytes (256-byte aligned) needed (absmax partials%s)", need_here,
+                      w_is_packed ? "" : " + packed fp16 filter");
+            return CONVIO_EINVAL;
+        }
+        if (reinterpret_cast<uintptr_t>(w) & 255) {
+            set_error("3xF16 filter operand must be 256-byte aligned");
+            return CONVIO_EINVAL;
+        }
+        const void *wq = w;
+        if (!w_is_packed) {
+            wq = (uint8_t *)workspace + f16c_partials_bytes();
+            rc = launch_pack_filter_f16x3(desc, (const float *)w, const_cast<void *>(wq), st);
+            if (rc) return rc;
+        }
+        int nred = 0;
+        rc = launch_absmax_partials(x, (int64_t)desc->n * desc->c * desc->h * desc->w, (int *)workspace, &nred, st);
+        if (rc) return rc;
+        pl.P.row_exp = (const int *)workspace;
+        pl.P.nred = nred;
+        pl.P.col_exp = (const int *)((const uint8_t *)wq + align256((size_t)4 * desc->k * desc->c * desc->r * desc->s));
+        return igemm_launch(pl, x, wq, bias, relu, y, st);
+    }
     const bool bf = kind == KIND_BF16;
     const size_t wbytes = (size_t)desc->k * desc->c * desc->r * desc->s * (bf ? 2 : 4);
     const size_t need = (size_t)igemm_workspace_bytes(desc, kind);

@@ -44,12 +44,41 @@ struct IgemmParams {
     int splits;                // split-K factor (blockIdx.z = split; > 1 only without ReLU)
     // KIND_3XF16 (batched only): power-of-two exponents the operands were scaled by;
     // the epilogue multiplies D[t][k] by 2^-(row_exp[g][t] + col_exp[g][k])
+    // KIND_3XF16C (conv): row_exp = the nred per-block |x| maxima (float bits) of
+    // absmax_partials_kernel, reduced by the kernel into ONE activation exponent;
+    // col_exp[k] = the packed filter's per-output-channel exponents
     const int *row_exp;
     const int *col_exp;
+    int nred;
 };
 
 // operand kinds of the tcgen05 contraction
-enum IgemmKind : int { KIND_TF32 = 0, KIND_3XTF32 = 1, KIND_BF16 = 2, KIND_3XF16 = 4 };
+//   KIND_3XF16  batched Winograd GEMMs: operands pre-split into fp16 hi / lo planes
+//   KIND_3XF16C direct conv: fp32 activations TMA-staged and split in shared
+//               memory by converter warps (one power-of-two scale per tensor),
+//               filters pre-split into fp16 planes (scale per output channel)
+enum IgemmKind : int { KIND_TF32 = 0, KIND_3XTF32 = 1, KIND_BF16 = 2, KIND_3XF16 = 4, KIND_3XF16C = 5 };
+
+// Power-of-two scale exponent for a row (or tensor) whose largest magnitude is
+// `mx`: the scaled values lie in (-2^15, 2^15), so their fp16 hi parts are
+// normal down to 2^-24 of the maximum and nothing overflows.  Clamped to
+// pow2f's range [-126, 127], so the exponent an epilogue undoes is always the
+// one that was applied.
+__device__ __forceinline__ int f16_row_exp(float mx) {
+    if (!(mx >= 1.17549435e-38f)) return 0;   // zero / subnormal: unscaled
+    const int ex = ((__float_as_int(mx) >> 23) & 0xff) - 126;   // mx = f * 2^ex, f in [0.5, 1)
+    return min(127, max(-126, 15 - ex));
+}
+
+// the activation exponent of KIND_3XF16C: max over the nred partial maxima
+// (non-negative float bits compare as ints), one warp, all lanes get it
+__device__ __forceinline__ int f16c_act_exp(const int *partials, int nred, int lane) {
+    int m = 0;
+    for (int i = lane; i < nred; i += 32) m = max(m, __ldg(partials + i));
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, off));
+    return f16_row_exp(__int_as_float(m));
+}
 
 // 2^e as a float for e in [-126, 127] (exponent bits; a multiply by it is exact
 // wherever the product stays normal) -- ldexpf costs ~20 instructions

@@ -184,18 +184,6 @@ __global__ void __launch_bounds__(128, 3) winograd_input_tc_kernel(const float *
     }
 }
 
-// Power-of-two scale exponent for a row whose largest magnitude is `mx`: the
-// scaled row lies in (-2^15, 2^15), so its fp16 hi parts are normal down to
-// 2^-24 of the row maximum and nothing overflows.
-// The exponent is clamped to pow2f's range [-126, 127] here, so the exponent the
-// epilogue undoes is always the one that was applied (rows near 2^-126 keep
-// fewer fp16 bits; they stay exact powers-of-two scalings).
-__device__ __forceinline__ int f16_row_exp(float mx) {
-    if (!(mx >= 1.17549435e-38f)) return 0;   // zero / subnormal rows: unscaled
-    const int ex = ((__float_as_int(mx) >> 23) & 0xff) - 126;   // mx = f * 2^ex, f in [0.5, 1)
-    return min(127, max(-126, 15 - ex));
-}
-
 __device__ __forceinline__ void split_f16(float v, float scale, __half &hi, __half &lo) {
     const float s = v * scale;
     hi = __float2half_rn(s);

@@ -84,7 +84,7 @@ def expand(layers: list[LayerSpec]) -> list[LayerSpec]:
 # oracle; Winograd F(e,3) is looser by construction, 1e-4 / 1e-3) -- the
 # headline plan picks among these; "igemm_tf32" is the reduced-precision variant.
 FP32_ALGORITHMS = ("direct", "winograd", "igemm_3xtf32", "winograd_tc_3xtf32", "winograd_nhwc",
-                   "winograd_tc_3xf16")
+                   "winograd_tc_3xf16", "igemm_3xf16")
 CUDA_CORE_ALGORITHMS = ("direct", "winograd", "winograd_nhwc")
 
 
@@ -146,6 +146,17 @@ def load_plans(workload: str, allowed=FP32_ALGORITHMS, n: int | None = None) -> 
     return plans
 
 
+# 3xF16 implicit GEMM: |x| maxima scratch (the C-ABI's absmax partials, 296 ints)
+F16X3_PARTIALS_BYTES = 256 * ((4 * 296 + 255) // 256)
+
+
+def _f16x3_filter_bytes(s: "LayerSpec") -> int:
+    from . import _native as N
+    import ctypes
+    desc = N.make_desc(1, s.c, s.r, s.r, s.k, s.r, s.r, 1, 0, 2)
+    return int(N.lib().convio_pack_filter_igemm_f16x3_bytes(ctypes.byref(desc)))
+
+
 class ConvLayer:
     """One conv layer: filters on the device plus its tuned plan."""
 
@@ -185,6 +196,8 @@ class ConvLayer:
             if self.algorithm == "winograd_tc_3xf16":   # fp32 U + fp16 hi / lo planes + exponents
                 return m * m * s.k * (2 * s.c + 1)
             return m * m * s.c * s.k
+        if self.algorithm == "igemm_3xf16":   # fp16 hi / lo planes + per-channel exponents
+            return -(-_f16x3_filter_bytes(s) // 4)
         return s.k * s.c * s.r * s.r
 
     def prepare(self, device, stream=None) -> None:
@@ -207,6 +220,9 @@ class ConvLayer:
         elif self.algorithm == "igemm_bf16":
             rc = N.lib().convio_pack_filter_igemm_bf16(ctypes.byref(desc), C._ptr(w),
                                                        C._ptr(self._ws), sp)
+        elif self.algorithm == "igemm_3xf16":
+            rc = N.lib().convio_pack_filter_igemm_f16x3(ctypes.byref(desc), C._ptr(w),
+                                                        C._ptr(self._ws), sp)
         elif self.algorithm == "winograd":
             rc = N.lib().convio_winograd_filter_transform(ctypes.byref(desc), self.e,
                                                           C._ptr(w), C._ptr(self._ws), sp)
@@ -236,6 +252,12 @@ class ConvLayer:
                                            dtype=torch.uint8)
             y = C.conv_igemm(x, self.weight, padding=s.pad, stride=s.stride, tile=self.tile,
                              precision="bf16", out=out, stream=stream, w_packed=self._ws,
+                             workspace=self._run_ws)
+        elif self.algorithm == "igemm_3xf16":
+            if self._run_ws is None or self._run_ws.device != x.device:
+                self._run_ws = torch.empty(F16X3_PARTIALS_BYTES, device=x.device, dtype=torch.uint8)
+            y = C.conv_igemm(x, self.weight, padding=s.pad, stride=s.stride, tile=self.tile,
+                             precision="3xf16", out=out, stream=stream, w_packed=self._ws,
                              workspace=self._run_ws)
         elif self.algorithm == "winograd":
             u = self._ws.view(-1)

@@ -77,9 +77,10 @@ def build(spec, kind, n, x, w, wcache):
             tile = TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, 2, layout="HWC")
         if TILE_OVERRIDE:
             tile = TileConfig(*TILE_OVERRIDE, layout="HWC")
-        key = ("ig", prec == "bf16")
+        key = ("ig", "bf16" if prec == "bf16" else ("f16x3" if prec == "3xf16" else "f32"))
         if key not in wcache:
-            wcache[key] = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
+            wcache[key] = (C.pack_filter_igemm_bf16(w) if prec == "bf16" else
+                           C.pack_filter_igemm_f16x3(w) if prec == "3xf16" else C.pack_filter_igemm(w))
         wp = wcache[key]
         out = C.empty_act(n, spec.k, spec.out_hw, spec.out_hw, "HWC", device="cuda")
         ws = torch.empty(max(1, n * spec.c * spec.hw * spec.hw * 2 + (1 << 20)), dtype=torch.uint8,

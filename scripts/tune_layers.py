@@ -97,7 +97,7 @@ def tune_igemm(shape, spec, prec, log):
     import math as _m
     from paper_2012_15667_b200.dataflow import TileConfig
     from paper_2012_15667_b200 import conv as C
-    cb = 64 if prec == "bf16" else 32
+    cb = 64 if prec in ("bf16", "3xf16") else 32
     if spec.c % cb or spec.stride > 2:
         return {"error": f"needs C % {cb} == 0 and stride <= 2"}
     q = shape.w_out
@@ -107,10 +107,13 @@ def tune_igemm(shape, spec, prec, log):
     x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
     xh = C.to_layout(x, "HWC")
     w = torch.empty((spec.k, spec.c, spec.r, spec.r), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
-    wq = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
+    wq = (C.pack_filter_igemm_bf16(w) if prec == "bf16" else
+          C.pack_filter_igemm_f16x3(w) if prec == "3xf16" else C.pack_filter_igemm(w))
     out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
     ws = torch.empty(2 * xh.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
     variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
+    if prec == "3xf16":    # CTA-pair tiles only
+        variants = [(z, 32768, 2) for z in zs]
     if prec == "3xtf32":   # pair with the A operand split into TMEM
         variants += [(z, 32768, 4) for z in zs if z <= 128]
     # halo-staged footprint tiles (pair kernel, stride 1): (x + S - 1) * y = 128
@@ -251,7 +254,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--exhaustive-cap", type=int, default=0)
     ap.add_argument("--algs", default="direct,direct_nhwc,winograd2,winograd4,igemm_3xtf32,igemm_tf32,"
-                    "igemm_bf16,winograd_tc_3xtf32_e2,winograd_tc_3xtf32_e4,"
+                    "igemm_bf16,igemm_3xf16,winograd_tc_3xtf32_e2,winograd_tc_3xtf32_e4,"
                     "winograd_tc_tf32_e4,winograd_tc_bf16_e4,winograd_nhwc_e2,winograd_nhwc_e4,"
                     "winograd_tc_3xf16_e4")
     ap.add_argument("--layers", default="")

@@ -1,0 +1,104 @@
+"""3xF16 tcgen05 implicit GEMM (CONVIO_PREC_3XF16 through convio_conv_igemm): the
+activations are TMA-staged as fp32 and split on chip into power-of-two-scaled fp16
+hi / lo planes (one scale per tensor), the filter into fp16 planes with one scale
+per output channel; 3 kind::f16 MMAs per k-step.  Parity against the float64
+oracle (restating reference pkg/src/convio/dag.py:247-285) at the 3xTF32 bound."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import conv_oracle as co
+from paper_2012_15667_b200 import TileConfig, InfeasibleTileError
+from paper_2012_15667_b200 import conv as C
+
+import os
+import sys
+sys.path.insert(0, os.path.dirname(__file__))
+from tolerances import tol_3xtf32  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+
+def _inputs(n, c, h, w, k, r=3, seed=0):
+    g = np.random.default_rng(seed)
+    x = g.uniform(-1, 1, (n, c, h, w)).astype(np.float32)
+    wt = (np.random.default_rng(seed + 1).uniform(-1, 1, (k, c, r, r)) / np.sqrt(c * r * r)).astype(np.float32)
+    return x, wt
+
+
+def _hwc(a):
+    return C.to_layout(torch.from_numpy(a).cuda(), "HWC")
+
+
+CASES = [
+    # (n, c, h, k, stride, tile, what)
+    (2, 64, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 2, layout="HWC"), "pair z=64"),
+    (3, 128, 14, 256, 1, TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC"), "pair z=256"),
+    (3, 64, 28, 128, 2, TileConfig(14, 7, 128, 32768, 1, 1, 2, layout="HWC"), "stride 2"),
+    (5, 64, 7, 64, 1, TileConfig(7, 7, 64, 32768, 1, 1, 2, layout="HWC"), "odd block count"),
+    (4, 128, 28, 256, 2, TileConfig(14, 7, 256, 32768, 1, 1, 2, layout="HWC"), "stride 2 z=256"),
+    (2, 64, 56, 128, 1, TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC"), "halo"),
+    (3, 128, 28, 256, 1, TileConfig(14, 8, 256, 32768, 2, 1, 2, layout="HWC"), "halo ragged"),
+    (2, 128, 14, 128, 1, TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC"), "halo ragged y"),
+    (2, 64, 56, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 2, layout="HWC"), "fold (3 taps per MMA)"),
+    (3, 64, 28, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 2, layout="HWC"), "fold 30x4"),
+    (16, 512, 14, 256, 2, TileConfig(1, 1, 256, 32768, 1, 1, 2, layout="HWC"), "split-K"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[-1] for c in CASES])
+def test_igemm_3xf16_matches_oracle(case):
+    n, c, h, k, stride, tile, what = case
+    x, wt = _inputs(n, c, h, h, k)
+    b = np.linspace(-0.25, 0.25, k).astype(np.float32)
+    info = C.query(x.shape, wt.shape, stride, 1, "HWC", tile, "igemm_3xf16")
+    assert info["rc"] == 0, info
+    if what.startswith("fold"):
+        assert "3 taps per MMA" in info["reason"], info
+    if what == "split-K":
+        assert "split-K" in info["reason"], info
+    y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, stride=stride, tile=tile,
+                     precision="3xf16", bias=torch.from_numpy(b).cuda())
+    ref = co.direct_conv(x, wt, stride, 1) + b[None, :, None, None]
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= tol_3xtf32(c), err
+    assert err > 0.0
+
+
+def test_igemm_3xf16_packed_filter_and_relu_match():
+    x, wt = _inputs(2, 128, 28, 28, 128)
+    tile = TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC")
+    w = torch.from_numpy(wt).cuda()
+    wp = C.pack_filter_igemm_f16x3(w)
+    y1 = C.conv_igemm(_hwc(x), w, padding=1, tile=tile, precision="3xf16", relu=True)
+    y2 = C.conv_igemm(_hwc(x), w, padding=1, tile=tile, precision="3xf16", relu=True, w_packed=wp)
+    assert torch.equal(y1, y2)
+    ref = np.maximum(co.direct_conv(x, wt, 1, 1), 0)
+    assert co.rel_err(y1.contiguous().cpu().numpy(), ref) <= tol_3xtf32(128)
+
+
+@pytest.mark.parametrize("sx,sw", [(-60, -60), (-70, -50), (60, 60), (-70, 60), (20, 0)],
+                         ids=["x2^-60,w2^-60", "x2^-70,w2^-50", "x2^60,w2^60", "x2^-70,w2^60", "x2^20"])
+def test_igemm_3xf16_extreme_operand_scales(sx, sw):
+    """Tensor / channel exponents whose sum passes pow2f's range: unscaled with two
+    exact multiplies, so only the split's relative error remains."""
+    x, wt = _inputs(2, 64, 28, 28, 128)
+    x = x * np.float32(2.0 ** sx)
+    wt = wt * np.float32(2.0 ** sw)
+    for tile in (TileConfig(14, 7, 128, 32768, 1, 1, 2, layout="HWC"),
+                 TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC")):
+        y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, tile=tile, precision="3xf16")
+        err = co.rel_err(y.contiguous().cpu().numpy(), co.direct_conv(x, wt, 1, 1))
+        assert np.isfinite(err) and err <= tol_3xtf32(64), (tile, err)
+
+
+def test_igemm_3xf16_rejects_single_cta_and_c_not_multiple_of_64():
+    x, wt = _inputs(1, 64, 14, 14, 64)
+    with pytest.raises(InfeasibleTileError):
+        C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, precision="3xf16",
+                     tile=TileConfig(14, 7, 64, 32768, 1, 1, 1, layout="HWC"))
+    x, wt = _inputs(1, 32, 14, 14, 64)
+    with pytest.raises(InfeasibleTileError):
+        C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, precision="3xf16",
+                     tile=TileConfig(14, 7, 64, 32768, 1, 1, 2, layout="HWC"))

@@ -55,7 +55,7 @@ def tol_for(algorithm: str, c: int, e: int | None = None, r: int = 3) -> float:
     """Tolerance of one tuned plan (runner algorithm names)."""
     if algorithm in ("direct",):
         return tol_fp32(c, r, r)
-    if algorithm == "igemm_3xtf32":
+    if algorithm in ("igemm_3xtf32", "igemm_3xf16"):
         return tol_3xtf32(c, r, r)
     if algorithm == "igemm_tf32":
         return TOL_TF32
