@@ -56,6 +56,13 @@ static PairFn pair_kernel_fold(int n, int kind) {
 
 // tsa: 3xTF32 with the A operand in tensor memory (BN <= 128, no halo)
 static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
+    if (tsa && kind == KIND_3XF16C) {   // 3xF16C, A in TMEM (BN = 256: one accumulator)
+        if (halo) return nullptr;
+        if (bn == 64) return &igemm_pair_kernel<64, KIND_3XF16C, false, true>;
+        if (bn == 128) return &igemm_pair_kernel<128, KIND_3XF16C, false, true>;
+        if (bn == 256) return &igemm_pair_kernel<256, KIND_3XF16C, false, true>;
+        return nullptr;
+    }
     if (tsa) {
         if (kind != KIND_3XTF32 || halo) return nullptr;
         if (bn == 64) return &igemm_pair_kernel<64, KIND_3XTF32, false, true>;
@@ -209,12 +216,12 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         PairFn pfn = pl->fold ? pair_kernel_fold(bn, kind) : pair_kernel(bn, kind, pl->halo, pl->tsa);
         if (!pfn)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
-                         pl->tsa ? "A-in-TMEM tiles need 3xTF32, z in {64, 128}, no halo"
+                         pl->tsa ? "A-in-TMEM tiles need 3xTF32 (z in {64, 128}) or 3xF16, no halo"
                                  : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
         const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16 || kind == KIND_3XF16C) ? 2 : 1;
         // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
         const bool loslot = kind == KIND_3XTF32 && !pl->halo && !pl->tsa && bn == 256;
-        const size_t stage_bytes = pl->tsa ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
+        const size_t stage_bytes = (pl->tsa && kind == KIND_3XTF32) ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
                                            : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) *
                                                  (loslot ? 1 : mult);
         const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : (loslot ? 2 * stage_bytes : 0);
@@ -387,7 +394,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
     if (t->n_xt != 1 || t->n_yt != 1 || (t->n_zt != 1 && t->n_zt != 2 && t->n_zt != 4))
         return fail(CONVIO_EINFEASIBLE,
                     "tcgen05 tiles take n_xt = n_yt = 1 and n_zt in {1 (one CTA), 2 (CTA pair), "
-                    "4 (CTA pair, 3xTF32 A operand in TMEM)}");
+                    "4 (CTA pair, 3xTF32 / 3xF16 A operand in TMEM)}");
     pl->tsa = t->n_zt == 4;
     int rc = plan_ring(pl, t->z, kind, t->s_b, t->n_zt >= 2, reason, rlen);
     if (rc) return rc;

@@ -252,6 +252,24 @@ __device__ __forceinline__ void umma_pair_ts_tf32(uint32_t tmem_d, uint32_t tmem
         "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
 }
 
+// 3xF16C with A in TMEM: tcgen05.mma kind::f16 [d], [a_tmem], b_desc
+__device__ __forceinline__ void umma_pair_ts_f16(uint32_t tmem_d, uint32_t tmem_a, uint64_t b,
+                                                 uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16};\n" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
@@ -326,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     // converters -- and the epilogue undoes the power-of-two row / column scales
     constexpr bool F16X3 = KIND == KIND_3XF16;
     static_assert(!F16X3 || (!HALO && !TSA && !FOLD), "3xF16: plain pair tiles");
-    static_assert(!F16C || !TSA, "3xF16C: A operand in shared memory");
+    static_assert(!F16C || !TSA || !HALO, "3xF16C with A in TMEM: no halo");
     constexpr int HB = BN / 2;                        // filter rows staged per CTA
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = HB * 128;
@@ -334,11 +352,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr int CB = (KIND == KIND_BF16 || F16X3 || F16C) ? 64 : 32;   // channels per k-block
     // TSA (3xTF32, BN <= 128): A_hi / A_lo live in TMEM columns after the two
     // accumulators, NTA k-block slots of 64 columns (32 hi + 32 lo)
-    static_assert(!TSA || (SPLIT && !HALO && BN <= 128), "TSA: 3xTF32, no halo, BN <= 128");
+    static_assert(!TSA || (SPLIT && !HALO && (BN <= 128 || F16C)), "TSA: 3xTF32 / 3xF16C, no halo");
+    // accumulator buffers: 2 (the epilogue drains one while the MMAs fill the other),
+    // 1 for 3xF16C TSA at BN = 256 (its 256 columns + 4 A slots fill the 512)
+    constexpr int NACC = (TSA && BN > 128) ? 1 : 2;
     // (power-of-two allocation; FOLD's 2 x 192 columns take 512)
     constexpr uint32_t TMEM_COLS = (TSA || 2 * BN > 256) ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
-    constexpr uint32_t A_COL0 = 2 * BN;
-    constexpr int NTA = TSA ? (512 - 2 * BN) / 64 : 1;
+    constexpr uint32_t A_COL0 = NACC * BN;
+    // TSA A slots of 64 columns: 3xTF32 32 hi + 32 lo fp32 channels; 3xF16C the same 64
+    // channels as fp16 pairs (32 hi + 32 lo columns)
+    constexpr int NTA = TSA ? (512 - NACC * BN) / 64 : 1;
     constexpr int NCW = pair_conv_warps<BN, TSA, KIND>();   // converter warps (3xTF32 / 3xF16C)
     const IgemmParams &P = PP.g;
     // stage layout: non-halo [A | B]; TSA [A | B | B_lo]; halo: A footprint slots,
@@ -352,7 +375,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr bool LOSLOT = KIND == KIND_3XTF32 && !HALO && !TSA && BN == 256;
     constexpr int NL = 2;
     constexpr int LO_SLOT = A_BYTES + B_BYTES;
-    const int STAGE = HALO ? B_BYTES * MULT : (TSA ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (LOSLOT ? 1 : MULT));
+    const int STAGE = HALO ? B_BYTES * MULT
+                           : ((TSA && !F16C) ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (LOSLOT ? 1 : MULT));
     const int ASLOT = HALO ? PP.a_slot * MULT : 0;
     const int NA = HALO ? PP.na : 0;
 
@@ -549,8 +573,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             uint32_t ph = 0, pha = 0, pht = 0;
             int t = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
-                const int acc = t & 1;
-                if (t >= 2) mbar_wait_cluster(tempty + acc, ((t >> 1) - 1) & 1);
+                const int acc = NACC == 2 ? (t & 1) : 0;
+                if (t >= NACC) mbar_wait_cluster(tempty + acc, ((t / NACC) - 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                 const uint32_t d = tmem + (uint32_t)(acc * BN);
                 int tap = 0;
@@ -562,16 +586,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         mbar_wait_cluster(tconv + ta, pht);
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                         const uint32_t b = smem_u32(bring + s * STAGE) + A_BYTES;
-                        const uint64_t bd = umma_desc_sw128(b), bdl = umma_desc_sw128(b + B_BYTES);
+                        // 3xTF32 stage [A | B | B_lo]; 3xF16C [A0 | B_hi | A1 | B_lo]
+                        const uint64_t bd = umma_desc_sw128(b),
+                                       bdl = umma_desc_sw128(b + (F16C ? A_BYTES + B_BYTES : B_BYTES));
                         const uint32_t ahi = tmem + A_COL0 + (uint32_t)(ta * 64);
                         const bool first = kb == kb_lo;
 #pragma unroll
                         for (int kk = 0; kk < 4; ++kk) {
                             const uint64_t o = (uint64_t)(kk * 2);
                             const uint32_t ak = ahi + (uint32_t)(kk * 8);
-                            umma_pair_ts_tf32(d, ak, bdl + o, idesc, !(first && kk == 0));
-                            umma_pair_ts_tf32(d, ak + 32, bd + o, idesc, 1);
-                            umma_pair_ts_tf32(d, ak, bd + o, idesc, 1);
+                            if constexpr (F16C) {
+                                umma_pair_ts_f16(d, ak, bdl + o, idesc, !(first && kk == 0));
+                                umma_pair_ts_f16(d, ak + 32, bd + o, idesc, 1);
+                                umma_pair_ts_f16(d, ak, bd + o, idesc, 1);
+                            } else {
+                                umma_pair_ts_tf32(d, ak, bdl + o, idesc, !(first && kk == 0));
+                                umma_pair_ts_tf32(d, ak + 32, bd + o, idesc, 1);
+                                umma_pair_ts_tf32(d, ak, bd + o, idesc, 1);
+                            }
                         }
                         umma_commit_pair(empty + s);
                         umma_commit_pair(tfree + ta);
@@ -667,8 +699,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             decode(item, grp, pair, nb);
             int kb_lo, kb_hi;
             const bool lead_split = krange(item, kb_lo, kb_hi) == 0;
-            const int acc = t & 1;
-            mbar_wait(tfull + acc, (t >> 1) & 1);
+            const int acc = NACC == 2 ? (t & 1) : 0;
+            mbar_wait(tfull + acc, (t / NACC) & 1);
             __syncwarp();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const int blk = pair * 2 + (int)rank;
@@ -779,6 +811,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
+        }
+    } else if (TSA && F16C && warp >= 8) {
+        // ---- 3xF16C TSA converters: warp (q, h) owns TMEM lanes 32q..32q+31 = A rows and
+        // channel half h (fp32 tile h of the stage); each thread splits its row's 32
+        // channels into scaled fp16 hi / lo pairs and tcgen05.st's them to the A slot ----
+        const int q = warp & 3, h = (warp >> 2) & 1;
+        const int m = q * 32 + lane;
+        const uint32_t tconv_leader = mapa_shared(smem_u32(tconv), 0);
+        const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(16 * h);
+        const float sc = pow2f(f16c_act_exp(P.row_exp, P.nred, lane));
+        int s = 0, ta = 0, it = 0;
+        uint32_t ph = 0, pht = 0;
+        for (int item = cluster_id; item < PP.items; item += nclusters) {
+            int kb_lo, kb_hi;
+            krange(item, kb_lo, kb_hi);
+            for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+                mbar_wait(full + s, ph);
+                if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
+                const uint32_t st = smem_u32(bring + s * STAGE);
+                const uint32_t row = st + (h ? (uint32_t)(A_BYTES + B_BYTES) : 0u) + (uint32_t)m * 128;
+                uint32_t hw[16], lw[16];
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {   // fp32 chunk c: channels 32h + 4c .. 4c + 3
+                    const float4 v = lds128(row + (uint32_t)((c ^ (m & 7)) << 4));
+                    const __half2 h0 = __floats2half2_rn(v.x * sc, v.y * sc);
+                    const __half2 h1 = __floats2half2_rn(v.z * sc, v.w * sc);
+                    const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
+                    const __half2 l0 = __floats2half2_rn(v.x * sc - f0.x, v.y * sc - f0.y);
+                    const __half2 l1 = __floats2half2_rn(v.z * sc - f1.x, v.w * sc - f1.y);
+                    hw[2 * c] = *reinterpret_cast<const uint32_t *>(&h0);
+                    hw[2 * c + 1] = *reinterpret_cast<const uint32_t *>(&h1);
+                    lw[2 * c] = *reinterpret_cast<const uint32_t *>(&l0);
+                    lw[2 * c + 1] = *reinterpret_cast<const uint32_t *>(&l1);
+                }
+                const uint32_t ta_col = (uint32_t)(ta * 64);
+                tmem_st_32x32b_x16(lane_base + ta_col, hw);
+                tmem_st_32x32b_x16(lane_base + ta_col + 32, lw);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(tconv_leader + (uint32_t)(ta * 8));
+                if (++ta == NTA) {
+                    ta = 0;
+                    pht ^= 1;
+                }
+                if (++s == NS) {
+                    s = 0;
+                    ph ^= 1;
+                }
+            }
         }
     } else if (TSA && warp >= 8) {
         // ---- TSA converters: warp q owns TMEM lanes 32q..32q+31 = A rows; each

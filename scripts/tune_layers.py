@@ -112,8 +112,8 @@ def tune_igemm(shape, spec, prec, log):
     out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
     ws = torch.empty(2 * xh.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
     variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
-    if prec == "3xf16":    # CTA-pair tiles only
-        variants = [(z, 32768, 2) for z in zs]
+    if prec == "3xf16":    # CTA-pair tiles only (n_zt = 4: the split A operand in TMEM)
+        variants = [(z, 32768, nzt) for z in zs for nzt in (2, 4)]
     if prec == "3xtf32":   # pair with the A operand split into TMEM
         variants += [(z, 32768, 4) for z in zs if z <= 128]
     # halo-staged footprint tiles (pair kernel, stride 1): (x + S - 1) * y = 128

@@ -44,6 +44,12 @@ CASES = [
     (2, 64, 56, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 2, layout="HWC"), "fold (3 taps per MMA)"),
     (3, 64, 28, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 2, layout="HWC"), "fold 30x4"),
     (16, 512, 14, 256, 2, TileConfig(1, 1, 256, 32768, 1, 1, 2, layout="HWC"), "split-K"),
+    # n_zt = 4: the split activations in tensor memory (tcgen05.mma A operand from TMEM)
+    (3, 128, 28, 128, 1, TileConfig(1, 1, 128, 32768, 1, 1, 4, layout="HWC"), "tsa z=128"),
+    (2, 64, 56, 64, 1, TileConfig(28, 4, 64, 32768, 1, 1, 4, layout="HWC"), "tsa z=64"),
+    (3, 256, 14, 256, 1, TileConfig(1, 1, 256, 32768, 1, 1, 4, layout="HWC"), "tsa z=256 (one accumulator)"),
+    (3, 128, 28, 128, 2, TileConfig(2, 1, 128, 32768, 1, 1, 4, layout="HWC"), "tsa stride 2"),
+    (16, 512, 14, 256, 2, TileConfig(1, 1, 256, 32768, 1, 1, 4, layout="HWC"), "tsa split-K"),
 ]
 
 
@@ -56,8 +62,10 @@ def test_igemm_3xf16_matches_oracle(case):
     assert info["rc"] == 0, info
     if what.startswith("fold"):
         assert "3 taps per MMA" in info["reason"], info
-    if what == "split-K":
+    if what.endswith("split-K"):
         assert "split-K" in info["reason"], info
+    if what.startswith("tsa"):
+        assert "A in TMEM" in info["reason"], info
     y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, stride=stride, tile=tile,
                      precision="3xf16", bias=torch.from_numpy(b).cuda())
     ref = co.direct_conv(x, wt, stride, 1) + b[None, :, None, None]
