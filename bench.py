@@ -133,6 +133,133 @@ def cpu_oracle_gflops(layers, images: int = 1, threads: int = 0):
     return flops / busy / 1e9, busy
 
 
+def onednn_gflops(specs, threads: int, images: int = 1, reps: int = 3):
+    """Numeric CPU conv baseline: torch.nn.functional.conv2d fp32 on the
+    host (oneDNN), all `threads`, `images` per layer; median of `reps` after a warm-up.
+    Returns (GFLOP/s, seconds of conv work per pass)."""
+    import torch
+    torch.set_num_threads(threads)
+    g = torch.Generator().manual_seed(0)
+    total = 0.0
+    flops = 0
+    for spec in specs:
+        x = torch.rand((images, spec.c, spec.hw, spec.hw), generator=g) * 2 - 1
+        w = (torch.rand((spec.k, spec.c, spec.r, spec.r), generator=g) * 2 - 1) / (spec.c * spec.r * spec.r) ** 0.5
+        torch.nn.functional.conv2d(x, w, stride=spec.stride, padding=spec.pad)
+        ts = []
+        for _ in range(reps):
+            t1 = time.perf_counter()
+            torch.nn.functional.conv2d(x, w, stride=spec.stride, padding=spec.pad)
+            ts.append(time.perf_counter() - t1)
+        total += statistics.median(ts)
+        flops += spec.flops(images)
+    return flops / total / 1e9, total
+
+
+def model_cpu_timings() -> dict:
+    """The reference's own CPU path (its model: SURVEY §8(a) a6-a21),
+    timed through this package's bit-exact restatement (the reference itself is not on
+    the GPU box): lower bound, analytic tile, schedule + simulate, Table-1 space and a
+    budget-32 GBR tune, on BASELINE config 1 and on ResNet-50 res4 at batch 256.
+    Single process, single thread, as the reference runs."""
+    from paper_2012_15667_b200.autotune import build_space, tune
+    from paper_2012_15667_b200.bounds import lower_bound_dc
+    from paper_2012_15667_b200.dataflow import optimal_tile_dc, plan_direct_dataflow, simulate
+    from paper_2012_15667_b200.device import b200_hw_model, shape_of
+    hw = b200_hw_model()
+    out = {}
+    for name, shape in (("config1", shape_of(1, 64, 56, 56, 64, 3, 1, 1)),
+                        ("res4_3x3_n256", shape_of(256, 256, 14, 14, 256, 3, 1, 1))):
+        def med(fn, reps):
+            ts = []
+            for _ in range(reps):
+                t1 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t1)
+            return statistics.median(ts)
+        tile = optimal_tile_dc(shape, hw)
+        row = {
+            "lower_bound_dc_us": round(1e6 * med(lambda: lower_bound_dc(shape, hw.s_sm), 200), 2),
+            "optimal_tile_dc_us": round(1e6 * med(lambda: optimal_tile_dc(shape, hw), 20), 1),
+            "plan_and_simulate_ms": round(1e3 * med(lambda: simulate(plan_direct_dataflow(shape, hw, tile), hw), 5), 3),
+        }
+        t1 = time.perf_counter()
+        space = build_space(shape, hw, "direct", thread_axes=False)
+        row["build_space_s"] = round(time.perf_counter() - t1, 3)
+        row["space_size"] = space.size
+        t1 = time.perf_counter()
+        tune(shape, hw, "direct", 32, 0, space=space)
+        row["tune_budget32_s"] = round(time.perf_counter() - t1, 3)
+        out[name] = row
+    return out
+
+
+def layer_io_bounds(spec, n: int, algorithm: str, e, hw) -> dict:
+    """The paper's I/O bounds for one layer call in bytes (fp32 words x 4): the
+    red-blue-pebble lower bound Omega(S) and q_exact(S) per image x n
+    (reference pkg/src/convio/bounds.py:230-271) at S = one SM's fast memory of the
+    B200 machine model (registers + shared memory, device.py), and the Eq. 18/19
+    I/O of the model's optimal tile (dataflow.py:377-378, 403-407).  These bound the
+    traffic between the SMs and the next level -- L2 -- not DRAM."""
+    from paper_2012_15667_b200.bounds import lower_bound_dc, lower_bound_wa
+    from paper_2012_15667_b200.dataflow import dc_io_at_optimum, wa_io_at_optimum
+    from paper_2012_15667_b200.device import shape_of
+    from paper_2012_15667_b200.model import WinogradParams
+    shape = shape_of(n, spec.c, spec.hw, spec.hw, spec.k, spec.r, spec.stride, spec.pad)
+    s = hw.s_sm
+    wino = algorithm.startswith("winograd") and bool(e)
+    if wino:
+        p = WinogradParams(e, spec.r)
+        rep_, opt = lower_bound_wa(shape, p, s), wa_io_at_optimum(shape, p, hw)
+    else:
+        rep_, opt = lower_bound_dc(shape, s), dc_io_at_optimum(shape, hw)
+    return {"dataflow": "WA" if wino else "DC", "s_words": s,
+            "omega_bytes": int(4 * n * rep_.omega), "q_exact_bytes": int(4 * n * rep_.q_exact),
+            "io_at_optimum_bytes": int(4 * opt)}
+
+
+def cudnn_layers(torch, specs, n: int, dev, reps: int = 10) -> dict:
+    """The GPU comparison point (north star): cuDNN through
+    torch.nn.functional.conv2d, cudnn.benchmark on, FP32 (TF32 off) and TF32, the
+    faster of NCHW / channels_last per layer; CUDA events over `reps` back-to-back
+    calls after warm-up.  {layer name: {"fp32": ms, "tf32": ms}}."""
+    F = torch.nn.functional
+    saved = (torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32)
+    torch.backends.cudnn.benchmark = True
+    out = {}
+    try:
+        for spec in {s.name: s for s in specs}.values():
+            g = torch.Generator(device=dev).manual_seed(0)
+            x = torch.rand((n, spec.c, spec.hw, spec.hw), device=dev, generator=g) * 2 - 1
+            w = (torch.rand((spec.k, spec.c, spec.r, spec.r), device=dev, generator=g) * 2 - 1) / (
+                spec.c * spec.r * spec.r) ** 0.5
+            row = {}
+            for prec in ("fp32", "tf32"):
+                torch.backends.cudnn.allow_tf32 = prec == "tf32"
+                best = float("inf")
+                for fmt in (torch.contiguous_format, torch.channels_last):
+                    xx, ww = x.contiguous(memory_format=fmt), w.contiguous(memory_format=fmt)
+                    for _ in range(3):
+                        F.conv2d(xx, ww, stride=spec.stride, padding=spec.pad)
+                    torch.cuda.synchronize(dev)
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record()
+                    for _ in range(reps):
+                        F.conv2d(xx, ww, stride=spec.stride, padding=spec.pad)
+                    b.record()
+                    b.synchronize()
+                    best = min(best, a.elapsed_time(b) / reps)
+                    del xx, ww
+                row[prec] = round(best, 4)
+            out[spec.name] = row
+            del x, w
+    finally:
+        torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32 = saved
+        torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, rank: int, world: int) -> None:
     """``--impl reference``: the CPU implementation of the path on host cores."""
     if rank != 0:
@@ -202,6 +329,15 @@ def load_profile_traffic() -> dict:
             except (OSError, ValueError):
                 pass
     return out
+
+
+def _l2_measured(tab: dict, workload: str, layer: str, algorithm: str, n: int):
+    """ncu L2->SM read bytes per layer call (lts__t_sectors_srcunit_tex_op_read x 32 B,
+    summed over the call's kernels) from the committed capture, or None."""
+    t = tab.get(f"{workload}:{layer}:{algorithm}")
+    if not isinstance(t, dict) or t.get("n") not in (None, n) or t.get("l2_sm_read_bytes_per_call") is None:
+        return None
+    return t
 
 
 def _traffic(tab: dict, workload: str, fam: dict, dom: str, n: int | None = None):
@@ -327,6 +463,7 @@ def main() -> None:
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
+    ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN comparison point")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU (gloo) rehearsal of the multi-rank logic; no GPU needed")
@@ -530,7 +667,7 @@ def main() -> None:
                             + n_local * s.k * s.out_hw * s.out_hw)
                 t = layer.tile
                 rows.append({
-                    "layer": s.name, "algorithm": name,
+                    "layer": s.name, "algorithm": name, "_alg": layer.algorithm, "_e": layer.e,
                     "tile": None if t is None else [t.x, t.y, t.z, t.s_b, t.n_xt, t.n_yt, t.n_zt, t.layout],
                     "ms": round(t_med, 4), "gflops": round(f_dir / (t_med / 1e3) / 1e9, 1),
                     "q_dram_bytes": comp,
@@ -736,18 +873,71 @@ def main() -> None:
         b.synchronize()
         gathered = {"allgather_ms_per_step": round(max_over_ranks(a.elapsed_time(b)), 3)}
 
+    # ---- comparison points: cuDNN on the same GPU, per layer and per step -------------
+    cudnn = None
+    if rank == 0 and world == 1 and not args.no_cudnn:
+        per = cudnn_layers(torch, specs, n_local, dev)
+        cudnn = {"method": "torch.nn.functional.conv2d, cudnn.benchmark, faster of NCHW / "
+                           "channels_last per layer, CUDA events over 10 eager calls"}
+        for prec in ("fp32", "tf32"):
+            ms = sum(per[s.name][prec] for s in specs)
+            cudnn[prec] = {"value": round(flops_local / (ms / 1e3) / 1e9, 3), "unit": "GFLOP/s",
+                           "ms_per_step": round(ms, 4),
+                           "ours_speedup": round(ms / (t_max_ms / args.steps), 3)}
+        for row in per_layer:
+            row["cudnn_fp32_ms"] = per[row["layer"]]["fp32"]
+            row["cudnn_tf32_ms"] = per[row["layer"]]["tf32"]
+
+    # ---- the paper's bound against the SM<->L2 traffic (per layer) --------------------
+    from paper_2012_15667_b200.device import b200_hw_model
+    hw_b200 = b200_hw_model()
+    bounds_cache = {}
+    for row, s in zip(per_layer, specs):
+        key = (s.name, row["_alg"], row["_e"])
+        if key not in bounds_cache:
+            b = layer_io_bounds(s, n_local, row["_alg"], row["_e"], hw_b200)
+            m = _l2_measured(traffic_tab, args.workload, s.name, row["_alg"], n_local)
+            if m is not None:
+                b["measured_l2_sm_read_bytes"] = m["l2_sm_read_bytes_per_call"]
+                b["measured_dram_bytes"] = m.get("dram_bytes_per_call")
+                b["measured_over_omega"] = round(m["l2_sm_read_bytes_per_call"] / b["omega_bytes"], 3)
+                b["measured_over_io_at_optimum"] = round(
+                    m["l2_sm_read_bytes_per_call"] / b["io_at_optimum_bytes"], 3)
+                b["source"] = m.get("source", "committed ncu capture (profiles/*_traffic.json)")
+            else:
+                b["measured_l2_sm_read_bytes"] = None
+            bounds_cache[key] = b
+        row["l2_sm_bytes_vs_bound"] = bounds_cache[key]
+    for row in per_layer:
+        row.pop("_alg", None)
+        row.pop("_e", None)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
         try:
-            cores = os.cpu_count() or 1
             sample_layers = specs
             gf, el = cpu_oracle_gflops(sample_layers, 1, cores)
             cpu = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                   "sample": f"1 image x {len(sample_layers)} layers, C oracle (oracle/conv_oracle.c), "
-                             f"{el:.1f} s"}
+                   "sample": f"1 image x {len(sample_layers)} layers, C oracle (oracle/conv_oracle.c, "
+                             f"fp64 accumulate, OpenMP), {el:.2f} s"}
         except Exception as exc:  # noqa: BLE001
-            cpu = {"value": None, "unit": "GFLOP/s", "cores": os.cpu_count(), "kind": "port",
+            cpu = {"value": None, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                    "sample": f"unavailable: {exc}"}
+        try:
+            gf, el = onednn_gflops(specs, cores, images=4)
+            cpu["onednn"] = {"value": round(gf, 3), "unit": "GFLOP/s", "cores": cores,
+                             "sample": f"4 images x {len(specs)} layers, torch.nn.functional.conv2d fp32 "
+                                       f"on the host (oneDNN), median of 3, {el:.2f} s per pass"}
+        except Exception as exc:  # noqa: BLE001
+            cpu["onednn"] = {"value": None, "sample": f"unavailable: {exc}"}
+        try:
+            cpu["model"] = model_cpu_timings()
+            cpu["model"]["what"] = ("the reference's CPU path (lower bound, analytic tile, schedule + "
+                                    "simulate, Table-1 space, GBR tune) via this package's bit-exact "
+                                    "restatement, 1 thread")
+        except Exception as exc:  # noqa: BLE001
+            cpu["model"] = {"unavailable": str(exc)}
 
     if rank == 0:
         line = {
@@ -773,6 +963,7 @@ def main() -> None:
             "roofline": roofline,
             "variants": variants,
             "cpu_baseline": cpu,
+            "cudnn": cudnn,
             "clocks": clk,
             "gpu_launches": launches,
             "per_layer": per_layer,

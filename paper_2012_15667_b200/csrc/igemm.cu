@@ -119,7 +119,11 @@ __global__ void __launch_bounds__(256) pack_filter_f16x3_kernel(const float *__r
 }
 
 // 3xF16C activation scale: per-block max |x| (float bits) into partials[blockIdx.x];
-// the GEMM reduces the nred partials into one exponent (f16c_act_exp)
+// the GEMM reduces the nred partials into one exponent (f16c_act_exp).
+// The grid walks x from its END to its start, so the most recently read ~L2-size
+// tail of the walk is the START of x -- where the GEMM's first work items (low
+// images first) read: for inputs larger than L2 about one L2's worth of the
+// GEMM's activation reads hit L2 instead of HBM.
 constexpr int kAbsmaxBlocks = 296;
 __global__ void __launch_bounds__(256) absmax_partials_kernel(const float *__restrict__ x, int64_t n,
                                                               int *__restrict__ partials) {
@@ -129,21 +133,21 @@ __global__ void __launch_bounds__(256) absmax_partials_kernel(const float *__res
     const int64_t n4 = n >> 2;
     const int64_t step = (int64_t)gridDim.x * blockDim.x;
     const float4 *x4 = reinterpret_cast<const float4 *>(x);
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    for (; i + 3 * step < n4; i += 4 * step) {
+    for (int64_t j = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += step)
+        m = fmaxf(m, fabsf(x[j]));
+    int64_t i = n4 - 1 - (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    for (; i - 3 * step >= 0; i -= 4 * step) {
         float4 v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = __ldg(x4 + i + j * step);
+        for (int j = 0; j < 4; ++j) v[j] = __ldg(x4 + i - j * step);
 #pragma unroll
         for (int j = 0; j < 4; ++j)
             m = fmaxf(m, fmaxf(fmaxf(fabsf(v[j].x), fabsf(v[j].y)), fmaxf(fabsf(v[j].z), fabsf(v[j].w))));
     }
-    for (; i < n4; i += step) {
+    for (; i >= 0; i -= step) {
         const float4 v = __ldg(x4 + i);
         m = fmaxf(m, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
     }
-    for (int64_t j = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += step)
-        m = fmaxf(m, fabsf(x[j]));
     for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();

@@ -57,6 +57,7 @@ def parse(paths, workload, out):
         ki, ni, vi, ii = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Value"), h.index("ID")
         per = {}
         names = {}
+        # ncu prints byte metrics with units (e.g. "Mbyte") unless --print-units base
         for r in rows[hdr + 1:]:
             if len(r) < len(h) or "pack_filter" in r[ki] or "filter_tc" in r[ki] or "filter_transform" in r[ki] or "u_split" in r[ki]:
                 continue
@@ -65,6 +66,8 @@ def parse(paths, workload, out):
         ids = sorted(per)
         calls = meta.get("reps", 2)
         last = ids[-(len(ids) // calls):] if calls and len(ids) >= calls else ids
+        l2 = sum(per[i].get("lts__t_sectors_srcunit_tex_op_read.sum", 0) for i in last) * 32
+        xbar = sum(per[i].get("l1tex__m_xbar2l1tex_read_bytes.sum", 0) for i in last)
         rd = sum(per[i].get("dram__bytes_read.sum", 0) for i in last)
         wr = sum(per[i].get("dram__bytes_write.sum", 0) for i in last)
         ns = sum(per[i].get("gpu__time_duration.sum", 0) for i in last)
@@ -73,6 +76,11 @@ def parse(paths, workload, out):
                       "kernels_per_call": len(last), "ncu_ns_per_call": ns,
                       "kernels": sorted({names[i] for i in last}), "n": meta.get("n"),
                       "tile": meta.get("tile")}
+        if l2:
+            table[key]["l2_sm_read_bytes_per_call"] = int(l2)
+            table[key]["l1tex_xbar_read_bytes_per_call"] = int(xbar)
+            table[key]["source"] = ("ncu --cache-control none, last of 3 calls: lts__t_sectors_srcunit_tex_op_read"
+                                    ".sum x 32 B (SM -> L2 reads incl. TMA), dram__bytes_read/write.sum")
     with open(out, "w") as fh:
         json.dump(table, fh, indent=1, sort_keys=True)
     print(json.dumps(table, indent=1))
