@@ -77,85 +77,6 @@ def tune_one(shape, hw, alg, wp, budget, seed, exhaustive_cap, log):
     return out
 
 
-def block_ok(bx, by, n):
-    """Pixel blocks of the stacked-pixel kernels: x*y <= 128 rows, and either
-    >= 32 pixels per image or a divisor of 128 (then 128/(x*y) images fill
-    every row: 2x2 blocks x 32 images on 14x14 maps, 1x1 x 128 on 7x7)."""
-    px = bx * by
-    return px <= 128 and (px >= 32 or (128 % px == 0 and n * px >= 128))
-
-
-def tune_igemm(shape, spec, prec, log):
-    """Tensor-core projection: small exhaustive device search over (x, y, z, kernel).
-
-    The Table-1 prune is derived for the FFMA machine model (outputs in
-    registers); the tcgen05 kernels keep outputs in TMEM, so their own small
-    space (x | Q, y | P, 32 <= x*y <= 128, z in {64, 128, 256}, n_zt in
-    {1 (one CTA, s_b 16384 / 32768 ring), 2 (persistent CTA pair)}) is
-    searched whole.
-    """
-    import math as _m
-    from paper_2012_15667_b200.dataflow import TileConfig
-    from paper_2012_15667_b200 import conv as C
-    cb = 64 if prec in ("bf16", "3xf16") else 32
-    if spec.c % cb or spec.stride > 2:
-        return {"error": f"needs C % {cb} == 0 and stride <= 2"}
-    q = shape.w_out
-    p = shape.h_out
-    zs = [z for z in (64, 128, 256) if spec.k % z == 0]
-    best, best_t, tried = None, _m.inf, 0
-    x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
-    xh = C.to_layout(x, "HWC")
-    w = torch.empty((spec.k, spec.c, spec.r, spec.r), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
-    wq = (C.pack_filter_igemm_bf16(w) if prec == "bf16" else
-          C.pack_filter_igemm_f16x3(w) if prec == "3xf16" else C.pack_filter_igemm(w))
-    out = C.empty_act(shape.n, spec.k, p, q, "HWC", device="cuda")
-    ws = torch.empty(2 * xh.numel() + (1 << 20), dtype=torch.uint8, device="cuda")
-    variants = [(z, sb, 1) for z in zs for sb in (16384, 32768)] + [(z, 32768, 2) for z in zs]
-    if prec == "3xf16":    # CTA-pair tiles only (n_zt = 4: the split A operand in TMEM)
-        variants = [(z, 32768, nzt) for z in zs for nzt in (2, 4)]
-    if prec == "3xtf32":   # pair with the A operand split into TMEM
-        variants += [(z, 32768, 4) for z in zs if z <= 128]
-    # halo-staged footprint tiles (pair kernel, stride 1): (x + S - 1) * y = 128
-    halo = []
-    if spec.stride == 1:
-        for fpr in (8, 16, 32, 64, 128):
-            x_, y_ = fpr - spec.r + 1, 128 // fpr
-            if 1 <= x_ <= q + spec.r - 1 and y_ <= p + spec.r - 1:
-                halo += [TileConfig(x_, y_, z, 32768, 2, 1, 2, layout="HWC") for z in zs
-                         if x_ % 2 == 0 and z % 2 == 0]
-    for tile in halo:
-        try:
-            t = DT.device_time(lambda: C.conv_igemm(xh, w, padding=spec.pad, tile=tile,
-                                                     precision=prec, w_packed=wq,
-                                                     stride=spec.stride, out=out, workspace=ws))
-        except Exception:  # noqa: BLE001 -- illegal projection
-            continue
-        tried += 1
-        if t < best_t:
-            best, best_t = tile, t
-    for bx in [d for d in range(1, q + 1) if q % d == 0]:
-        for by in [d for d in range(1, p + 1) if p % d == 0]:
-            if not block_ok(bx, by, shape.n):
-                continue
-            for z, sb, nzt in variants:
-                tile = TileConfig(bx, by, z, sb, 1, 1, nzt, layout="HWC")
-                try:
-                    t = DT.device_time(lambda: C.conv_igemm(xh, w, padding=spec.pad, tile=tile,
-                                                             precision=prec, w_packed=wq,
-                                                             stride=spec.stride, out=out,
-                                                             workspace=ws))
-                except Exception:  # noqa: BLE001 -- illegal projection
-                    continue
-                tried += 1
-                if t < best_t:
-                    best, best_t = tile, t
-    log(f"    igemm_{prec}: {tried} tiles, best {best} {best_t}")
-    return {"tuner": {"best": best.to_dict() if best else None,
-                      "seconds": best_t if best else None, "measurements": tried},
-            "space": "exhaustive tcgen05 projection"}
-
-
 def tune_direct_nhwc(shape, spec, log):
     """Channels-last FFMA direct kernel (stacked pixels): exhaustive device
     search over its own space (x | Q, y | P, 32 <= x*y <= 128, z in {64, 128},
@@ -185,7 +106,7 @@ def tune_direct_nhwc(shape, spec, log):
             pass
     for bx in [d for d in range(1, q + 1) if q % d == 0 and not small_c]:
         for by in [d for d in range(1, p + 1) if p % d == 0]:
-            if not block_ok(bx, by, shape.n):
+            if not DT._block_ok(bx, by, shape.n):
                 continue
             for z in [z for z in (64, 128) if spec.k % z == 0]:
                 for sb in (16384, 32768):
@@ -203,47 +124,6 @@ def tune_direct_nhwc(shape, spec, log):
     return {"tuner": {"best": best.to_dict() if best else None,
                       "seconds": best_t if best else None, "measurements": tried},
             "space": "exhaustive channels-last FFMA projection"}
-
-
-def tune_winograd_tc(shape, spec, prec, e, log):
-    """Tensor-core Winograd: exhaustive over (z, n_zt); the GEMM's M tile is
-    fixed at 128 Winograd tiles per CTA (256 per pair)."""
-    import math as _m
-    from paper_2012_15667_b200.dataflow import TileConfig
-    from paper_2012_15667_b200 import conv as C
-    cb = 64 if prec == "bf16" else 32
-    if spec.c % cb or spec.stride != 1 or spec.r != 3:
-        return {"error": f"needs C % {cb} == 0, stride 1, 3x3"}
-    x = torch.empty((shape.n, spec.c, spec.hw, spec.hw), device="cuda").uniform_(-1, 1)
-    xh = C.to_layout(x, "HWC")
-    w = torch.empty((spec.k, spec.c, 3, 3), device="cuda").uniform_(-1, 1) / (spec.c * 9) ** 0.5
-    u = C.winograd_filter_transform_tc(w, e, prec)
-    out = C.empty_act(shape.n, spec.k, shape.h_out, shape.w_out, "HWC", device="cuda")
-    best, best_t, tried = None, _m.inf, 0
-    zs = (64, 128) if prec == "fp32" else (64, 128, 256)
-    for z, nzt, sb in [(z, nzt, sb) for z in zs if spec.k % z == 0
-                   for nzt in ((1,) if prec == "fp32" else
-                               (1, 2, 4) if prec == "3xtf32" and z <= 128 else (1, 2))
-                   for sb in (2048, 8192, 16384, 32768)]:   # chunk (V + M) = 16 KB x s_b
-        tile = TileConfig(e, e, z, sb, 1, 1, nzt, layout="HWC", e=e)
-        info = C.query(tuple(xh.shape), tuple(w.shape), 1, spec.pad, "HWC", tile,
-                       "winograd_nhwc" if prec == "fp32" else f"winograd_tc_{prec}")
-        if info["rc"]:
-            continue
-        ws = torch.empty(info["workspace_bytes"], dtype=torch.uint8, device="cuda")
-        try:
-            t = DT.device_time(lambda: C.conv_winograd_tc(xh, w, e=e, padding=spec.pad, tile=tile,
-                                                           precision=prec, u=u, out=out,
-                                                           workspace=ws))
-        except Exception:  # noqa: BLE001
-            continue
-        tried += 1
-        if t < best_t:
-            best, best_t = tile, t
-    log(f"    {'winograd_nhwc' if prec == 'fp32' else 'winograd_tc_' + prec}_e{e}: {tried} tiles, best {best} {best_t}")
-    return {"tuner": {"best": best.to_dict() if best else None,
-                      "seconds": best_t if best else None, "measurements": tried},
-            "space": "exhaustive tcgen05 projection"}
 
 
 def main():
@@ -293,15 +173,18 @@ def main():
                                            args.exhaustive_cap, log)
             elif alg == "direct_nhwc":
                 cands[alg] = tune_direct_nhwc(shape, spec, log)
-            elif alg.startswith("igemm"):
-                cands[alg] = tune_igemm(shape, spec, alg[len("igemm_"):], log)
-            elif alg.startswith("winograd_tc_"):
-                if spec.stride == 1 and spec.r == 3:
-                    prec, _, e = alg[len("winograd_tc_"):].partition("_e")
-                    cands[alg] = tune_winograd_tc(shape, spec, prec, int(e), log)
+            elif alg.startswith("igemm") or alg.startswith("winograd_tc_"):
+                # the tensor-core engines: the reference tuner over the I/O-pruned tcgen05
+                # domain (device_tuner.tune_layer; budget >= domain size = its optimum)
+                if alg.startswith("igemm") or (spec.stride == 1 and spec.r == 3):
+                    cands.update(DT.tune_layer(spec, args.n, [alg], budget=args.budget, seed=args.seed,
+                                               log=log))
             elif alg.startswith("winograd_nhwc_e"):
                 if spec.stride == 1 and spec.r == 3:
-                    cands[alg] = tune_winograd_tc(shape, spec, "fp32", int(alg[-1]), log)
+                    got = DT.tune_layer(spec, args.n, [f"winograd_tc_fp32_e{alg[-1]}"], budget=args.budget,
+                                        seed=args.seed, log=log)
+                    if got:
+                        cands[alg] = next(iter(got.values()))
             elif alg.startswith("winograd") and spec.stride == 1 and spec.r == 3:
                 e = int(alg[len("winograd"):])
                 cands[alg] = tune_one(shape, hw, "winograd", WinogradParams(e, 3), args.budget,

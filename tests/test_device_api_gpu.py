@@ -100,3 +100,29 @@ def test_cli_simulate_tune_report_device_modes(capsys, tmp_path):
     assert cli_main(["report", *base, "--device"]) == 0
     rep = json.loads(capsys.readouterr().out)
     assert "device_projection" in rep
+
+
+def test_reference_tune_over_tcgen05_domain_reproduces_the_plan_table():
+    """The shipped tensor-core kernels through the reference tuner API: tune(shape, hw,
+    "direct", ..., backend="device") under the igemm_3xf16 engine, over the I/O-pruned
+    tcgen05 domain, lands on the committed res4 plan or within 5 % of its time."""
+    from paper_2012_15667_b200 import device_tuner as DT
+    from paper_2012_15667_b200.autotune import tune
+    from paper_2012_15667_b200.device import shape_of
+    from paper_2012_15667_b200.runner import WORKLOADS, load_plans
+    spec = next(s for s in WORKLOADS["resnet50"] if s.name == "res4_3x3")
+    plan = load_plans("resnet50", allowed=("igemm_3xf16",), n=256)[spec.name]
+    DT.set_padding(spec.pad)
+    try:
+        shape = shape_of(256, spec.c, spec.hw, spec.hw, spec.k, spec.r, spec.stride, spec.pad)
+        with DT.use_engine("igemm_3xf16"):
+            hw = DT.tcgen05_hw_model()
+            space = DT.tcgen05_space(shape, hw, "igemm_3xf16")
+            assert plan["tile"] in space, (plan["tile"], space.size)
+            assert space.size < space.unconstrained_size
+            sess = tune(shape, hw, "direct", space.size, 0, n_s=8, space=space, backend="device")
+            t_plan = DT.measure_device(plan["tile"], shape, hw, "direct")
+        assert sess.best is not None and math.isfinite(sess.best.cost)
+        assert sess.best.config == plan["tile"] or sess.best.cost <= 1.05 * t_plan, (sess.best, t_plan)
+    finally:
+        DT.set_padding(0)
