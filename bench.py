@@ -260,6 +260,104 @@ def cudnn_layers(torch, specs, n: int, dev, reps: int = 10) -> dict:
     return out
 
 
+def network_bench(torch, dev, steps: int, warmup: int, n: int = 32) -> dict:
+    """The chained network forward: VGG-16's 13 convs +
+    5 max pools + the NCHW -> NHWC staging, batch ``n`` (BASELINE config 3), all our
+    kernels, replayed as one CUDA graph; beside it the same network through
+    torch/cuDNN (fp32 and TF32, channels_last, cudnn.benchmark), and end to end
+    from a pinned NCHW host batch to host features."""
+    from paper_2012_15667_b200.network import Vgg16Features
+    F = torch.nn.functional
+    net = Vgg16Features(n, dev, seed=11)
+    x = torch.rand((n, 3, 224, 224), device=dev) * 2 - 1
+    net.prepare()
+    stream = torch.cuda.current_stream(dev)
+
+    def graph_of(fn):
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(stream)
+        with torch.cuda.stream(side):
+            for _ in range(max(1, warmup)):
+                fn(side)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            fn(side)
+        torch.cuda.synchronize(dev)
+        return g
+
+    def timed(g):
+        g.replay()
+        torch.cuda.synchronize(dev)
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(steps):
+            g.replay()
+        b.record(stream)
+        b.synchronize()
+        return a.elapsed_time(b) / steps
+
+    ours = timed(graph_of(lambda st: net.forward(x, stream=st)))
+    flops = net.flops()
+    out = {"model": f"VGG-16 conv features (13 conv + bias + ReLU, 5 max pools), batch {n}, 224x224, "
+                    "NCHW input staged to NHWC on the device",
+           "ms_per_forward": round(ours, 4), "images_per_s": round(n / (ours / 1e3), 1),
+           "gflops_direct_equiv": round(flops / (ours / 1e3) / 1e9, 1),
+           "launches_per_forward": net.launches_per_forward(),
+           "plans": {l.name: l.algorithm for l in net.conv_layers}}
+    # cuDNN through torch, same weights, channels_last
+    saved = (torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32)
+    torch.backends.cudnn.benchmark = True
+    ws = [(l.weight.contiguous(memory_format=torch.channels_last), l.bias) for l in net.conv_layers]
+    xl = x.contiguous(memory_format=torch.channels_last)
+
+    def torch_forward(st):
+        with torch.cuda.stream(st):
+            h, j = xl, 0
+            for layer in net.layers:
+                if layer is None:
+                    h = F.max_pool2d(h, 2)
+                else:
+                    h = torch.relu(F.conv2d(h, ws[j][0], ws[j][1], padding=1))
+                    j += 1
+            return h
+    try:
+        for prec in ("fp32", "tf32"):
+            torch.backends.cudnn.allow_tf32 = prec == "tf32"
+            t = timed(graph_of(torch_forward))
+            out[f"cudnn_{prec}_ms_per_forward"] = round(t, 4)
+            out[f"ours_speedup_vs_cudnn_{prec}"] = round(t / ours, 3)
+    finally:
+        torch.backends.cudnn.benchmark, torch.backends.cudnn.allow_tf32 = saved
+    # end to end: pinned NCHW host batch -> device -> features -> pinned host
+    hx = torch.empty((n, 3, 224, 224), pin_memory=True).copy_(x)
+    hy = torch.empty((n, 512, 7, 7), pin_memory=True)
+    dx = torch.empty_like(x)
+
+    def e2e(st):
+        with torch.cuda.stream(st):
+            dx.copy_(hx, non_blocking=True)
+            y = net.forward(dx, stream=st, nchw_out=True)
+            hy.copy_(y, non_blocking=True)
+    for _ in range(2):
+        e2e(stream)
+    torch.cuda.synchronize(dev)
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(steps):
+        e2e(stream)
+    b.record(stream)
+    b.synchronize()
+    te = a.elapsed_time(b) / steps
+    out["e2e"] = {"ms_per_forward": round(te, 4), "images_per_s": round(n / (te / 1e3), 1),
+                  "h2d_bytes": hx.numel() * 4, "d2h_bytes": hy.numel() * 4}
+    del net
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_reference(args, rank: int, world: int) -> None:
     """``--impl reference``: the CPU implementation of the path on host cores."""
     if rank != 0:
@@ -464,6 +562,7 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN comparison point")
+    ap.add_argument("--no-network", action="store_true", help="skip the chained VGG-16 forward")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU (gloo) rehearsal of the multi-rank logic; no GPU needed")
@@ -912,6 +1011,13 @@ def main() -> None:
         row.pop("_alg", None)
         row.pop("_e", None)
 
+    network = None
+    if rank == 0 and world == 1 and not args.no_network:
+        try:
+            network = network_bench(torch, dev, args.steps, args.warmup)
+        except Exception as exc:  # noqa: BLE001
+            network = {"unavailable": str(exc)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         cores = os.cpu_count() or 1
@@ -964,6 +1070,7 @@ def main() -> None:
             "variants": variants,
             "cpu_baseline": cpu,
             "cudnn": cudnn,
+            "network": network,
             "clocks": clk,
             "gpu_launches": launches,
             "per_layer": per_layer,

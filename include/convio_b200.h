@@ -245,6 +245,20 @@ int convio_ffma_peak(float *sink, int32_t blocks, int32_t iters, int64_t *flops,
 /* Number of kernel launches the last convio_conv_* call on this thread issued. */
 int convio_last_launch_count(void);
 
+/* ---- steps either side of the conv path in a chained network forward ----------
+ * (the reference's layout axis CHW / HWC,
+ * pkg/src/convio/dataflow.py:23, staged on the device as a counted kernel) */
+
+/* y[n][h][w][c] = x[n][c][h][w] (both fp32, contiguous). */
+int convio_nchw_to_nhwc(const float *x, float *y, int32_t n, int32_t c, int32_t h, int32_t w, void *stream);
+
+/* y[n][c][h][w] = x[n][h][w][c]. */
+int convio_nhwc_to_nchw(const float *x, float *y, int32_t n, int32_t c, int32_t h, int32_t w, void *stream);
+
+/* 2x2 / stride-2 max pooling of NHWC activations (C % 4 == 0, 16-byte aligned;
+ * floor for odd H / W): y is n x h/2 x w/2 x c. */
+int convio_maxpool2x2_nhwc(const float *x, float *y, int32_t n, int32_t h, int32_t w, int32_t c, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

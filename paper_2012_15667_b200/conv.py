@@ -26,7 +26,7 @@ from .dataflow import LAYOUTS, TileConfig
 __all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "conv_igemm", "conv_winograd_tc",
            "winograd_filter_transform", "winograd_filter_transform_tc",
            "pack_filter_direct", "pack_filter_igemm", "pack_filter_igemm_bf16", "pack_filter_igemm_f16x3",
-           "infer_layout", "to_layout", "empty_act", "query", "last_launch_count"]
+           "infer_layout", "to_layout", "maxpool2x2", "empty_act", "query", "last_launch_count"]
 
 
 def _strides_for(layout: str, n: int, c: int, h: int, w: int) -> tuple[int, int, int, int]:
@@ -55,13 +55,36 @@ def empty_act(n: int, c: int, h: int, w: int, layout: str = "CHW",
                                device=device, dtype=dtype)
 
 
-def to_layout(x: torch.Tensor, layout: str) -> torch.Tensor:
-    """Copy ``x`` into ``layout`` (a separate, explicitly requested staging step)."""
-    if infer_layout(x) == layout:
+def to_layout(x: torch.Tensor, layout: str, stream=None) -> torch.Tensor:
+    """Copy ``x`` into ``layout`` (a separate, explicitly requested staging step).
+
+    CUDA fp32 NCHW <-> NHWC goes through the library's transpose kernels
+    (``convio_nchw_to_nhwc`` / ``convio_nhwc_to_nchw``: a counted launch, one read
+    and one write of every element); other cases (the CWH axis, host tensors) are
+    a framework copy."""
+    src = infer_layout(x)
+    if src == layout:
         return x
     y = empty_act(*x.shape, layout=layout, device=x.device, dtype=x.dtype)
+    if x.is_cuda and x.dtype == torch.float32 and {src, layout} == {"CHW", "HWC"} and x.numel():
+        n, c, h, w = x.shape
+        fn = N.lib().convio_nchw_to_nhwc if layout == "HWC" else N.lib().convio_nhwc_to_nchw
+        N.check(fn(_ptr(x), _ptr(y), n, c, h, w, _stream_ptr(stream)), "to_layout")
+        return y
     y.copy_(x)
     return y
+
+
+def maxpool2x2(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """2x2 / stride-2 max pooling of a channels-last (HWC) activation."""
+    _check_tensor(x, "x")
+    if infer_layout(x) != "HWC":
+        raise ValueError("maxpool2x2 needs a channels-last (HWC) input")
+    n, c, h, w = x.shape
+    if out is None:
+        out = empty_act(n, c, h // 2, w // 2, "HWC", device=x.device)
+    N.check(N.lib().convio_maxpool2x2_nhwc(_ptr(x), _ptr(out), n, h, w, c, _stream_ptr(stream)), "maxpool2x2")
+    return out
 
 
 def _check_tensor(t: torch.Tensor, name: str) -> None:

@@ -173,6 +173,9 @@ class ConvLayer:
         self._ws = None
         self._run_ws = None
         self.launches = 0
+        # fused epilogue of a network layer (network.py): bias per output channel, ReLU
+        self.bias: torch.Tensor | None = None
+        self.relu = False
 
     @property
     def precision(self) -> str | None:
@@ -245,32 +248,32 @@ class ConvLayer:
                                            dtype=torch.uint8)
             y = C.conv_winograd_tc(x, self.weight, e=self.e, padding=s.pad, tile=self.tile,
                                    precision=self.precision, out=out, stream=stream,
-                                   u=self._ws, workspace=self._run_ws)
+                                   u=self._ws, workspace=self._run_ws, bias=self.bias, relu=self.relu)
         elif self.algorithm == "igemm_bf16":
             if self._run_ws is None or self._run_ws.device != x.device:
                 self._run_ws = torch.empty(2 * x.numel() + (1 << 20), device=x.device,
                                            dtype=torch.uint8)
             y = C.conv_igemm(x, self.weight, padding=s.pad, stride=s.stride, tile=self.tile,
                              precision="bf16", out=out, stream=stream, w_packed=self._ws,
-                             workspace=self._run_ws)
+                             workspace=self._run_ws, bias=self.bias, relu=self.relu)
         elif self.algorithm == "igemm_3xf16":
             if self._run_ws is None or self._run_ws.device != x.device:
                 self._run_ws = torch.empty(F16X3_PARTIALS_BYTES, device=x.device, dtype=torch.uint8)
             y = C.conv_igemm(x, self.weight, padding=s.pad, stride=s.stride, tile=self.tile,
                              precision="3xf16", out=out, stream=stream, w_packed=self._ws,
-                             workspace=self._run_ws)
+                             workspace=self._run_ws, bias=self.bias, relu=self.relu)
         elif self.algorithm == "winograd":
             u = self._ws.view(-1)
             y = C.conv_winograd(x, self.weight, e=self.e, padding=s.pad, tile=self.tile, out=out,
-                                stream=stream, u=u)
+                                stream=stream, u=u, bias=self.bias, relu=self.relu)
         elif self.algorithm.startswith("igemm"):
             y = C.conv_igemm_tf32(x, self.weight, padding=s.pad, tile=self.tile, out=out,
                                   stream=stream, w_packed=self._ws, stride=s.stride,
-                                  split=self.algorithm == "igemm_3xtf32")
+                                  split=self.algorithm == "igemm_3xtf32", bias=self.bias, relu=self.relu)
         else:
             wp = self._ws.view(s.c, s.r, s.r, s.k)
             y = C.conv_direct(x, self.weight, stride=s.stride, padding=s.pad, tile=self.tile,
-                              out=out, stream=stream, w_packed=wp)
+                              out=out, stream=stream, w_packed=wp, bias=self.bias, relu=self.relu)
         self.launches = C.last_launch_count()
         return y
 
