@@ -1,6 +1,9 @@
 """BASELINE config 5: lower-bound-pruned search vs exhaustive, on the device.
 
     python scripts/tuner_sweep.py [--n 8] [--budget 64] [--cap 6000] [--out FILE]
+    python scripts/tuner_sweep.py --engine igemm_3xf16 --n 32 --budget 16
+        (the shipped tensor-core kernels: I/O-pruned tcgen05 domain vs its
+         unpruned legal domain, device_tuner.tcgen05_space)
 
 For 10 MobileNet-v1 / SqueezeNet-1.1 / ResNet-50 layers:
   * unconstrained domain = divisor constraints and xyz <= s_b only
@@ -90,23 +93,38 @@ def main():
     ap.add_argument("--budget", type=int, default=64)
     ap.add_argument("--cap", type=int, default=6000)
     ap.add_argument("--seed", type=int, default=0)
-    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "tuner_sweep.json"))
+    ap.add_argument("--engine", default="ffma", choices=DT.ENGINES)
+    ap.add_argument("--out", default="")
     args = ap.parse_args()
+    args.out = args.out or os.path.join(ROOT, "gpurun_out", f"tuner_sweep_{args.engine}.json")
     warnings.simplefilter("ignore")
     DT.TIMING.update(target_ms=0.5, batches=3)
-    hw = b200_hw_model()
+    DT.set_engine(args.engine)
+    tc = args.engine != "ffma"
+    hw = DT.tcgen05_hw_model() if tc else b200_hw_model()
     rows = []
     for name, c, hw_in, k, r, stride, pad in LAYERS:
         DT.set_padding(pad)
         shape = shape_of(args.n, c, hw_in, hw_in, k, r, stride, pad)
-        pruned = DT.legal_projection(A.build_space(shape, hw, "direct", layouts=("CHW",)))
-        unc_full = unconstrained_space(shape, hw)
-        unc = DT.legal_projection(unc_full)
+        try:
+            if tc:
+                pruned = DT.tcgen05_space(shape, hw, args.engine)
+                unc = DT.tcgen05_space(shape, hw, args.engine, prune=None)
+            else:
+                pruned = DT.legal_projection(A.build_space(shape, hw, "direct", layouts=("CHW",)))
+                unc = DT.legal_projection(unconstrained_space(shape, hw))
+        except A.InfeasibleTileError as exc:
+            row = {"layer": name, "shape": str(shape), "error": str(exc)}
+            print(json.dumps(row), flush=True)
+            rows.append(row)
+            continue
         row = {"layer": name, "shape": str(shape),
                "unconstrained_legal": unc.size, "pruned_legal": pruned.size,
                "reduction_ratio": round(pruned.size / unc.size, 4),
-               "model_reduction_ratio": round(A.build_space(shape, hw, "direct", layouts=("CHW",))
-                                              .reduction_ratio, 4)}
+               "model_reduction_ratio": (round(unc.unconstrained_size and pruned.size / unc.unconstrained_size, 4)
+                                         if tc else
+                                         round(A.build_space(shape, hw, "direct", layouts=("CHW",))
+                                               .reduction_ratio, 4))}
         row["exhaustive_unconstrained"] = exhaustive(unc, args.cap, args.seed)
         row["exhaustive_pruned"] = exhaustive(pruned, args.cap, args.seed)
         t0 = time.time()
@@ -127,7 +145,8 @@ def main():
         rows.append(row)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as fh:
-        json.dump({"n": args.n, "budget": args.budget, "cap": args.cap, "layers": rows}, fh, indent=1)
+        json.dump({"n": args.n, "budget": args.budget, "cap": args.cap, "engine": args.engine,
+                   "layers": rows}, fh, indent=1)
     print(f"wrote {args.out}")
 
 
