@@ -413,10 +413,14 @@ def ffma_peak_tflops(torch, stream) -> float:
     return best
 
 
+PROFILE_ROUND = "r2"   # the committed evidence of the current round: profiles/r2/
+
+
 def load_profile_traffic() -> dict:
-    """DRAM bytes per launch from the committed ncu summaries (profiles/*.json)."""
+    """DRAM / L2 bytes per layer call from the committed ncu summaries
+    (profiles/<round>/*_traffic.json, written by scripts/run_layer.py --parse)."""
     out = {}
-    pdir = os.path.join(ROOT, "profiles")
+    pdir = os.path.join(ROOT, "profiles", PROFILE_ROUND)
     if not os.path.isdir(pdir):
         return out
     for fn in sorted(os.listdir(pdir)):
@@ -440,7 +444,7 @@ def _l2_measured(tab: dict, workload: str, layer: str, algorithm: str, n: int):
 
 def _traffic(tab: dict, workload: str, fam: dict, dom: str, n: int | None = None):
     """DRAM bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum, one capture
-    per layer call, committed under profiles/*_traffic.json) of the dominant family's
+    per layer call, committed under profiles/<round>/*_traffic.json) of the dominant family's
     layers: {layer: bytes}; None if no capture is committed."""
     alg = dom.split()[0]
     out = {}
@@ -1002,7 +1006,7 @@ def main() -> None:
                 b["measured_over_omega"] = round(m["l2_sm_read_bytes_per_call"] / b["omega_bytes"], 3)
                 b["measured_over_io_at_optimum"] = round(
                     m["l2_sm_read_bytes_per_call"] / b["io_at_optimum_bytes"], 3)
-                b["source"] = m.get("source", "committed ncu capture (profiles/*_traffic.json)")
+                b["source"] = m.get("source", f"committed ncu capture (profiles/{PROFILE_ROUND}/*_traffic.json)")
             else:
                 b["measured_l2_sm_read_bytes"] = None
             bounds_cache[key] = b

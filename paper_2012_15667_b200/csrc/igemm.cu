@@ -12,6 +12,10 @@
 
 namespace convio {
 
+#ifdef CONVIO_TRACE
+unsigned long long *g_trace_ptr = nullptr;   // dev builds: the pair kernel's pipeline trace
+#endif
+
 template <int KIND>
 static IgemmFn igemm_kernel_kind(int bn) {
     switch (bn) {
@@ -530,6 +534,14 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.fp_bytes = pl.fp_bytes;
         PP.a_slot = pl.a_slot;
         PP.na = pl.na;
+        PP.trace = nullptr;
+#ifdef CONVIO_TRACE
+        static unsigned long long *d_trace = nullptr;
+        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 8 * 1024 * sizeof(unsigned long long)));
+        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 8 * 1024 * sizeof(unsigned long long), stream));
+        PP.trace = d_trace;
+        g_trace_ptr = d_trace;
+#endif
         if (PP.g.splits > 1)   // after a memset node: a plain stream dependency
             pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
         else
@@ -680,6 +692,17 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
     }
     return launch_pack_filter_f16x3(desc, w, w_packed, (cudaStream_t)stream);
 }
+
+#ifdef CONVIO_TRACE
+// dev builds only: copy the last pair-kernel pipeline trace (8 x 1024 clock64 stamps)
+int convio_dev_trace(unsigned long long *host) {
+    if (!g_trace_ptr) return CONVIO_EINVAL;
+    return cudaMemcpy(host, g_trace_ptr, 8 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+                   cudaSuccess
+               ? CONVIO_OK
+               : CONVIO_EINTERNAL;
+}
+#endif
 
 int64_t convio_pack_filter_igemm_f16x3_bytes(const convio_conv_desc *desc) {
     if (!desc) return -1;

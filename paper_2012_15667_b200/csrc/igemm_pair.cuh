@@ -62,7 +62,23 @@ struct PairParams {
     int fp_bytes;
     int a_slot;
     int na;                 // footprint slots
+    unsigned long long *trace;   // CONVIO_TRACE builds: per-role clock64 stamps of cluster 0
 };
+
+// Pipeline trace (dev builds with -DCONVIO_TRACE): the leader CTA of cluster 0
+// stamps clock64() at each role's hand-off points into trace[row][i] (row: 0
+// producer may issue k-block i, 1 converter saw its data, 2 converter done, 3 MMA
+// issuer saw it converted, 4 MMAs issued, 5 epilogue saw accumulator i, 6 drained)
+#ifdef CONVIO_TRACE
+#define PAIR_TRACE(row, i)                                                                      \
+    do {                                                                                        \
+        if (PP.trace && blockIdx.x == 0 && (i) < 1024) PP.trace[(row) * 1024 + (i)] = clock64(); \
+    } while (0)
+#else
+#define PAIR_TRACE(row, i) \
+    do {                   \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
@@ -514,6 +530,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         }
                     }
                     if (it >= NS) mbar_wait(empty + s, ph ^ 1);
+                    PAIR_TRACE(0, it);
                     const int r = tap / P.ks, sx = tap - r * P.ks;
                     uint8_t *a = bring + s * STAGE;
                     uint8_t *b = HALO ? a : a + A_BYTES;
@@ -569,7 +586,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         if (leader && lane == 0) {
             // ---- MMA issuer (leader CTA, one thread) -----------------------------------
             constexpr uint32_t idesc = idesc_m256<BN, KIND>();
-            int s = 0, sa = 0, ta = 0, l = 0;
+            int s = 0, sa = 0, ta = 0, l = 0, kbc = 0;
             uint32_t ph = 0, pha = 0, pht = 0;
             int t = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
@@ -584,6 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int kb = kb_lo; kb < kb_hi; ++kb) {
                     if constexpr (TSA) {
                         mbar_wait_cluster(tconv + ta, pht);
+                        PAIR_TRACE(3, kbc);
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                         const uint32_t b = smem_u32(bring + s * STAGE) + A_BYTES;
                         // 3xTF32 stage [A | B | B_lo]; 3xF16C [A0 | B_hi | A1 | B_lo]
@@ -607,6 +625,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         }
                         umma_commit_pair(empty + s);
                         umma_commit_pair(tfree + ta);
+                        PAIR_TRACE(4, kbc);
+                        ++kbc;
                         if (++ta == NTA) {
                             ta = 0;
                             pht ^= 1;
@@ -624,6 +644,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     }
                     if constexpr (SPLIT) mbar_wait_cluster(conv + s, ph);
                     else mbar_wait(full + s, ph);   // F16X3: all four planes by TMA
+                    PAIR_TRACE(3, kbc);
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     const uint32_t st = smem_u32(bring + s * STAGE);
                     uint32_t a, b;
@@ -666,6 +687,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                                             !(first && kk == 0));
                     }
                     umma_commit_pair(empty + s);
+                    PAIR_TRACE(4, kbc);
+                    ++kbc;
                     if constexpr (LOSLOT) {
                         umma_commit_pair(lofree + l);   // lo slot consumed
                         if (++l == NL) l = 0;
@@ -701,6 +724,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             const bool lead_split = krange(item, kb_lo, kb_hi) == 0;
             const int acc = NACC == 2 ? (t & 1) : 0;
             mbar_wait(tfull + acc, (t / NACC) & 1);
+            if (q == 0 && lane == 0) PAIR_TRACE(5, t);
             __syncwarp();
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const int blk = pair * 2 + (int)rank;
@@ -811,6 +835,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
+            if (q == 0 && lane == 0) PAIR_TRACE(6, t);
         }
     } else if (TSA && F16C && warp >= 8) {
         // ---- 3xF16C TSA converters: warp (q, h) owns TMEM lanes 32q..32q+31 = A rows and
@@ -829,6 +854,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                 mbar_wait(full + s, ph);
                 if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
+                if (warp == 8 && lane == 0) PAIR_TRACE(1, it);
                 const uint32_t st = smem_u32(bring + s * STAGE);
                 const uint32_t row = st + (h ? (uint32_t)(A_BYTES + B_BYTES) : 0u) + (uint32_t)m * 128;
                 uint32_t hw[16], lw[16];
@@ -849,6 +875,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 tmem_st_32x32b_x16(lane_base + ta_col, hw);
                 tmem_st_32x32b_x16(lane_base + ta_col + 32, lw);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                if (warp == 8 && lane == 0) PAIR_TRACE(2, it);
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tconv_leader + (uint32_t)(ta * 8));
@@ -922,7 +949,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const float sc = pow2f(f16c_act_exp(P.row_exp, P.nred, lane));
         const int a_rows = P.bx * P.by * P.imgs;
         const int fp_rows = PP.fp_bytes / 128;
-        int s = 0, sa = 0;
+        int s = 0, sa = 0, kbc = 0;
         uint32_t ph = 0, pha = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
             int tap = 0;
@@ -944,6 +971,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     }
                 }
                 mbar_wait(full + s, ph);
+                if (warp == 8 && lane == 0) PAIR_TRACE(1, kbc);
                 if constexpr (!HALO) {
                     const uint32_t st = smem_u32(bring + s * STAGE);
 #ifndef CONVIO_ABL_NOCONV
@@ -952,6 +980,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
                 __syncwarp();
+                if (warp == 8 && lane == 0) PAIR_TRACE(2, kbc);
+                ++kbc;
                 if (lane == 0) mbar_arrive_cluster(conv_leader + (uint32_t)(s * 8));
                 if (HALO && ++tap == taps) tap = 0;
                 if (++s == NS) {

@@ -11,13 +11,15 @@
 
 using namespace convio;
 
-template <int NN, int KIND, bool TS>
+// PAT = 0: one operand pair; PAT = 1: the 3-product split pattern of the conv kernels
+// (hi*lo, lo*hi, hi*hi with distinct A / B planes per product)
+template <int NN, int KIND, bool TS, int PAT = 0>
 __global__ void __cluster_dims__(2, 1, 1) k_rate(long long *cycles, int iters) {
     extern __shared__ __align__(1024) uint8_t raw[];
     uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *a = sm;                       // 128 x 128 B
-    uint8_t *b = sm + 128 * 128;           // NN/2 x 128 B
-    uint64_t *done = reinterpret_cast<uint64_t *>(b + 128 * 128);
+    uint8_t *a = sm;                       // 2 planes x 128 x 128 B
+    uint8_t *b = sm + 2 * 128 * 128;       // 2 planes x 128 x 128 B (NN/2 rows used)
+    uint64_t *done = reinterpret_cast<uint64_t *>(b + 2 * 128 * 128);
     uint32_t *slot = reinterpret_cast<uint32_t *>(done + 1);
     const int warp = threadIdx.x >> 5;
     const uint32_t rank = cluster_ctarank();
@@ -35,13 +37,24 @@ __global__ void __cluster_dims__(2, 1, 1) k_rate(long long *cycles, int iters) {
     const uint32_t tmem = *slot;
     if (rank == 0 && threadIdx.x == 0) {
         const uint64_t ad = umma_desc_sw128(smem_u32(a)), bd = umma_desc_sw128(smem_u32(b));
+        const uint64_t adl = umma_desc_sw128(smem_u32(a) + 128 * 128), bdl = umma_desc_sw128(smem_u32(b) + 128 * 128);
         constexpr uint32_t idesc = idesc_m256<NN, KIND>();
         const uint32_t ta = tmem + 256;    // A operand columns (TS)
         const long long t0 = clock64();
         for (int it = 0; it < iters; ++it)
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk) {
-                if constexpr (TS) {
+                if constexpr (PAT == 1) {
+                    if constexpr (TS) {
+                        umma_pair_ts_f16(tmem, ta + kk * 8, bdl + kk * 2, idesc, 1);
+                        umma_pair_ts_f16(tmem, ta + 32 + kk * 8, bd + kk * 2, idesc, 1);
+                        umma_pair_ts_f16(tmem, ta + kk * 8, bd + kk * 2, idesc, 1);
+                    } else {
+                        umma_pair<KIND>(tmem, ad + kk * 2, bdl + kk * 2, idesc, 1);
+                        umma_pair<KIND>(tmem, adl + kk * 2, bd + kk * 2, idesc, 1);
+                        umma_pair<KIND>(tmem, ad + kk * 2, bd + kk * 2, idesc, 1);
+                    }
+                } else if constexpr (TS) {
                     if constexpr (KIND == KIND_3XF16C) umma_pair_ts_f16(tmem, ta + kk * 8, bd + kk * 2, idesc, 1);
                     else umma_pair_ts_tf32(tmem, ta + kk * 8, bd + kk * 2, idesc, 1);
                 } else {
@@ -50,7 +63,7 @@ __global__ void __cluster_dims__(2, 1, 1) k_rate(long long *cycles, int iters) {
             }
         umma_commit_pair(done);
         mbar_wait(done, 0);
-        *cycles = (clock64() - t0) / (4LL * iters);
+        *cycles = (clock64() - t0) / ((PAT ? 12LL : 4LL) * iters);
     } else if (rank == 1 && threadIdx.x == 0) {
         mbar_wait(done, 0);
     }
@@ -60,16 +73,17 @@ __global__ void __cluster_dims__(2, 1, 1) k_rate(long long *cycles, int iters) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
 
-template <int NN, int KIND, bool TS>
+template <int NN, int KIND, bool TS, int PAT = 0>
 static void rate(long long *dcyc) {
-    const size_t smem = 1024 + 2 * 128 * 128 + 64;
-    cudaFuncSetAttribute(k_rate<NN, KIND, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = 1024 + 4 * 128 * 128 + 64;
+    cudaFuncSetAttribute(k_rate<NN, KIND, TS, PAT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     long long cyc = 0;
-    k_rate<NN, KIND, TS><<<2, 128, smem>>>(dcyc, 4096);
+    k_rate<NN, KIND, TS, PAT><<<2, 128, smem>>>(dcyc, 4096);
     cudaError_t e = cudaDeviceSynchronize();
     cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
-    printf("pair M256 N%3d %s %s: %lld cycles per MMA (K = 32 B) %s\n", NN,
-           KIND == KIND_3XF16C ? "f16 " : "tf32", TS ? "A in TMEM" : "A in smem", cyc,
+    printf("pair M256 N%3d %s %s%s: %lld cycles per MMA (K = 32 B) %s\n", NN,
+           KIND == KIND_3XF16C ? "f16 " : "tf32", TS ? "A in TMEM" : "A in smem",
+           PAT ? " 3-product split pattern" : "", cyc,
            e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
@@ -87,5 +101,11 @@ int main() {
     rate<128, KIND_3XF16C, true>(dcyc);
     rate<256, KIND_3XF16C, true>(dcyc);
     rate<128, KIND_TF32, true>(dcyc);
+    rate<64, KIND_3XF16C, false, 1>(dcyc);
+    rate<128, KIND_3XF16C, false, 1>(dcyc);
+    rate<192, KIND_3XF16C, false, 1>(dcyc);
+    rate<256, KIND_3XF16C, false, 1>(dcyc);
+    rate<128, KIND_3XF16C, true, 1>(dcyc);
+    rate<256, KIND_3XF16C, true, 1>(dcyc);
     return 0;
 }

@@ -4,7 +4,7 @@ for the per-launch DRAM traffic that bench.py reports as ``roofline.traffic``.
     ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
         --csv --log-file gpurun_out/traffic_res4.csv \
         python scripts/run_layer.py --workload resnet50 --layer res4_3x3
-    python scripts/run_layer.py --parse gpurun_out/traffic_*.csv --out profiles/r1_resnet50_traffic.json
+    python scripts/run_layer.py --parse gpurun_out/traffic_*.csv --out profiles/r2/r2_resnet50_traffic.json
 """
 
 import argparse
