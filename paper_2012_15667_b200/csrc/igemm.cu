@@ -49,9 +49,17 @@ static PairFn pair_kernel_h(int bn, int kind) {
     return pair_kernel_kind<KIND_TF32, HALO>(bn);
 }
 
-// fold: halo + S taps per MMA, N = 3 K (K = 64 -> N = 192)
-static PairFn pair_kernel_fold(int n, int kind) {
+// fold: halo + S taps per MMA, N = 3 K (K = 64 -> N = 192); 3xF16C may take the
+// A operand in TMEM (tsa, the converters apply the row shift) with the filter
+// resident in shared memory (resb)
+static PairFn pair_kernel_fold(int n, int kind, bool tsa = false, bool resb = false) {
     if (n != 192) return nullptr;
+    if (tsa) {
+        if (kind != KIND_3XF16C) return nullptr;
+        return resb ? &igemm_pair_kernel<192, KIND_3XF16C, true, true, true, true>
+                    : &igemm_pair_kernel<192, KIND_3XF16C, true, true, true, false>;
+    }
+    if (resb) return nullptr;
     if (kind == KIND_3XF16C) return &igemm_pair_kernel<192, KIND_3XF16C, true, false, true>;
     if (kind == KIND_3XTF32) return &igemm_pair_kernel<192, KIND_3XTF32, true, false, true>;
     if (kind == KIND_BF16) return &igemm_pair_kernel<192, KIND_BF16, true, false, true>;
@@ -60,8 +68,13 @@ static PairFn pair_kernel_fold(int n, int kind) {
 
 // tsa: 3xTF32 with the A operand in tensor memory (BN <= 128, no halo)
 static PairFn pair_kernel(int bn, int kind, bool halo, bool tsa) {
+    if (tsa && kind == KIND_3XF16C && halo) {   // halo footprint, converters shift rows into TMEM
+        if (bn == 64) return &igemm_pair_kernel<64, KIND_3XF16C, true, true>;
+        if (bn == 128) return &igemm_pair_kernel<128, KIND_3XF16C, true, true>;
+        if (bn == 256) return &igemm_pair_kernel<256, KIND_3XF16C, true, true>;
+        return nullptr;
+    }
     if (tsa && kind == KIND_3XF16C) {   // 3xF16C, A in TMEM (BN = 256: one accumulator)
-        if (halo) return nullptr;
         if (bn == 64) return &igemm_pair_kernel<64, KIND_3XF16C, false, true>;
         if (bn == 128) return &igemm_pair_kernel<128, KIND_3XF16C, false, true>;
         if (bn == 256) return &igemm_pair_kernel<256, KIND_3XF16C, false, true>;
@@ -221,10 +234,11 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
     if (pair) {
         // persistent pair: one CTA per SM, the whole shared memory is the ring
         // (halo: two footprint slots first, the filter stages in the rest)
-        PairFn pfn = pl->fold ? pair_kernel_fold(bn, kind) : pair_kernel(bn, kind, pl->halo, pl->tsa);
+        PairFn pfn = pl->fold ? pair_kernel_fold(bn, kind, pl->tsa, pl->resb_slots > 0)
+                              : pair_kernel(bn, kind, pl->halo, pl->tsa);
         if (!pfn)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE,
-                         pl->tsa ? "A-in-TMEM tiles need 3xTF32 (z in {64, 128}) or 3xF16, no halo"
+                         pl->tsa ? "A-in-TMEM tiles need 3xTF32 (z in {64, 128}, no halo) or 3xF16"
                                  : "tcgen05 tiles need z in {64, 128, 256}, got %d", bn);
         const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16 || kind == KIND_3XF16C) ? 2 : 1;
         // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
@@ -241,6 +255,11 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         int stages = (int)std::min<size_t>(16, (budget - a_ring) / stage_bytes);
         if (const char *cap = getenv("CONVIO_DEV_MAX_STAGES"))   // dev knob: ring-depth sensitivity
             stages = std::max(2, std::min(stages, atoi(cap)));
+        if (pl->resb_slots > 0) {   // resident filter: exactly one slot per k-block
+            if (a_ring + (size_t)pl->resb_slots * stage_bytes > budget)
+                return pfail(reason, rlen, CONVIO_EINFEASIBLE, "resident filter slice does not fit");
+            stages = pl->resb_slots;
+        }
         if (stages < 2)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair ring does not fit");
         pl->P.stages = stages;
@@ -322,9 +341,10 @@ static int finish_pair_grid(IgemmPlan *pl) {
 // P % y) are zero-filled by TMA and masked in the epilogue.
 static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
                            size_t rlen, int kind, int p, int q) {
-    if (t->n_yt != 1 || t->n_zt != 2)
+    if (t->n_yt != 1 || (t->n_zt != 2 && !(t->n_zt == 4 && kind == KIND_3XF16C)))
         return pfail(reason, rlen, CONVIO_EINFEASIBLE,
-                     "halo-staged tcgen05 tiles take n_xt = 2, n_yt = 1, n_zt = 2 (CTA pair)");
+                     "halo-staged tcgen05 tiles take n_xt = 2, n_yt = 1, n_zt = 2 (CTA pair; "
+                     "3xF16 also n_zt = 4: A operand in TMEM)");
     if (d->stride != 1)
         return pfail(reason, rlen, CONVIO_EINFEASIBLE, "halo staging needs stride 1");
     const int fpr = t->x + d->s - 1;
@@ -346,6 +366,15 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
     pl->fp_bytes = fp_rows * 128;
     pl->a_slot = ((fp_rows + d->s - 1) * 128 + 1023) & ~1023;
     pl->na = 2;
+    pl->tsa = t->n_zt == 4;
+    // halo TSA fold with one n-block: the CTA's whole filter slice stays resident when
+    // it fits next to the footprint slots (ResNet-50 res2 / VGG conv1_2: 3 x 24 KB)
+    if (pl->tsa && pl->fold) {
+        const int kblocks = d->r * (d->c / kblock_channels(kind));
+        const size_t slice = (size_t)kblocks * (d->s * t->z / 2) * 128 * 2;
+        const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
+        if ((size_t)pl->na * pl->a_slot * 2 + slice <= budget) pl->resb_slots = kblocks;
+    }
     int rc = plan_ring(pl, pl->fold ? d->s * t->z : t->z, kind, t->s_b, true, reason, rlen);
     if (rc) return rc;
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
@@ -537,8 +566,8 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.trace = nullptr;
 #ifdef CONVIO_TRACE
         static unsigned long long *d_trace = nullptr;
-        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 8 * 1024 * sizeof(unsigned long long)));
-        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 8 * 1024 * sizeof(unsigned long long), stream));
+        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 16 * 1024 * sizeof(unsigned long long)));
+        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 16 * 1024 * sizeof(unsigned long long), stream));
         PP.trace = d_trace;
         g_trace_ptr = d_trace;
 #endif
@@ -606,7 +635,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
     out->grid_z = pl.grid.z;
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages%s",
-             kind_name(kind), pl.fold ? " CTA pair (persistent, halo footprint, 3 taps per MMA)" : pl.halo ? " CTA pair (persistent, halo-staged footprint)" : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
+             kind_name(kind), pl.fold ? (pl.tsa ? (pl.resb_slots ? " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA, resident filter)" : " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA)") : " CTA pair (persistent, halo footprint, 3 taps per MMA)") : pl.halo ? (pl.tsa ? " CTA pair (persistent, halo footprint shifted into TMEM)" : " CTA pair (persistent, halo-staged footprint)") : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages,
              pl.P.splits > 1 ? ", split-K" : "");
     return CONVIO_OK;
@@ -697,7 +726,7 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
 // dev builds only: copy the last pair-kernel pipeline trace (8 x 1024 clock64 stamps)
 int convio_dev_trace(unsigned long long *host) {
     if (!g_trace_ptr) return CONVIO_EINVAL;
-    return cudaMemcpy(host, g_trace_ptr, 8 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+    return cudaMemcpy(host, g_trace_ptr, 16 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                    cudaSuccess
                ? CONVIO_OK
                : CONVIO_EINTERNAL;

@@ -72,7 +72,7 @@ struct PairParams {
 #ifdef CONVIO_TRACE
 #define PAIR_TRACE(row, i)                                                                      \
     do {                                                                                        \
-        if (PP.trace && blockIdx.x == 0 && (i) < 1024) PP.trace[(row) * 1024 + (i)] = clock64(); \
+        if (PP.trace && blockIdx.x < 2 && (i) < 1024) PP.trace[((row) + 8 * blockIdx.x) * 1024 + (i)] = clock64(); \
     } while (0)
 #else
 #define PAIR_TRACE(row, i) \
@@ -110,6 +110,34 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 // wait on a barrier that the peer CTA also arrives on (default acquire, as the
 // CUTLASS 2-SM consumer waits)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
+
+// one lane of the (converged) warp: tcgen05.mma / commit are issued once per warp
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred;
+    asm volatile(
+        "{\n.reg .pred P;\n"
+        "elect.sync _|P, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, P;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
+// Non-blocking probe of a barrier phase.  The MMA issuer probes the NEXT k-block's
+// barrier while the current k-block's MMAs drain: a blocking wait between
+// k-blocks costs ~130-230 issue cycles even on a completed phase, long enough to
+// empty the tensor core's short MMA queue at N = 128 (64 -> 83 cycles per MMA,
+// scripts/dev/umma_contention_probe.cu).
+__device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n.reg .pred P1;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n}\n"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 
 // TMA load whose completion is signalled on the LEADER CTA's barrier (peer bit cleared)
 __device__ __forceinline__ void tma_load_4d_pair(void *dst, uint64_t map, int c0, int c1, int c2, int c3,
@@ -343,7 +371,14 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return 
 // by s rows (warp shuffles: the s-shift stays inside a footprint row).  R MMAs
 // of N = 192 per channel block instead of R*S of N = 64 (48 cycles each on the
 // tensor core: 67 % of its rate at N = 64).
-template <int BN, int KIND, bool HALO, bool TSA, bool FOLD = false>
+// HALO + TSA (3xF16C): the converter warps apply the tap shift themselves -- lane m
+// of tap (r, s) reads footprint row m + r * fpr + s from the fp32 footprint slot,
+// splits it and tcgen05.st's the hi / lo pair into an A slot of TMEM -- so the
+// footprint crosses L2 once per channel block (halo) while the tensor core reads
+// only the filter from shared memory (TSA).  RESB (halo TSA, one n-block): the
+// CTA's whole filter slice is staged ONCE at kernel start (the ring holds
+// kblocks filter slots) and only footprints stream per work item.
+template <int BN, int KIND, bool HALO, bool TSA, bool FOLD = false, bool RESB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND, TSA>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
                       const __grid_constant__ CUtensorMap tm_w) {
@@ -360,7 +395,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     // converters -- and the epilogue undoes the power-of-two row / column scales
     constexpr bool F16X3 = KIND == KIND_3XF16;
     static_assert(!F16X3 || (!HALO && !TSA && !FOLD), "3xF16: plain pair tiles");
-    static_assert(!F16C || !TSA || !HALO, "3xF16C with A in TMEM: no halo");
+    static_assert(!(TSA && HALO) || F16C, "halo tiles with A in TMEM: 3xF16C only");
+    static_assert(!RESB || (TSA && HALO), "resident filter: halo tiles with A in TMEM");
     constexpr int HB = BN / 2;                        // filter rows staged per CTA
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = HB * 128;
@@ -368,10 +404,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr int CB = (KIND == KIND_BF16 || F16X3 || F16C) ? 64 : 32;   // channels per k-block
     // TSA (3xTF32, BN <= 128): A_hi / A_lo live in TMEM columns after the two
     // accumulators, NTA k-block slots of 64 columns (32 hi + 32 lo)
-    static_assert(!TSA || (SPLIT && !HALO && (BN <= 128 || F16C)), "TSA: 3xTF32 / 3xF16C, no halo");
+    static_assert(!TSA || (SPLIT && (!HALO || F16C) && (BN <= 128 || F16C)), "TSA: 3xTF32 / 3xF16C");
     // accumulator buffers: 2 (the epilogue drains one while the MMAs fill the other),
     // 1 for 3xF16C TSA at BN = 256 (its 256 columns + 4 A slots fill the 512)
-    constexpr int NACC = (TSA && BN > 128) ? 1 : 2;
+    // (FOLD's N = 192 keeps two: 384 columns + 2 A slots)
+    constexpr int NACC = (TSA && BN > 128 && !FOLD) ? 1 : 2;
     // (power-of-two allocation; FOLD's 2 x 192 columns take 512)
     constexpr uint32_t TMEM_COLS = (TSA || 2 * BN > 256) ? 512 : (2 * BN < 32 ? 32 : 2 * BN);
     constexpr uint32_t A_COL0 = NACC * BN;
@@ -417,7 +454,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofree + NL);
 
     const int tid = threadIdx.x;
-    const int warp = tid >> 5, lane = tid & 31;
+    // warp index through a shuffle: the compiler then knows it is warp-uniform
+    const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0), lane = tid & 31;
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
     const int cluster_id = blockIdx.x >> 1;
@@ -435,7 +473,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 8);
             mbar_init(afull + a, 1);
-            mbar_init(aempty + a, 1);
+            mbar_init(aempty + a, (TSA && HALO) ? NCW : 1);   // halo TSA: the converters read it
             mbar_init(aconv + a, 2 * NCW);
         }
         for (int l = 0; l < NL && LOSLOT; ++l) mbar_init(lofree + l, 1);
@@ -494,6 +532,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             int s = 0, sa = 0;
             uint32_t ph = 0, pha = 0;
             int it = 0, ita = 0;
+            if constexpr (RESB) {   // the CTA's filter slice, once: slot cb * taps + tap (halo order)
+                mbar_arrive_expect_tx(full, (uint32_t)(P.kblocks * STAGE));
+                for (int cb = 0, slot = 0; cb < P.cblocks; ++cb)
+                    for (int tap = 0; tap < taps; ++tap, ++slot) {
+                        uint8_t *b = bring + slot * STAGE;
+                        if (FOLD) {
+                            const int frow = tap * P.ks * P.k + (int)rank * HB;
+                            tma_load_2d(b, map_w, cb * CB, frow, full);
+                            tma_load_2d(b + B_BYTES, map_w, cb * CB, frow + lo_tap * P.k, full);
+                        } else {
+                            tma_load_3d(b, map_w, cb * CB, (int)rank * HB, tap, full);
+                            tma_load_3d(b + B_BYTES, map_w, cb * CB, (int)rank * HB, tap + lo_tap, full);
+                        }
+                    }
+            }
             for (int item = cluster_id; item < PP.items; item += nclusters) {
                 int grp, pair, nb;
                 decode(item, grp, pair, nb);
@@ -529,6 +582,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             pha ^= 1;
                         }
                     }
+                    if constexpr (!RESB) {
                     if (it >= NS) mbar_wait(empty + s, ph ^ 1);
                     PAIR_TRACE(0, it);
                     const int r = tap / P.ks, sx = tap - r * P.ks;
@@ -565,6 +619,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             tma_load_3d_pair(b + A_BYTES + B_BYTES, map_w, cb * CB, n0, wc + P.n, full + s);
                         }
                     }
+                    if (++s == NS) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                    }   // !RESB
                     // halo: channel block outer, taps inner (footprint reused by all taps)
                     if (HALO) {
                         if (++tap == taps) {
@@ -575,16 +634,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         cb = 0;
                         ++tap;
                     }
-                    if (++s == NS) {
-                        s = 0;
-                        ph ^= 1;
-                    }
                 }
             }
         }
     } else if (warp == 1) {
-        if (leader && lane == 0) {
-            // ---- MMA issuer (leader CTA, one thread) -----------------------------------
+        if (leader) {
+            // ---- MMA issuer (leader CTA): the whole warp runs the loop, so descriptors and
+            // counters stay warp-uniform (uniform registers); one elected lane issues.  A
+            // single-lane issuer made the compiler wrap every tcgen05.mma in an ELECT +
+            // 4 x R2UR.BROADCAST loop, ~90 issue cycles per MMA: slower than an N = 128 MMA
+            // (64 cycles), so the tensor core starved ----------------------------------
             constexpr uint32_t idesc = idesc_m256<BN, KIND>();
             int s = 0, sa = 0, ta = 0, l = 0, kbc = 0;
             uint32_t ph = 0, pha = 0, pht = 0;
@@ -603,35 +662,43 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         mbar_wait_cluster(tconv + ta, pht);
                         PAIR_TRACE(3, kbc);
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                        const uint32_t b = smem_u32(bring + s * STAGE) + A_BYTES;
-                        // 3xTF32 stage [A | B | B_lo]; 3xF16C [A0 | B_hi | A1 | B_lo]
+                        // 3xTF32 stage [A | B | B_lo]; 3xF16C [A0 | B_hi | A1 | B_lo]; halo [B_hi | B_lo]
+                        // (RESB: filter slot kb of the resident slice)
+                        const uint32_t b = smem_u32(bring + (RESB ? kb : s) * STAGE) + (HALO ? 0 : A_BYTES);
                         const uint64_t bd = umma_desc_sw128(b),
-                                       bdl = umma_desc_sw128(b + (F16C ? A_BYTES + B_BYTES : B_BYTES));
+                                       bdl = umma_desc_sw128(b + ((F16C && !HALO) ? A_BYTES + B_BYTES : B_BYTES));
                         const uint32_t ahi = tmem + A_COL0 + (uint32_t)(ta * 64);
                         const bool first = kb == kb_lo;
+                        if (elect_one()) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t o = (uint64_t)(kk * 2);
-                            const uint32_t ak = ahi + (uint32_t)(kk * 8);
-                            if constexpr (F16C) {
-                                umma_pair_ts_f16(d, ak, bdl + o, idesc, !(first && kk == 0));
-                                umma_pair_ts_f16(d, ak + 32, bd + o, idesc, 1);
-                                umma_pair_ts_f16(d, ak, bd + o, idesc, 1);
-                            } else {
-                                umma_pair_ts_tf32(d, ak, bdl + o, idesc, !(first && kk == 0));
-                                umma_pair_ts_tf32(d, ak + 32, bd + o, idesc, 1);
-                                umma_pair_ts_tf32(d, ak, bd + o, idesc, 1);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t o = (uint64_t)(kk * 2);
+                                const uint32_t ak = ahi + (uint32_t)(kk * 8);
+#ifdef CONVIO_ABL_1MMA   // ablation (timing only, wrong numerics): hi*hi alone
+                                umma_pair_ts_f16(d, ak, bd + o, idesc, !(first && kk == 0));
+                                continue;
+#endif
+                                if constexpr (F16C) {
+                                    umma_pair_ts_f16(d, ak, bdl + o, idesc, !(first && kk == 0));
+                                    umma_pair_ts_f16(d, ak + 32, bd + o, idesc, 1);
+                                    umma_pair_ts_f16(d, ak, bd + o, idesc, 1);
+                                } else {
+                                    umma_pair_ts_tf32(d, ak, bdl + o, idesc, !(first && kk == 0));
+                                    umma_pair_ts_tf32(d, ak + 32, bd + o, idesc, 1);
+                                    umma_pair_ts_tf32(d, ak, bd + o, idesc, 1);
+                                }
                             }
+                            if constexpr (!RESB) umma_commit_pair(empty + s);
+                            umma_commit_pair(tfree + ta);
                         }
-                        umma_commit_pair(empty + s);
-                        umma_commit_pair(tfree + ta);
+                        __syncwarp();
                         PAIR_TRACE(4, kbc);
                         ++kbc;
                         if (++ta == NTA) {
                             ta = 0;
                             pht ^= 1;
                         }
-                        if (++s == NS) {
+                        if (!RESB && ++s == NS) {
                             s = 0;
                             ph ^= 1;
                         }
@@ -659,43 +726,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const uint64_t ad = HALO ? umma_desc_sw128_row(a) : umma_desc_sw128(a);
                     const uint64_t bd = umma_desc_sw128(b);
                     const bool first = kb == kb_lo;
+                    const uint32_t lo = smem_u32(loring + l * LO_SLOT);
+                    const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : (LOSLOT ? lo : a + A_BYTES + B_BYTES);
+                    const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : (LOSLOT ? lo + A_BYTES : b + A_BYTES + B_BYTES);
+                    const uint64_t adl = HALO ? umma_desc_sw128_row(alo) : umma_desc_sw128(alo);
+                    const uint64_t bdl = umma_desc_sw128(blo);
+                    if (elect_one()) {
 #ifdef CONVIO_ABL_1MMA   // ablation (timing only, wrong numerics): hi*hi alone
-                    if constexpr (F16C) {
+                        if constexpr (F16C) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                                            !(first && kk == 0));
-                    } else
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                                                !(first && kk == 0));
+                        } else
 #endif
-                    if constexpr (SPLIT || F16X3) {
-                        const uint32_t lo = smem_u32(loring + l * LO_SLOT);
-                        const uint32_t alo = HALO ? a + (uint32_t)PP.a_slot : (LOSLOT ? lo : a + A_BYTES + B_BYTES);
-                        const uint32_t blo = HALO ? b + (uint32_t)B_BYTES : (LOSLOT ? lo + A_BYTES : b + A_BYTES + B_BYTES);
-                        const uint64_t adl = HALO ? umma_desc_sw128_row(alo) : umma_desc_sw128(alo);
-                        const uint64_t bdl = umma_desc_sw128(blo);
+                        if constexpr (SPLIT || F16X3) {
 #pragma unroll
-                        for (int kk = 0; kk < 4; ++kk) {
-                            const uint64_t o = (uint64_t)(kk * 2);
-                            umma_pair<KIND>(d, ad + o, bdl + o, idesc, !(first && kk == 0));
-                            umma_pair<KIND>(d, adl + o, bd + o, idesc, 1);
-                            umma_pair<KIND>(d, ad + o, bd + o, idesc, 1);
+                            for (int kk = 0; kk < 4; ++kk) {
+                                const uint64_t o = (uint64_t)(kk * 2);
+                                umma_pair<KIND>(d, ad + o, bdl + o, idesc, !(first && kk == 0));
+                                umma_pair<KIND>(d, adl + o, bd + o, idesc, 1);
+                                umma_pair<KIND>(d, ad + o, bd + o, idesc, 1);
+                            }
+                        } else {
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
+                                                !(first && kk == 0));
                         }
-                    } else {
-#pragma unroll
-                        for (int kk = 0; kk < 4; ++kk)
-                            umma_pair<KIND>(d, ad + (uint64_t)(kk * 2), bd + (uint64_t)(kk * 2), idesc,
-                                            !(first && kk == 0));
+                        umma_commit_pair(empty + s);
+                        if constexpr (LOSLOT) umma_commit_pair(lofree + l);   // lo slot consumed
+                        if (HALO && tap + 1 == taps)
+                            umma_commit_pair(aempty + sa);   // footprint consumed by all taps
                     }
-                    umma_commit_pair(empty + s);
+                    __syncwarp();
                     PAIR_TRACE(4, kbc);
                     ++kbc;
                     if constexpr (LOSLOT) {
-                        umma_commit_pair(lofree + l);   // lo slot consumed
                         if (++l == NL) l = 0;
                     }
                     if (HALO && ++tap == taps) {
                         tap = 0;
-                        umma_commit_pair(aempty + sa);   // footprint consumed by all taps
                         if (++sa == NA) {
                             sa = 0;
                             pha ^= 1;
@@ -706,7 +777,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         ph ^= 1;
                     }
                 }
-                umma_commit_pair(tfull + acc);
+                if (elect_one()) umma_commit_pair(tfull + acc);
+                __syncwarp();
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -839,28 +911,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         }
     } else if (TSA && F16C && warp >= 8) {
         // ---- 3xF16C TSA converters: warp (q, h) owns TMEM lanes 32q..32q+31 = A rows and
-        // channel half h (fp32 tile h of the stage); each thread splits its row's 32
-        // channels into scaled fp16 hi / lo pairs and tcgen05.st's them to the A slot ----
+        // channel half h (fp32 tile h of the stage / footprint); each thread splits its row's
+        // 32 channels into scaled fp16 hi / lo pairs and tcgen05.st's them to the A slot.
+        // Halo: the row is footprint row m + r * fpr + s of tap (r, s) ----
         const int q = warp & 3, h = (warp >> 2) & 1;
         const int m = q * 32 + lane;
         const uint32_t tconv_leader = mapa_shared(smem_u32(tconv), 0);
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(16 * h);
         const float sc = pow2f(f16c_act_exp(P.row_exp, P.nred, lane));
-        int s = 0, ta = 0, it = 0;
-        uint32_t ph = 0, pht = 0;
+        int s = 0, ta = 0, it = 0, sa = 0;
+        uint32_t ph = 0, pht = 0, pha = 0;
+        uint32_t fa = 0;
+        if constexpr (RESB) mbar_wait(full, 0);   // the resident filter slice has landed
         for (int item = cluster_id; item < PP.items; item += nclusters) {
             int kb_lo, kb_hi;
             krange(item, kb_lo, kb_hi);
+            int tap = 0;
             for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
-                mbar_wait(full + s, ph);
+                uint32_t row;
+                int sw;
+                if constexpr (HALO) {
+                    if (tap == 0) {
+                        mbar_wait(afull + sa, pha);
+                        fa = smem_u32(aring + sa * ASLOT);
+                    }
+                    // B of this tap landed (the MMA issuer learns it through tconv)
+                    if constexpr (!RESB) mbar_wait(full + s, ph);
+                    const int r = FOLD ? tap : tap / P.ks, sx = FOLD ? 0 : tap - r * P.ks;
+                    const int fr = m + r * PP.fpr + sx;
+                    row = fa + (h ? (uint32_t)PP.a_slot : 0u) + (uint32_t)fr * 128;
+                    sw = fr & 7;
+                } else {
+                    mbar_wait(full + s, ph);
+                    row = smem_u32(bring + s * STAGE) + (h ? (uint32_t)(A_BYTES + B_BYTES) : 0u) + (uint32_t)m * 128;
+                    sw = m & 7;
+                }
                 if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
                 if (warp == 8 && lane == 0) PAIR_TRACE(1, it);
-                const uint32_t st = smem_u32(bring + s * STAGE);
-                const uint32_t row = st + (h ? (uint32_t)(A_BYTES + B_BYTES) : 0u) + (uint32_t)m * 128;
                 uint32_t hw[16], lw[16];
+#ifdef CONVIO_ABL_NOCONV   // ablation (timing only, wrong numerics): no smem reads / split
+#pragma unroll
+                for (int c = 0; c < 16; ++c) hw[c] = lw[c] = row + c;
+                if (0)
+#endif
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {   // fp32 chunk c: channels 32h + 4c .. 4c + 3
-                    const float4 v = lds128(row + (uint32_t)((c ^ (m & 7)) << 4));
+                    const float4 v = lds128(row + (uint32_t)((c ^ sw) << 4));
                     const __half2 h0 = __floats2half2_rn(v.x * sc, v.y * sc);
                     const __half2 h1 = __floats2half2_rn(v.z * sc, v.w * sc);
                     const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
@@ -883,7 +979,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     ta = 0;
                     pht ^= 1;
                 }
-                if (++s == NS) {
+                if constexpr (HALO) {
+                    if (++tap == taps) {   // this warp is done reading the footprint
+                        tap = 0;
+                        if (lane == 0) mbar_arrive(aempty + sa);
+                        if (++sa == NA) {
+                            sa = 0;
+                            pha ^= 1;
+                        }
+                    }
+                }
+                if (!RESB && ++s == NS) {
                     s = 0;
                     ph ^= 1;
                 }

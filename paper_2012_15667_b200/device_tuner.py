@@ -306,7 +306,8 @@ def tcgen05_space(shape: ConvShape, hw: HwModel, engine: str,
     z in {64, 128, 256}; threads select the kernel -- (1,1,1) one CTA,
     (1,1,2) CTA pair, (1,1,4) pair with the split A operand in TMEM, (2,1,2)
     halo-staged footprint (stride 1; ``(x + S - 1) * y = 128``, x not
-    necessarily dividing Q); Winograd engines: x = y = e, z over the GEMM's N
+    necessarily dividing Q), (2,1,4) (3xF16) the halo footprint with the
+    converters shifting each tap's rows into TMEM; Winograd engines: x = y = e, z over the GEMM's N
     tiles, n_zt in {1, 2, 4}.  ``unconstrained_size`` counts the raw product of
     the axes; ``check_legal`` keeps only members with a device projection.
     ``prune`` (implicit GEMM): the I/O-model cut -- members whose modelled SM <-> L2
@@ -336,9 +337,10 @@ def tcgen05_space(shape: ConvShape, hw: HwModel, engine: str,
         if shape.stride == 1:
             for fpr in (8, 16, 32, 64, 128):
                 x_, y_ = fpr - shape.w_ker + 1, 128 // fpr
-                raw += len(zs)
+                nzts = (2, 4) if prec == "3xf16" else (2,)   # 4: footprint rows shifted into TMEM
+                raw += len(zs) * len(nzts)
                 if 1 <= x_ <= q + shape.w_ker - 1 and y_ <= p + shape.h_ker - 1 and x_ % 2 == 0:
-                    members += [TileConfig(x_, y_, z, 32768, 2, 1, 2, layout="HWC") for z in zs]
+                    members += [TileConfig(x_, y_, z, 32768, 2, 1, nz, layout="HWC") for z in zs for nz in nzts]
         if prune and members:
             io = {m: tcgen05_io_words(shape, m) for m in members}
             floor = min(io.values())

@@ -43,15 +43,18 @@ def main():
     torch.cuda.synchronize()
     C.conv_igemm(x, w, padding=1, stride=spec.stride, tile=tile, precision=args.prec)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (8 * 1024))()
+    buf = (ctypes.c_ulonglong * (16 * 1024))()
     lib = N.lib()
     assert lib.convio_dev_trace(buf) == 0, "not a CONVIO_TRACE build"
-    tr = np.frombuffer(buf, dtype=np.uint64).reshape(8, 1024).astype(np.int64)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(16, 1024).astype(np.int64)
+    peer = tr[8:16]
+    tr = tr[0:8]
     nz = [int((tr[r] > 0).sum()) for r in range(7)]
     print("stamps per row:", nz, "info:", C.query(tuple(x.shape), tuple(w.shape), spec.stride, 1, "HWC",
                                                    tile, f"igemm_{args.prec}")["reason"])
     t0 = min(tr[r][tr[r] > 0].min() for r in range(7) if nz[r])
-    P, C1, C2, M3, M4, E5, E6 = (tr[r] - t0 for r in range(7))
+    P, C1, C2, M3, M4, E5, E6, M7 = (tr[r] - t0 for r in range(8))
+    pP, pC1, pC2 = (peer[r] - t0 for r in range(3))   # the peer CTA (clock64 of another SM: offset unknown)
     k = min(nz[0], nz[3], nz[4])
     k1 = min(k, nz[1], nz[2]) if nz[1] else 0
 
@@ -70,9 +73,10 @@ def main():
     if ne:
         print(f"epilogue: drain (E6-E5) med {med(E6[:ne] - E5[:ne]):.0f} cyc, items {ne}, "
               f"item period med {med(np.diff(E5[:ne])):.0f}")
-    print(" i      P     C1     C2     M3     M4")
+    print(" i      P     C1     C2     M3  M7(1st MMA)  M4 | peer P  C1  C2 (own clock)")
     for i in range(min(args.show, k)):
-        print(f"{i:3d} {P[i]:7d} {C1[i] if k1 else 0:7d} {C2[i] if k1 else 0:7d} {M3[i]:7d} {M4[i]:7d}")
+        print(f"{i:3d} {P[i]:7d} {C1[i] if k1 else 0:7d} {C2[i] if k1 else 0:7d} {M3[i]:7d} {M7[i]:7d} {M4[i]:7d} | "
+              f"{pP[i]:7d} {pC1[i]:7d} {pC2[i]:7d}")
 
 
 if __name__ == "__main__":

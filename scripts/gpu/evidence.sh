@@ -5,7 +5,7 @@
 #     SM<->L2 read bytes per layer call (--cache-control none, last of 3 calls)
 #     -> gpurun_out/<ROUND>_{resnet50,vgg16}_traffic.json (bench.py reads them)
 #  2. the bench step's kernel launch list (gpu__time_duration, --clock-control none)
-#  3. one `ncu --set full` capture of the dominant kernel of each ResNet-50 layer family
+#  3. one `ncu --set full` capture of each ResNet-50 layer family's tuned plan
 R=${1:-r2}
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,l1tex__m_xbar2l1tex_read_bytes.sum
 mkdir -p gpurun_out/traffic_$R
@@ -21,9 +21,9 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_bench_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-variants --no-cudnn --no-network > gpurun_out/${R}_bench_ncu.log 2>&1
 python scripts/ncu_summary.py launches gpurun_out/${R}_bench_launches.csv --out gpurun_out/${R}_bench_launches.json > /dev/null
-for spec in "res2_3x3 igemm_3xf16:64:2:h32" "res4_3x3 igemm_3xf16:256:2" "res3_3x3_s2 igemm_3xf16:128:4" "res5_3x3 winograd_tc_3xf16:4:256"; do
-  set -- $spec
-  timeout 300 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair|winograd" -c 3 \
-    -o gpurun_out/${R}_ncu_$1 -f python scripts/probe_tc.py --one $2 --layers $1 --reps 2 > /dev/null 2>&1
+# full captures of the tuned plan of each ResNet-50 layer family (run_layer.py = the bench plan)
+for L in res2_3x3 res3_3x3_s2 res3_3x3 res4_3x3 res5_3x3; do
+  timeout 400 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair|winograd|igemm" -s 1 -c 3 \
+    -o gpurun_out/${R}_ncu_$L -f python scripts/run_layer.py --workload resnet50 --layer $L --reps 3 > /dev/null 2>&1
 done
 ls -la gpurun_out/${R}_*

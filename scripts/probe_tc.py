@@ -74,7 +74,7 @@ def build(spec, kind, n, x, w, wcache):
             if spec.stride != 1:
                 return None
             fpr = int(rest[2][1:])
-            tile = TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, 2, layout="HWC")
+            tile = TileConfig(fpr - 2, 128 // fpr, z, 32768, 2, 1, nzt, layout="HWC")   # nzt 4: rows into TMEM
         if TILE_OVERRIDE:
             tile = TileConfig(*TILE_OVERRIDE, layout="HWC")
         key = ("ig", "bf16" if prec == "bf16" else ("f16x3" if prec == "3xf16" else "f32"))

@@ -50,6 +50,13 @@ CASES = [
     (3, 256, 14, 256, 1, TileConfig(1, 1, 256, 32768, 1, 1, 4, layout="HWC"), "tsa z=256 (one accumulator)"),
     (3, 128, 28, 128, 2, TileConfig(2, 1, 128, 32768, 1, 1, 4, layout="HWC"), "tsa stride 2"),
     (16, 512, 14, 256, 2, TileConfig(1, 1, 256, 32768, 1, 1, 4, layout="HWC"), "tsa split-K"),
+    # (2, 1, 4): halo footprint, the converters shift each tap's rows into TMEM
+    (2, 64, 56, 128, 1, TileConfig(14, 8, 128, 32768, 2, 1, 4, layout="HWC"), "halo tsa z=128"),
+    (3, 128, 28, 128, 1, TileConfig(30, 4, 128, 32768, 2, 1, 4, layout="HWC"), "halo tsa 30x4 ragged x"),
+    (3, 128, 28, 256, 1, TileConfig(14, 8, 256, 32768, 2, 1, 4, layout="HWC"), "halo tsa z=256 ragged y"),
+    (2, 128, 14, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 4, layout="HWC"), "halo tsa z=64"),
+    (2, 64, 56, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 4, layout="HWC"), "fold tsa resident filter"),
+    (3, 128, 28, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 4, layout="HWC"), "fold tsa 30x4 2 channel blocks"),
 ]
 
 
@@ -66,6 +73,10 @@ def test_igemm_3xf16_matches_oracle(case):
         assert "split-K" in info["reason"], info
     if what.startswith("tsa"):
         assert "A in TMEM" in info["reason"], info
+    if "halo tsa" in what or "fold tsa" in what:
+        assert "shifted into TMEM" in info["reason"], info
+    if "resident" in what:
+        assert "resident filter" in info["reason"], info
     y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, stride=stride, tile=tile,
                      precision="3xf16", bias=torch.from_numpy(b).cuda())
     ref = co.direct_conv(x, wt, stride, 1) + b[None, :, None, None]
@@ -95,7 +106,8 @@ def test_igemm_3xf16_extreme_operand_scales(sx, sw):
     x = x * np.float32(2.0 ** sx)
     wt = wt * np.float32(2.0 ** sw)
     for tile in (TileConfig(14, 7, 128, 32768, 1, 1, 2, layout="HWC"),
-                 TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC")):
+                 TileConfig(14, 8, 128, 32768, 2, 1, 2, layout="HWC"),
+                 TileConfig(14, 8, 128, 32768, 2, 1, 4, layout="HWC")):
         y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, tile=tile, precision="3xf16")
         err = co.rel_err(y.contiguous().cpu().numpy(), co.direct_conv(x, wt, 1, 1))
         assert np.isfinite(err) and err <= tol_3xtf32(64), (tile, err)
