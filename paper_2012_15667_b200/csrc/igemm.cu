@@ -243,10 +243,15 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16 || kind == KIND_3XF16C) ? 2 : 1;
         // non-halo 3xTF32 without TSA: hi-only TMA stages + 2 decoupled lo slots
         const bool loslot = kind == KIND_3XTF32 && !pl->halo && !pl->tsa && bn == 256;
+        // 3xF16C with A in TMEM, no halo: the fp32 activation boxes in their own ring of
+        // na [A0 | A1] slots (released by the converters), the stages hold the filter planes
+        const bool aring = pl->tsa && kind == KIND_3XF16C && !pl->halo;
+        if (aring) pl->na = bn >= 256 ? 3 : (bn >= 128 ? 4 : 5);
         const size_t stage_bytes = (pl->tsa && kind == KIND_3XTF32) ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
-                                           : (size_t)((pl->halo ? 0 : 128 * 128) + (bn / 2) * 128) *
+                                           : (size_t)((pl->halo || aring ? 0 : 128 * 128) + (bn / 2) * 128) *
                                                  (loslot ? 1 : mult);
-        const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult : (loslot ? 2 * stage_bytes : 0);
+        const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult
+                                       : (aring ? (size_t)pl->na * 2 * 128 * 128 : (loslot ? 2 * stage_bytes : 0));
         const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
@@ -365,15 +370,24 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
     const int fp_rows = (t->y + d->r - 1) * fpr;
     pl->fp_bytes = fp_rows * 128;
     pl->a_slot = ((fp_rows + d->s - 1) * 128 + 1023) & ~1023;
-    pl->na = 2;
     pl->tsa = t->n_zt == 4;
-    // halo TSA fold with one n-block: the CTA's whole filter slice stays resident when
-    // it fits next to the footprint slots (ResNet-50 res2 / VGG conv1_2: 3 x 24 KB)
-    if (pl->tsa && pl->fold) {
-        const int kblocks = d->r * (d->c / kblock_channels(kind));
-        const size_t slice = (size_t)kblocks * (d->s * t->z / 2) * 128 * 2;
+    // footprint slots: 3 when the ring keeps >= 3 filter stages (short items -- fold tiles,
+    // 3 k-blocks -- need the next footprints in flight across a whole item: its TMA
+    // latency under load is ~1.5 us); halo TSA fold with one n-block: the CTA's whole
+    // filter slice stays resident when it fits next to the footprint slots (ResNet-50
+    // res2 / VGG conv1_2: 3 x 24 KB)
+    {
+        const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16C) ? 2 : 1;
         const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
-        if ((size_t)pl->na * pl->a_slot * 2 + slice <= budget) pl->resb_slots = kblocks;
+        const size_t stage = (size_t)((pl->fold ? d->s * t->z : t->z) / 2) * 128 * mult;
+        const size_t slot = (size_t)pl->a_slot * mult;
+        const int kblocks = (pl->fold ? d->r : d->r * d->s) * (d->c / kblock_channels(kind));
+        const size_t slice = (size_t)kblocks * stage;
+        pl->na = 3 * slot + 3 * stage <= budget ? 3 : 2;
+        if (pl->tsa && pl->fold) {
+            if (3 * slot + slice <= budget) pl->na = 3;
+            if ((size_t)pl->na * slot + slice <= budget) pl->resb_slots = kblocks;
+        }
     }
     int rc = plan_ring(pl, pl->fold ? d->s * t->z : t->z, kind, t->s_b, true, reason, rlen);
     if (rc) return rc;
@@ -490,6 +504,18 @@ int plan_igemm_batched(int kind, int bn, int s_b, bool pair, bool tsa, int xi, i
     return CONVIO_OK;
 }
 
+// the pair kernel's output map: fp32 NHWC [K][Q][P][N] (batched: [K][T][1][xi]), box =
+// one 32-channel slice of a CTA's block (halo: its x valid columns), 128-B swizzle
+static bool make_output_map(const IgemmPlan &pl, float *y, CUtensorMap *ty) {
+    const IgemmParams &P = pl.P;
+    if (reinterpret_cast<uintptr_t>(y) & 15) return false;
+    cuuint64_t yd[4] = {(cuuint64_t)P.k, (cuuint64_t)P.q, (cuuint64_t)P.p, (cuuint64_t)P.n};
+    cuuint64_t ys[3] = {(cuuint64_t)P.k * 4, (cuuint64_t)P.q * P.k * 4, (cuuint64_t)P.p * P.q * P.k * 4};
+    cuuint32_t yb[4] = {32, (cuuint32_t)P.bx, (cuuint32_t)P.by, (cuuint32_t)P.imgs};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return encode_tensor_map_tiled_ex(ty, 4, y, yd, ys, yb, es, true);
+}
+
 static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, CUtensorMap *tx,
                             CUtensorMap *tw) {
     const IgemmParams &P = pl.P;
@@ -538,8 +564,8 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
 
 int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias, int relu, float *y,
                  cudaStream_t stream) {
-    CUtensorMap tx, tw;
-    if (!make_igemm_maps(pl, x, wq, &tx, &tw)) {
+    CUtensorMap tx, tw, ty;
+    if (!make_igemm_maps(pl, x, wq, &tx, &tw) || (pl.pair && !make_output_map(pl, y, &ty))) {
         set_error("TMA descriptors cannot describe these tensors (alignment)");
         return CONVIO_EINFEASIBLE;
     }
@@ -572,9 +598,9 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         g_trace_ptr = d_trace;
 #endif
         if (PP.g.splits > 1)   // after a memset node: a plain stream dependency
-            pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw);
+            pl.pfn<<<pl.grid, pl.threads, pl.smem, stream>>>(PP, tx, tw, ty);
         else
-            CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw));
+            CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw, ty));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
         return CONVIO_OK;

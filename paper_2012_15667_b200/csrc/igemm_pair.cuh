@@ -111,6 +111,19 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
 // CUTLASS 2-SM consumer waits)
 __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity) { mbar_wait(bar, parity); }
 
+// TMA store of a staged output box (shared::cta -> global, bulk-group completion)
+__device__ __forceinline__ void tma_store_4d(uint64_t map, uint32_t src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
+        "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// named barrier among the 4 epilogue warps (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
 // one lane of the (converged) warp: tcgen05.mma / commit are issued once per warp
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred;
@@ -381,7 +394,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return 
 template <int BN, int KIND, bool HALO, bool TSA, bool FOLD = false, bool RESB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND, TSA>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
-                      const __grid_constant__ CUtensorMap tm_w) {
+                      const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_y) {
     // KIND_3XF16C (direct conv): the activation k-block (64 channels) arrives as two
     // fp32 TMA boxes (channels 0..31 where the hi operand goes, 32..63 where the lo
     // operand goes) and the converter warps rewrite them in place into the fp16
@@ -428,10 +441,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr bool LOSLOT = KIND == KIND_3XTF32 && !HALO && !TSA && BN == 256;
     constexpr int NL = 2;
     constexpr int LO_SLOT = A_BYTES + B_BYTES;
-    const int STAGE = HALO ? B_BYTES * MULT
+    // ARING (3xF16C, A in TMEM, no halo): the fp32 activation boxes get their own ring
+    // of NA slots [A0 | A1], released by the converters as soon as the rows are in TMEM;
+    // the filter planes stay in the stage ring [B_hi | B_lo] until the MMAs complete --
+    // an A box then lives ~TMA latency + split instead of until its MMAs retire
+    constexpr bool ARING = TSA && F16C && !HALO;
+    const int STAGE = (HALO || ARING) ? B_BYTES * MULT
                            : ((TSA && !F16C) ? A_BYTES + 2 * B_BYTES : (A_BYTES + B_BYTES) * (LOSLOT ? 1 : MULT));
-    const int ASLOT = HALO ? PP.a_slot * MULT : 0;
-    const int NA = HALO ? PP.na : 0;
+    const int ASLOT = HALO ? PP.a_slot * MULT : (ARING ? 2 * A_BYTES : 0);
+    const int NA = (HALO || ARING) ? PP.na : 0;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -445,10 +463,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     uint64_t *conv = empty + NS;
     uint64_t *tfull = conv + NS;
     uint64_t *tempty = tfull + 2;
-    uint64_t *afull = tempty + 2;                     // halo: footprint slot barriers
-    uint64_t *aempty = afull + 2;
-    uint64_t *aconv = aempty + 2;
-    uint64_t *tconv = aconv + 2;                      // TSA: A slot in TMEM converted
+    uint64_t *afull = tempty + 2;                     // halo: footprint slot barriers (ARING: A slots)
+    uint64_t *aempty = afull + 6;
+    uint64_t *aconv = aempty + 6;
+    uint64_t *tconv = aconv + 6;                      // TSA: A slot in TMEM converted
     uint64_t *tfree = tconv + 6;                      // TSA: A slot in TMEM consumed
     uint64_t *lofree = tfree + 6;                     // LOSLOT: lo slot consumed by the MMAs
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofree + NL);
@@ -462,6 +480,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     const int nclusters = gridDim.x >> 1;
     const uint64_t map_x = reinterpret_cast<uint64_t>(&tm_x);
     const uint64_t map_w = reinterpret_cast<uint64_t>(&tm_w);
+    const uint64_t map_y = reinterpret_cast<uint64_t>(&tm_y);
 
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -472,9 +491,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         for (int a = 0; a < 2; ++a) {
             mbar_init(tfull + a, 1);
             mbar_init(tempty + a, 8);
-            mbar_init(afull + a, 1);
-            mbar_init(aempty + a, (TSA && HALO) ? NCW : 1);   // halo TSA: the converters read it
+        }
+        for (int a = 0; a < 6; ++a) {
             mbar_init(aconv + a, 2 * NCW);
+            mbar_init(afull + a, 1);
+            mbar_init(aempty + a, TSA ? NCW : 1);   // A in TMEM: the converters read the slot
         }
         for (int l = 0; l < NL && LOSLOT; ++l) mbar_init(lofree + l, 1);
         for (int a = 0; a < NTA && TSA; ++a) {
@@ -527,7 +548,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             // ---- TMA producer (both CTAs) -------------------------------------------
             const uint32_t a_rows_bytes = (uint32_t)(P.bx * P.by * P.imgs * 128);
             // 3xF16C: two activation boxes and two filter planes per k-block
-            const uint32_t cta_bytes = (HALO ? (uint32_t)B_BYTES : a_rows_bytes + B_BYTES) * (F16C ? 2u : 1u);
+            const uint32_t cta_bytes = ((HALO || ARING) ? (uint32_t)B_BYTES : a_rows_bytes + B_BYTES) * (F16C ? 2u : 1u);
             const int lo_tap = P.ks * P.ks;                   // 3xF16C: filter lo plane offset (taps)
             int s = 0, sa = 0;
             uint32_t ph = 0, pha = 0;
@@ -583,7 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         }
                     }
                     if constexpr (!RESB) {
-                    if (it >= NS) mbar_wait(empty + s, ph ^ 1);
+                    if (!ARING && it >= NS) mbar_wait(empty + s, ph ^ 1);
                     PAIR_TRACE(0, it);
                     const int r = tap / P.ks, sx = tap - r * P.ks;
                     uint8_t *a = bring + s * STAGE;
@@ -591,9 +612,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const int xc = ox0 * P.stride + sx - P.pad, yc = oy0 * P.stride + r - P.pad;
                     const int wc = P.batched ? img0 : tap;
                     if constexpr (F16C) {    // own barrier, as 3xTF32; [A0 | B_hi | A1 | B_lo]
+                        if constexpr (ARING) {   // A slot [A0 | A1]; stage [B_hi | B_lo]
+                            if (ita >= NA) mbar_wait(aempty + sa, pha ^ 1);
+                            uint8_t *as = aring + sa * ASLOT;
+                            mbar_arrive_expect_tx(afull + sa, 2u * a_rows_bytes);
+                            tma_load_4d(as, map_x, cb * CB, xc, yc, img0, afull + sa);
+                            tma_load_4d(as + A_BYTES, map_x, cb * CB + 32, xc, yc, img0, afull + sa);
+                            ++ita;
+                            if (++sa == NA) {
+                                sa = 0;
+                                pha ^= 1;
+                            }
+                        } else {
                         mbar_arrive_expect_tx(full + s, cta_bytes);
-                        uint8_t *blo = HALO ? b + B_BYTES : b + A_BYTES + B_BYTES;
-                        if (!HALO) {
+                        uint8_t *blo = (HALO || ARING) ? b + B_BYTES : b + A_BYTES + B_BYTES;
+                        if (!HALO && !ARING) {
                             tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
                             tma_load_4d(a + A_BYTES + B_BYTES, map_x, cb * CB + 32, xc, yc, img0, full + s);
                         }
@@ -604,6 +637,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             tma_load_3d(b, map_w, cb * CB, n0, wc, full + s);
                             tma_load_3d(blo, map_w, cb * CB, n0, wc + lo_tap, full + s);
                         }
+                        }   // !ARING (its filter planes come from warp 2)
                     } else if constexpr (SPLIT) {   // own barrier: the converters need a local signal
                         mbar_arrive_expect_tx(full + s, cta_bytes);
                         if (!HALO) tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
@@ -619,7 +653,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             tma_load_3d_pair(b + A_BYTES + B_BYTES, map_w, cb * CB, n0, wc + P.n, full + s);
                         }
                     }
-                    if (++s == NS) {
+                    if (!ARING && ++s == NS) {
                         s = 0;
                         ph ^= 1;
                     }
@@ -633,6 +667,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     } else if (++cb == P.cblocks) {
                         cb = 0;
                         ++tap;
+                    }
+                }
+            }
+        }
+    } else if (ARING && warp == 2) {
+        if (lane == 0) {
+            // ---- ARING filter producer: the [B_hi | B_lo] stages run on their own ring, so a
+            // stage still held by in-flight MMAs never blocks the activation loads of warp 0 ----
+            const int lo_tap = P.ks * P.ks;
+            int s = 0, it = 0;
+            uint32_t ph = 0;
+            for (int item = cluster_id; item < PP.items; item += nclusters) {
+                int grp, pair, nb;
+                decode(item, grp, pair, nb);
+                const int n0 = nb * BN + (int)rank * HB;
+                int kb_lo, kb_hi;
+                krange(item, kb_lo, kb_hi);
+                int tap = kb_lo / P.cblocks, cb = kb_lo - tap * P.cblocks;
+                for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
+                    if (it >= NS) mbar_wait(empty + s, ph ^ 1);
+                    uint8_t *b = bring + s * STAGE;
+                    // both CTAs' planes complete on the LEADER's barrier: the MMA issuer waits on
+                    // it directly, the converters never wait for filter data
+                    if (leader) mbar_arrive_expect_tx(full + s, 4u * (uint32_t)B_BYTES);
+                    tma_load_3d_pair(b, map_w, cb * CB, n0, tap, full + s);
+                    tma_load_3d_pair(b + B_BYTES, map_w, cb * CB, n0, tap + lo_tap, full + s);
+                    if (++cb == P.cblocks) {
+                        cb = 0;
+                        ++tap;
+                    }
+                    if (++s == NS) {
+                        s = 0;
+                        ph ^= 1;
                     }
                 }
             }
@@ -660,13 +727,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 for (int kb = kb_lo; kb < kb_hi; ++kb) {
                     if constexpr (TSA) {
                         mbar_wait_cluster(tconv + ta, pht);
+                        if constexpr (ARING) mbar_wait(full + s, ph);   // both CTAs' filter planes
                         PAIR_TRACE(3, kbc);
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                         // 3xTF32 stage [A | B | B_lo]; 3xF16C [A0 | B_hi | A1 | B_lo]; halo [B_hi | B_lo]
                         // (RESB: filter slot kb of the resident slice)
-                        const uint32_t b = smem_u32(bring + (RESB ? kb : s) * STAGE) + (HALO ? 0 : A_BYTES);
+                        const uint32_t b = smem_u32(bring + (RESB ? kb : s) * STAGE) + ((HALO || ARING) ? 0 : A_BYTES);
                         const uint64_t bd = umma_desc_sw128(b),
-                                       bdl = umma_desc_sw128(b + ((F16C && !HALO) ? A_BYTES + B_BYTES : B_BYTES));
+                                       bdl = umma_desc_sw128(b + ((F16C && !HALO && !ARING) ? A_BYTES + B_BYTES : B_BYTES));
                         const uint32_t ahi = tmem + A_COL0 + (uint32_t)(ta * 64);
                         const bool first = kb == kb_lo;
                         if (elect_one()) {
@@ -781,6 +849,115 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 __syncwarp();
             }
         }
+    } else if (warp >= 4 && warp < 8 && P.splits <= 1) {
+        // ---- epilogue (one K range per item): TMEM -> registers (unscale, bias, ReLU) ->
+        // a 128-B-swizzled staging box in shared memory -> ONE TMA store per 32 channels.
+        // Each lane owns an accumulator row (no transposes, no per-lane global stores),
+        // and the accumulator is released to the MMA issuer as soon as its last
+        // columns are in registers ----
+        const int q = warp - 4;                       // TMEM lane quadrant
+        const int m = q * 32 + lane;                  // pixel row of this CTA's A block
+        const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
+        const uint32_t stg = smem_u32(ring_end + 1024);
+        const int act_exp = F16C ? f16c_act_exp(P.row_exp, P.nred, lane) : 0;   // one per tensor
+        // staging row = position in the store box [img][y][x] (halo: the x valid columns)
+        int srow;
+        bool inbox;
+        if (HALO) {
+            const int py = m / PP.fpr, px = m - py * PP.fpr;
+            srow = py * P.bx + px;
+            inbox = px < P.bx;
+        } else {
+            srow = m;
+            inbox = m < P.bx * P.by * P.imgs;
+        }
+        const bool issuer = q == 0 && lane == 0;
+        int t = 0;
+        for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
+            int grp, pair, nb;
+            decode(item, grp, pair, nb);
+            const int acc = NACC == 2 ? (t & 1) : 0;
+            mbar_wait(tfull + acc, (t / NACC) & 1);
+            if (q == 0 && lane == 0) PAIR_TRACE(5, t);
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const int blk = pair * 2 + (int)rank;
+            int ox0, oy0, img0;
+            pair_block_origin(P, grp, blk, ox0, oy0, img0);
+            const int k0 = nb * KOUT;
+            float rs = 1.f;   // the row's operand scale (3xF16 families)
+            if constexpr (F16X3) {
+                const int per_img = P.bx * P.by;
+                const int im = m / per_img, pix = m - im * per_img;
+                const int py = pix / P.bx, px = pix - py * P.bx;
+                const int img = img0 + im, ox = ox0 + px;
+                const bool ok = inbox && img < P.n && oy0 + py < P.p && ox < P.q;
+                rs = pow2f(-(ok ? __ldg(P.row_exp + (int64_t)img * P.q + ox) : 0));
+            } else if constexpr (F16C) {
+                rs = pow2f(-act_exp);
+            }
+#pragma unroll 1
+            for (int c0 = 0; c0 < KOUT; c0 += 32) {
+                float v[32];
+                tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                if constexpr (FOLD) {
+                    // y[p] = E[p][0:K] + E[p+1][K:2K] + E[p+2][2K:3K]: rows p+1, p+2 are
+                    // lanes +1, +2 of this warp (valid columns never cross a footprint row)
+#pragma unroll
+                    for (int sft = 1; sft < 3; ++sft) {
+                        float u[32];
+                        tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) +
+                                               (uint32_t)(acc * BN + sft * KOUT + c0), u);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += __shfl_down_sync(0xffffffffu, u[j], sft);
+                    }
+                }
+                if (c0 + 32 >= KOUT) {   // accumulator fully read: hand it back to the MMA issuer
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
+                    if (q == 0 && lane == 0) PAIR_TRACE(6, t);
+                }
+                // unscale (exact powers of two, two multiplies: the exponent sum may pass
+                // pow2f's range), bias, ReLU
+                const int kc = k0 + c0;
+#pragma unroll
+                for (int j4 = 0; j4 < 8; ++j4) {
+                    const float4 bv = P.bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4)
+                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float cs[4] = {1.f, 1.f, 1.f, 1.f};
+                    if constexpr (F16X3 || F16C) {
+                        const int4 ce = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + kc) + j4);
+                        cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
+                    }
+                    const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        float o = v[4 * j4 + u];
+                        if constexpr (F16X3 || F16C) o = (o * rs) * cs[u];
+                        o += b4[u];
+                        v[4 * j4 + u] = P.relu ? fmaxf(o, 0.f) : o;
+                    }
+                }
+                if (issuer) bulk_wait_read0();   // the previous chunk's store has read the box
+                epi_bar();
+                if (inbox) {
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4)
+                        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
+                                         stg + (uint32_t)srow * 128 + (uint32_t)((j4 ^ (srow & 7)) << 4)),
+                                     "f"(v[4 * j4]), "f"(v[4 * j4 + 1]), "f"(v[4 * j4 + 2]), "f"(v[4 * j4 + 3])
+                                     : "memory");
+                }
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                epi_bar();
+                if (issuer) {
+                    tma_store_4d(map_y, stg, kc, ox0, oy0, img0);
+                    bulk_commit();
+                }
+            }
+        }
+        if (issuer) bulk_wait0();
     } else if (warp >= 4 && warp < 8) {
         // ---- epilogue: TMEM -> registers -> NHWC global, both CTAs ------------------
         const int q = warp - 4;                       // TMEM lane quadrant
@@ -941,9 +1118,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const int fr = m + r * PP.fpr + sx;
                     row = fa + (h ? (uint32_t)PP.a_slot : 0u) + (uint32_t)fr * 128;
                     sw = fr & 7;
-                } else {
-                    mbar_wait(full + s, ph);
-                    row = smem_u32(bring + s * STAGE) + (h ? (uint32_t)(A_BYTES + B_BYTES) : 0u) + (uint32_t)m * 128;
+                } else {   // ARING: the A slot (the filter planes are the MMA issuer's to wait for)
+                    mbar_wait(afull + sa, pha);
+                    row = smem_u32(aring + sa * ASLOT) + (h ? (uint32_t)A_BYTES : 0u) + (uint32_t)m * 128;
                     sw = m & 7;
                 }
                 if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
@@ -987,6 +1164,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             sa = 0;
                             pha ^= 1;
                         }
+                    }
+                } else {   // ARING: the A slot is in TMEM now
+                    if (lane == 0) mbar_arrive(aempty + sa);
+                    if (++sa == NA) {
+                        sa = 0;
+                        pha ^= 1;
                     }
                 }
                 if (!RESB && ++s == NS) {

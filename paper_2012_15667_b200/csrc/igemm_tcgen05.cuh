@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(igemm_threads<BN, KIND>(), 1)
 using IgemmFn = void (*)(const IgemmParams, const CUtensorMap, const CUtensorMap);
 
 struct PairParams;   // igemm_pair.cuh
-using PairFn = void (*)(const PairParams, const CUtensorMap, const CUtensorMap);
+using PairFn = void (*)(const PairParams, const CUtensorMap, const CUtensorMap, const CUtensorMap);
 
 struct IgemmPlan {
     IgemmParams P;
