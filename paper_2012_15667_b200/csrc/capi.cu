@@ -168,7 +168,8 @@ int launch_fit_cluster(const void *fn, int threads, size_t smem, int *regs) {
     *regs = fa.numRegs;
     if ((int)smem > dev.max_smem_optin || fa.numRegs * threads > 65536) fit = 0;
     // opt in to the device maximum once per kernel (any later config of it then fits)
-    if (fit && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dev.max_smem_optin) != cudaSuccess) {
+    if (fit && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    dev.max_smem_optin - (int)fa.sharedSizeBytes) != cudaSuccess) {
         cudaGetLastError();
         fit = 0;
     }

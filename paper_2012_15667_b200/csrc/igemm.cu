@@ -122,14 +122,24 @@ __global__ void __launch_bounds__(256) pack_filter_f16x3_kernel(const float *__r
         for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
         const int e = f16_row_exp(mx);
         const float sc = pow2f(e);
-        for (int j = lane; j < crs; j += 32) {   // j = cc * rs + tap (KCRS)
-            const int cc = j / rs, tap = j - cc * rs;
-            const float v = wr[j] * sc;
-            const __half hi = __float2half_rn(v);
-            const __half lo = __float2half_rn(v - __half2float(hi));
-            const int64_t o = ((int64_t)tap * k + kk) * c + cc;
-            wq[o] = hi;
-            wq[plane + o] = lo;
+        // tap-major: lane pairs of channels, so each warp store is 128 contiguous bytes of
+        // a [tap][k][c] plane row (the KCRS row re-reads hit L1 after the max pass)
+        for (int tap = 0; tap < rs; ++tap) {
+            __half *hrow = wq + ((int64_t)tap * k + kk) * c;
+            for (int cc = 2 * lane; cc < c; cc += 64) {
+                const float v0 = wr[cc * rs + tap] * sc;
+                const float v1 = cc + 1 < c ? wr[(cc + 1) * rs + tap] * sc : 0.0f;
+                const __half2 hi = __floats2half2_rn(v0, v1);
+                const float2 hf = __half22float2(hi);
+                const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+                if (cc + 1 < c) {
+                    *reinterpret_cast<__half2 *>(hrow + cc) = hi;
+                    *reinterpret_cast<__half2 *>(hrow + plane + cc) = lo;
+                } else {
+                    hrow[cc] = __low2half(hi);
+                    hrow[plane + cc] = __low2half(lo);
+                }
+            }
         }
         if (lane == 0) col_exp[kk] = e;
     }
@@ -308,28 +318,39 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
 }
 
 // persistent grid: one CTA pair per TPC (fewer if there are fewer work items).
-// Split-K (non-halo conv tiles): when the last wave of work items would leave
-// pairs idle -- e.g. ResNet-50 res5 stride 2, 98 items on 74 pairs: 2 rounds for
-// 1.32 rounds of work -- each item's K loop is split so items * splits fills
-// the rounds evenly; partial tiles are added with fp32 vector atomics into the
-// zeroed output (bias by the first split; never with ReLU, see igemm_launch).
+// Tail split-K (non-halo conv tiles): when the last round of tile items would leave
+// pairs idle -- ResNet-50 res4 at batch 256: 196 items on 74 pairs, 3 rounds for
+// 2.65 rounds of work -- the last T tile items are split into S K ranges so the
+// partial tiles fill the final round; the epilogue reduce-adds them (TMA .add) into
+// the output zeroed from the tail's first image on (bias by the first split; never
+// with ReLU, see igemm_launch).  (T, S) minimise the modelled rounds of k-blocks,
+// and are kept only if they save >= 5 %.
 static int finish_pair_grid(IgemmPlan *pl) {
     const int pairs = (pl->blocks_per_group + 1) / 2;
     const int64_t base = (int64_t)pl->groups * pairs * (pl->fold ? 1 : pl->P.k / pl->bn);
     const int64_t nclus = std::max(1, device_sms() / 2);
     pl->P.splits = 1;
-    if (!pl->halo && !pl->P.batched && base < 8 * nclus) {
-        auto eff = [&](int64_t it) { return (double)it / (double)(((it + nclus - 1) / nclus) * nclus); };
-        double best = eff(base);
-        for (int sp = 2; sp <= 4; ++sp) {
-            if (pl->P.kblocks / sp < 16) break;
-            if (eff(base * sp) > best * 1.2) {   // atomics + memset cost ~10-15 %
-                best = eff(base * sp);
-                pl->P.splits = sp;
+    pl->tail_start = base;
+    static const bool no_tail = getenv("CONVIO_DEV_NO_TAIL") != nullptr;   // dev knob: A/B timing
+    if (!pl->halo && !pl->P.batched && base % nclus && !no_tail) {
+        const int64_t kb = pl->P.kblocks;
+        const double whole = (double)((base + nclus - 1) / nclus) * kb;
+        double best = whole * 0.95;
+        for (int64_t T = base % nclus; T <= base; T += nclus) {
+            for (int sp = 2; sp <= 8; ++sp) {
+                if (kb / sp < 6) break;
+                const double t = (double)((base - T) / nclus) * kb +
+                                 (double)((T * sp + nclus - 1) / nclus) * (double)((kb + sp - 1) / sp);
+                if (t < best) {
+                    best = t;
+                    pl->P.splits = sp;
+                    pl->tail_start = base - T;
+                }
             }
+            if (T >= 2 * nclus) break;   // the tail is at most the last two rounds
         }
     }
-    const int64_t items = base * pl->P.splits;
+    const int64_t items = pl->tail_start + (base - pl->tail_start) * pl->P.splits;
     if (items >= ((int64_t)1 << 31)) {
         set_error("too many work items");
         return CONVIO_EINFEASIBLE;
@@ -580,20 +601,34 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.pairs_per_group = (pl.blocks_per_group + 1) / 2;
         PP.nblocks = pl.fold ? 1 : pl.P.k / pl.bn;
         PP.base_items = PP.groups * PP.pairs_per_group * PP.nblocks;
-        if (PP.g.splits < 1 || relu) PP.g.splits = 1;   // ReLU does not commute with the split sum
-        PP.items = PP.base_items * PP.g.splits;
-        if (PP.g.splits > 1)
-            CONVIO_CUDA_TRY(cudaMemsetAsync(y, 0, (size_t)PP.g.n * PP.g.p * PP.g.q * PP.g.k * sizeof(float),
-                                            stream));
+        PP.tail_start = (int)pl.tail_start;
+        if (PP.g.splits < 1 || relu) {   // ReLU does not commute with the split sum
+            PP.g.splits = 1;
+            PP.tail_start = PP.base_items;
+        }
+        PP.items = PP.tail_start + (PP.base_items - PP.tail_start) * PP.g.splits;
+        if (PP.g.splits > 1) {
+            // zero the output from the image group of the tail's first block on (whole
+            // tiles before it overwrite their part of that range with plain stores)
+            const int first_block = 2 * ((PP.tail_start / PP.nblocks) % PP.pairs_per_group);
+            const int64_t img_lo = (int64_t)(first_block / (PP.g.tiles_x * PP.g.tiles_y)) * PP.g.imgs;
+            const size_t per_img = (size_t)PP.g.p * PP.g.q * PP.g.k;
+            if (img_lo < PP.g.n)
+                CONVIO_CUDA_TRY(cudaMemsetAsync(y + img_lo * per_img, 0,
+                                                (size_t)(PP.g.n - img_lo) * per_img * sizeof(float), stream));
+        }
         PP.fpr = pl.fpr;
         PP.fp_bytes = pl.fp_bytes;
         PP.a_slot = pl.a_slot;
         PP.na = pl.na;
+        PP.scale_state = pl.scale_state;
+        PP.fallback = 0;
+        PP.spec_ctas = 0;
         PP.trace = nullptr;
 #ifdef CONVIO_TRACE
         static unsigned long long *d_trace = nullptr;
-        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 16 * 1024 * sizeof(unsigned long long)));
-        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 16 * 1024 * sizeof(unsigned long long), stream));
+        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 18 * 1024 * sizeof(unsigned long long)));
+        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 18 * 1024 * sizeof(unsigned long long), stream));
         PP.trace = d_trace;
         g_trace_ptr = d_trace;
 #endif
@@ -603,6 +638,20 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
             CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw, ty));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
+        if (pl.kind == KIND_3XF16C) {
+            // the checking launch: exits at once when the speculative scale held, else redoes
+            // the whole conv with the exact scale (whole tiles, plain stores over the output)
+            PairParams PF = PP;
+            PF.fallback = 1;
+            PF.g.splits = 1;
+            PF.tail_start = PF.base_items;
+            PF.items = PF.base_items;
+            PF.spec_ctas = (int)pl.grid.x;
+            const unsigned clus = (unsigned)std::max(1, std::min(PF.items, device_sms() / 2));
+            CONVIO_CUDA_TRY(launch_pdl(pl.pfn, dim3(2 * clus), dim3(pl.threads), pl.smem, stream, PF, tx, tw, ty));
+            note_launch();
+            CONVIO_CUDA_TRY(cudaGetLastError());
+        }
         return CONVIO_OK;
     }
     if (pl.P.splits > 1 && relu) {   // ReLU does not commute with the split sum
@@ -752,7 +801,7 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
 // dev builds only: copy the last pair-kernel pipeline trace (8 x 1024 clock64 stamps)
 int convio_dev_trace(unsigned long long *host) {
     if (!g_trace_ptr) return CONVIO_EINVAL;
-    return cudaMemcpy(host, g_trace_ptr, 16 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+    return cudaMemcpy(host, g_trace_ptr, 18 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                    cudaSuccess
                ? CONVIO_OK
                : CONVIO_EINTERNAL;
@@ -802,7 +851,7 @@ int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int
         // filter (convio_pack_filter_igemm_f16x3) leaves only the partials here
         const size_t need_here = w_is_packed ? f16c_partials_bytes() : (size_t)igemm_workspace_bytes(desc, kind);
         if (!workspace || workspace_bytes < need_here || (reinterpret_cast<uintptr_t>(workspace) & 255)) {
-            set_error("workspace of %zu bytes (256-byte aligned) needed (absmax partials%s)", need_here,
+            set_error("workspace of %zu bytes (256-byte aligned) needed (activation scale state%s)", need_here,
                       w_is_packed ? "" : " + packed fp16 filter");
             return CONVIO_EINVAL;
         }
@@ -816,11 +865,9 @@ int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int
             rc = launch_pack_filter_f16x3(desc, (const float *)w, const_cast<void *>(wq), st);
             if (rc) return rc;
         }
-        int nred = 0;
-        rc = launch_absmax_partials(x, (int64_t)desc->n * desc->c * desc->h * desc->w, (int *)workspace, &nred, st);
-        if (rc) return rc;
-        pl.P.row_exp = (const int *)workspace;
-        pl.P.nred = nred;
+        // speculative activation scale: the state lives in the workspace's first 16 bytes
+        // (zeroed by the caller before a workspace's first use: no speculation yet)
+        pl.scale_state = (int *)workspace;
         pl.P.col_exp = (const int *)((const uint8_t *)wq + align256((size_t)4 * desc->k * desc->c * desc->r * desc->s));
         return igemm_launch(pl, x, wq, bias, relu, y, st);
     }

@@ -42,8 +42,8 @@
 
 namespace convio {
 
-// epilogue transpose buffer after the ring + barriers: 4 warps x 32 rows x 36 floats
-constexpr size_t kPairEpiBytes = 4 * 32 * 36 * sizeof(float);
+// epilogue staging box after the ring + barriers: 128 rows x 32 fp32 channels (one TMA store)
+constexpr size_t kPairEpiBytes = 128 * 32 * sizeof(float);
 
 struct PairParams {
     IgemmParams g;          // geometry as in the single-CTA kernel
@@ -51,8 +51,17 @@ struct PairParams {
     int blocks_per_group;   // pixel blocks per group
     int pairs_per_group;    // ceil(blocks_per_group / 2)
     int nblocks;            // K / BN
-    int items;              // base_items * splits
+    int items;              // tail_start + (base_items - tail_start) * splits
     int base_items;         // groups * pairs_per_group * nblocks (one K range each)
+    int tail_start;         // tile items from here on are split into g.splits K ranges
+    // 3xF16C speculative activation scale (see f16c_spec_ok): scale_state[0] = the max |x|
+    // (float bits) to speculate with, [1] = [0] ^ kScaleTag, [2] = the value the speculative
+    // launch used, [4 + cta] = each speculative CTA's observed max |x|.  fallback = 1: the
+    // checking launch -- exits at once if the speculation held, else redoes the conv with
+    // the observed (exact) max
+    int *scale_state;
+    int fallback;
+    int spec_ctas;          // the speculative launch's CTA count (its partial maxima)
     // halo staging (HALO kernels): the (y + R - 1) x fpr input footprint of a
     // 128-row block is staged ONCE per channel block; tap (r, s) is the view
     // starting (r * fpr + s) rows into it (rows = y x fpr pixels, x = fpr - S + 1
@@ -115,6 +124,13 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity
 __device__ __forceinline__ void tma_store_4d(uint64_t map, uint32_t src, int c0, int c1, int c2, int c3) {
     asm volatile(
         "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
+        "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+// the same with an fp32 add into global (partial tiles of the split-K tail)
+__device__ __forceinline__ void tma_reduce_add_4d(uint64_t map, uint32_t src, int c0, int c1, int c2, int c3) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.4d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4, %5}], [%1];\n" ::"l"(map),
         "r"(src), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
 }
@@ -252,7 +268,8 @@ constexpr int pair_threads() {
 // safe); per 8-thread LDS/STS phase 4 rows x 2 halves hit 8 distinct 16-B
 // chunks (the h = 1 thread walks its chunks rotated by half a row).
 template <int NT>
-__device__ __forceinline__ void convert_f16_rows(uint32_t b0, uint32_t b1, int nrows, int ct, float sc) {
+__device__ __forceinline__ void convert_f16_rows(uint32_t b0, uint32_t b1, int nrows, int ct, float sc,
+                                                 float &amax) {
     const int h = ct & 1;
     for (int base = 0; base < nrows; base += NT / 2) {
         const int m = base + (ct >> 1);
@@ -277,6 +294,10 @@ __device__ __forceinline__ void convert_f16_rows(uint32_t b0, uint32_t b1, int n
                 const float f[8] = {v[2 * i].x * sc, v[2 * i].y * sc, v[2 * i].z * sc, v[2 * i].w * sc,
                                     v[2 * i + 1].x * sc, v[2 * i + 1].y * sc, v[2 * i + 1].z * sc,
                                     v[2 * i + 1].w * sc};
+                amax = fmaxf(amax, fmaxf(fmaxf(fmaxf(fabsf(v[2 * i].x), fabsf(v[2 * i].y)),
+                                               fmaxf(fabsf(v[2 * i].z), fabsf(v[2 * i].w))),
+                                         fmaxf(fmaxf(fabsf(v[2 * i + 1].x), fabsf(v[2 * i + 1].y)),
+                                               fmaxf(fabsf(v[2 * i + 1].z), fabsf(v[2 * i + 1].w)))));
                 uint32_t hw[4], lw[4];
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -297,6 +318,42 @@ __device__ __forceinline__ void convert_f16_rows(uint32_t b0, uint32_t b1, int n
         }
         __syncwarp();
     }
+}
+
+// ---- 3xF16C speculative activation scale --------------------------------------------
+// The speculative launch scales x by 2^e, e = f16_row_exp(spec), spec = the max |x| the
+// previous call on this workspace observed (state[0], valid iff state[1] = state[0] ^
+// kScaleTag: a fresh or foreign workspace means no speculation), records spec in state[2]
+// and stores each CTA's observed max |x| in state[4 + cta] -- plain stores, nothing to
+// reset between calls.  The speculation held iff the observed max, scaled, neither
+// overflows fp16 nor sits more than 2 binades below the exact scale's [2^14, 2^15) (so
+// the split keeps its 22 significant bits for everything within 2^-16 of the max).
+// Otherwise the fallback launch redoes the conv with e = f16_row_exp(observed max) -- the
+// exact per-tensor scale; either way it leaves the observed max as the next speculation.
+constexpr int kScaleTag = 0x5ca1ab1e;
+__device__ __forceinline__ bool f16c_spec_ok(int spec, int obs) {
+    if (spec <= 0 || obs <= 0) return false;
+    const float top = __int_as_float(obs) * pow2f(f16_row_exp(__int_as_float(spec)));
+    return top < 65504.f && top >= 4096.f;
+}
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p) {
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// the max |x| a speculative launch scales with (0: none)
+__device__ __forceinline__ int f16c_spec_value(const int *state) {
+    const int s0 = ld_relaxed_gpu(state), s1 = ld_relaxed_gpu(state + 1);
+    return (s0 ^ kScaleTag) == s1 ? s0 : 0;
+}
+// speculative launch: the converter warps' max |x| -> this CTA's slot
+__device__ __forceinline__ void f16c_publish_max(const PairParams &PP, float amax, int *cta_max, int nconv) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, off));
+    if (PP.fallback) return;
+    if ((threadIdx.x & 31) == 0) atomicMax(cta_max, __float_as_int(amax));
+    asm volatile("bar.sync 2, %0;\n" ::"r"(32 * nconv) : "memory");   // the converter warps only
+    if (threadIdx.x == 256) PP.scale_state[4 + blockIdx.x] = *cta_max;
 }
 
 // A operand from tensor memory (TSA): tcgen05.mma [d], [a_tmem], b_desc -- the
@@ -470,6 +527,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     uint64_t *tfree = tconv + 6;                      // TSA: A slot in TMEM consumed
     uint64_t *lofree = tfree + 6;                     // LOSLOT: lo slot consumed by the MMAs
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(lofree + NL);
+    int &f16c_scale_max = reinterpret_cast<int *>(tmem_slot)[1];   // 3xF16C: the max |x| scaled with
+    int &f16c_cta_max = reinterpret_cast<int *>(tmem_slot)[2];     // 3xF16C: this CTA's observed max
+    // 3xF16C: the max |x| this launch scales with (speculative: the previous call's
+    // observation; fallback: this call's), and the per-CTA max its converters reduce into
+    if constexpr (F16C) {
+        if (threadIdx.x == 0) {
+            f16c_cta_max = 0;
+            if (PP.fallback) {   // the checking launch: reduce the speculative launch's maxima
+                pdl_wait();
+                int obs = 0;
+                for (int i = 0; i < PP.spec_ctas; ++i) obs = max(obs, ld_relaxed_gpu(PP.scale_state + 4 + i));
+                const int spec = ld_relaxed_gpu(PP.scale_state + 2);
+                f16c_scale_max = f16c_spec_ok(spec, obs) ? -1 : obs;   // -1: the speculation held
+                if (blockIdx.x == 0) {   // the next call speculates with this call's max
+                    PP.scale_state[0] = obs;
+                    PP.scale_state[1] = obs ^ kScaleTag;
+                }
+            }
+        }
+        __syncthreads();
+        if (PP.fallback && f16c_scale_max < 0) return;   // every thread of the pair: nothing to redo
+    }
 
     const int tid = threadIdx.x;
     // warp index through a shuffle: the compiler then knows it is warp-uniform
@@ -517,23 +596,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = *tmem_slot;
     pdl_wait();   // the prologue above overlapped the previous kernel's tail
+    if constexpr (F16C) {   // the speculation (state written by the previous call's fallback launch)
+        if (!PP.fallback) {
+            if (tid == 0) {
+                f16c_scale_max = f16c_spec_value(PP.scale_state);
+                if (blockIdx.x == 0) PP.scale_state[2] = f16c_scale_max;
+            }
+            __syncthreads();
+        }
+    }
+#ifdef CONVIO_TRACE   // per-CTA start / end (globaltimer ns): rows 16 / 17
+    if (PP.trace && tid == 0 && blockIdx.x < 1024) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        PP.trace[16 * 1024 + blockIdx.x] = g;
+    }
+#endif
 
     // work item -> (group, pair, n-block); n fastest
-    // split-K (P.splits > 1, non-halo): item = split * base_items + tile item; the
-    // split reduces k-blocks [kb_lo, kb_hi) and the epilogue adds its partial tile
+    // tail split-K (non-halo): tile items [0, tail_start) keep their whole K range; each
+    // later tile item is split into P.splits K ranges (work items tail_start + j, j =
+    // tile * splits + split), so the last round of the persistent grid is filled with
+    // partial tiles that the epilogue reduce-adds into the zeroed output
     auto krange = [&](int item, int &kb_lo, int &kb_hi) {
         if constexpr (HALO) {   // halo tiles never split (compile-time: no cost)
             kb_lo = 0;
             kb_hi = P.kblocks;
-            return 0;
+            return -1;
         }
-        const int spl = item / PP.base_items;
+        if (item < PP.tail_start) {
+            kb_lo = 0;
+            kb_hi = P.kblocks;
+            return -1;   // a whole tile
+        }
+        const int spl = (item - PP.tail_start) % P.splits;
         kb_lo = (int)(((int64_t)P.kblocks * spl) / P.splits);
         kb_hi = (int)(((int64_t)P.kblocks * (spl + 1)) / P.splits);
         return spl;
     };
     auto decode = [&](int item, int &grp, int &pair, int &nb) {
-        if constexpr (!HALO) item %= PP.base_items;
+        if constexpr (!HALO) {
+            if (item >= PP.tail_start) item = PP.tail_start + (item - PP.tail_start) / P.splits;
+        }
         nb = item % PP.nblocks;
         const int rest = item / PP.nblocks;
         pair = rest % PP.pairs_per_group;
@@ -849,7 +953,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 __syncwarp();
             }
         }
-    } else if (warp >= 4 && warp < 8 && P.splits <= 1) {
+    } else if (warp >= 4 && warp < 8) {
         // ---- epilogue (one K range per item): TMEM -> registers (unscale, bias, ReLU) ->
         // a 128-B-swizzled staging box in shared memory -> ONE TMA store per 32 channels.
         // Each lane owns an accumulator row (no transposes, no per-lane global stores),
@@ -859,7 +963,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int m = q * 32 + lane;                  // pixel row of this CTA's A block
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         const uint32_t stg = smem_u32(ring_end + 1024);
-        const int act_exp = F16C ? f16c_act_exp(P.row_exp, P.nred, lane) : 0;   // one per tensor
+        const int act_exp = F16C ? f16_row_exp(__int_as_float(f16c_scale_max)) : 0;   // one per tensor
         // staging row = position in the store box [img][y][x] (halo: the x valid columns)
         int srow;
         bool inbox;
@@ -876,6 +980,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
             int grp, pair, nb;
             decode(item, grp, pair, nb);
+            int kb_lo, kb_hi;
+            const int spl = krange(item, kb_lo, kb_hi);   // -1: a whole tile
+            const bool with_bias = P.bias != nullptr && spl <= 0;
             const int acc = NACC == 2 ? (t & 1) : 0;
             mbar_wait(tfull + acc, (t / NACC) & 1);
             if (q == 0 && lane == 0) PAIR_TRACE(5, t);
@@ -923,8 +1030,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 const int kc = k0 + c0;
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
-                    const float4 bv = P.bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4)
-                                             : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 bv = with_bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4)
+                                                : make_float4(0.f, 0.f, 0.f, 0.f);
                     float cs[4] = {1.f, 1.f, 1.f, 1.f};
                     if constexpr (F16X3 || F16C) {
                         const int4 ce = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + kc) + j4);
@@ -952,140 +1059,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 epi_bar();
                 if (issuer) {
-                    tma_store_4d(map_y, stg, kc, ox0, oy0, img0);
+                    if (spl >= 0) tma_reduce_add_4d(map_y, stg, kc, ox0, oy0, img0);
+                    else tma_store_4d(map_y, stg, kc, ox0, oy0, img0);
                     bulk_commit();
                 }
             }
         }
         if (issuer) bulk_wait0();
-    } else if (warp >= 4 && warp < 8) {
-        // ---- epilogue: TMEM -> registers -> NHWC global, both CTAs ------------------
-        const int q = warp - 4;                       // TMEM lane quadrant
-        const int m = q * 32 + lane;                  // pixel row of this CTA's A block
-        const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
-        float *stg = reinterpret_cast<float *>(ring_end + 1024) + q * (32 * 36);
-        const int act_exp = F16C ? f16c_act_exp(P.row_exp, P.nred, lane) : 0;   // one per tensor
-        int t = 0;
-        for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
-            int grp, pair, nb;
-            decode(item, grp, pair, nb);
-            int kb_lo, kb_hi;
-            const bool lead_split = krange(item, kb_lo, kb_hi) == 0;
-            const int acc = NACC == 2 ? (t & 1) : 0;
-            mbar_wait(tfull + acc, (t / NACC) & 1);
-            if (q == 0 && lane == 0) PAIR_TRACE(5, t);
-            __syncwarp();
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const int blk = pair * 2 + (int)rank;
-            int ox0, oy0, img0;
-            pair_block_origin(P, grp, blk, ox0, oy0, img0);
-            int img, oy, ox;
-            bool valid;
-            if (HALO) {   // row = (footprint row, column); wrap-around columns are not outputs
-                const int py = m / PP.fpr, px = m - py * PP.fpr;
-                img = img0; oy = oy0 + py; ox = ox0 + px;
-                valid = blk < PP.blocks_per_group && px < P.bx && img < P.n && oy < P.p && ox < P.q;
-            } else {
-                const int per_img = P.bx * P.by;
-                const int im = m / per_img, pix = m - im * per_img;
-                const int py = pix / P.bx, px = pix - py * P.bx;
-                img = img0 + im; oy = oy0 + py; ox = ox0 + px;
-                valid = blk < PP.blocks_per_group && m < per_img * P.imgs && img < P.n && oy < P.p &&
-                        ox < P.q;
-            }
-            const int k0 = nb * KOUT;
-            float *dst = P.y + (((int64_t)img * P.p + oy) * P.q + ox) * P.k + k0;
-            // coalesced stores: each warp transposes its 32 rows x 32 columns through
-            // shared memory so 8 lanes write one row's 128 contiguous bytes (a
-            // lane-per-row STG.128 touches 32 lines per instruction and made the
-            // epilogue, not the MMA, the limit of short-K tiles: Winograd GEMMs)
-            const int cc = 4 * (lane & 7);
-            float *drow[8];
-            bool vrow[8];
-            int rexp[8];   // F16X3: the rows' operand scale exponents
-            const int my_re = F16C ? act_exp
-                                   : ((F16X3 && valid) ? __ldg(P.row_exp + (int64_t)img * P.q + ox) : 0);
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int row = i * 4 + (lane >> 3);
-                drow[i] = reinterpret_cast<float *>(
-                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(dst), row));
-                vrow[i] = __shfl_sync(0xffffffffu, (int)valid, row) != 0;
-                rexp[i] = F16X3 ? __shfl_sync(0xffffffffu, my_re, row) : my_re;
-            }
-            // F16X3: every chunk's column exponents up front (a per-chunk load left its
-            // latency on the critical path of the epilogue, which then paced the MMAs)
-            constexpr bool UNSCALE = F16X3 || F16C;
-            constexpr int NCH = UNSCALE ? KOUT / 32 : 1;
-            int4 cexp_all[NCH];
-            if constexpr (UNSCALE) {
-#pragma unroll
-                for (int j = 0; j < NCH; ++j)
-                    cexp_all[j] = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + k0 + j * 32 + cc));
-            }
-            constexpr int EPI_UNROLL = UNSCALE ? NCH : 1;
-#pragma unroll EPI_UNROLL
-            for (int c0 = 0; c0 < KOUT; c0 += 32) {
-                float v[32];
-                tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
-                if constexpr (FOLD) {
-                    // y[p] = E[p][0:K] + E[p+1][K:2K] + E[p+2][2K:3K]: rows p+1, p+2 are
-                    // lanes +1, +2 of this warp (valid columns never cross a footprint row)
-#pragma unroll
-                    for (int sft = 1; sft < 3; ++sft) {
-                        float u[32];
-                        tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) +
-                                               (uint32_t)(acc * BN + sft * KOUT + c0), u);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += __shfl_down_sync(0xffffffffu, u[j], sft);
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < 32; j += 4)
-                    *reinterpret_cast<float4 *>(stg + lane * 36 + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                __syncwarp();
-                const int4 cexp = cexp_all[UNSCALE ? c0 / 32 : 0];
-                const float4 bv = P.bias && lead_split
-                                      ? __ldg(reinterpret_cast<const float4 *>(P.bias + k0 + c0 + cc))
-                                         : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                for (int i = 0; i < 8; ++i) {
-                    const int row = i * 4 + (lane >> 3);
-                    float4 o = *reinterpret_cast<const float4 *>(stg + row * 36 + cc);
-                    if constexpr (UNSCALE) {
-                        // exact powers of two, applied as two multiplies: each exponent is
-                        // within pow2f's range but their sum need not be (operands near
-                        // 2^-60 give row + column exponents past 126)
-                        const float rs = pow2f(-rexp[i]);
-                        o.x = (o.x * rs) * pow2f(-cexp.x);
-                        o.y = (o.y * rs) * pow2f(-cexp.y);
-                        o.z = (o.z * rs) * pow2f(-cexp.z);
-                        o.w = (o.w * rs) * pow2f(-cexp.w);
-                    }
-                    o.x += bv.x; o.y += bv.y; o.z += bv.z; o.w += bv.w;
-                    if (P.relu) {
-                        o.x = fmaxf(o.x, 0.f); o.y = fmaxf(o.y, 0.f);
-                        o.z = fmaxf(o.z, 0.f); o.w = fmaxf(o.w, 0.f);
-                    }
-#ifdef CONVIO_ABL_NOEPI
-                    if (vrow[i] && o.x == 12345.f) {
-#else
-                    if (vrow[i]) {
-#endif
-                        if (!HALO && P.splits > 1)   // partial sum of a K range: fp32 vector atomics
-                            atomicAdd(reinterpret_cast<float4 *>(drow[i] + c0 + cc), o);
-                        else
-                            *reinterpret_cast<float4 *>(drow[i] + c0 + cc) = o;
-                    }
-                }
-                __syncwarp();
-            }
-            // accumulator buffer drained: tell the leader's MMA issuer
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_leader + (uint32_t)(acc * 8));
-            if (q == 0 && lane == 0) PAIR_TRACE(6, t);
-        }
     } else if (TSA && F16C && warp >= 8) {
         // ---- 3xF16C TSA converters: warp (q, h) owns TMEM lanes 32q..32q+31 = A rows and
         // channel half h (fp32 tile h of the stage / footprint); each thread splits its row's
@@ -1095,7 +1075,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int m = q * 32 + lane;
         const uint32_t tconv_leader = mapa_shared(smem_u32(tconv), 0);
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(16 * h);
-        const float sc = pow2f(f16c_act_exp(P.row_exp, P.nred, lane));
+        const float sc = pow2f(f16_row_exp(__int_as_float(f16c_scale_max)));
+        const int a_rows = P.bx * P.by * P.imgs;      // rows the TMA boxes fill (no halo)
+        const int fp_rows = PP.fp_bytes / 128;        // footprint rows (halo)
+        float amax = 0.f;                             // max |x| over the real (loaded) rows
         int s = 0, ta = 0, it = 0, sa = 0;
         uint32_t ph = 0, pht = 0, pha = 0;
         uint32_t fa = 0;
@@ -1107,6 +1090,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             for (int kb = kb_lo; kb < kb_hi; ++kb, ++it) {
                 uint32_t row;
                 int sw;
+                bool real;   // a TMA-loaded row (not a wrap-around / beyond-the-box row)
                 if constexpr (HALO) {
                     if (tap == 0) {
                         mbar_wait(afull + sa, pha);
@@ -1118,10 +1102,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     const int fr = m + r * PP.fpr + sx;
                     row = fa + (h ? (uint32_t)PP.a_slot : 0u) + (uint32_t)fr * 128;
                     sw = fr & 7;
+                    real = fr < fp_rows;
                 } else {   // ARING: the A slot (the filter planes are the MMA issuer's to wait for)
                     mbar_wait(afull + sa, pha);
                     row = smem_u32(aring + sa * ASLOT) + (h ? (uint32_t)A_BYTES : 0u) + (uint32_t)m * 128;
                     sw = m & 7;
+                    real = m < a_rows;
                 }
                 if (it >= NTA) mbar_wait(tfree + ta, pht ^ 1);
                 if (warp == 8 && lane == 0) PAIR_TRACE(1, it);
@@ -1134,6 +1120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {   // fp32 chunk c: channels 32h + 4c .. 4c + 3
                     const float4 v = lds128(row + (uint32_t)((c ^ sw) << 4));
+                    if (real) amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
                     const __half2 h0 = __floats2half2_rn(v.x * sc, v.y * sc);
                     const __half2 h1 = __floats2half2_rn(v.z * sc, v.w * sc);
                     const float2 f0 = __half22float2(h0), f1 = __half22float2(h1);
@@ -1178,6 +1165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 }
             }
         }
+        f16c_publish_max(PP, amax, &f16c_cta_max, NCW);
     } else if (TSA && warp >= 8) {
         // ---- TSA converters: warp q owns TMEM lanes 32q..32q+31 = A rows; each
         // thread reads its row's 32 channels from the SW128 stage, writes the
@@ -1235,9 +1223,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int ct = tid - 256;                    // 0 .. 255
         const uint32_t conv_leader = mapa_shared(smem_u32(conv), 0);
         const uint32_t aconv_leader = mapa_shared(smem_u32(aconv), 0);
-        const float sc = pow2f(f16c_act_exp(P.row_exp, P.nred, lane));
+        const float sc = pow2f(f16_row_exp(__int_as_float(f16c_scale_max)));
         const int a_rows = P.bx * P.by * P.imgs;
         const int fp_rows = PP.fp_bytes / 128;
+        float amax = 0.f;
         int s = 0, sa = 0, kbc = 0;
         uint32_t ph = 0, pha = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
@@ -1249,7 +1238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     mbar_wait(afull + sa, pha);
                     const uint32_t f0 = smem_u32(aring + sa * ASLOT);
 #ifndef CONVIO_ABL_NOCONV
-                    convert_f16_rows<32 * NCW>(f0, f0 + (uint32_t)PP.a_slot, fp_rows, ct, sc);
+                    convert_f16_rows<32 * NCW>(f0, f0 + (uint32_t)PP.a_slot, fp_rows, ct, sc, amax);
 #endif
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     __syncwarp();
@@ -1264,7 +1253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 if constexpr (!HALO) {
                     const uint32_t st = smem_u32(bring + s * STAGE);
 #ifndef CONVIO_ABL_NOCONV
-                    convert_f16_rows<32 * NCW>(st, st + A_BYTES + B_BYTES, a_rows, ct, sc);
+                    convert_f16_rows<32 * NCW>(st, st + A_BYTES + B_BYTES, a_rows, ct, sc, amax);
 #endif
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 }
@@ -1279,6 +1268,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 }
             }
         }
+        f16c_publish_max(PP, amax, &f16c_cta_max, NCW);
     } else if (SPLIT && !TSA && warp >= 8) {
         // ---- converters: lo = v - tf32(v) of this CTA's staged operands (3xTF32) ----
         const int ct = tid - 256;                    // 0 .. 32*NCW-1
@@ -1330,6 +1320,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         }
     }
     // ---- teardown ---------------------------------------------------------------------
+#ifdef CONVIO_TRACE
+    if (PP.trace && warp == 4 && lane == 0 && blockIdx.x < 1024) {
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        PP.trace[17 * 1024 + blockIdx.x] = g;
+    }
+#endif
     __syncwarp();   // role lanes rejoin their warps before the .aligned cluster barrier
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     cluster_sync_all();

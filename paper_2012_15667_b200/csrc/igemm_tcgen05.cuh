@@ -415,6 +415,8 @@ struct IgemmPlan {
     bool tsa = false;        // 3xTF32 pair kernel with the A operand in TMEM
     bool fold = false;       // halo + the S horizontal taps in one MMA of N = S * K
     int resb_slots = 0;      // halo TSA: filter slice resident in smem (one slot per k-block)
+    int64_t tail_start = 0;  // pair kernel: tile items from here on are split-K (P.splits)
+    int *scale_state = nullptr;   // 3xF16C: speculative activation scale state (workspace)
     PairFn pfn = nullptr;
     int groups = 1, blocks_per_group = 0;
     int fpr = 0, fp_bytes = 0, a_slot = 0, na = 0;

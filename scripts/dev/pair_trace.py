@@ -43,10 +43,17 @@ def main():
     torch.cuda.synchronize()
     C.conv_igemm(x, w, padding=1, stride=spec.stride, tile=tile, precision=args.prec)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (16 * 1024))()
+    buf = (ctypes.c_ulonglong * (18 * 1024))()
     lib = N.lib()
     assert lib.convio_dev_trace(buf) == 0, "not a CONVIO_TRACE build"
-    tr = np.frombuffer(buf, dtype=np.uint64).reshape(16, 1024).astype(np.int64)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(18, 1024).astype(np.int64)
+    st, en = tr[16], tr[17]
+    ok = (st > 0) & (en > 0)
+    if ok.any():
+        t0g = st[ok].min()
+        dur = (en[ok] - t0g) / 1e3
+        print(f"per-CTA end (us after first start): min {dur.min():.1f} med {np.median(dur):.1f} max {dur.max():.1f}; "
+              f"start spread {(st[ok].max() - t0g) / 1e3:.1f} us; CTAs {int(ok.sum())}")
     peer = tr[8:16]
     tr = tr[0:8]
     nz = [int((tr[r] > 0).sum()) for r in range(7)]

@@ -30,6 +30,10 @@ def test_tuned_resnet50_plans_replay_in_a_cuda_graph():
         layers.append(layer)
         xs.append(x)
         ys.append(layer.run(x))
+        # a second eager call: the steady state the graph replays (3xF16 implicit GEMMs
+        # speculate their activation scale from the previous call on the same workspace;
+        # the first call on a fresh one takes the exact-scale fallback with whole-K tiles)
+        layer.run(x, out=ys[-1])
     torch.cuda.synchronize()
     eager = [y.clone() for y in ys]
     side = torch.cuda.Stream(dev)

@@ -122,3 +122,29 @@ def test_igemm_3xf16_rejects_single_cta_and_c_not_multiple_of_64():
     with pytest.raises(InfeasibleTileError):
         C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, precision="3xf16",
                      tile=TileConfig(14, 7, 64, 32768, 1, 1, 2, layout="HWC"))
+
+
+@pytest.mark.parametrize("tile", [TileConfig(14, 7, 128, 32768, 1, 1, 2, layout="HWC"),
+                                  TileConfig(2, 1, 128, 32768, 1, 1, 4, layout="HWC"),
+                                  TileConfig(14, 8, 128, 32768, 2, 1, 4, layout="HWC")],
+                         ids=["pair", "tsa", "halo tsa"])
+def test_igemm_3xf16_speculative_scale(tile):
+    """The activation scale is speculated from the previous call on the same workspace
+    (state in its first bytes) and checked on the device against this call's max |x|:
+    the same data reuses it; a 2^20 jump (fp16 overflow) or a 2^-20 drop (lost bits)
+    makes the checking launch redo the conv with the exact scale.  Every call must match
+    the oracle, and the state must end up holding the last call's max |x|."""
+    x, wt = _inputs(2, 64, 28, 28, 128)
+    w = torch.from_numpy(wt).cuda()
+    info = C.query(x.shape, wt.shape, 1, 1, "HWC", tile, "igemm_3xf16")
+    assert info["rc"] == 0, info
+    ws = torch.full((info["workspace_bytes"],), 0x7f, dtype=torch.uint8, device="cuda")   # foreign bytes
+    ref = co.direct_conv(x, wt, 1, 1)
+    for scale in (1.0, 1.0, 2.0 ** 20, 2.0 ** 20, 2.0 ** -20, 1.0, 3.0):
+        xs = (x * np.float32(scale)).astype(np.float32)
+        y = C.conv_igemm(_hwc(xs), w, padding=1, tile=tile, precision="3xf16", workspace=ws)
+        err = co.rel_err(y.contiguous().cpu().numpy(), ref * scale)
+        assert np.isfinite(err) and err <= tol_3xtf32(64), (scale, err)
+        state = ws[:8].view(torch.int32).cpu().numpy()
+        assert state[0] == np.float32(np.abs(xs).max()).view(np.int32), (scale, state)
+        assert state[1] == state[0] ^ 0x5CA1AB1E
