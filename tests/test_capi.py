@@ -134,10 +134,16 @@ def test_tensor_core_projections_plan_pairs_split_k_and_chunks():
     s2 = query((256, 512, 14, 14), (512, 512, 3, 3), 2, 1, hwc,
                TileConfig(1, 1, 256, 32768, 1, 1, 2, layout=hwc), "igemm_3xtf32")
     assert s2["rc"] == 0 and "CTA pair" in s2["reason"] and "split-K" in s2["reason"]
-    # res4 stride 2: 196 items, 88 % rounds efficiency -> not worth the atomics
+    # res4 stride 2: 196 items = 2.65 rounds -> the last 48 tile items split 3 ways
+    # (2 x 36 + 2 x 12 k-blocks per pair instead of 3 x 36)
     s4 = query((256, 256, 28, 28), (256, 256, 3, 3), 2, 1, hwc,
                TileConfig(1, 2, 256, 32768, 1, 1, 2, layout=hwc), "igemm_3xtf32")
-    assert s4["rc"] == 0 and "split-K" not in s4["reason"]
+    assert s4["rc"] == 0 and "split-K" in s4["reason"]
+    # res3 A-in-TMEM at batch 256: 784 items = 10.6 rounds of 18 k-blocks; a split tail
+    # saves < 5 % -> whole tiles
+    s3 = query((256, 128, 28, 28), (128, 128, 3, 3), 1, 1, hwc,
+               TileConfig(1, 4, 128, 32768, 1, 1, 4, layout=hwc), "igemm_3xf16")
+    assert s3["rc"] == 0 and "split-K" not in s3["reason"]
     # halo + fold tiles never split
     fold = query((4, 64, 56, 56), (64, 64, 3, 3), 1, 1, hwc,
                  TileConfig(30, 4, 64, 32768, 2, 1, 2, layout=hwc), "igemm_3xtf32")
