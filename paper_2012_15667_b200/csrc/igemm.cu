@@ -106,42 +106,47 @@ static int kblock_channels(int kind) {
 
 // 3xF16C filter operand: KCRS -> fp16 hi / lo planes [2][R*S][K][C] with one
 // power-of-two scale per output channel k over its C*R*S weights (col_exp[k],
-// undone by the GEMM epilogue).  One warp per output channel.
+// undone by the GEMM epilogue).  One block per output channel: the row's max by a
+// block reduction, then tap-major passes where each thread writes __half2 pairs of
+// channels (coalesced plane rows; the strided KCRS re-reads hit L1).
 __global__ void __launch_bounds__(256) pack_filter_f16x3_kernel(const float *__restrict__ w,
                                                                 __half *__restrict__ wq,
                                                                 int *__restrict__ col_exp, int k, int c,
                                                                 int rs) {
     pdl_wait();
-    const int lane = threadIdx.x & 31;
+    __shared__ float red[8];
     const int crs = c * rs;
     const int64_t plane = (int64_t)rs * k * c;
-    for (int kk = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; kk < k; kk += (gridDim.x * blockDim.x) >> 5) {
+    for (int kk = blockIdx.x; kk < k; kk += gridDim.x) {
         const float *wr = w + (int64_t)kk * crs;
         float mx = 0.0f;
-        for (int j = lane; j < crs; j += 32) mx = fmaxf(mx, fabsf(wr[j]));
+        for (int j = threadIdx.x; j < crs; j += blockDim.x) mx = fmaxf(mx, fabsf(wr[j]));
         for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = red[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
         const int e = f16_row_exp(mx);
         const float sc = pow2f(e);
-        // tap-major: lane pairs of channels, so each warp store is 128 contiguous bytes of
-        // a [tap][k][c] plane row (the KCRS row re-reads hit L1 after the max pass)
-        for (int tap = 0; tap < rs; ++tap) {
+        const int pairs = (c + 1) / 2;
+        for (int t = threadIdx.x; t < rs * pairs; t += blockDim.x) {
+            const int tap = t / pairs, cc = 2 * (t - tap * pairs);
             __half *hrow = wq + ((int64_t)tap * k + kk) * c;
-            for (int cc = 2 * lane; cc < c; cc += 64) {
-                const float v0 = wr[cc * rs + tap] * sc;
-                const float v1 = cc + 1 < c ? wr[(cc + 1) * rs + tap] * sc : 0.0f;
-                const __half2 hi = __floats2half2_rn(v0, v1);
-                const float2 hf = __half22float2(hi);
-                const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
-                if (cc + 1 < c) {
-                    *reinterpret_cast<__half2 *>(hrow + cc) = hi;
-                    *reinterpret_cast<__half2 *>(hrow + plane + cc) = lo;
-                } else {
-                    hrow[cc] = __low2half(hi);
-                    hrow[plane + cc] = __low2half(lo);
-                }
+            const float v0 = wr[cc * rs + tap] * sc;
+            const float v1 = cc + 1 < c ? wr[(cc + 1) * rs + tap] * sc : 0.0f;
+            const __half2 hi = __floats2half2_rn(v0, v1);
+            const float2 hf = __half22float2(hi);
+            const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+            if (cc + 1 < c) {
+                *reinterpret_cast<__half2 *>(hrow + cc) = hi;
+                *reinterpret_cast<__half2 *>(hrow + plane + cc) = lo;
+            } else {
+                hrow[cc] = __low2half(hi);
+                hrow[plane + cc] = __low2half(lo);
             }
         }
-        if (lane == 0) col_exp[kk] = e;
+        if (threadIdx.x == 0) col_exp[kk] = e;
+        __syncthreads();   // red[] is reused by the next row
     }
 }
 
@@ -717,7 +722,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
 }
 
 int launch_pack_filter_f16x3(const convio_conv_desc *desc, const float *w, void *packed, cudaStream_t stream) {
-    const int blocks = std::max(1, std::min((desc->k + 7) / 8, 148 * 8));
+    const int blocks = std::max(1, std::min(desc->k, 148 * 8));
     __half *planes = (__half *)packed;
     int *col_exp = (int *)((uint8_t *)packed + align256((size_t)4 * desc->k * desc->c * desc->r * desc->s));
     CONVIO_CUDA_TRY(launch_pdl(pack_filter_f16x3_kernel, dim3(blocks), dim3(256), 0, stream, w, planes, col_exp,

@@ -532,18 +532,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     // 3xF16C: the max |x| this launch scales with (speculative: the previous call's
     // observation; fallback: this call's), and the per-CTA max its converters reduce into
     if constexpr (F16C) {
-        if (threadIdx.x == 0) {
-            f16c_cta_max = 0;
-            if (PP.fallback) {   // the checking launch: reduce the speculative launch's maxima
-                pdl_wait();
-                int obs = 0;
-                for (int i = 0; i < PP.spec_ctas; ++i) obs = max(obs, ld_relaxed_gpu(PP.scale_state + 4 + i));
+        if (threadIdx.x == 0) f16c_cta_max = 0;
+        if (PP.fallback) {   // the checking launch: reduce the speculative launch's per-CTA maxima
+            pdl_wait();
+            int obs = threadIdx.x < PP.spec_ctas ? ld_relaxed_gpu(PP.scale_state + 4 + threadIdx.x) : 0;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) obs = max(obs, __shfl_xor_sync(0xffffffffu, obs, off));
+            if (threadIdx.x == 0) f16c_scale_max = 0;
+            __syncthreads();
+            if ((threadIdx.x & 31) == 0 && obs > 0) atomicMax(&f16c_scale_max, obs);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                const int o = f16c_scale_max;
                 const int spec = ld_relaxed_gpu(PP.scale_state + 2);
-                f16c_scale_max = f16c_spec_ok(spec, obs) ? -1 : obs;   // -1: the speculation held
                 if (blockIdx.x == 0) {   // the next call speculates with this call's max
-                    PP.scale_state[0] = obs;
-                    PP.scale_state[1] = obs ^ kScaleTag;
+                    PP.scale_state[0] = o;
+                    PP.scale_state[1] = o ^ kScaleTag;
                 }
+                if (f16c_spec_ok(spec, o)) f16c_scale_max = -1;   // the speculation held
             }
         }
         __syncthreads();
