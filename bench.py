@@ -871,7 +871,7 @@ def main() -> None:
         for vname, allowed in (("fp32_cuda_cores", CUDA_CORE_ALGORITHMS),
                                # the direct (DC) dataflows only: every layer within the
                                # 1.5 x Q_DRAM gate (Winograd's V / M planes exceed it)
-                               ("fp32_direct_only", ("direct", "igemm_3xtf32")),
+                               ("fp32_direct_only", ("direct", "igemm_3xtf32", "igemm_3xf16")),
                                ("tf32_tcgen05", ("igemm_tf32", "winograd_tc_tf32")),
                                ("bf16_tcgen05", ("igemm_bf16", "winograd_tc_bf16"))):
             vplans = load_plans(args.workload, allowed, n=n_local)

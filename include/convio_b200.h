@@ -187,10 +187,17 @@ int convio_conv_igemm_3xtf32(const convio_conv_desc *desc, const convio_tile *ti
  * BF16 the fp32 activations are converted to bf16 NHWC in the workspace first
  * (C % 64 == 0), filters packed to bf16 [R*S][K][C] unless `w_is_packed`
  * (then w holds convio_pack_filter_igemm_bf16 output).  For 3xF16 (CTA pair
- * tiles, C % 64 == 0) the workspace (256-byte aligned) holds the |x| maxima and,
- * unless `w_is_packed` (convio_pack_filter_igemm_f16x3 output), the packed
- * filter; the activations stay fp32 in HBM and are split on chip.  Replaces the
- * same schedule as convio_conv_direct_f32 (dataflow.py:219-250). */
+ * tiles, C % 64 == 0) the workspace (256-byte aligned) starts with the
+ * activation-scale state and, unless `w_is_packed` (convio_pack_filter_igemm_f16x3
+ * output), holds the packed filter; the activations stay fp32 in HBM and are split
+ * on chip with one power-of-two scale per tensor.  That scale is speculated from the
+ * max |x| the previous call on the SAME workspace observed; every call checks it on
+ * the device (a second launch) and redoes the conv with the exact scale when it
+ * would overflow fp16 or lose precision, so results never depend on the state --
+ * reusing a layer's workspace across calls only makes them faster (any bytes,
+ * e.g. a fresh or foreign workspace, mean "no speculation").  Two launches per
+ * call; not reentrant on one workspace.  Replaces the same schedule as
+ * convio_conv_direct_f32 (dataflow.py:219-250). */
 int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
                       const float *x, const void *w, int32_t w_is_packed, const float *bias,
                       int32_t relu, float *y, void *workspace, size_t workspace_bytes, void *stream);

@@ -146,7 +146,9 @@ def load_plans(workload: str, allowed=FP32_ALGORITHMS, n: int | None = None) -> 
     return plans
 
 
-# 3xF16 implicit GEMM: |x| maxima scratch (the C-ABI's absmax partials, 296 ints)
+# 3xF16 implicit GEMM: the speculative activation-scale state (tagged max |x| of the
+# previous call + one observed max per CTA) at the start of the layer's workspace; it
+# persists across calls, which is what lets the second and later calls skip the redo
 F16X3_PARTIALS_BYTES = 256 * ((4 * 296 + 255) // 256)
 
 
