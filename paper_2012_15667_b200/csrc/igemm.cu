@@ -267,7 +267,7 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
                                                  (loslot ? 1 : mult);
         const size_t a_ring = pl->halo ? (size_t)pl->na * pl->a_slot * mult
                                        : (aring ? (size_t)pl->na * 2 * 128 * 128 : (loslot ? 2 * stage_bytes : 0));
-        const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
+        const size_t budget = 227 * 1024 - 1024 - 1024 - pair_epi_bytes(pl->fold) - pair_epi_const_bytes(pl->P.k);
         if (a_ring + 2 * stage_bytes > budget)
             return pfail(reason, rlen, CONVIO_EINFEASIBLE, "tcgen05 pair footprint ring does not fit");
         // small stages (narrow BN, no lo copy) need many in flight to cover the
@@ -286,7 +286,8 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         pl->pair = true;
         pl->pfn = pfn;
         pl->fn = nullptr;
-        pl->smem = a_ring + stages * stage_bytes + 1024 + 1024 + kPairEpiBytes;
+        pl->smem = a_ring + stages * stage_bytes + 1024 + 1024 + pair_epi_bytes(pl->fold) +
+                   pair_epi_const_bytes(pl->P.k);
         pl->bn = bn;
         pl->kind = kind;
         pl->threads = kind == KIND_3XF16C ? 512 : (kind == KIND_3XTF32 ? ((bn >= 256 || pl->tsa) ? 384 : 512) : 256);
@@ -404,7 +405,7 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
     // res2 / VGG conv1_2: 3 x 24 KB)
     {
         const int mult = (kind == KIND_3XTF32 || kind == KIND_3XF16C) ? 2 : 1;
-        const size_t budget = 227 * 1024 - 1024 - 1024 - kPairEpiBytes;
+        const size_t budget = 227 * 1024 - 1024 - 1024 - pair_epi_bytes(pl->fold) - pair_epi_const_bytes(d->k);
         const size_t stage = (size_t)((pl->fold ? d->s * t->z : t->z) / 2) * 128 * mult;
         const size_t slot = (size_t)pl->a_slot * mult;
         const int kblocks = (pl->fold ? d->r : d->r * d->s) * (d->c / kblock_channels(kind));
@@ -415,6 +416,7 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
             if ((size_t)pl->na * slot + slice <= budget) pl->resb_slots = kblocks;
         }
     }
+    P.k = d->k;   // (plan_ring sizes the epilogue's per-channel constants by K)
     int rc = plan_ring(pl, pl->fold ? d->s * t->z : t->z, kind, t->s_b, true, reason, rlen);
     if (rc) return rc;
     P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
@@ -473,6 +475,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
                     "tcgen05 tiles take n_xt = n_yt = 1 and n_zt in {1 (one CTA), 2 (CTA pair), "
                     "4 (CTA pair, 3xTF32 / 3xF16 A operand in TMEM)}");
     pl->tsa = t->n_zt == 4;
+    P.k = d->k;   // (plan_ring sizes the epilogue's per-channel constants by K)
     int rc = plan_ring(pl, t->z, kind, t->s_b, t->n_zt >= 2, reason, rlen);
     if (rc) return rc;
     const int imgs = std::max(1, std::min(128 / px, d->n));
@@ -512,6 +515,7 @@ int plan_igemm_batched(int kind, int bn, int s_b, bool pair, bool tsa, int xi, i
     IgemmParams &P = pl->P;
     memset(&P, 0, sizeof(P));
     pl->tsa = pair && tsa;
+    P.k = k;   // (plan_ring sizes the epilogue's per-channel constants by K)
     int rc = plan_ring(pl, bn, kind, s_b, pair, reason, rlen);
     if (rc) return rc;
     P.n = xi; P.c = c; P.h = 1; P.w = t_count; P.k = k; P.p = 1; P.q = t_count;
@@ -599,7 +603,7 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
     pl.P.y = y;
     pl.P.relu = relu;
     if (pl.pair) {
-        PairParams PP;
+        PairParams PP{};   // value-initialised: every field not set below is 0
         PP.g = pl.P;
         PP.groups = pl.groups;
         PP.blocks_per_group = pl.blocks_per_group;
@@ -632,8 +636,8 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.trace = nullptr;
 #ifdef CONVIO_TRACE
         static unsigned long long *d_trace = nullptr;
-        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 18 * 1024 * sizeof(unsigned long long)));
-        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 18 * 1024 * sizeof(unsigned long long), stream));
+        if (!d_trace) CONVIO_CUDA_TRY(cudaMalloc(&d_trace, 24 * 1024 * sizeof(unsigned long long)));
+        CONVIO_CUDA_TRY(cudaMemsetAsync(d_trace, 0, 24 * 1024 * sizeof(unsigned long long), stream));
         PP.trace = d_trace;
         g_trace_ptr = d_trace;
 #endif
@@ -806,7 +810,7 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
 // dev builds only: copy the last pair-kernel pipeline trace (8 x 1024 clock64 stamps)
 int convio_dev_trace(unsigned long long *host) {
     if (!g_trace_ptr) return CONVIO_EINVAL;
-    return cudaMemcpy(host, g_trace_ptr, 18 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
+    return cudaMemcpy(host, g_trace_ptr, 24 * 1024 * sizeof(unsigned long long), cudaMemcpyDeviceToHost) ==
                    cudaSuccess
                ? CONVIO_OK
                : CONVIO_EINTERNAL;

@@ -42,8 +42,17 @@
 
 namespace convio {
 
-// epilogue staging box after the ring + barriers: 128 rows x 32 fp32 channels (one TMA store)
+// epilogue staging box after the ring + barriers: 128 rows x 32 fp32 channels (one TMA store);
+// FOLD tiles (3-k-block items: the drain paces the MMAs) double-buffer it
 constexpr size_t kPairEpiBytes = 128 * 32 * sizeof(float);
+constexpr size_t pair_epi_bytes(bool fold) { return fold ? 2 * kPairEpiBytes : kPairEpiBytes; }
+// after the staging box(es): the epilogue's per-channel constants in shared memory --
+// bias[K] and the 3xF16 column scales 2^-e[k] as floats (K <= kEpiConstK; larger K
+// reads them from global memory).  Per-lane __ldg's of 32 biases + 32 exponents per
+// chunk (~2k cycles of dependent L1/L2 latency) had made the drain the pacer of short
+// items (fold tiles: 3 k-blocks)
+constexpr int kEpiConstK = 1024;
+inline size_t pair_epi_const_bytes(int k) { return k <= kEpiConstK ? (size_t)8 * k : 0; }
 
 struct PairParams {
     IgemmParams g;          // geometry as in the single-CTA kernel
@@ -62,6 +71,12 @@ struct PairParams {
     int *scale_state;
     int fallback;
     int spec_ctas;          // the speculative launch's CTA count (its partial maxima)
+    // gather halo (HALO + TSA, gather = 1): A row m = output pixel (img, py, px) of an
+    // exact x * y * imgs block (no wrap-around columns); the footprint box is
+    // [imgs][fh][fw] pixels, fw = (x - 1) * stride + S, and the converters read tap (r, s)
+    // of row m at footprint pixel (img, py * stride + r, px * stride + s)
+    int gather;
+    int fw, fh;
     // halo staging (HALO kernels): the (y + R - 1) x fpr input footprint of a
     // 128-row block is staged ONCE per channel block; tap (r, s) is the view
     // starting (r * fpr + s) rows into it (rows = y x fpr pixels, x = fpr - S + 1
@@ -83,9 +98,17 @@ struct PairParams {
     do {                                                                                        \
         if (PP.trace && blockIdx.x < 2 && (i) < 1024) PP.trace[((row) + 8 * blockIdx.x) * 1024 + (i)] = clock64(); \
     } while (0)
+// fine epilogue stamps (leader CTA of cluster 0, warp 4 lane 0): rows 18..23
+#define EPI_TRACE(row, i)                                                                       \
+    do {                                                                                        \
+        if (PP.trace && blockIdx.x == 0 && (i) < 1024) PP.trace[(row) * 1024 + (i)] = clock64(); \
+    } while (0)
 #else
 #define PAIR_TRACE(row, i) \
     do {                   \
+    } while (0)
+#define EPI_TRACE(row, i) \
+    do {                  \
     } while (0)
 #endif
 
@@ -136,6 +159,20 @@ __device__ __forceinline__ void tma_reduce_add_4d(uint64_t map, uint32_t src, in
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+// tcgen05.ld without the wait: several loads in flight, one tcgen05.wait::ld
+__device__ __forceinline__ void tmem_ld_x32_nowait(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+        "%12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, "
+        "%30, %31}, [%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+          "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+          "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+}
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 // named barrier among the 4 epilogue warps (id 1; id 0 is __syncthreads)
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
@@ -969,11 +1006,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const int m = q * 32 + lane;                  // pixel row of this CTA's A block
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         const uint32_t stg = smem_u32(ring_end + 1024);
+        // per-channel epilogue constants (not for the batched Winograd GEMMs: their column
+        // exponents differ per xi) staged once by the 4 epilogue warps
+        const bool cs_smem = !F16X3 && P.k <= kEpiConstK;
+        float *ebias = reinterpret_cast<float *>(ring_end + 1024 + pair_epi_bytes(FOLD));
+        float *escale = ebias + P.k;
         const int act_exp = F16C ? f16_row_exp(__int_as_float(f16c_scale_max)) : 0;   // one per tensor
+        // 3xF16C: one FFMA per output, y = acc * 2^-(e_act + e_k) + b_k, when every channel's
+        // exponent sum is a normal power of two (always, but for operands near 2^-60); else
+        // the two exact multiplies
+        bool fused_scale = false;
+        if (cs_smem) {
+            bool ok = true;
+            for (int k = m; k < P.k; k += 128) {
+                ebias[k] = P.bias ? __ldg(P.bias + k) : 0.f;
+                if constexpr (F16C) {
+                    const int ek = __ldg(P.col_exp + k), e = act_exp + ek;
+                    ok = ok && e >= -126 && e <= 127;
+                    escale[k] = pow2f(-ek);
+                } else {
+                    escale[k] = 1.f;
+                }
+            }
+            uint32_t all;
+            asm volatile("{\n.reg .pred p, q;\nsetp.ne.u32 q, %1, 0;\nbar.red.and.pred p, 1, 128, q;\n"
+                         "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(all) : "r"((uint32_t)ok) : "memory");
+            fused_scale = F16C && all;
+            if (fused_scale)   // fold the tensor scale into the column scales
+                for (int k = m; k < P.k; k += 128) escale[k] = pow2f(-(act_exp + __ldg(P.col_exp + k)));
+            epi_bar();
+        }
         // staging row = position in the store box [img][y][x] (halo: the x valid columns)
         int srow;
         bool inbox;
-        if (HALO) {
+        if (HALO && !PP.gather) {
             const int py = m / PP.fpr, px = m - py * PP.fpr;
             srow = py * P.bx + px;
             inbox = px < P.bx;
@@ -982,6 +1048,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             inbox = m < P.bx * P.by * P.imgs;
         }
         const bool issuer = q == 0 && lane == 0;
+        int nbox = 0;
         int t = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters, ++t) {
             int grp, pair, nb;
@@ -990,15 +1057,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             const int spl = krange(item, kb_lo, kb_hi);   // -1: a whole tile
             const bool with_bias = P.bias != nullptr && spl <= 0;
             const int acc = NACC == 2 ? (t & 1) : 0;
-            mbar_wait(tfull + acc, (t / NACC) & 1);
-            if (q == 0 && lane == 0) PAIR_TRACE(5, t);
-            __syncwarp();
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            // the item's geometry (integer divisions) before the wait, not after it
             const int blk = pair * 2 + (int)rank;
             int ox0, oy0, img0;
             pair_block_origin(P, grp, blk, ox0, oy0, img0);
             const int k0 = nb * KOUT;
-            float rs = 1.f;   // the row's operand scale (3xF16 families)
+            float rs = 1.f;   // the row's operand scale (3xF16 families; 1 when folded into escale)
             if constexpr (F16X3) {
                 const int per_img = P.bx * P.by;
                 const int im = m / per_img, pix = m - im * per_img;
@@ -1007,24 +1071,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 const bool ok = inbox && img < P.n && oy0 + py < P.p && ox < P.q;
                 rs = pow2f(-(ok ? __ldg(P.row_exp + (int64_t)img * P.q + ox) : 0));
             } else if constexpr (F16C) {
-                rs = pow2f(-act_exp);
+                rs = fused_scale ? 1.f : pow2f(-act_exp);
             }
+            mbar_wait(tfull + acc, (t / NACC) & 1);
+            if (q == 0 && lane == 0) PAIR_TRACE(5, t);
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (q == 0 && lane == 0) EPI_TRACE(18, t);
 #pragma unroll 1
             for (int c0 = 0; c0 < KOUT; c0 += 32) {
                 float v[32];
-                tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
                 if constexpr (FOLD) {
                     // y[p] = E[p][0:K] + E[p+1][K:2K] + E[p+2][2K:3K]: rows p+1, p+2 are
-                    // lanes +1, +2 of this warp (valid columns never cross a footprint row)
+                    // lanes +1, +2 of this warp (valid columns never cross a footprint row);
+                    // the three loads in flight together, one wait
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0);
+                    uint32_t r0[32], r1[32], r2[32];
+                    tmem_ld_x32_nowait(ta, r0);
+                    tmem_ld_x32_nowait(ta + (uint32_t)KOUT, r1);
+                    tmem_ld_x32_nowait(ta + (uint32_t)(2 * KOUT), r2);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    if (c0 == 0 && q == 0 && lane == 0) EPI_TRACE(19, t);
 #pragma unroll
-                    for (int sft = 1; sft < 3; ++sft) {
-                        float u[32];
-                        tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) +
-                                               (uint32_t)(acc * BN + sft * KOUT + c0), u);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += __shfl_down_sync(0xffffffffu, u[j], sft);
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        v[j] = __uint_as_float(r0[j]) +
+                               __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1) +
+                               __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
+                } else {
+                    tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
+                    if (c0 == 0 && q == 0 && lane == 0) EPI_TRACE(19, t);
                 }
+                if (c0 == 0 && q == 0 && lane == 0) EPI_TRACE(20, t);
                 if (c0 + 32 >= KOUT) {   // accumulator fully read: hand it back to the MMA issuer
                     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                     __syncwarp();
@@ -1036,37 +1113,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 const int kc = k0 + c0;
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
-                    const float4 bv = with_bias ? __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4)
-                                                : make_float4(0.f, 0.f, 0.f, 0.f);
+                    float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
                     float cs[4] = {1.f, 1.f, 1.f, 1.f};
-                    if constexpr (F16X3 || F16C) {
-                        const int4 ce = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + kc) + j4);
-                        cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
+                    if (cs_smem) {   // broadcast LDS.128: every lane reads the same channels
+                        if (with_bias) bv = *reinterpret_cast<const float4 *>(ebias + kc + 4 * j4);
+                        if constexpr (F16C) {
+                            const float4 c4 = *reinterpret_cast<const float4 *>(escale + kc + 4 * j4);
+                            cs[0] = c4.x; cs[1] = c4.y; cs[2] = c4.z; cs[3] = c4.w;
+                        }
+                    } else {
+                        if (with_bias) bv = __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4);
+                        if constexpr (F16X3 || F16C) {
+                            const int4 ce = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + kc) + j4);
+                            cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
+                        }
                     }
                     const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         float o = v[4 * j4 + u];
-                        if constexpr (F16X3 || F16C) o = (o * rs) * cs[u];
-                        o += b4[u];
+                        if constexpr (F16X3 || F16C) o = fmaf(fused_scale ? o : o * rs, cs[u], b4[u]);
+                        else o += b4[u];
                         v[4 * j4 + u] = P.relu ? fmaxf(o, 0.f) : o;
                     }
                 }
-                if (issuer) bulk_wait_read0();   // the previous chunk's store has read the box
+                if (c0 == 0 && q == 0 && lane == 0) PAIR_TRACE(7, t);   // chunk 0 in registers
+                // staging box: FOLD alternates two (the store of chunk i-1 may still be reading)
+                const uint32_t box = FOLD ? stg + (uint32_t)((nbox++ & 1) * kPairEpiBytes) : stg;
+                if (issuer) {
+                    if constexpr (FOLD) bulk_wait_read1();
+                    else bulk_wait_read0();   // the previous chunk's store has read the box
+                }
                 epi_bar();
                 if (inbox) {
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4)
                         asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(
-                                         stg + (uint32_t)srow * 128 + (uint32_t)((j4 ^ (srow & 7)) << 4)),
+                                         box + (uint32_t)srow * 128 + (uint32_t)((j4 ^ (srow & 7)) << 4)),
                                      "f"(v[4 * j4]), "f"(v[4 * j4 + 1]), "f"(v[4 * j4 + 2]), "f"(v[4 * j4 + 3])
                                      : "memory");
                 }
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 epi_bar();
+                if (RESB && c0 == 0 && q == 0 && lane == 0) PAIR_TRACE(0, t);   // chunk 0 staged
                 if (issuer) {
-                    if (spl >= 0) tma_reduce_add_4d(map_y, stg, kc, ox0, oy0, img0);
-                    else tma_store_4d(map_y, stg, kc, ox0, oy0, img0);
+                    if (spl >= 0) tma_reduce_add_4d(map_y, box, kc, ox0, oy0, img0);
+                    else tma_store_4d(map_y, box, kc, ox0, oy0, img0);
                     bulk_commit();
                 }
             }
@@ -1082,8 +1174,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const uint32_t tconv_leader = mapa_shared(smem_u32(tconv), 0);
         const uint32_t lane_base = tmem + ((uint32_t)(q * 32) << 16) + A_COL0 + (uint32_t)(16 * h);
         const float sc = pow2f(f16_row_exp(__int_as_float(f16c_scale_max)));
-        const int a_rows = P.bx * P.by * P.imgs;      // rows the TMA boxes fill (no halo)
+        const int a_rows = P.bx * P.by * P.imgs;      // rows the TMA boxes fill (no halo; gather: real rows)
         const int fp_rows = PP.fp_bytes / 128;        // footprint rows (halo)
+        // gather halo: this row's footprint pixel for tap (0, 0)
+        int g_base = 0;
+        if (HALO && PP.gather) {
+            const int per_img = P.bx * P.by;
+            const int im = m / per_img, pix = m - im * per_img;
+            const int py = pix / P.bx, px = pix - py * P.bx;
+            g_base = (im * PP.fh + py * P.stride) * PP.fw + px * P.stride;
+        }
         float amax = 0.f;                             // max |x| over the real (loaded) rows
         int s = 0, ta = 0, it = 0, sa = 0;
         uint32_t ph = 0, pht = 0, pha = 0;
@@ -1105,10 +1205,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     // B of this tap landed (the MMA issuer learns it through tconv)
                     if constexpr (!RESB) mbar_wait(full + s, ph);
                     const int r = FOLD ? tap : tap / P.ks, sx = FOLD ? 0 : tap - r * P.ks;
-                    const int fr = m + r * PP.fpr + sx;
+                    const int fr = PP.gather ? g_base + r * PP.fw + sx : m + r * PP.fpr + sx;
                     row = fa + (h ? (uint32_t)PP.a_slot : 0u) + (uint32_t)fr * 128;
                     sw = fr & 7;
-                    real = fr < fp_rows;
+                    real = PP.gather ? m < a_rows : fr < fp_rows;
                 } else {   // ARING: the A slot (the filter planes are the MMA issuer's to wait for)
                     mbar_wait(afull + sa, pha);
                     row = smem_u32(aring + sa * ASLOT) + (h ? (uint32_t)A_BYTES : 0u) + (uint32_t)m * 128;

@@ -43,10 +43,11 @@ def main():
     torch.cuda.synchronize()
     C.conv_igemm(x, w, padding=1, stride=spec.stride, tile=tile, precision=args.prec)
     torch.cuda.synchronize()
-    buf = (ctypes.c_ulonglong * (18 * 1024))()
+    buf = (ctypes.c_ulonglong * (24 * 1024))()
     lib = N.lib()
     assert lib.convio_dev_trace(buf) == 0, "not a CONVIO_TRACE build"
-    tr = np.frombuffer(buf, dtype=np.uint64).reshape(18, 1024).astype(np.int64)
+    tr = np.frombuffer(buf, dtype=np.uint64).reshape(24, 1024).astype(np.int64)
+    fine = tr[18:24]
     st, en = tr[16], tr[17]
     ok = (st > 0) & (en > 0)
     if ok.any():
@@ -56,13 +57,13 @@ def main():
               f"start spread {(st[ok].max() - t0g) / 1e3:.1f} us; CTAs {int(ok.sum())}")
     peer = tr[8:16]
     tr = tr[0:8]
-    nz = [int((tr[r] > 0).sum()) for r in range(7)]
+    nz = [int((tr[r] > 0).sum()) for r in range(8)]
     print("stamps per row:", nz, "info:", C.query(tuple(x.shape), tuple(w.shape), spec.stride, 1, "HWC",
                                                    tile, f"igemm_{args.prec}")["reason"])
     t0 = min(tr[r][tr[r] > 0].min() for r in range(7) if nz[r])
     P, C1, C2, M3, M4, E5, E6, M7 = (tr[r] - t0 for r in range(8))
     pP, pC1, pC2 = (peer[r] - t0 for r in range(3))   # the peer CTA (clock64 of another SM: offset unknown)
-    k = min(nz[0], nz[3], nz[4])
+    k = min(nz[0] or nz[3], nz[3], nz[4])   # (resident-filter tiles stamp no producer k-blocks)
     k1 = min(k, nz[1], nz[2]) if nz[1] else 0
 
     def med(a):
@@ -77,6 +78,14 @@ def main():
     ns = next((i for i in range(1, k) if P[i] > M4[0]), None)
     print(f"ring: producer stalls (P[i] after M4[i-NS]) from k-block {ns}")
     ne = min(nz[5], nz[6])
+    if ne and (fine[0] > 0).sum():
+        f18, f19, f20 = (fine[i][:ne] - t0 for i in range(3))
+        print(f"epilogue fine: tfull -> origin {med(f18 - E5[:ne]):.0f}, -> TMEM loads waited {med(f19 - f18):.0f}, "
+              f"-> fold adds {med(f20 - f19):.0f}, -> unscaled {med(M7[:ne] - f20):.0f}")
+    if ne and nz[7]:
+        print(f"epilogue: tfull -> chunk 0 in registers med {med(M7[:ne] - E5[:ne]):.0f}, "
+              f"-> staged (resident-filter builds) med {med(P[:ne] - E5[:ne]) if not nz[0] or nz[0] == ne else float('nan'):.0f}, "
+              f"-> accumulator released med {med(E6[:ne] - E5[:ne]):.0f}")
     if ne:
         print(f"epilogue: drain (E6-E5) med {med(E6[:ne] - E5[:ne]):.0f} cyc, items {ne}, "
               f"item period med {med(np.diff(E5[:ne])):.0f}")

@@ -100,9 +100,12 @@ __global__ void __cluster_dims__(2, 1, 1) k_cont(long long *cycles, int iters, c
             }
             if (BG & 4) {   // epilogue-like TMEM reads: 32 columns per warp per round
                 float v[32];
+                const long long t0 = clock64();
                 tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + 384, v);
+                const long long t1 = clock64();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) acc += v[j];
+                if (warp == 4 && lane == 0 && rank == 0) { cycles[1] += t1 - t0; cycles[2] += 1; }
             }
             if (BG & 2) {   // 8 x LDS.128 per thread per round
 #pragma unroll
@@ -136,9 +139,13 @@ static void run(long long *dcyc, int ctas = 2) {
     long long cyc = 0;
     static uint8_t *g = nullptr;
     if (!g) cudaMalloc(&g, 64 << 20);
+    cudaMemset(dcyc, 0, 24);
     k_cont<NN, TS, BG, NC><<<ctas, 384, smem>>>(dcyc, ctas > 2 ? 65536 : 2048, g);
     cudaError_t e = cudaDeviceSynchronize();
-    cudaMemcpy(&cyc, dcyc, 8, cudaMemcpyDeviceToHost);
+    long long all[3] = {0, 0, 0};
+    cudaMemcpy(all, dcyc, 24, cudaMemcpyDeviceToHost);
+    cyc = all[0];
+    if (all[2]) printf("   tcgen05.ld x32 + wait under MMA load: %lld cycles avg over %lld\n", all[1] / all[2], all[2]);
     static const char *bg[] = {"idle", "tcgen05.st", "LDS.128", "tcgen05.st + LDS.128", "tcgen05.ld", "", "", "",
                                "bulk copy", "", "", "", "tcgen05.ld + bulk", "", "", "all"};
     printf("%d commits/k-block %3d CTAs: pair M256 N%3d f16 3-product %s, 8 background warps: %-20s %lld cycles per MMA %s\n", NC, ctas, NN,
@@ -148,7 +155,9 @@ static void run(long long *dcyc, int ctas = 2) {
 int main() {
     setvbuf(stdout, nullptr, _IONBF, 0);
     long long *dcyc;
-    cudaMalloc(&dcyc, 8);
+    cudaMalloc(&dcyc, 24);
+    run<256, false, 4>(dcyc); run<128, true, 4>(dcyc); run<256, false, 4>(dcyc, 148);
+    return 0;
     run<128, true, 0, 3>(dcyc); run<128, true, 0, 4>(dcyc); run<128, true, 0, 5>(dcyc);
     run<128, false, 0, 3>(dcyc); run<128, false, 0, 4>(dcyc); run<128, false, 0, 5>(dcyc);
     run<256, false, 0, 3>(dcyc);
