@@ -429,6 +429,54 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
     return finish_pair_grid(pl);
 }
 
+// Gather halo (3xF16C, tile threads (1, 1, 8)): exact x * y pixel blocks of
+// imgs = 128 / (x * y) stacked images (x | Q, y | P: no wrap-around columns, no ragged
+// edges); the [imgs][fh][fw] input footprint (fw = (x - 1) * stride + S) is staged once
+// per channel block and the converters gather each tap's rows from it into TMEM.
+static int plan_igemm_gather(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
+                             size_t rlen, int kind, int p, int q) {
+    if (kind != KIND_3XF16C)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "gathered-footprint tiles (n_zt = 8) take 3xF16");
+    if (q % t->x || p % t->y || d->k % t->z)
+        return pfail(reason, rlen, schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x,
+                     t->y, t->z, q, p, d->k);
+    const int px = t->x * t->y;
+    if (px > 128) return pfail(reason, rlen, CONVIO_EINFEASIBLE, "x*y=%d pixels exceed the M=128 MMA tile", px);
+    const int imgs = std::max(1, std::min(128 / px, d->n));
+    const int fw = (t->x - 1) * d->stride + d->s, fh = (t->y - 1) * d->stride + d->r;
+    if (fw > 256 || fh > 256 || imgs > 256)
+        return pfail(reason, rlen, CONVIO_EINFEASIBLE, "footprint box dims > 256");
+    const int cb = kblock_channels(kind);
+    IgemmParams &P = pl->P;
+    memset(&P, 0, sizeof(P));
+    pl->halo = true;
+    pl->gather = true;
+    pl->tsa = true;
+    pl->fw = fw;
+    pl->fh = fh;
+    pl->fpr = fw;
+    const int fp_rows = fw * fh * imgs;
+    pl->fp_bytes = fp_rows * 128;
+    pl->a_slot = (fp_rows * 128 + 1023) & ~1023;
+    pl->na = 2;
+    {
+        const size_t budget = 227 * 1024 - 1024 - 1024 - pair_epi_bytes(false) - pair_epi_const_bytes(d->k);
+        const size_t stage = (size_t)(t->z / 2) * 128 * 2;
+        if (3 * (size_t)pl->a_slot * 2 + 3 * stage <= budget) pl->na = 3;
+    }
+    P.k = d->k;
+    int rc = plan_ring(pl, t->z, kind, t->s_b, true, reason, rlen);
+    if (rc) return rc;
+    P.n = d->n; P.c = d->c; P.h = d->h; P.w = d->w; P.k = d->k; P.p = p; P.q = q;
+    P.pad = d->pad; P.stride = d->stride; P.ks = d->r;
+    P.bx = t->x; P.by = t->y; P.imgs = imgs;
+    P.tiles_x = q / t->x; P.tiles_y = p / t->y; P.img_groups = (d->n + imgs - 1) / imgs;
+    P.cblocks = d->c / cb; P.kblocks = d->r * d->s * P.cblocks;
+    pl->groups = 1;
+    pl->blocks_per_group = P.tiles_x * P.tiles_y * P.img_groups;
+    return finish_pair_grid(pl);
+}
+
 static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan *pl, char *reason,
                       size_t rlen, int kind) {
     auto fail = [&](int code, const char *fmt, ...) {
@@ -455,6 +503,7 @@ static int plan_igemm(const convio_conv_desc *d, const convio_tile *t, IgemmPlan
         return fail(CONVIO_EINFEASIBLE, "C=%d is not a multiple of %d (one 128-B K block)", d->c, cb);
     if (t->x < 1 || t->y < 1 || t->z < 1 || t->s_b < 1)
         return fail(CONVIO_EINFEASIBLE, "tile fields must be >= 1");
+    if (t->n_xt == 1 && t->n_yt == 1 && t->n_zt == 8) return plan_igemm_gather(d, t, pl, reason, rlen, kind, p, q);
     if (t->n_xt == 2) return plan_igemm_halo(d, t, pl, reason, rlen, kind, p, q);
     if (q % t->x || p % t->y || d->k % t->z)
         return fail(schedule_error(), "tile %dx%dx%d does not divide output %dx%dx%d", t->x, t->y,
@@ -567,12 +616,16 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     // stride: box spans stride*(pixels) input positions, traversal stride picks every stride-th
     cuuint32_t xb[4] = {cb, (cuuint32_t)(P.bx * P.stride), (cuuint32_t)(P.by * P.stride),
                         (cuuint32_t)P.imgs};
-    if (pl.halo) {   // the block's whole input footprint: y + R - 1 rows of fpr pixels
+    if (pl.gather) {   // [imgs][fh][fw] pixels, every one (no traversal stride)
+        xb[1] = (cuuint32_t)pl.fw;
+        xb[2] = (cuuint32_t)pl.fh;
+        xb[3] = (cuuint32_t)P.imgs;
+    } else if (pl.halo) {   // the block's whole input footprint: y + R - 1 rows of fpr pixels
         xb[1] = (cuuint32_t)pl.fpr;
         xb[2] = (cuuint32_t)(P.by + P.ks - 1);
         xb[3] = 1;
     }
-    cuuint32_t xes[4] = {1, (cuuint32_t)P.stride, (cuuint32_t)P.stride, 1};
+    cuuint32_t xes[4] = {1, (cuuint32_t)(pl.gather ? 1 : P.stride), (cuuint32_t)(pl.gather ? 1 : P.stride), 1};
     cuuint32_t es[4] = {1, 1, 1, 1};
     const int taps = P.batched ? P.n : P.ks * P.ks;
     cuuint64_t wd[3] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps * wplanes};
@@ -631,6 +684,9 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         PP.a_slot = pl.a_slot;
         PP.na = pl.na;
         PP.scale_state = pl.scale_state;
+        PP.gather = pl.gather ? 1 : 0;
+        PP.fw = pl.fw;
+        PP.fh = pl.fh;
         PP.fallback = 0;
         PP.spec_ctas = 0;
         PP.trace = nullptr;
@@ -647,7 +703,8 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
             CONVIO_CUDA_TRY(launch_pdl(pl.pfn, pl.grid, dim3(pl.threads), pl.smem, stream, PP, tx, tw, ty));
         note_launch();
         CONVIO_CUDA_TRY(cudaGetLastError());
-        if (pl.kind == KIND_3XF16C) {
+        static const bool skip_check = getenv("CONVIO_DEV_SKIP_CHECK") != nullptr;   // dev: timing A/B only
+        if (pl.kind == KIND_3XF16C && !skip_check) {
             // the checking launch: exits at once when the speculative scale held, else redoes
             // the whole conv with the exact scale (whole tiles, plain stores over the output)
             PairParams PF = PP;
@@ -719,7 +776,7 @@ int igemm_query(const convio_conv_desc *d, const convio_tile *t, convio_launch_i
     out->workspace_bytes = igemm_workspace_bytes(d, kind);
     out->grid_z = pl.grid.z;
     snprintf(out->reason, sizeof(out->reason), "tcgen05 %s%s: M=%d (%d px x %d img per CTA), N=%d, %d stages%s",
-             kind_name(kind), pl.fold ? (pl.tsa ? (pl.resb_slots ? " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA, resident filter)" : " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA)") : " CTA pair (persistent, halo footprint, 3 taps per MMA)") : pl.halo ? (pl.tsa ? " CTA pair (persistent, halo footprint shifted into TMEM)" : " CTA pair (persistent, halo-staged footprint)") : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
+             kind_name(kind), pl.fold ? (pl.tsa ? (pl.resb_slots ? " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA, resident filter)" : " CTA pair (persistent, halo footprint shifted into TMEM, 3 taps per MMA)") : " CTA pair (persistent, halo footprint, 3 taps per MMA)") : pl.gather ? " CTA pair (persistent, footprint gathered into TMEM)" : pl.halo ? (pl.tsa ? " CTA pair (persistent, halo footprint shifted into TMEM)" : " CTA pair (persistent, halo-staged footprint)") : (pl.tsa ? " CTA pair (persistent, A in TMEM)" : (pl.pair ? " CTA pair (persistent)" : "")), pl.pair ? 256 : 128,
              pl.P.bx * pl.P.by, pl.P.imgs, pl.bn, pl.P.stages,
              pl.P.splits > 1 ? ", split-K" : "");
     return CONVIO_OK;

@@ -732,7 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         // the block's input footprint for channel block cb, once
                         if (ita >= NA) mbar_wait(aempty + sa, pha ^ 1);
                         uint8_t *fa = aring + sa * ASLOT;
-                        const int xc = ox0 - P.pad, yc = oy0 - P.pad;
+                        const int xc = ox0 * P.stride - P.pad, yc = oy0 * P.stride - P.pad;
                         if constexpr (F16C) {   // channels 0..31 -> hi slot, 32..63 -> lo slot
                             mbar_arrive_expect_tx(afull + sa, 2u * (uint32_t)PP.fp_bytes);
                             tma_load_4d(fa, map_x, cb * CB, xc, yc, img0, afull + sa);

@@ -420,6 +420,8 @@ struct IgemmPlan {
     PairFn pfn = nullptr;
     int groups = 1, blocks_per_group = 0;
     int fpr = 0, fp_bytes = 0, a_slot = 0, na = 0;
+    bool gather = false;     // halo TSA with exact x * y * imgs blocks (converters gather taps)
+    int fw = 0, fh = 0;      // gather: footprint width / height per image
     dim3 grid;
     size_t smem = 0;
     int regs = 0;

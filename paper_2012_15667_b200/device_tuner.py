@@ -276,7 +276,13 @@ def tcgen05_io_words(shape: ConvShape, tile: TileConfig) -> float:
     rows, shared by the two CTAs of a pair), then the outputs once."""
     n, q, p, c, k = shape.n, shape.w_out, shape.h_out, shape.c_in, shape.c_out
     rs = shape.w_ker * shape.h_ker
-    if tile.n_xt == 2:   # halo: footprint rows (y + R - 1) * fpr, x valid columns per row
+    if tile.n_zt == 8:   # gather: [imgs][fh][fw] footprint per exact block
+        imgs = max(1, min(128 // (tile.x * tile.y), n))
+        fw = (tile.x - 1) * shape.stride + shape.w_ker
+        fh = (tile.y - 1) * shape.stride + shape.h_ker
+        rows_valid = tile.x * tile.y * imgs
+        a = fw * fh * imgs * c
+    elif tile.n_xt == 2:   # halo: footprint rows (y + R - 1) * fpr, x valid columns per row
         fpr = tile.x + shape.w_ker - 1
         rows_valid = tile.x * tile.y
         a = (tile.y + shape.h_ker - 1) * fpr * c
@@ -307,7 +313,8 @@ def tcgen05_space(shape: ConvShape, hw: HwModel, engine: str,
     (1,1,2) CTA pair, (1,1,4) pair with the split A operand in TMEM, (2,1,2)
     halo-staged footprint (stride 1; ``(x + S - 1) * y = 128``, x not
     necessarily dividing Q), (2,1,4) (3xF16) the halo footprint with the
-    converters shifting each tap's rows into TMEM; Winograd engines: x = y = e, z over the GEMM's N
+    converters shifting each tap's rows into TMEM, (1,1,8) (3xF16) exact blocks
+    whose [imgs][fh][fw] footprint the converters gather tap by tap into TMEM; Winograd engines: x = y = e, z over the GEMM's N
     tiles, n_zt in {1, 2, 4}.  ``unconstrained_size`` counts the raw product of
     the axes; ``check_legal`` keeps only members with a device projection.
     ``prune`` (implicit GEMM): the I/O-model cut -- members whose modelled SM <-> L2
@@ -334,6 +341,14 @@ def tcgen05_space(shape: ConvShape, hw: HwModel, engine: str,
                             if t[2] >= 2 and sb != 32768:   # persistent pair: the whole smem is the ring
                                 continue
                             members.append(TileConfig(bx, by, z, sb, *t, layout="HWC"))
+        if prec == "3xf16":   # (1,1,8): exact blocks, footprint gathered into TMEM
+            for bx in range(1, q + 1):
+                for by in range(1, p + 1):
+                    for z in zs:
+                        raw += 1
+                        if q % bx or p % by or not _block_ok(bx, by, shape.n) or bx * by > 64:
+                            continue
+                        members.append(TileConfig(bx, by, z, 32768, 1, 1, 8, layout="HWC"))
         if shape.stride == 1:
             for fpr in (8, 16, 32, 64, 128):
                 x_, y_ = fpr - shape.w_ker + 1, 128 // fpr

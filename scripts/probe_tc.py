@@ -176,8 +176,10 @@ def main():
             torch.cuda.synchronize()
             print("ran", args.one, spec.name)
             continue
+        saved, TILE_OVERRIDE = TILE_OVERRIDE, None   # the reference keeps its own tile
         ref = build(spec, "igemm_3xtf32:128:1" if spec.k % 128 == 0 else "igemm_3xtf32:64:1",
                     args.n, x, w, wcache)().clone()
+        TILE_OVERRIDE = saved
         flops = spec.flops(args.n)
         for kind in args.kinds.split(","):
             try:

@@ -57,6 +57,11 @@ CASES = [
     (2, 128, 14, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 4, layout="HWC"), "halo tsa z=64"),
     (2, 64, 56, 64, 1, TileConfig(14, 8, 64, 32768, 2, 1, 4, layout="HWC"), "fold tsa resident filter"),
     (3, 128, 28, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 4, layout="HWC"), "fold tsa 30x4 2 channel blocks"),
+    # (1, 1, 8): exact x * y * imgs blocks, the footprint gathered into TMEM tap by tap
+    (10, 128, 28, 128, 1, TileConfig(4, 4, 128, 32768, 1, 1, 8, layout="HWC"), "gather 4x4 x 8 img, ragged image group"),
+    (2, 64, 56, 128, 1, TileConfig(8, 8, 128, 32768, 1, 1, 8, layout="HWC"), "gather 8x8 x 2 img"),
+    (4, 256, 14, 256, 1, TileConfig(2, 2, 256, 32768, 1, 1, 8, layout="HWC"), "gather 2x2 x 32 img z=256"),
+    (4, 64, 28, 128, 2, TileConfig(2, 2, 128, 32768, 1, 1, 8, layout="HWC"), "gather stride 2"),
 ]
 
 
@@ -75,6 +80,8 @@ def test_igemm_3xf16_matches_oracle(case):
         assert "A in TMEM" in info["reason"], info
     if "halo tsa" in what or "fold tsa" in what:
         assert "shifted into TMEM" in info["reason"], info
+    if what.startswith("gather"):
+        assert "gathered into TMEM" in info["reason"], info
     if "resident" in what:
         assert "resident filter" in info["reason"], info
     y = C.conv_igemm(_hwc(x), torch.from_numpy(wt).cuda(), padding=1, stride=stride, tile=tile,
