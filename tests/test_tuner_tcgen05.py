@@ -38,7 +38,7 @@ def test_domain_contains_plans_and_pruning_keeps_them(args, committed):
     assert committed in full and committed in pruned
     assert pruned.size <= full.size < full.unconstrained_size
     assert set(pruned.members) <= set(full.members)
-    assert all(m.layout == "HWC" and m.n_zt in (2, 4) for m in full.members)   # 3xF16: pair tiles
+    assert all(m.layout == "HWC" and m.n_zt in (2, 4, 8) for m in full.members)   # 3xF16: pair tiles
     # members stay in the reference's sorted order (autotune.py:154-155)
     keys = [(m.s_b, m.x, m.y, m.z, m.n_xt, m.n_yt, m.n_zt) for m in full.members]
     assert keys == sorted(keys)
