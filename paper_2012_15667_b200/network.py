@@ -13,8 +13,9 @@ and the features can be returned NCHW (``convio_nhwc_to_nchw``).
 
 Filter preparation (repacking / Winograd transforms / fp16 splits) happens once
 in :meth:`Vgg16Features.prepare`, as a deployed network would cache it; a
-forward is then ``1 + 13 + 5`` kernel launches (+ the 3xF16 layers' |x| max
-pass), capturable as one CUDA graph.
+forward is then ``1 + 13 + 5`` kernel launches (+ the 3xF16 layers' checking
+launches, which exit at once when the speculated activation scale held),
+capturable as one CUDA graph.
 """
 
 from __future__ import annotations
