@@ -21,9 +21,12 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_bench_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-variants --no-cudnn --no-network > gpurun_out/${R}_bench_ncu.log 2>&1
 python scripts/ncu_summary.py launches gpurun_out/${R}_bench_launches.csv --out gpurun_out/${R}_bench_launches.json > /dev/null
-# full captures of the tuned plan of each ResNet-50 layer family (run_layer.py = the bench plan)
-for L in res2_3x3 res3_3x3_s2 res3_3x3 res4_3x3 res5_3x3; do
-  timeout 400 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair|winograd|igemm" -s 1 -c 3 \
+# full captures of the tuned plan of each ResNet-50 layer family (run_layer.py = the bench plan),
+# one kernel each (the reports must fit gpurun's 64 MiB return), summarised to JSON
+for L in res2_3x3 res3_3x3_s2 res3_3x3 res4_3x3; do
+  timeout 400 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair" -s 2 -c 1 \
     -o gpurun_out/${R}_ncu_$L -f python scripts/run_layer.py --workload resnet50 --layer $L --reps 3 > /dev/null 2>&1
 done
+python scripts/ncu_summary.py rep gpurun_out/${R}_ncu_*.ncu-rep --out gpurun_out/${R}_ncu_kernels.json > /dev/null 2>&1
+rm -rf gpurun_out/traffic_$R/*.csv
 ls -la gpurun_out/${R}_*
