@@ -592,7 +592,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, shard_range, tuned_table,
+        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, prepare_layers, shard_range,
+        tuned_table,
         gather_outputs, CUDA_CORE_ALGORITHMS)
     from paper_2012_15667_b200.device import winograd_gemm_flops
 
@@ -659,10 +660,9 @@ def main() -> None:
 
         def step(self, events=None, st=None):
             st = st or stream
-            launches = 0
+            # the step's filter prep (all 3xF16 splits in one launch), then the convs
+            launches = prepare_layers(self.layers, dev, st)
             for i, layer in enumerate(self.layers):
-                layer.prepare(dev, st)
-                launches += 1
                 if events is not None:
                     events[i][0].record(st)
                 layer.run(self.xs[i], out=self.ys[i], stream=st)

@@ -209,6 +209,11 @@ int convio_conv_igemm(const convio_conv_desc *desc, const convio_tile *tile, int
  * the same schedule (dataflow.py:219-250). */
 int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w, void *w_packed,
                                    void *stream);
+/* The same for `count` <= 32 filters in ONE launch (a step's filter prep: the
+ * per-filter launches each occupied only K blocks of the GPU).  Arrays of
+ * descriptors, KCRS filters and 256-byte aligned outputs; same layout per job. */
+int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_desc *descs, const float *const *w,
+                                            void *const *w_packed, void *stream);
 int64_t convio_pack_filter_igemm_f16x3_bytes(const convio_conv_desc *desc);
 
 /* KCRS fp32 -> [R*S][K][C] bf16 (round to nearest even). */

@@ -150,6 +150,63 @@ __global__ void __launch_bounds__(256) pack_filter_f16x3_kernel(const float *__r
     }
 }
 
+// Batched form: every filter of a step in one launch (block b -> job, output channel
+// through the kcum prefix sums): the per-layer launches each filled only K blocks
+constexpr int kPackJobs = 32;
+struct PackJob {
+    const float *w;
+    __half *wq;
+    int *col_exp;
+    int k, c, rs;
+};
+struct PackBatch {
+    int n;
+    int kcum[kPackJobs + 1];
+    PackJob job[kPackJobs];
+};
+__global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const __grid_constant__ PackBatch B) {
+    pdl_wait();
+    __shared__ float red[8];
+    const int total = B.kcum[B.n];
+    for (int g = blockIdx.x; g < total; g += gridDim.x) {
+        int j = 0;
+        while (B.kcum[j + 1] <= g) ++j;
+        const PackJob &J = B.job[j];
+        const int kk = g - B.kcum[j], c = J.c, rs = J.rs, k = J.k;
+        const int crs = c * rs;
+        const int64_t plane = (int64_t)rs * k * c;
+        const float *wr = J.w + (int64_t)kk * crs;
+        float mx = 0.0f;
+        for (int i = threadIdx.x; i < crs; i += blockDim.x) mx = fmaxf(mx, fabsf(wr[i]));
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+        __syncthreads();
+        mx = red[0];
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
+        const int e = f16_row_exp(mx);
+        const float sc = pow2f(e);
+        const int pairs = (c + 1) / 2;
+        for (int t = threadIdx.x; t < rs * pairs; t += blockDim.x) {
+            const int tap = t / pairs, cc = 2 * (t - tap * pairs);
+            __half *hrow = J.wq + ((int64_t)tap * k + kk) * c;
+            const float v0 = wr[cc * rs + tap] * sc;
+            const float v1 = cc + 1 < c ? wr[(cc + 1) * rs + tap] * sc : 0.0f;
+            const __half2 hi = __floats2half2_rn(v0, v1);
+            const float2 hf = __half22float2(hi);
+            const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
+            if (cc + 1 < c) {
+                *reinterpret_cast<__half2 *>(hrow + cc) = hi;
+                *reinterpret_cast<__half2 *>(hrow + plane + cc) = lo;
+            } else {
+                hrow[cc] = __low2half(hi);
+                hrow[plane + cc] = __low2half(lo);
+            }
+        }
+        if (threadIdx.x == 0) J.col_exp[kk] = e;
+        __syncthreads();
+    }
+}
+
 // 3xF16C activation scale: per-block max |x| (float bits) into partials[blockIdx.x];
 // the GEMM reduces the nred partials into one exponent (f16c_act_exp).
 // The grid walks x from its END to its start, so the most recently read ~L2-size
@@ -861,6 +918,39 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
         return CONVIO_EINVAL;
     }
     return launch_pack_filter_f16x3(desc, w, w_packed, (cudaStream_t)stream);
+}
+
+int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_desc *descs, const float *const *w,
+                                            void *const *w_packed, void *stream) {
+    clear_error();
+    if (count < 0 || count > kPackJobs || (count && (!descs || !w || !w_packed))) {
+        set_error("count must be in [0, %d] with non-null arrays", kPackJobs);
+        return CONVIO_EINVAL;
+    }
+    if (!count) return CONVIO_OK;
+    PackBatch B;
+    memset(&B, 0, sizeof(B));
+    B.n = count;
+    for (int i = 0; i < count; ++i) {
+        const convio_conv_desc *d = descs + i;
+        if (!w[i] || !w_packed[i] || (reinterpret_cast<uintptr_t>(w_packed[i]) & 255) || d->k < 1 || d->c < 1 ||
+            d->r < 1 || d->s < 1) {
+            set_error("job %d: null / unaligned buffer or empty filter", i);
+            return CONVIO_EINVAL;
+        }
+        B.job[i].w = w[i];
+        B.job[i].wq = (__half *)w_packed[i];
+        B.job[i].col_exp = (int *)((uint8_t *)w_packed[i] + align256((size_t)4 * d->k * d->c * d->r * d->s));
+        B.job[i].k = d->k;
+        B.job[i].c = d->c;
+        B.job[i].rs = d->r * d->s;
+        B.kcum[i + 1] = B.kcum[i] + d->k;
+    }
+    const int blocks = std::max(1, std::min(B.kcum[count], 148 * 8));
+    CONVIO_CUDA_TRY(launch_pdl(pack_filters_f16x3_batched_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, B));
+    note_launch();
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
 }
 
 #ifdef CONVIO_TRACE

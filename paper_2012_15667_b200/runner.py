@@ -159,6 +159,31 @@ def _f16x3_filter_bytes(s: "LayerSpec") -> int:
     return int(N.lib().convio_pack_filter_igemm_f16x3_bytes(ctypes.byref(desc)))
 
 
+def prepare_layers(layers, device, stream=None) -> int:
+    """Filter prep of a whole step: the 3xF16 implicit-GEMM layers' fp16 splits in ONE
+    launch (``convio_pack_filters_igemm_f16x3_batched``), every other layer its own
+    prep.  Returns the number of launches."""
+    import ctypes
+    from . import _native as N
+    f16 = [l for l in layers if l.algorithm == "igemm_3xf16"]
+    launches = 0
+    for i in range(0, len(f16), 32):
+        chunk = f16[i:i + 32]
+        jobs = [l._f16x3_pack_job(device) for l in chunk]
+        descs = (N.ConvDesc * len(jobs))(*[j[0] for j in jobs])
+        ws = (ctypes.c_void_p * len(jobs))(*[j[1].data_ptr() for j in jobs])
+        outs = (ctypes.c_void_p * len(jobs))(*[j[2].data_ptr() for j in jobs])
+        N.check(N.lib().convio_pack_filters_igemm_f16x3_batched(len(jobs), descs, ws, outs,
+                                                                 C._stream_ptr(stream)),
+                "pack_filters_igemm_f16x3_batched")
+        launches += 1
+    for l in layers:
+        if l.algorithm != "igemm_3xf16":
+            l.prepare(device, stream)
+            launches += 1
+    return launches
+
+
 class ConvLayer:
     """One conv layer: filters on the device plus its tuned plan."""
 
@@ -238,6 +263,15 @@ class ConvLayer:
             rc = N.lib().convio_pack_filter_direct(ctypes.byref(desc), C._ptr(w),
                                                    C._ptr(self._ws), sp)
         N.check(rc, "filter prep")
+
+    def _f16x3_pack_job(self, device):
+        """(descriptor, filter, packed buffer) of this layer's 3xF16 filter prep."""
+        from . import _native as N
+        s = self.spec
+        if self._ws is None or self._ws.device != torch.device(device) or self._ws.dtype != torch.float32:
+            self._ws = torch.empty(self.filter_elems(), device=device, dtype=torch.float32)
+        desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 2)
+        return desc, self.weight, self._ws
 
     def run(self, x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """The conv kernel alone, on the prepared filter."""

@@ -155,3 +155,35 @@ def test_igemm_3xf16_speculative_scale(tile):
         state = ws[:8].view(torch.int32).cpu().numpy()
         assert state[0] == np.float32(np.abs(xs).max()).view(np.int32), (scale, state)
         assert state[1] == state[0] ^ 0x5CA1AB1E
+
+
+def test_batched_filter_packing_matches_per_filter_packing():
+    """convio_pack_filters_igemm_f16x3_batched (a step's 3xF16 filter prep in one launch)
+    writes exactly what the per-filter packing writes, and the runner uses it."""
+    from paper_2012_15667_b200 import runner as R
+    g = torch.Generator(device="cuda").manual_seed(5)
+    shapes = [(64, 64, 3), (128, 64, 3), (256, 128, 3), (512, 256, 1), (64, 128, 3)]
+    ws = [torch.rand((k, c, r, r), device="cuda", generator=g) - 0.5 for k, c, r in shapes]
+    singles = [C.pack_filter_igemm_f16x3(w) for w in ws]
+    import ctypes
+    from paper_2012_15667_b200 import _native as N
+    outs = [torch.empty_like(s) for s in singles]
+    descs = (N.ConvDesc * len(ws))(*[N.make_desc(1, w.shape[1], 8, 8, w.shape[0], w.shape[2], w.shape[3], 1, 0, 2)
+                                     for w in ws])
+    rc = N.lib().convio_pack_filters_igemm_f16x3_batched(
+        len(ws), descs, (ctypes.c_void_p * len(ws))(*[w.data_ptr() for w in ws]),
+        (ctypes.c_void_p * len(ws))(*[o.data_ptr() for o in outs]), None)
+    assert rc == 0, N.last_error()
+    torch.cuda.synchronize()
+    for s1, o in zip(singles, outs):
+        assert torch.equal(s1, o)
+    # the runner's step prep: 3xF16 layers batched, the others one by one
+    specs = [s for s in R.WORKLOADS["resnet50"]][:4]
+    layers = [R.ConvLayer(s, R.make_weights(s, torch.device("cuda"), i),
+                          {"algorithm": "igemm_3xf16", "tile": TileConfig(2, 2, s.k if s.k <= 256 else 256, 32768,
+                                                                          1, 1, 2, layout="HWC"), "e": None})
+              for i, s in enumerate(specs)]
+    assert R.prepare_layers(layers, torch.device("cuda")) == 1
+    for l in layers:
+        ref = C.pack_filter_igemm_f16x3(l.weight)
+        assert torch.equal(l._ws.view(torch.uint8)[:ref.numel()], ref)
