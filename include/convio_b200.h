@@ -212,6 +212,12 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
 /* The same for `count` <= 32 filters in ONE launch (a step's filter prep: the
  * per-filter launches each occupied only K blocks of the GPU).  Arrays of
  * descriptors, KCRS filters and 256-byte aligned outputs; same layout per job. */
+/* The tensor-core Winograd filter transform (convio_winograd_filter_transform_tc) of
+ * `count` <= 32 filters of one e and one precision in one launch (two for 3xF16:
+ * the transform, then the fp16 split); fp32-U precisions (TF32, 3xTF32, 3xF16). */
+int convio_winograd_filter_transform_tc_batched(int32_t count, const convio_conv_desc *descs, int32_t e,
+                                                int32_t precision, const float *const *w, void *const *u,
+                                                void *stream);
 int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_desc *descs, const float *const *w,
                                             void *const *w_packed, void *stream);
 int64_t convio_pack_filter_igemm_f16x3_bytes(const convio_conv_desc *desc);

@@ -367,6 +367,71 @@ __global__ void winograd_filter_tc_kernel(const float *__restrict__ w, T *__rest
     }
 }
 
+// Batched step 2 (a step's filter prep in one launch): jobs of one e and a float U,
+// thread index over the concatenated (k, c) pairs of all jobs
+constexpr int kWinoJobs = 32;
+struct WinoFilterBatch {
+    int n;
+    int64_t cum[kWinoJobs + 1];   // pair (or, for the split, row) prefix sums
+    const float *w[kWinoJobs];
+    float *u[kWinoJobs];
+    int k[kWinoJobs], c[kWinoJobs];
+};
+template <int E>
+__global__ void winograd_filter_tc_batched_kernel(const __grid_constant__ WinoFilterBatch B) {
+    pdl_wait();
+    constexpr int M = WinoTf<E>::M;
+    for (int64_t gi = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; gi < B.cum[B.n];
+         gi += (int64_t)gridDim.x * blockDim.x) {
+        int j = 0;
+        while (B.cum[j + 1] <= gi) ++j;
+        const int64_t i = gi - B.cum[j], pairs = B.cum[j + 1] - B.cum[j];
+        const float *g = B.w[j] + i * 9;
+        float t[M][3];
+#pragma unroll
+        for (int jj = 0; jj < 3; ++jj) {
+            float col[3] = {g[jj], g[3 + jj], g[6 + jj]}, o[M];
+            WinoTf<E>::g(col, o);
+#pragma unroll
+            for (int a = 0; a < M; ++a) t[a][jj] = o[a];
+        }
+#pragma unroll
+        for (int a = 0; a < M; ++a) {
+            float o[M];
+            WinoTf<E>::g(t[a], o);
+#pragma unroll
+            for (int b = 0; b < M; ++b) B.u[j][(int64_t)(a * M + b) * pairs + i] = o[b];
+        }
+    }
+}
+// batched 3xF16 split of U (one warp per (job, xi * k) row, rows concatenated)
+__global__ void __launch_bounds__(256) winograd_u_split_f16x3_batched_kernel(const __grid_constant__ WinoFilterBatch B) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    for (int64_t gr = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; gr < B.cum[B.n];
+         gr += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        int j = 0;
+        while (B.cum[j + 1] <= gr) ++j;
+        const int64_t r = gr - B.cum[j], rows = B.cum[j + 1] - B.cum[j];
+        const int c = B.c[j];
+        const float *ur = B.u[j] + r * c;
+        __half *u16 = reinterpret_cast<__half *>(B.u[j] + rows * c);
+        int *col_exp = reinterpret_cast<int *>(B.u[j] + 2 * rows * c);
+        float mx = 0.0f;
+        for (int i = lane; i < c; i += 32) mx = fmaxf(mx, fabsf(ur[i]));
+        for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        const int e = f16_row_exp(mx);
+        const float sc = pow2f(e);
+        for (int i = lane; i < c; i += 32) {
+            __half h, l;
+            split_f16(ur[i], sc, h, l);
+            u16[r * c + i] = h;
+            u16[rows * c + r * c + i] = l;
+        }
+        if (lane == 0) col_exp[r] = e;
+    }
+}
+
 // Step 4: one thread per (tile, output channel), k fastest (coalesced M
 // loads and NHWC stores); bias + ReLU fused; ragged tiles masked.
 template <int E>
@@ -635,6 +700,55 @@ int convio_winograd_filter_transform_tc(const convio_conv_desc *desc, int32_t e,
         return CONVIO_EINVAL;
     }
     return launch_filter_tc(pl, w, u, (cudaStream_t)stream);
+}
+
+int convio_winograd_filter_transform_tc_batched(int32_t count, const convio_conv_desc *descs, int32_t e,
+                                                int32_t precision, const float *const *w, void *const *u,
+                                                void *stream) {
+    clear_error();
+    reset_launches();
+    if (count < 0 || count > kWinoJobs || (count && (!descs || !w || !u))) {
+        set_error("count must be in [0, %d] with non-null arrays", kWinoJobs);
+        return CONVIO_EINVAL;
+    }
+    if (!count) return CONVIO_OK;
+    WinoFilterBatch B, S;
+    memset(&B, 0, sizeof(B));
+    memset(&S, 0, sizeof(S));
+    B.n = S.n = count;
+    int kind = -1;
+    for (int i = 0; i < count; ++i) {
+        WinoTcPlan pl;
+        char why[160];
+        int rc = plan_wino_tc(descs + i, nullptr, e, precision, &pl, why, sizeof(why));
+        if (rc) return rc;
+        if (pl.kind == KIND_FFMA || pl.kind == KIND_BF16) {
+            set_error("batched Winograd filter transform: fp32 U only (TF32 / 3xTF32 / 3xF16)");
+            return CONVIO_EINVAL;
+        }
+        if (!w[i] || !u[i]) {
+            set_error("job %d: null filter pointer", i);
+            return CONVIO_EINVAL;
+        }
+        kind = pl.kind;
+        B.w[i] = S.w[i] = w[i];
+        B.u[i] = S.u[i] = (float *)u[i];
+        B.k[i] = S.k[i] = pl.g.k;
+        B.c[i] = S.c[i] = pl.g.c;
+        B.cum[i + 1] = B.cum[i] + (int64_t)pl.g.k * pl.g.c;
+        S.cum[i + 1] = S.cum[i] + (int64_t)pl.m * pl.m * pl.g.k;
+    }
+    const int blocks = (int)std::min<int64_t>((B.cum[count] + 255) / 256, 148 * 8);
+    if (e == 2) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_batched_kernel<2>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, B));
+    else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_batched_kernel<4>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, B));
+    note_launch();
+    if (kind == KIND_3XF16) {
+        const int sblocks = (int)std::min<int64_t>(S.cum[count] / 8 + 1, 148 * 16);
+        CONVIO_CUDA_TRY(launch_pdl(winograd_u_split_f16x3_batched_kernel, dim3(sblocks), dim3(256), 0, (cudaStream_t)stream, S));
+        note_launch();
+    }
+    CONVIO_CUDA_TRY(cudaGetLastError());
+    return CONVIO_OK;
 }
 
 int convio_winograd_bgemm(const convio_conv_desc *desc, const convio_tile *tile, int32_t e,

@@ -161,8 +161,9 @@ def _f16x3_filter_bytes(s: "LayerSpec") -> int:
 
 def prepare_layers(layers, device, stream=None) -> int:
     """Filter prep of a whole step: the 3xF16 implicit-GEMM layers' fp16 splits in ONE
-    launch (``convio_pack_filters_igemm_f16x3_batched``), every other layer its own
-    prep.  Returns the number of launches."""
+    launch (``convio_pack_filters_igemm_f16x3_batched``), the tensor-core Winograd
+    transforms one launch per (e, precision) group, every other layer its own prep.
+    Returns the number of launches."""
     import ctypes
     from . import _native as N
     f16 = [l for l in layers if l.algorithm == "igemm_3xf16"]
@@ -177,8 +178,30 @@ def prepare_layers(layers, device, stream=None) -> int:
                                                                  C._stream_ptr(stream)),
                 "pack_filters_igemm_f16x3_batched")
         launches += 1
+    # tensor-core Winograd filter transforms with an fp32 U, grouped by (e, precision)
+    groups = {}
     for l in layers:
-        if l.algorithm != "igemm_3xf16":
+        if l.algorithm.startswith("winograd_tc") and l.precision in ("tf32", "3xtf32", "3xf16"):
+            groups.setdefault((l.e, l.precision), []).append(l)
+    batched = {id(l) for g in groups.values() for l in g}
+    for (e, prec), g in groups.items():
+        for i in range(0, len(g), 32):
+            chunk = g[i:i + 32]
+            descs, ws, us = [], [], []
+            for l in chunk:
+                s = l.spec
+                if l._ws is None or l._ws.device != torch.device(device) or l._ws.dtype != torch.float32:
+                    l._ws = torch.empty(l.filter_elems(), device=device, dtype=torch.float32)
+                descs.append(N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 2))
+                ws.append(l.weight.data_ptr())
+                us.append(l._ws.data_ptr())
+            N.check(N.lib().convio_winograd_filter_transform_tc_batched(
+                len(chunk), (N.ConvDesc * len(chunk))(*descs), e, N.PRECISIONS[prec],
+                (ctypes.c_void_p * len(chunk))(*ws), (ctypes.c_void_p * len(chunk))(*us),
+                C._stream_ptr(stream)), "winograd_filter_transform_tc_batched")
+            launches += 2 if prec == "3xf16" else 1
+    for l in layers:
+        if l.algorithm != "igemm_3xf16" and id(l) not in batched:
             l.prepare(device, stream)
             launches += 1
     return launches

@@ -187,3 +187,24 @@ def test_batched_filter_packing_matches_per_filter_packing():
     for l in layers:
         ref = C.pack_filter_igemm_f16x3(l.weight)
         assert torch.equal(l._ws.view(torch.uint8)[:ref.numel()], ref)
+
+
+@pytest.mark.parametrize("prec", ["3xf16", "3xtf32"])
+def test_batched_winograd_filter_transform_matches_per_filter(prec):
+    """convio_winograd_filter_transform_tc_batched == the per-filter transform, bit for bit."""
+    g = torch.Generator(device="cuda").manual_seed(9)
+    shapes = [(256, 128), (512, 512), (128, 64)]
+    ws = [torch.rand((k, c, 3, 3), device="cuda", generator=g) - 0.5 for k, c in shapes]
+    singles = [C.winograd_filter_transform_tc(w, 4, prec) for w in ws]
+    import ctypes
+    from paper_2012_15667_b200 import _native as N
+    outs = [torch.zeros_like(s) for s in singles]
+    descs = (N.ConvDesc * len(ws))(*[N.make_desc(1, w.shape[1], 8, 8, w.shape[0], 3, 3, 1, 0, 2) for w in ws])
+    rc = N.lib().convio_winograd_filter_transform_tc_batched(
+        len(ws), descs, 4, N.PRECISIONS[prec], (ctypes.c_void_p * len(ws))(*[w.data_ptr() for w in ws]),
+        (ctypes.c_void_p * len(ws))(*[o.data_ptr() for o in outs]), None)
+    assert rc == 0, N.last_error()
+    torch.cuda.synchronize()
+    for s1, o in zip(singles, outs):
+        n = s1.numel() * s1.element_size()
+        assert torch.equal(s1.view(torch.uint8).flatten()[:n], o.view(torch.uint8).flatten()[:n])
