@@ -567,6 +567,8 @@ def main() -> None:
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cudnn", action="store_true", help="skip the cuDNN comparison point")
     ap.add_argument("--no-network", action="store_true", help="skip the chained VGG-16 forward")
+    ap.add_argument("--no-group", action="store_true",
+                    help="one launch per layer in the timed step (no grouped same-plan launches)")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of a CUDA graph")
     ap.add_argument("--dry-run", action="store_true",
                     help="CPU (gloo) rehearsal of the multi-rank logic; no GPU needed")
@@ -592,7 +594,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, load_plans, make_input, make_weights, prepare_layers, shard_range,
+        WORKLOADS, ConvLayer, expand, group_layers, load_plans, make_input, make_weights, prepare_layers,
+        shard_range,
         tuned_table,
         gather_outputs, CUDA_CORE_ALGORITHMS)
     from paper_2012_15667_b200.device import winograd_gemm_flops
@@ -656,18 +659,35 @@ def main() -> None:
                        for i, (s, lay) in enumerate(zip(specs, self.layers))]
             self.ys = [C.empty_act(n_local, s.k, s.out_hw, s.out_hw, lay.layout, device=dev)
                        for s, lay in zip(specs, self.layers)]
+            # same-shape, same-plan 3xF16 layers (res2 x3, res3 x3, res4 x5) run as grouped
+            # launches in the timed step; their inputs / outputs are slices of the stacked buffers
+            self.units = group_layers(self.layers, n_local, dev) if not args.no_group else \
+                [("single", l, [i]) for i, l in enumerate(self.layers)]
+            for kind, unit, idx in self.units:
+                if kind == "group":
+                    for g_i, li in enumerate(idx):
+                        unit.x_of(g_i).copy_(self.xs[li])
+                        self.xs[li], self.ys[li] = unit.x_of(g_i), unit.y_of(g_i)
             self.work_bytes = sum(x.numel() * 4 for x in self.xs) + sum(y.numel() * 4 for y in self.ys)
 
         def step(self, events=None, st=None):
             st = st or stream
-            # the step's filter prep (all 3xF16 splits in one launch), then the convs
+            # the step's filter prep (all 3xF16 splits in one launch), then the convs:
+            # grouped launches for same-plan layers; the per-layer breakdown (events)
+            # runs every layer on its own so each gets its own timing
             launches = prepare_layers(self.layers, dev, st)
+            if events is None:
+                for kind, unit, idx in self.units:
+                    if kind == "group":
+                        unit.run(st)
+                    else:
+                        unit.run(self.xs[idx[0]], out=self.ys[idx[0]], stream=st)
+                    launches += unit.launches
+                return launches
             for i, layer in enumerate(self.layers):
-                if events is not None:
-                    events[i][0].record(st)
+                events[i][0].record(st)
                 layer.run(self.xs[i], out=self.ys[i], stream=st)
-                if events is not None:
-                    events[i][1].record(st)
+                events[i][1].record(st)
                 launches += layer.launches
             return launches
 
@@ -681,7 +701,7 @@ def main() -> None:
             torch.cuda.synchronize(dev)
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g, stream=side):
-                self.step(st=side)
+                self.graph_launches = self.step(st=side)
             torch.cuda.synchronize(dev)
             return g
 
@@ -799,6 +819,7 @@ def main() -> None:
         g.replay()
         torch.cuda.synchronize(dev)
         total_ms = arm.timed_graph(args.steps, g, scratch)
+        launches = arm.graph_launches * args.steps   # the replayed step (grouped launches)
         graph_used = True
     clk = clocks.stop()
     t_max_ms = max_over_ranks(total_ms)
@@ -1061,9 +1082,12 @@ def main() -> None:
                 "l2": ("flushed between steps" if flush else
                        f"per-step working set {work_bytes / 2**30:.2f} GiB per GPU > 126 MB L2"),
                 "tuned_plans": bool(plans),
-                "step": ("filter prep + all convs replayed as one CUDA graph; per_layer / roofline "
-                         f"from an eager pass with per-layer events ({eager_ms / args.steps:.4f} ms/step)"
-                         if graph_used else "eager launches"),
+                "step": ("filter prep + all convs replayed as one CUDA graph, repeated same-plan 3xF16 "
+                         "layers as grouped launches (" + ", ".join(
+                             f"{arm.layers[idx[0]].spec.name} x{len(idx)}" for kind, _, idx in arm.units
+                             if kind == "group") + "); per_layer / roofline from an eager pass with one "
+                         f"launch per layer and per-layer events ({eager_ms / args.steps:.4f} ms/step)"
+                         if graph_used else "eager launches, one per layer"),
                 "tuned_table": os.path.basename(tuned_table(args.workload, n_local)),
                 "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
                          "(FFMA), 3xTF32 tcgen05 implicit GEMM or 3xTF32 tcgen05 Winograd "

@@ -212,6 +212,16 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
 /* The same for `count` <= 32 filters in ONE launch (a step's filter prep: the
  * per-filter launches each occupied only K blocks of the GPU).  Arrays of
  * descriptors, KCRS filters and 256-byte aligned outputs; same layout per job. */
+/* `layers` independent 3xF16 convolutions of ONE shape and tile (desc->n images each)
+ * in one persistent launch: x / y stacked along N (layers * n images), the packed
+ * filters (convio_pack_filter_igemm_f16x3) as 256-byte aligned slices `layer_bytes`
+ * apart, bias layers x K (or null), one activation-scale state for the group.  The
+ * tile's image stack must divide n; the same schedule per layer as convio_conv_igemm
+ * (dataflow.py:219-250), grouped like a grouped GEMM. */
+int convio_conv_igemm_grouped(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
+                              int32_t layers, const float *x, const void *w_packed, size_t layer_bytes,
+                              const float *bias, int32_t relu, float *y, void *workspace, size_t workspace_bytes,
+                              void *stream);
 /* The tensor-core Winograd filter transform (convio_winograd_filter_transform_tc) of
  * `count` <= 32 filters of one e and one precision in one launch (two for 3xF16:
  * the transform, then the fp16 split); fp32-U precisions (TF32, 3xTF32, 3xF16). */

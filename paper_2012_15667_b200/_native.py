@@ -101,6 +101,7 @@ def lib() -> ctypes.CDLL:
             "convio_pack_filter_igemm_f16x3": ([D, P, P, P], ctypes.c_int),
             "convio_pack_filter_igemm_f16x3_bytes": ([D], I64),
             "convio_pack_filters_igemm_f16x3_batched": ([I32, D, P, P, P], ctypes.c_int),
+            "convio_conv_igemm_grouped": ([D, T, I32, I32, P, P, SZ, P, I32, P, P, SZ, P], ctypes.c_int),
             "convio_winograd_filter_transform_tc_batched": ([I32, D, I32, I32, P, P, P], ctypes.c_int),
             "convio_nchw_to_nhwc": ([P, P, I32, I32, I32, I32, P], ctypes.c_int),
             "convio_nhwc_to_nchw": ([P, P, I32, I32, I32, I32, P], ctypes.c_int),
@@ -123,6 +124,7 @@ EXPORTED = (
     "convio_convert_bf16", "convio_winograd_filter_transform_tc", "convio_winograd_bgemm",
     "convio_pack_filter_igemm_f16x3", "convio_pack_filter_igemm_f16x3_bytes",
     "convio_pack_filters_igemm_f16x3_batched", "convio_winograd_filter_transform_tc_batched",
+    "convio_conv_igemm_grouped",
     "convio_nchw_to_nhwc", "convio_nhwc_to_nchw", "convio_maxpool2x2_nhwc",
 )
 

@@ -26,6 +26,7 @@ from .dataflow import LAYOUTS, TileConfig
 __all__ = ["conv_direct", "conv_winograd", "conv_igemm_tf32", "conv_igemm", "conv_winograd_tc",
            "winograd_filter_transform", "winograd_filter_transform_tc",
            "pack_filter_direct", "pack_filter_igemm", "pack_filter_igemm_bf16", "pack_filter_igemm_f16x3",
+           "conv_igemm_grouped", "f16x3_slice_bytes",
            "infer_layout", "to_layout", "maxpool2x2", "empty_act", "query", "last_launch_count"]
 
 
@@ -324,6 +325,45 @@ def pack_filter_igemm_f16x3(w: torch.Tensor, stream=None) -> torch.Tensor:
     return out
 
 
+def f16x3_slice_bytes(k: int, c: int, r: int, s: int) -> int:
+    """Bytes of one packed 3xF16 filter (``pack_filter_igemm_f16x3``), rounded to 256."""
+    desc = N.make_desc(1, c, max(8, r), max(8, s), k, r, s, 1, 0, 2)
+    return 256 * ((int(N.lib().convio_pack_filter_igemm_f16x3_bytes(ctypes.byref(desc))) + 255) // 256)
+
+
+def conv_igemm_grouped(x: torch.Tensor, w_shape, w_packed: torch.Tensor, layers: int, slice_bytes: int,
+                       padding: int = 0, stride: int = 1, tile: TileConfig | None = None,
+                       bias: torch.Tensor | None = None, relu: bool = False,
+                       out: torch.Tensor | None = None, stream=None,
+                       workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """``layers`` independent 3xF16 convolutions of one shape and tile in ONE launch
+    (``convio_conv_igemm_grouped``): ``x`` channels-last with the layers' batches
+    stacked along N, ``w_packed`` the layers' :func:`pack_filter_igemm_f16x3` outputs
+    as ``slice_bytes``-apart slices, ``bias`` ``layers x K``; returns the stacked
+    outputs.  Layer l's images are ``[l * N / layers, (l + 1) * N / layers)``."""
+    _check_tensor(x, "x")
+    if infer_layout(x) != "HWC":
+        raise ValueError("conv_igemm_grouped needs a channels-last (HWC) input")
+    if tile is None:
+        raise ValueError("conv_igemm_grouped needs an explicit tile")
+    n_all = x.shape[0]
+    if layers < 1 or n_all % layers:
+        raise ValueError(f"{n_all} stacked images do not split into {layers} layers")
+    k, c, r, s_ = w_shape
+    desc = N.make_desc(n_all // layers, x.shape[1], x.shape[2], x.shape[3], k, r, s_, stride, padding, 2)
+    p, q = _out_hw(desc.h, desc.w, r, s_, stride, padding)
+    if out is None:
+        out = empty_act(n_all, k, p, q, "HWC", device=x.device)
+    need = 256 * ((4 * 296 + 255) // 256)
+    if workspace is None or workspace.numel() * workspace.element_size() < need:
+        workspace = torch.zeros(need, device=x.device, dtype=torch.uint8)
+    rc = N.lib().convio_conv_igemm_grouped(
+        ctypes.byref(desc), ctypes.byref(N.make_tile(tile, 2)), N.PREC_3XF16, layers, _ptr(x), _ptr(w_packed),
+        slice_bytes, _ptr(bias), int(bool(relu)), _ptr(out), _ptr(workspace), need, _stream_ptr(stream))
+    N.check(rc, "conv_igemm_grouped[3xf16]")
+    return out
+
+
 # conv_igemm precisions -> the C-ABI algorithm ids (workspace size / query)
 _IGEMM_ALG = {"tf32": N.ALG_IGEMM_TF32, "3xtf32": N.ALG_IGEMM_3XTF32, "bf16": N.ALG_IGEMM_BF16,
               "3xf16": N.ALG_IGEMM_3XF16}
@@ -370,7 +410,7 @@ def conv_igemm(x: torch.Tensor, w: torch.Tensor, padding: int = 0, stride: int =
     need = int(N.lib().convio_workspace_bytes(ctypes.byref(desc), None, _IGEMM_ALG[precision]))
     wsrc, is_packed = (w_packed, 1) if w_packed is not None else (w.contiguous(), 0)
     if w_packed is not None and prec == N.PREC_3XF16:
-        need = 256 * ((4 * 296 + 255) // 256)   # the |x| maxima only
+        need = 256 * ((4 * 296 + 255) // 256)   # the activation-scale state only
     elif w_packed is not None and prec != N.PREC_BF16:
         need = 0
     if need and (workspace is None or workspace.numel() * workspace.element_size() < need):

@@ -468,7 +468,7 @@ static int plan_igemm_halo(const convio_conv_desc *d, const convio_tile *t, Igem
         const int kblocks = (pl->fold ? d->r : d->r * d->s) * (d->c / kblock_channels(kind));
         const size_t slice = (size_t)kblocks * stage;
         pl->na = 3 * slot + 3 * stage <= budget ? 3 : 2;
-        if (pl->tsa && pl->fold) {
+        if (pl->tsa && pl->fold && !pl->no_resb) {
             if (3 * slot + slice <= budget) pl->na = 3;
             if ((size_t)pl->na * slot + slice <= budget) pl->resb_slots = kblocks;
         }
@@ -691,6 +691,19 @@ static bool make_igemm_maps(const IgemmPlan &pl, const void *x, const void *wq, 
     const bool xok = bf ? encode_tensor_map_bf16_sw128(tx, 4, const_cast<void *>(x), xd, xs, xb, xes)
                         : encode_tensor_map_tiled_ex(tx, 4, const_cast<void *>(x), xd, xs, xb, xes, true);
     if (!xok) return false;
+    if (pl.layers > 1) {   // grouped conv: G packed slices, layer_bytes apart
+        if (pl.layer_bytes & 15) return false;
+        if (pl.fold) {
+            cuuint64_t fd[3] = {(cuuint64_t)P.c, (cuuint64_t)taps * P.k * wplanes, (cuuint64_t)pl.layers};
+            cuuint64_t fs[2] = {(cuuint64_t)P.c * wes_b, (cuuint64_t)pl.layer_bytes};
+            cuuint32_t fb[3] = {wcb, (cuuint32_t)(pl.bn / 2), 1};
+            return encode_tensor_map_bf16_sw128(tw, 3, const_cast<void *>(wq), fd, fs, fb, es);
+        }
+        cuuint64_t gd[4] = {(cuuint64_t)P.c, (cuuint64_t)P.k, (cuuint64_t)taps * wplanes, (cuuint64_t)pl.layers};
+        cuuint64_t gs[3] = {(cuuint64_t)P.c * wes_b, (cuuint64_t)P.k * P.c * wes_b, (cuuint64_t)pl.layer_bytes};
+        cuuint32_t gb[4] = {wcb, (cuuint32_t)(pl.pair ? pl.bn / 2 : pl.bn), 1, 1};
+        return encode_tensor_map_bf16_sw128(tw, 4, const_cast<void *>(wq), gd, gs, gb, es);
+    }
     if (pl.fold) {   // packed filter as [R*S*K rows][C]: a kernel row's S*K rows are contiguous
         cuuint64_t fd[2] = {(cuuint64_t)P.c, (cuuint64_t)taps * P.k * wplanes};
         cuuint64_t fs[1] = {(cuuint64_t)P.c * wes_b};
@@ -729,8 +742,10 @@ int igemm_launch(IgemmPlan &pl, const void *x, const void *wq, const float *bias
         if (PP.g.splits > 1) {
             // zero the output from the image group of the tail's first block on (whole
             // tiles before it overwrite their part of that range with plain stores)
-            const int first_block = 2 * ((PP.tail_start / PP.nblocks) % PP.pairs_per_group);
-            const int64_t img_lo = (int64_t)(first_block / (PP.g.tiles_x * PP.g.tiles_y)) * PP.g.imgs;
+            const int first_pair = PP.tail_start / PP.nblocks;
+            const int first_block = 2 * (first_pair % PP.pairs_per_group);
+            const int64_t img_lo = (int64_t)(first_block / (PP.g.tiles_x * PP.g.tiles_y)) * PP.g.imgs +
+                                   (PP.g.layer_imgs ? (int64_t)(first_pair / PP.pairs_per_group) * PP.g.layer_imgs : 0);
             const size_t per_img = (size_t)PP.g.p * PP.g.q * PP.g.k;
             if (img_lo < PP.g.n)
                 CONVIO_CUDA_TRY(cudaMemsetAsync(y + img_lo * per_img, 0,
@@ -918,6 +933,57 @@ int convio_pack_filter_igemm_f16x3(const convio_conv_desc *desc, const float *w,
         return CONVIO_EINVAL;
     }
     return launch_pack_filter_f16x3(desc, w, w_packed, (cudaStream_t)stream);
+}
+
+int convio_conv_igemm_grouped(const convio_conv_desc *desc, const convio_tile *tile, int32_t precision,
+                              int32_t layers, const float *x, const void *w_packed, size_t layer_bytes,
+                              const float *bias, int32_t relu, float *y, void *workspace, size_t workspace_bytes,
+                              void *stream) {
+    clear_error();
+    reset_launches();
+    const int kind = prec_kind(precision);
+    if (kind != KIND_3XF16C) {
+        set_error("grouped implicit GEMMs: 3xF16 only");
+        return CONVIO_EINVAL;
+    }
+    if (!x || !w_packed || !y || !tile || !desc || layers < 1 || desc->n < 1) {
+        set_error("null tensor pointer / descriptor / tile, or layers < 1");
+        return CONVIO_EINVAL;
+    }
+    if ((reinterpret_cast<uintptr_t>(w_packed) & 255) || (layer_bytes & 255) ||
+        layer_bytes < f16c_filter_bytes(desc) || (reinterpret_cast<uintptr_t>(workspace) & 255) ||
+        !workspace || workspace_bytes < f16c_partials_bytes()) {
+        set_error("grouped 3xF16: 256-byte aligned packed slices of >= %zu bytes and a %zu-byte workspace",
+                  f16c_filter_bytes(desc), f16c_partials_bytes());
+        return CONVIO_EINVAL;
+    }
+    convio_conv_desc dg = *desc;
+    dg.n = desc->n * layers;   // the stacked batch
+    IgemmPlan pl;
+    pl.no_resb = true;
+    char why[160];
+    int rc = plan_igemm(&dg, tile, &pl, why, sizeof(why), kind);
+    if (rc) return rc;
+    if (!pl.pair || desc->n % pl.P.imgs) {
+        set_error("grouped 3xF16 needs CTA-pair tiles whose image stack (%d) divides the per-layer batch %d",
+                  pl.P.imgs, desc->n);
+        return CONVIO_EINFEASIBLE;
+    }
+    pl.layers = layers;
+    pl.layer_bytes = layer_bytes;
+    pl.P.layer_imgs = layers > 1 ? desc->n : 0;
+    if (layers > 1) {   // one group per layer: a pair never spans two layers' blocks
+        pl.P.img_groups = (desc->n + pl.P.imgs - 1) / pl.P.imgs;
+        pl.groups = layers;
+        pl.blocks_per_group = pl.P.tiles_x * pl.P.tiles_y * pl.P.img_groups;
+        rc = finish_pair_grid(&pl);
+        if (rc) return rc;
+    }
+    pl.P.col_stride = (int)(layer_bytes / 4);
+    pl.scale_state = (int *)workspace;
+    pl.P.col_exp = (const int *)((const uint8_t *)w_packed +
+                                 align256((size_t)4 * desc->k * desc->c * desc->r * desc->s));
+    return igemm_launch(pl, x, w_packed, bias, relu, y, (cudaStream_t)stream);
 }
 
 int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_desc *descs, const float *const *w,

@@ -280,7 +280,7 @@ __device__ __forceinline__ void pair_block_origin(const IgemmParams &P, int grp,
         const int ig = rest / P.tiles_y;
         ox0 = xt * P.bx;
         oy0 = yt * P.by;
-        img0 = ig * P.imgs;
+        img0 = ig * P.imgs + (P.layer_imgs ? grp * P.layer_imgs : 0);   // grouped conv: group = layer
     }
 }
 
@@ -783,7 +783,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             tma_load_4d(a, map_x, cb * CB, xc, yc, img0, full + s);
                             tma_load_4d(a + A_BYTES + B_BYTES, map_x, cb * CB + 32, xc, yc, img0, full + s);
                         }
-                        if (FOLD) {
+                        if (P.layer_imgs) {   // grouped: the item's layer (its group) -- both CTAs
+                            const int layer = grp;   // of a pair use ITS filter, spare blocks included
+                            if (FOLD) {
+                                tma_load_3d(b, map_w, cb * CB, frow, layer, full + s);
+                                tma_load_3d(blo, map_w, cb * CB, frow + lo_tap * P.k, layer, full + s);
+                            } else {
+                                tma_load_4d(b, map_w, cb * CB, n0, wc, layer, full + s);
+                                tma_load_4d(blo, map_w, cb * CB, n0, wc + lo_tap, layer, full + s);
+                            }
+                        } else if (FOLD) {
                             tma_load_2d(b, map_w, cb * CB, frow, full + s);
                             tma_load_2d(blo, map_w, cb * CB, frow + lo_tap * P.k, full + s);
                         } else {
@@ -844,8 +853,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     // both CTAs' planes complete on the LEADER's barrier: the MMA issuer waits on
                     // it directly, the converters never wait for filter data
                     if (leader) mbar_arrive_expect_tx(full + s, 4u * (uint32_t)B_BYTES);
-                    tma_load_3d_pair(b, map_w, cb * CB, n0, tap, full + s);
-                    tma_load_3d_pair(b + B_BYTES, map_w, cb * CB, n0, tap + lo_tap, full + s);
+                    if (P.layer_imgs) {   // grouped: the item's layer (its group)
+                        const int layer = grp;
+                        tma_load_4d_pair(b, map_w, cb * CB, n0, tap, layer, full + s);
+                        tma_load_4d_pair(b + B_BYTES, map_w, cb * CB, n0, tap + lo_tap, layer, full + s);
+                    } else {
+                        tma_load_3d_pair(b, map_w, cb * CB, n0, tap, full + s);
+                        tma_load_3d_pair(b + B_BYTES, map_w, cb * CB, n0, tap + lo_tap, full + s);
+                    }
                     if (++cb == P.cblocks) {
                         cb = 0;
                         ++tap;
@@ -1014,7 +1029,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const uint32_t stg = smem_u32(ring_end + 1024);
         // per-channel epilogue constants (not for the batched Winograd GEMMs: their column
         // exponents differ per xi) staged once by the 4 epilogue warps
-        const bool cs_smem = !F16X3 && P.k <= kEpiConstK;
+        const bool cs_smem = !F16X3 && P.k <= kEpiConstK && !P.layer_imgs;
         float *ebias = reinterpret_cast<float *>(ring_end + 1024 + pair_epi_bytes(FOLD));
         float *escale = ebias + P.k;
         const int act_exp = F16C ? f16_row_exp(__int_as_float(f16c_scale_max)) : 0;   // one per tensor
@@ -1068,6 +1083,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             int ox0, oy0, img0;
             pair_block_origin(P, grp, blk, ox0, oy0, img0);
             const int k0 = nb * KOUT;
+            const int layer = P.layer_imgs ? grp : 0;   // grouped conv: group = layer
             float rs = 1.f;   // the row's operand scale (3xF16 families; 1 when folded into escale)
             if constexpr (F16X3) {
                 const int per_img = P.bx * P.by;
@@ -1128,9 +1144,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                             cs[0] = c4.x; cs[1] = c4.y; cs[2] = c4.z; cs[3] = c4.w;
                         }
                     } else {
-                        if (with_bias) bv = __ldg(reinterpret_cast<const float4 *>(P.bias + kc) + j4);
+                        if (with_bias) bv = __ldg(reinterpret_cast<const float4 *>(P.bias + (int64_t)layer * P.k + kc) + j4);
                         if constexpr (F16X3 || F16C) {
-                            const int4 ce = __ldg(reinterpret_cast<const int4 *>(P.col_exp + (int64_t)grp * P.k + kc) + j4);
+                            const int4 ce = __ldg(reinterpret_cast<const int4 *>(
+                                P.col_exp + (P.batched ? (int64_t)grp * P.k : (int64_t)layer * P.col_stride) + kc) + j4);
                             cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
                         }
                     }
@@ -1162,7 +1179,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                 epi_bar();
                 if (RESB && c0 == 0 && q == 0 && lane == 0) PAIR_TRACE(0, t);   // chunk 0 staged
-                if (issuer) {
+                if (issuer && blk < PP.blocks_per_group) {   // (a pair's spare block stores nothing)
                     if (spl >= 0) tma_reduce_add_4d(map_y, box, kc, ox0, oy0, img0);
                     else tma_store_4d(map_y, box, kc, ox0, oy0, img0);
                     bulk_commit();

@@ -44,12 +44,16 @@ struct IgemmParams {
     int splits;                // split-K factor (blockIdx.z = split; > 1 only without ReLU)
     // KIND_3XF16 (batched only): power-of-two exponents the operands were scaled by;
     // the epilogue multiplies D[t][k] by 2^-(row_exp[g][t] + col_exp[g][k])
-    // KIND_3XF16C (conv): row_exp = the nred per-block |x| maxima (float bits) of
-    // absmax_partials_kernel, reduced by the kernel into ONE activation exponent;
-    // col_exp[k] = the packed filter's per-output-channel exponents
+    // KIND_3XF16C (conv): col_exp[k] = the packed filter's per-output-channel exponents
     const int *row_exp;
     const int *col_exp;
     int nred;
+    // grouped conv (3xF16C pair kernels): G independent layers of one shape and plan in
+    // one launch -- inputs / outputs stacked along N (layer_imgs images each), filters
+    // as G packed slices (filter map gains a layer dimension), bias G x K, the packed
+    // slice's exponents col_stride ints apart.  layer_imgs = 0: one layer
+    int layer_imgs;
+    int col_stride;
 };
 
 // operand kinds of the tcgen05 contraction
@@ -417,6 +421,9 @@ struct IgemmPlan {
     int resb_slots = 0;      // halo TSA: filter slice resident in smem (one slot per k-block)
     int64_t tail_start = 0;  // pair kernel: tile items from here on are split-K (P.splits)
     int *scale_state = nullptr;   // 3xF16C: speculative activation scale state (workspace)
+    bool no_resb = false;    // planning option: never keep the filter resident (grouped convs)
+    int layers = 1;          // grouped conv: layers stacked along N (filter map gains a dim)
+    size_t layer_bytes = 0;  // grouped conv: bytes between consecutive packed filter slices
     PairFn pfn = nullptr;
     int groups = 1, blocks_per_group = 0;
     int fpr = 0, fp_bytes = 0, a_slot = 0, na = 0;

@@ -159,6 +159,79 @@ def _f16x3_filter_bytes(s: "LayerSpec") -> int:
     return int(N.lib().convio_pack_filter_igemm_f16x3_bytes(ctypes.byref(desc)))
 
 
+def _on(t: torch.Tensor, device) -> bool:
+    """``t`` lives on ``device`` ("cuda" meaning the current CUDA device)."""
+    d = torch.device(device)
+    if d.type == "cuda" and d.index is None:
+        d = torch.device("cuda", torch.cuda.current_device())
+    return t.device == d
+
+
+class LayerGroup:
+    """``G`` independent layers of one shape and one 3xF16 implicit-GEMM plan run as ONE
+    persistent launch (``conv.conv_igemm_grouped``, like a grouped GEMM): their inputs and
+    outputs are slices of stacked buffers, their packed filters slices of one buffer (the
+    layers' own filter workspaces point into it, so :func:`prepare_layers` fills it).
+    Saves the per-layer launch, ramp, drain, last-round imbalance and checking launch."""
+
+    def __init__(self, layers, n: int, device):
+        s = layers[0].spec
+        self.layers, self.n, self.spec = layers, n, s
+        self.tile = layers[0].tile
+        g = len(layers)
+        self.slice_bytes = C.f16x3_slice_bytes(s.k, s.c, s.r, s.r)
+        self.wbuf = torch.zeros(g * self.slice_bytes, dtype=torch.uint8, device=device)
+        for i, l in enumerate(layers):
+            off = i * self.slice_bytes
+            l._ws = self.wbuf[off:off + 4 * l.filter_elems()].view(torch.float32)
+        self.x = C.empty_act(g * n, s.c, s.hw, s.hw, "HWC", device=device)
+        self.y = C.empty_act(g * n, s.k, s.out_hw, s.out_hw, "HWC", device=device)
+        biases = [l.bias for l in layers]
+        self.bias = torch.cat(biases) if all(b is not None for b in biases) else None
+        if self.bias is None and any(b is not None for b in biases):
+            raise ValueError("a group's layers must all have a bias or none")
+        self.relu = layers[0].relu
+        self.ws = torch.zeros(4096, dtype=torch.uint8, device=device)   # activation-scale state
+        self.launches = 0
+
+    def x_of(self, i: int) -> torch.Tensor:
+        return self.x[i * self.n:(i + 1) * self.n]
+
+    def y_of(self, i: int) -> torch.Tensor:
+        return self.y[i * self.n:(i + 1) * self.n]
+
+    def run(self, stream=None) -> torch.Tensor:
+        s = self.spec
+        C.conv_igemm_grouped(self.x, (s.k, s.c, s.r, s.r), self.wbuf, len(self.layers), self.slice_bytes,
+                             padding=s.pad, stride=s.stride, tile=self.tile, bias=self.bias, relu=self.relu,
+                             out=self.y, stream=stream, workspace=self.ws)
+        self.launches = C.last_launch_count()
+        return self.y
+
+
+def group_layers(layers, n: int, device) -> list:
+    """Runs of consecutive layers with the same shape and the same 3xF16 implicit-GEMM
+    plan (CTA-pair tiles whose image stack divides ``n``) as :class:`LayerGroup`; other
+    layers stay single.  Returns units ``(kind, obj, [layer indices])``."""
+    units, i = [], 0
+    while i < len(layers):
+        l = layers[i]
+        j = i + 1
+        if l.algorithm == "igemm_3xf16" and l.tile is not None and l.tile.n_zt >= 2:
+            while (j < len(layers) and layers[j].algorithm == "igemm_3xf16" and layers[j].spec == l.spec
+                   and layers[j].tile == l.tile and (layers[j].bias is None) == (l.bias is None)):
+                j += 1
+        if j - i >= 2:
+            try:
+                units.append(("group", LayerGroup(layers[i:j], n, device), list(range(i, j))))
+            except ValueError:
+                units += [("single", layers[k], [k]) for k in range(i, j)]
+        else:
+            units += [("single", layers[k], [k]) for k in range(i, j)]
+        i = j
+    return units
+
+
 def prepare_layers(layers, device, stream=None) -> int:
     """Filter prep of a whole step: the 3xF16 implicit-GEMM layers' fp16 splits in ONE
     launch (``convio_pack_filters_igemm_f16x3_batched``), the tensor-core Winograd
@@ -190,7 +263,7 @@ def prepare_layers(layers, device, stream=None) -> int:
             descs, ws, us = [], [], []
             for l in chunk:
                 s = l.spec
-                if l._ws is None or l._ws.device != torch.device(device) or l._ws.dtype != torch.float32:
+                if l._ws is None or not _on(l._ws, device) or l._ws.dtype != torch.float32:
                     l._ws = torch.empty(l.filter_elems(), device=device, dtype=torch.float32)
                 descs.append(N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 2))
                 ws.append(l.weight.data_ptr())
@@ -260,7 +333,7 @@ class ConvLayer:
         s = self.spec
         prec = self.precision
         dtype = torch.bfloat16 if prec == "bf16" else torch.float32
-        if self._ws is None or self._ws.device != torch.device(device) or self._ws.dtype != dtype:
+        if self._ws is None or not _on(self._ws, device) or self._ws.dtype != dtype:
             self._ws = torch.empty(self.filter_elems(), device=device, dtype=dtype)
         w = self.weight
         desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0,
@@ -291,7 +364,7 @@ class ConvLayer:
         """(descriptor, filter, packed buffer) of this layer's 3xF16 filter prep."""
         from . import _native as N
         s = self.spec
-        if self._ws is None or self._ws.device != torch.device(device) or self._ws.dtype != torch.float32:
+        if self._ws is None or not _on(self._ws, device) or self._ws.dtype != torch.float32:
             self._ws = torch.empty(self.filter_elems(), device=device, dtype=torch.float32)
         desc = N.make_desc(1, s.c, max(s.hw, s.r), max(s.hw, s.r), s.k, s.r, s.r, 1, 0, 2)
         return desc, self.weight, self._ws

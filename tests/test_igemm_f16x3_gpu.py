@@ -208,3 +208,36 @@ def test_batched_winograd_filter_transform_matches_per_filter(prec):
     for s1, o in zip(singles, outs):
         n = s1.numel() * s1.element_size()
         assert torch.equal(s1.view(torch.uint8).flatten()[:n], o.view(torch.uint8).flatten()[:n])
+
+
+@pytest.mark.parametrize("case", [
+    (3, 16, 128, 28, 128, 1, TileConfig(4, 2, 128, 32768, 1, 1, 4, layout="HWC")),  # A in TMEM
+    (2, 4, 64, 56, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 4, layout="HWC")),     # halo fold
+    (4, 32, 256, 14, 256, 1, TileConfig(2, 2, 256, 32768, 1, 1, 2, layout="HWC")),  # pair (+ tail split)
+    (2, 32, 128, 28, 128, 2, TileConfig(2, 2, 128, 32768, 1, 1, 4, layout="HWC")),  # stride 2
+], ids=["tsa", "fold", "pair", "stride2"])
+def test_grouped_3xf16_conv_matches_per_layer_and_oracle(case):
+    """convio_conv_igemm_grouped: G independent layers (own filters and biases) of one
+    shape in one launch == G single-layer launches, and the oracle."""
+    layers, n, c, hw, k, stride, tile = case
+    g = np.random.default_rng(11)
+    xs = [g.uniform(-1, 1, (n, c, hw, hw)).astype(np.float32) for _ in range(layers)]
+    wts = [(g.uniform(-1, 1, (k, c, 3, 3)) / np.sqrt(c * 9)).astype(np.float32) for _ in range(layers)]
+    bs = [g.uniform(-0.2, 0.2, k).astype(np.float32) for _ in range(layers)]
+    sb = C.f16x3_slice_bytes(k, c, 3, 3)
+    packed = torch.zeros(layers * sb, dtype=torch.uint8, device="cuda")
+    for l, wt in enumerate(wts):
+        p1 = C.pack_filter_igemm_f16x3(torch.from_numpy(wt).cuda())
+        packed[l * sb:l * sb + p1.numel()] = p1
+    xg = _hwc(np.concatenate(xs))
+    bias = torch.from_numpy(np.concatenate(bs)).cuda()
+    yg = C.conv_igemm_grouped(xg, (k, c, 3, 3), packed, layers, sb, padding=1, stride=stride, tile=tile,
+                              bias=bias)
+    yg = yg.contiguous().cpu().numpy()
+    for l in range(layers):
+        y1 = C.conv_igemm(_hwc(xs[l]), torch.from_numpy(wts[l]).cuda(), padding=1, stride=stride, tile=tile,
+                          precision="3xf16", bias=torch.from_numpy(bs[l]).cuda())
+        ref = co.direct_conv(xs[l], wts[l], stride, 1) + bs[l][None, :, None, None]
+        got = yg[l * n:(l + 1) * n]
+        assert co.rel_err(got, ref) <= tol_3xtf32(c), l
+        assert np.abs(got - y1.contiguous().cpu().numpy()).max() <= 1e-5 * np.abs(ref).max(), l

@@ -4,6 +4,7 @@ import json
 import os
 
 import pytest
+import torch
 
 from paper_2012_15667_b200 import runner
 from paper_2012_15667_b200.dataflow import TileConfig
@@ -101,3 +102,30 @@ def test_per_batch_table_preferred_for_the_local_batch(tmp_path, monkeypatch):
     assert runner.load_plans("toy")["L"]["tile"].z == 256
     assert runner.load_plans("toy", n=32)["L"]["tile"].z == 128
     assert runner.load_plans("toy", n=64)["L"]["tile"].z == 256   # no n64 table: full-batch one
+
+
+@pytest.mark.parametrize("n", [256, 32])
+def test_group_layers_stacks_repeated_3xf16_layers(n):
+    """bench.py's timed step runs the repeated same-plan ResNet-50 3x3 layers as grouped
+    launches: the groups are exactly the runs of identical specs on one 3xF16 pair plan,
+    and each layer's filter workspace is its slice of the group's packed buffer."""
+    specs = runner.expand(runner.WORKLOADS["resnet50"])
+    plans = runner.load_plans("resnet50", n=n)
+    layers = [runner.ConvLayer(s, torch.zeros(s.k, s.c, s.r, s.r), plans.get(s.name)) for s in specs]
+    units = runner.group_layers(layers, n, "cpu")
+    assert sorted(i for _, _, idx in units for i in idx) == list(range(len(layers)))
+    for kind, unit, idx in units:
+        if kind != "group":
+            continue
+        assert len(idx) >= 2 and idx == list(range(idx[0], idx[-1] + 1))
+        assert {layers[i].spec for i in idx} == {unit.spec} and unit.tile.n_zt >= 2
+        assert all(layers[i].algorithm == "igemm_3xf16" for i in idx)
+        s = unit.spec
+        assert unit.x.shape == (len(idx) * n, s.c, s.hw, s.hw) and unit.x.stride()[1] == 1
+        for g, i in enumerate(idx):
+            ws = layers[i]._ws
+            assert ws.data_ptr() == unit.wbuf.data_ptr() + g * unit.slice_bytes
+            assert ws.numel() * 4 <= unit.slice_bytes
+            assert unit.x_of(g).data_ptr() == unit.x.data_ptr() + g * n * s.c * s.hw * s.hw * 4
+    grouped = [idx for kind, _, idx in units if kind == "group"]
+    assert grouped, "the tuned ResNet-50 tables put the repeated layers on 3xF16 pair tiles"
