@@ -164,9 +164,16 @@ struct PackBatch {
     int kcum[kPackJobs + 1];
     PackJob job[kPackJobs];
 };
+// STAGED: the row's C*R*S weights come in once with 16-B coalesced loads into shared
+// memory (max |w| on the way), and the tap-major plane writes read them from there
+// (rows up to kPackStageFloats; larger filters read the strided KCRS row from global)
+constexpr int kPackStageFloats = 12288;   // 48 KB: C*R*S <= 12288 (C <= 1365 at 3x3)
+template <bool STAGED>
 __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const __grid_constant__ PackBatch B) {
     pdl_wait();
     __shared__ float red[8];
+    extern __shared__ float4 stage4[];
+    float *stage = reinterpret_cast<float *>(stage4);
     const int total = B.kcum[B.n];
     for (int g = blockIdx.x; g < total; g += gridDim.x) {
         int j = 0;
@@ -177,7 +184,24 @@ __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const _
         const int64_t plane = (int64_t)rs * k * c;
         const float *wr = J.w + (int64_t)kk * crs;
         float mx = 0.0f;
-        for (int i = threadIdx.x; i < crs; i += blockDim.x) mx = fmaxf(mx, fabsf(wr[i]));
+        if (STAGED) {
+            if (((reinterpret_cast<uintptr_t>(wr) & 15) == 0) && (crs & 3) == 0) {
+                const float4 *w4 = reinterpret_cast<const float4 *>(wr);
+                for (int i = threadIdx.x; i < (crs >> 2); i += blockDim.x) {
+                    const float4 v = __ldg(w4 + i);
+                    stage4[i] = v;
+                    mx = fmaxf(mx, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+                }
+            } else {
+                for (int i = threadIdx.x; i < crs; i += blockDim.x) {
+                    const float v = wr[i];
+                    stage[i] = v;
+                    mx = fmaxf(mx, fabsf(v));
+                }
+            }
+        } else {
+            for (int i = threadIdx.x; i < crs; i += blockDim.x) mx = fmaxf(mx, fabsf(wr[i]));
+        }
         for (int off = 16; off > 0; off >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, off));
         if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
         __syncthreads();
@@ -185,12 +209,13 @@ __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const _
         for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mx = fmaxf(mx, red[i]);
         const int e = f16_row_exp(mx);
         const float sc = pow2f(e);
+        const float *src = STAGED ? stage : wr;
         const int pairs = (c + 1) / 2;
         for (int t = threadIdx.x; t < rs * pairs; t += blockDim.x) {
             const int tap = t / pairs, cc = 2 * (t - tap * pairs);
             __half *hrow = J.wq + ((int64_t)tap * k + kk) * c;
-            const float v0 = wr[cc * rs + tap] * sc;
-            const float v1 = cc + 1 < c ? wr[(cc + 1) * rs + tap] * sc : 0.0f;
+            const float v0 = src[cc * rs + tap] * sc;
+            const float v1 = cc + 1 < c ? src[(cc + 1) * rs + tap] * sc : 0.0f;
             const __half2 hi = __floats2half2_rn(v0, v1);
             const float2 hf = __half22float2(hi);
             const __half2 lo = __floats2half2_rn(v0 - hf.x, v1 - hf.y);
@@ -203,7 +228,7 @@ __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const _
             }
         }
         if (threadIdx.x == 0) J.col_exp[kk] = e;
-        __syncthreads();
+        __syncthreads();   // red[] and the stage are reused by the next row
     }
 }
 
@@ -1012,8 +1037,24 @@ int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_des
         B.job[i].rs = d->r * d->s;
         B.kcum[i + 1] = B.kcum[i] + d->k;
     }
+    int max_crs = 0;
+    for (int i = 0; i < count; ++i) max_crs = std::max(max_crs, B.job[i].c * B.job[i].rs);
     const int blocks = std::max(1, std::min(B.kcum[count], 148 * 8));
-    CONVIO_CUDA_TRY(launch_pdl(pack_filters_f16x3_batched_kernel, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, B));
+    if (max_crs <= kPackStageFloats) {
+        const size_t smem = (size_t)((max_crs + 3) & ~3) * 4;
+        static bool attr = false;
+        if (!attr) {
+            CONVIO_CUDA_TRY(cudaFuncSetAttribute(pack_filters_f16x3_batched_kernel<true>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 kPackStageFloats * 4));
+            attr = true;
+        }
+        CONVIO_CUDA_TRY(launch_pdl(pack_filters_f16x3_batched_kernel<true>, dim3(blocks), dim3(256), smem,
+                                   (cudaStream_t)stream, B));
+    } else {
+        CONVIO_CUDA_TRY(launch_pdl(pack_filters_f16x3_batched_kernel<false>, dim3(blocks), dim3(256), 0,
+                                   (cudaStream_t)stream, B));
+    }
     note_launch();
     CONVIO_CUDA_TRY(cudaGetLastError());
     return CONVIO_OK;

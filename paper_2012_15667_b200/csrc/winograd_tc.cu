@@ -432,6 +432,126 @@ __global__ void __launch_bounds__(256) winograd_u_split_f16x3_batched_kernel(con
     }
 }
 
+// U = G g G^T of one 3x3 filter g (9 contiguous floats), o[a * M + b]: the same
+// arithmetic as winograd_filter_tc_kernel, so both give identical bits
+template <int E>
+__device__ __forceinline__ void wino_filter_u(const float *__restrict__ g, float (&o)[WinoTf<E>::M * WinoTf<E>::M]) {
+    constexpr int M = WinoTf<E>::M;
+    float t[M][3];
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+        float col[3] = {g[jj], g[3 + jj], g[6 + jj]}, oc[M];
+        WinoTf<E>::g(col, oc);
+#pragma unroll
+        for (int a = 0; a < M; ++a) t[a][jj] = oc[a];
+    }
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+        float orow[M];
+        WinoTf<E>::g(t[a], orow);
+#pragma unroll
+        for (int b = 0; b < M; ++b) o[a * M + b] = orow[b];
+    }
+}
+
+// Batched 3xF16 U in ONE pass (no fp32 U round trip through HBM, one launch instead
+// of transform + split): one block per (job, output channel k); pass 1 recomputes U
+// over the C channels for the per-xi max |U| (-> the row exponents), pass 2 recomputes
+// it and writes the hi / lo planes, a channel pair per thread (half2 stores).  B.cum
+// here is the prefix sum of K.  Bit-identical to winograd_filter_tc_batched_kernel +
+// winograd_u_split_f16x3_batched_kernel (same arithmetic, same split).
+template <int E>
+__global__ void __launch_bounds__(256) winograd_filter_f16x3_batched_kernel(const __grid_constant__ WinoFilterBatch B) {
+    pdl_wait();
+    constexpr int M = WinoTf<E>::M, MM = M * M;
+    __shared__ float red[8][MM];
+    __shared__ float scs[MM];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t gr = blockIdx.x; gr < B.cum[B.n]; gr += gridDim.x) {
+        int j = 0;
+        while (B.cum[j + 1] <= gr) ++j;
+        const int kk = (int)(gr - B.cum[j]), k = B.k[j], c = B.c[j];
+        const float *wk = B.w[j] + (int64_t)kk * c * 9;
+        const int64_t rows = (int64_t)MM * k;
+        __half *u16 = reinterpret_cast<__half *>(B.u[j] + rows * c);
+        int *col_exp = reinterpret_cast<int *>(B.u[j] + 2 * rows * c);
+        float mx[MM];
+#pragma unroll
+        for (int q = 0; q < MM; ++q) mx[q] = 0.0f;
+        for (int cc = threadIdx.x; cc < c; cc += blockDim.x) {
+            const float *g = wk + (int64_t)cc * 9;
+            float t[M][3];
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) {
+                float col[3] = {g[jj], g[3 + jj], g[6 + jj]}, oc[M];
+                WinoTf<E>::g(col, oc);
+#pragma unroll
+                for (int a = 0; a < M; ++a) t[a][jj] = oc[a];
+            }
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                float r[M];
+                WinoTf<E>::g(t[a], r);
+#pragma unroll
+                for (int b = 0; b < M; ++b) mx[a * M + b] = fmaxf(mx[a * M + b], fabsf(r[b]));
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < MM; ++q) {
+            float v = mx[q];
+            for (int off = 16; off > 0; off >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+            if (lane == 0) red[warp][q] = v;
+        }
+        __syncthreads();
+        if (threadIdx.x < MM) {
+            float v = red[0][threadIdx.x];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmaxf(v, red[w][threadIdx.x]);
+            const int e = f16_row_exp(v);
+            scs[threadIdx.x] = pow2f(e);
+            col_exp[(int64_t)threadIdx.x * k + kk] = e;
+        }
+        __syncthreads();
+        volatile float *vscs = scs;
+        const int64_t kc = (int64_t)k * c, lo_off = rows * c;
+        for (int p = threadIdx.x; 2 * p < c; p += blockDim.x) {
+            // G g (the column pass) for both channels, then one row of U at a time
+            float t0[M][3], t1[M][3];
+            const float *g0 = wk + (int64_t)(2 * p) * 9, *g1 = g0 + 9;
+#pragma unroll
+            for (int jj = 0; jj < 3; ++jj) {
+                float col0[3] = {g0[jj], g0[3 + jj], g0[6 + jj]}, col1[3] = {g1[jj], g1[3 + jj], g1[6 + jj]};
+                float oc0[M], oc1[M];
+                WinoTf<E>::g(col0, oc0);
+                WinoTf<E>::g(col1, oc1);
+#pragma unroll
+                for (int a = 0; a < M; ++a) {
+                    t0[a][jj] = oc0[a];
+                    t1[a][jj] = oc1[a];
+                }
+            }
+            __half *ph = u16 + (int64_t)kk * c + 2 * p;
+#pragma unroll
+            for (int a = 0; a < M; ++a) {
+                float r0[M], r1[M];
+                WinoTf<E>::g(t0[a], r0);
+                WinoTf<E>::g(t1[a], r1);
+#pragma unroll
+                for (int b = 0; b < M; ++b) {
+                    const int q = a * M + b;
+                    __half h0, l0, h1, l1;
+                    const float sc = vscs[q];   // re-read per use: keeps 36 scales out of registers
+                    split_f16(r0[b], sc, h0, l0);
+                    split_f16(r1[b], sc, h1, l1);
+                    *reinterpret_cast<__half2 *>(ph) = __halves2half2(h0, h1);
+                    *reinterpret_cast<__half2 *>(ph + lo_off) = __halves2half2(l0, l1);
+                    ph += kc;   // next xi row: a pointer walk, not 36 hoisted offsets
+                }
+            }
+        }
+        __syncthreads();   // red / scs are reused by the next row
+    }
+}
+
 // Step 4: one thread per (tile, output channel), k fastest (coalesced M
 // loads and NHWC stores); bias + ReLU fused; ragged tiles masked.
 template <int E>
@@ -737,6 +857,18 @@ int convio_winograd_filter_transform_tc_batched(int32_t count, const convio_conv
         B.c[i] = S.c[i] = pl.g.c;
         B.cum[i + 1] = B.cum[i] + (int64_t)pl.g.k * pl.g.c;
         S.cum[i + 1] = S.cum[i] + (int64_t)pl.m * pl.m * pl.g.k;
+    }
+    bool even_c = true;
+    for (int i = 0; i < count; ++i) even_c = even_c && (B.c[i] % 2 == 0);
+    if (kind == KIND_3XF16 && even_c) {   // fused transform + split, one launch
+        WinoFilterBatch F = B;
+        for (int i = 0; i < count; ++i) F.cum[i + 1] = F.cum[i] + F.k[i];
+        const int fblocks = (int)std::min<int64_t>(F.cum[count], 148 * 8);
+        if (e == 2) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_f16x3_batched_kernel<2>, dim3(fblocks), dim3(256), 0, (cudaStream_t)stream, F));
+        else CONVIO_CUDA_TRY(launch_pdl(winograd_filter_f16x3_batched_kernel<4>, dim3(fblocks), dim3(256), 0, (cudaStream_t)stream, F));
+        note_launch();
+        CONVIO_CUDA_TRY(cudaGetLastError());
+        return CONVIO_OK;
     }
     const int blocks = (int)std::min<int64_t>((B.cum[count] + 255) / 256, 148 * 8);
     if (e == 2) CONVIO_CUDA_TRY(launch_pdl(winograd_filter_tc_batched_kernel<2>, dim3(blocks), dim3(256), 0, (cudaStream_t)stream, B));

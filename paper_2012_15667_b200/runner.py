@@ -272,7 +272,7 @@ def prepare_layers(layers, device, stream=None) -> int:
                 len(chunk), (N.ConvDesc * len(chunk))(*descs), e, N.PRECISIONS[prec],
                 (ctypes.c_void_p * len(chunk))(*ws), (ctypes.c_void_p * len(chunk))(*us),
                 C._stream_ptr(stream)), "winograd_filter_transform_tc_batched")
-            launches += 2 if prec == "3xf16" else 1
+            launches += C.last_launch_count()
     for l in layers:
         if l.algorithm != "igemm_3xf16" and id(l) not in batched:
             l.prepare(device, stream)

@@ -162,7 +162,7 @@ def test_batched_filter_packing_matches_per_filter_packing():
     writes exactly what the per-filter packing writes, and the runner uses it."""
     from paper_2012_15667_b200 import runner as R
     g = torch.Generator(device="cuda").manual_seed(5)
-    shapes = [(64, 64, 3), (128, 64, 3), (256, 128, 3), (512, 256, 1), (64, 128, 3)]
+    shapes = [(64, 64, 3), (128, 64, 3), (256, 128, 3), (512, 256, 1), (64, 128, 3), (64, 34, 3)]
     ws = [torch.rand((k, c, r, r), device="cuda", generator=g) - 0.5 for k, c, r in shapes]
     singles = [C.pack_filter_igemm_f16x3(w) for w in ws]
     import ctypes
@@ -177,6 +177,15 @@ def test_batched_filter_packing_matches_per_filter_packing():
     torch.cuda.synchronize()
     for s1, o in zip(singles, outs):
         assert torch.equal(s1, o)
+    # a filter row over the shared-memory staging limit (C*R*S > 12288): the unstaged form
+    big = [torch.rand((32, 2048, 3, 3), device="cuda", generator=g) - 0.5]
+    ref, out = C.pack_filter_igemm_f16x3(big[0]), None
+    out = torch.empty_like(ref)
+    rc = N.lib().convio_pack_filters_igemm_f16x3_batched(
+        1, (N.ConvDesc * 1)(N.make_desc(1, 2048, 8, 8, 32, 3, 3, 1, 0, 2)),
+        (ctypes.c_void_p * 1)(big[0].data_ptr()), (ctypes.c_void_p * 1)(out.data_ptr()), None)
+    assert rc == 0, N.last_error()
+    assert torch.equal(ref, out)
     # the runner's step prep: 3xF16 layers batched, the others one by one
     specs = [s for s in R.WORKLOADS["resnet50"]][:4]
     layers = [R.ConvLayer(s, R.make_weights(s, torch.device("cuda"), i),
@@ -189,25 +198,33 @@ def test_batched_filter_packing_matches_per_filter_packing():
         assert torch.equal(l._ws.view(torch.uint8)[:ref.numel()], ref)
 
 
+@pytest.mark.parametrize("e", [2, 4])
 @pytest.mark.parametrize("prec", ["3xf16", "3xtf32"])
-def test_batched_winograd_filter_transform_matches_per_filter(prec):
-    """convio_winograd_filter_transform_tc_batched == the per-filter transform, bit for bit."""
+def test_batched_winograd_filter_transform_matches_per_filter(prec, e):
+    """convio_winograd_filter_transform_tc_batched == the per-filter transform, bit for bit.
+    For 3xF16 the batched form is one fused launch (transform + split, no fp32 U): the
+    hi / lo planes and exponents the GEMM reads must equal the two-kernel per-filter
+    path's; the fp32 U region ahead of them is scratch the fused kernel never writes."""
     g = torch.Generator(device="cuda").manual_seed(9)
     shapes = [(256, 128), (512, 512), (128, 64)]
     ws = [torch.rand((k, c, 3, 3), device="cuda", generator=g) - 0.5 for k, c in shapes]
-    singles = [C.winograd_filter_transform_tc(w, 4, prec) for w in ws]
+    ws[1][:7] *= 2.0 ** -30   # rows whose exponents differ widely from the rest
+    singles = [C.winograd_filter_transform_tc(w, e, prec) for w in ws]
     import ctypes
     from paper_2012_15667_b200 import _native as N
     outs = [torch.zeros_like(s) for s in singles]
     descs = (N.ConvDesc * len(ws))(*[N.make_desc(1, w.shape[1], 8, 8, w.shape[0], 3, 3, 1, 0, 2) for w in ws])
     rc = N.lib().convio_winograd_filter_transform_tc_batched(
-        len(ws), descs, 4, N.PRECISIONS[prec], (ctypes.c_void_p * len(ws))(*[w.data_ptr() for w in ws]),
+        len(ws), descs, e, N.PRECISIONS[prec], (ctypes.c_void_p * len(ws))(*[w.data_ptr() for w in ws]),
         (ctypes.c_void_p * len(ws))(*[o.data_ptr() for o in outs]), None)
     assert rc == 0, N.last_error()
+    assert C.last_launch_count() == 1
     torch.cuda.synchronize()
-    for s1, o in zip(singles, outs):
+    m = e + 2
+    for (k, c), s1, o in zip(shapes, singles, outs):
         n = s1.numel() * s1.element_size()
-        assert torch.equal(s1.view(torch.uint8).flatten()[:n], o.view(torch.uint8).flatten()[:n])
+        skip = m * m * k * c * 4 if prec == "3xf16" else 0   # the fp32 U scratch
+        assert torch.equal(s1.view(torch.uint8).flatten()[skip:n], o.view(torch.uint8).flatten()[skip:n])
 
 
 @pytest.mark.parametrize("case", [
