@@ -985,7 +985,6 @@ int convio_conv_igemm_grouped(const convio_conv_desc *desc, const convio_tile *t
     convio_conv_desc dg = *desc;
     dg.n = desc->n * layers;   // the stacked batch
     IgemmPlan pl;
-    pl.no_resb = true;
     char why[160];
     int rc = plan_igemm(&dg, tile, &pl, why, sizeof(why), kind);
     if (rc) return rc;

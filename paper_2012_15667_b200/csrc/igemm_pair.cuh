@@ -488,9 +488,10 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_row(uint32_t addr) { return 
 // of tap (r, s) reads footprint row m + r * fpr + s from the fp32 footprint slot,
 // splits it and tcgen05.st's the hi / lo pair into an A slot of TMEM -- so the
 // footprint crosses L2 once per channel block (halo) while the tensor core reads
-// only the filter from shared memory (TSA).  RESB (halo TSA, one n-block): the
-// CTA's whole filter slice is staged ONCE at kernel start (the ring holds
-// kblocks filter slots) and only footprints stream per work item.
+// only the filter from shared memory (TSA).  RESB (halo TSA fold, one n-block): the
+// CTA's whole filter slice is staged ONCE (the ring holds kblocks filter slots) and
+// only footprints stream per work item; a grouped launch reloads it when the CTA's
+// items move on to the next layer, after the MMAs on the old slice have completed.
 template <int BN, int KIND, bool HALO, bool TSA, bool FOLD = false, bool RESB = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIND, TSA>(), 1)
     igemm_pair_kernel(const __grid_constant__ PairParams PP, const __grid_constant__ CUtensorMap tm_x,
@@ -509,7 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
     constexpr bool F16X3 = KIND == KIND_3XF16;
     static_assert(!F16X3 || (!HALO && !TSA && !FOLD), "3xF16: plain pair tiles");
     static_assert(!(TSA && HALO) || F16C, "halo tiles with A in TMEM: 3xF16C only");
-    static_assert(!RESB || (TSA && HALO), "resident filter: halo tiles with A in TMEM");
+    static_assert(!RESB || (TSA && HALO && FOLD), "resident filter: fold halo tiles with A in TMEM");
     constexpr int HB = BN / 2;                        // filter rows staged per CTA
     constexpr int A_BYTES = 128 * 128;
     constexpr int B_BYTES = HB * 128;
@@ -706,24 +707,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             int s = 0, sa = 0;
             uint32_t ph = 0, pha = 0;
             int it = 0, ita = 0;
-            if constexpr (RESB) {   // the CTA's filter slice, once: slot cb * taps + tap (halo order)
-                mbar_arrive_expect_tx(full, (uint32_t)(P.kblocks * STAGE));
-                for (int cb = 0, slot = 0; cb < P.cblocks; ++cb)
-                    for (int tap = 0; tap < taps; ++tap, ++slot) {
-                        uint8_t *b = bring + slot * STAGE;
-                        if (FOLD) {
-                            const int frow = tap * P.ks * P.k + (int)rank * HB;
-                            tma_load_2d(b, map_w, cb * CB, frow, full);
-                            tma_load_2d(b + B_BYTES, map_w, cb * CB, frow + lo_tap * P.k, full);
-                        } else {
-                            tma_load_3d(b, map_w, cb * CB, (int)rank * HB, tap, full);
-                            tma_load_3d(b + B_BYTES, map_w, cb * CB, (int)rank * HB, tap + lo_tap, full);
-                        }
-                    }
-            }
+            // RESB: the CTA's filter slice stays resident (slot cb * taps + tap, halo order),
+            // loaded once -- per layer when grouped: before a reload the producer waits for
+            // the MMAs on the old slice (the issuer commits `empty`, unused by the ring here)
+            int resident = -1;
+            uint32_t rph = 0;
             for (int item = cluster_id; item < PP.items; item += nclusters) {
                 int grp, pair, nb;
                 decode(item, grp, pair, nb);
+                if constexpr (RESB) {
+                    const int layer = P.layer_imgs ? grp : 0;
+                    if (layer != resident) {
+                        if (resident >= 0) {
+                            mbar_wait(empty, rph);
+                            rph ^= 1;
+                        }
+                        mbar_arrive_expect_tx(full, (uint32_t)(P.kblocks * STAGE));
+                        for (int cb = 0, slot = 0; cb < P.cblocks; ++cb)
+                            for (int tap = 0; tap < taps; ++tap, ++slot) {
+                                uint8_t *b = bring + slot * STAGE;
+                                const int frow = tap * P.ks * P.k + (int)rank * HB;
+                                if (P.layer_imgs) {
+                                    tma_load_3d(b, map_w, cb * CB, frow, layer, full);
+                                    tma_load_3d(b + B_BYTES, map_w, cb * CB, frow + lo_tap * P.k, layer, full);
+                                } else {
+                                    tma_load_2d(b, map_w, cb * CB, frow, full);
+                                    tma_load_2d(b + B_BYTES, map_w, cb * CB, frow + lo_tap * P.k, full);
+                                }
+                            }
+                        resident = layer;
+                    }
+                }
                 int ox0, oy0, img0;
                 pair_block_origin(P, grp, pair * 2 + (int)rank, ox0, oy0, img0);
                 const int n0 = nb * BN + (int)rank * HB;
@@ -892,6 +906,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 uint32_t fa = 0;
                 int kb_lo, kb_hi;
                 krange(item, kb_lo, kb_hi);
+                int cur_layer = 0, next_layer = -1;   // RESB grouped: the slice's layer changes
+                if (RESB && P.layer_imgs) {
+                    int g_, p_, n_;
+                    decode(item, g_, p_, n_);
+                    cur_layer = g_;
+                    if (item + nclusters < PP.items) {
+                        decode(item + nclusters, g_, p_, n_);
+                        next_layer = g_;
+                    }
+                }
                 for (int kb = kb_lo; kb < kb_hi; ++kb) {
                     if constexpr (TSA) {
                         mbar_wait_cluster(tconv + ta, pht);
@@ -925,6 +949,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                                 }
                             }
                             if constexpr (!RESB) umma_commit_pair(empty + s);
+                            else if (kb + 1 == kb_hi && next_layer >= 0 && next_layer != cur_layer)
+                                umma_commit_pair(empty);   // the resident slice may be reloaded
                             umma_commit_pair(tfree + ta);
                         }
                         __syncwarp();
@@ -1028,8 +1054,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         const uint32_t tempty_leader = mapa_shared(smem_u32(tempty), 0);
         const uint32_t stg = smem_u32(ring_end + 1024);
         // per-channel epilogue constants (not for the batched Winograd GEMMs: their column
-        // exponents differ per xi) staged once by the 4 epilogue warps
-        const bool cs_smem = !F16X3 && P.k <= kEpiConstK && !P.layer_imgs;
+        // exponents differ per xi) staged by the 4 epilogue warps -- once, or per layer
+        // of a grouped launch when the CTA's items reach the next layer
+        const bool cs_smem = !F16X3 && P.k <= kEpiConstK;
         float *ebias = reinterpret_cast<float *>(ring_end + 1024 + pair_epi_bytes(FOLD));
         float *escale = ebias + P.k;
         const int act_exp = F16C ? f16_row_exp(__int_as_float(f16c_scale_max)) : 0;   // one per tensor
@@ -1037,12 +1064,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         // exponent sum is a normal power of two (always, but for operands near 2^-60); else
         // the two exact multiplies
         bool fused_scale = false;
-        if (cs_smem) {
+        int staged = -1;   // the layer whose constants are in shared memory
+        auto stage_consts = [&](int layer) {
+            const float *bias = P.bias ? P.bias + (int64_t)layer * P.k : nullptr;
+            const int *cexp = F16C ? P.col_exp + (int64_t)layer * P.col_stride : nullptr;
             bool ok = true;
             for (int k = m; k < P.k; k += 128) {
-                ebias[k] = P.bias ? __ldg(P.bias + k) : 0.f;
+                ebias[k] = bias ? __ldg(bias + k) : 0.f;
                 if constexpr (F16C) {
-                    const int ek = __ldg(P.col_exp + k), e = act_exp + ek;
+                    const int ek = __ldg(cexp + k), e = act_exp + ek;
                     ok = ok && e >= -126 && e <= 127;
                     escale[k] = pow2f(-ek);
                 } else {
@@ -1054,9 +1084,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                          "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(all) : "r"((uint32_t)ok) : "memory");
             fused_scale = F16C && all;
             if (fused_scale)   // fold the tensor scale into the column scales
-                for (int k = m; k < P.k; k += 128) escale[k] = pow2f(-(act_exp + __ldg(P.col_exp + k)));
+                for (int k = m; k < P.k; k += 128) escale[k] = pow2f(-(act_exp + __ldg(cexp + k)));
             epi_bar();
-        }
+            staged = layer;
+        };
+        if (cs_smem) stage_consts(0);
         // staging row = position in the store box [img][y][x] (halo: the x valid columns)
         int srow;
         bool inbox;
@@ -1084,6 +1116,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
             pair_block_origin(P, grp, blk, ox0, oy0, img0);
             const int k0 = nb * KOUT;
             const int layer = P.layer_imgs ? grp : 0;   // grouped conv: group = layer
+            // (the previous item's last epi_bar: every lane is done with the old constants)
+            if (cs_smem && layer != staged) stage_consts(layer);
             float rs = 1.f;   // the row's operand scale (3xF16 families; 1 when folded into escale)
             if constexpr (F16X3) {
                 const int per_img = P.bx * P.by;
@@ -1211,8 +1245,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
         int s = 0, ta = 0, it = 0, sa = 0;
         uint32_t ph = 0, pht = 0, pha = 0;
         uint32_t fa = 0;
-        if constexpr (RESB) mbar_wait(full, 0);   // the resident filter slice has landed
+        int resident = -1;   // RESB: the layer whose filter slice has landed
+        uint32_t rph = 0;
         for (int item = cluster_id; item < PP.items; item += nclusters) {
+            if constexpr (RESB) {
+                int g_, p_, n_;
+                decode(item, g_, p_, n_);
+                const int layer = P.layer_imgs ? g_ : 0;
+                if (layer != resident) {
+                    mbar_wait(full, rph);
+                    rph ^= 1;
+                    resident = layer;
+                }
+            }
             int kb_lo, kb_hi;
             krange(item, kb_lo, kb_hi);
             int tap = 0;

@@ -421,7 +421,7 @@ struct IgemmPlan {
     int resb_slots = 0;      // halo TSA: filter slice resident in smem (one slot per k-block)
     int64_t tail_start = 0;  // pair kernel: tile items from here on are split-K (P.splits)
     int *scale_state = nullptr;   // 3xF16C: speculative activation scale state (workspace)
-    bool no_resb = false;    // planning option: never keep the filter resident (grouped convs)
+    bool no_resb = false;    // planning option: never keep the filter resident
     int layers = 1;          // grouped conv: layers stacked along N (filter map gains a dim)
     size_t layer_bytes = 0;  // grouped conv: bytes between consecutive packed filter slices
     PairFn pfn = nullptr;

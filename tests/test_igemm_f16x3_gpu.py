@@ -185,7 +185,8 @@ def test_batched_filter_packing_matches_per_filter_packing():
         1, (N.ConvDesc * 1)(N.make_desc(1, 2048, 8, 8, 32, 3, 3, 1, 0, 2)),
         (ctypes.c_void_p * 1)(big[0].data_ptr()), (ctypes.c_void_p * 1)(out.data_ptr()), None)
     assert rc == 0, N.last_error()
-    assert torch.equal(ref, out)
+    used = 4 * 32 * 2048 * 9 + 4 * 32   # hi / lo planes, then the 32 column exponents (no tail padding)
+    assert torch.equal(ref[:used], out[:used])
     # the runner's step prep: 3xF16 layers batched, the others one by one
     specs = [s for s in R.WORKLOADS["resnet50"]][:4]
     layers = [R.ConvLayer(s, R.make_weights(s, torch.device("cuda"), i),
