@@ -594,7 +594,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, group_layers, load_plans, make_input, make_weights, prepare_layers,
+        WORKLOADS, ConvLayer, expand, group_layers, load_group_plans, load_plans, make_input, make_weights,
+        prepare_layers,
         shard_range,
         tuned_table,
         gather_outputs, CUDA_CORE_ALGORITHMS)
@@ -661,7 +662,8 @@ def main() -> None:
                        for s, lay in zip(specs, self.layers)]
             # same-shape, same-plan 3xF16 layers (res2 x3, res3 x3, res4 x5) run as grouped
             # launches in the timed step; their inputs / outputs are slices of the stacked buffers
-            self.units = group_layers(self.layers, n_local, dev) if not args.no_group else \
+            self.units = group_layers(self.layers, n_local, dev, load_group_plans(args.workload, n_local)) \
+                if not args.no_group else \
                 [("single", l, [i]) for i, l in enumerate(self.layers)]
             for kind, unit, idx in self.units:
                 if kind == "group":

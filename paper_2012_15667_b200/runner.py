@@ -209,10 +209,32 @@ class LayerGroup:
         return self.y
 
 
-def group_layers(layers, n: int, device) -> list:
+def group_table(workload: str) -> str:
+    """Path of the grouped-launch table (``scripts/tune_groups.py``)."""
+    return os.path.join(TUNED_DIR, f"b200_{workload}_groups.json")
+
+
+def load_group_plans(workload: str, n: int) -> dict:
+    """``{layer name: TileConfig}`` for the grouped launches at per-layer batch ``n``:
+    the fastest measured tile for the G-layer launch (a G*n-image GEMM prefers the
+    tiles tuned at larger batches), or ``{}`` when untuned."""
+    try:
+        with open(group_table(workload)) as fh:
+            tab = json.load(fh)
+    except (OSError, ValueError):
+        return {}
+    out = {}
+    for name, ent in tab.get("groups", {}).get(str(n), {}).items():
+        if ent.get("tile"):
+            out[name] = TileConfig(**ent["tile"])
+    return out
+
+
+def group_layers(layers, n: int, device, group_plans: dict | None = None) -> list:
     """Runs of consecutive layers with the same shape and the same 3xF16 implicit-GEMM
     plan (CTA-pair tiles whose image stack divides ``n``) as :class:`LayerGroup`; other
-    layers stay single.  Returns units ``(kind, obj, [layer indices])``."""
+    layers stay single.  ``group_plans`` (:func:`load_group_plans`) may give a group
+    its own tile.  Returns units ``(kind, obj, [layer indices])``."""
     units, i = [], 0
     while i < len(layers):
         l = layers[i]
@@ -223,7 +245,10 @@ def group_layers(layers, n: int, device) -> list:
                 j += 1
         if j - i >= 2:
             try:
-                units.append(("group", LayerGroup(layers[i:j], n, device), list(range(i, j))))
+                grp = LayerGroup(layers[i:j], n, device)
+                if group_plans and l.spec.name in group_plans:
+                    grp.tile = group_plans[l.spec.name]
+                units.append(("group", grp, list(range(i, j))))
             except ValueError:
                 units += [("single", layers[k], [k]) for k in range(i, j)]
         else:

@@ -19,8 +19,9 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2012_15667_b200 import conv as C  # noqa: E402
-from paper_2012_15667_b200.runner import (WORKLOADS, ConvLayer, expand, group_layers, load_plans,  # noqa: E402
-                                           make_input, make_weights, prepare_layers)
+from paper_2012_15667_b200.runner import (WORKLOADS, ConvLayer, expand, group_layers,  # noqa: E402
+                                           load_group_plans, load_plans, make_input, make_weights,
+                                           prepare_layers)
 
 
 def graph_of(fn, stream):
@@ -68,7 +69,7 @@ def main():
     xs = [make_input(s, n, dev, seed=7919 * (i + 1), layout=l.layout) for i, (s, l) in enumerate(zip(specs, layers))]
     ys = [C.empty_act(n, s.k, s.out_hw, s.out_hw, l.layout, device=dev) for s, l in zip(specs, layers)]
     units = ([("single", l, [i]) for i, l in enumerate(layers)] if args.no_group else
-             group_layers(layers, n, dev))
+             group_layers(layers, n, dev, load_group_plans(args.workload, n)))
     for kind, u, idx in units:
         if kind == "group":
             for g, i in enumerate(idx):

@@ -129,3 +129,24 @@ def test_group_layers_stacks_repeated_3xf16_layers(n):
             assert unit.x_of(g).data_ptr() == unit.x.data_ptr() + g * n * s.c * s.hw * s.hw * 4
     grouped = [idx for kind, _, idx in units if kind == "group"]
     assert grouped, "the tuned ResNet-50 tables put the repeated layers on 3xF16 pair tiles"
+
+
+def test_group_plans_table_gives_feasible_tiles():
+    """The committed grouped-launch table (scripts/tune_groups.py): every per-batch group
+    entry names a real repeated layer, its best tile is one of its measured candidates,
+    and the tile's CTA-pair image stack divides the per-layer batch."""
+    path = runner.group_table("resnet50")
+    if not os.path.exists(path):
+        pytest.skip("no grouped-launch table")
+    tab = json.load(open(path))
+    names = {s.name: s for s in runner.WORKLOADS["resnet50"]}
+    for n, groups in tab["groups"].items():
+        plans = runner.load_group_plans("resnet50", int(n))
+        assert set(plans) == set(groups)
+        for name, ent in groups.items():
+            assert names[name].count == ent["layers"] >= 2
+            measured = [c for c in ent["candidates"] if "us" in c]
+            assert ent["us"] == min(c["us"] for c in measured)
+            assert ent["tile"] in [c["tile"] for c in measured]
+            t = plans[name]
+            assert t.n_zt >= 2 and t.layout == "HWC"
