@@ -672,13 +672,13 @@ def main() -> None:
                         self.xs[li], self.ys[li] = unit.x_of(g_i), unit.y_of(g_i)
             self.work_bytes = sum(x.numel() * 4 for x in self.xs) + sum(y.numel() * 4 for y in self.ys)
 
-        def step(self, events=None, st=None):
+        def step(self, events=None, st=None, per_layer=False):
             st = st or stream
             # the step's filter prep (all 3xF16 splits in one launch), then the convs:
             # grouped launches for same-plan layers; the per-layer breakdown (events)
             # runs every layer on its own so each gets its own timing
             launches = prepare_layers(self.layers, dev, st)
-            if events is None:
+            if events is None and not per_layer:
                 for kind, unit, idx in self.units:
                     if kind == "group":
                         unit.run(st)
@@ -687,9 +687,11 @@ def main() -> None:
                     launches += unit.launches
                 return launches
             for i, layer in enumerate(self.layers):
-                events[i][0].record(st)
+                if events is not None:
+                    events[i][0].record(st)
                 layer.run(self.xs[i], out=self.ys[i], stream=st)
-                events[i][1].record(st)
+                if events is not None:
+                    events[i][1].record(st)
                 launches += layer.launches
             return launches
 
@@ -799,12 +801,71 @@ def main() -> None:
                 })
             return rows, fam
 
+        def unit_families(self, reps, flush_buf=None):
+            """Kernel families of the TIMED step: each unit (a grouped launch or a single
+            layer, filter prep excluded) captured as its own CUDA graph and replayed
+            ``reps`` times with CUDA events around each replay on the launching stream (L2
+            flushed between replays when the step is flushed): device time without the
+            host gaps an eager per-layer pass has at small batches."""
+            fam = {}
+            for kind, unit, idx in self.units:
+                if kind == "group":
+                    def fn(st, unit=unit):
+                        unit.run(st)
+                else:
+                    def fn(st, unit=unit, i=idx[0]):
+                        unit.run(self.xs[i], out=self.ys[i], stream=st)
+                side = torch.cuda.Stream(dev)
+                side.wait_stream(stream)
+                with torch.cuda.stream(side):
+                    fn(side)
+                    fn(side)
+                torch.cuda.synchronize(dev)
+                g = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(g, stream=side):
+                    fn(side)
+                torch.cuda.synchronize(dev)
+                ts = []
+                for _ in range(reps):
+                    if flush_buf is not None:
+                        flush_buf.fill_(1.0)
+                    a = torch.cuda.Event(enable_timing=True)
+                    b = torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    g.replay()
+                    b.record(stream)
+                    b.synchronize()
+                    ts.append(a.elapsed_time(b))
+                del g
+                layer = self.layers[idx[0]]
+                s = specs[idx[0]]
+                if layer.algorithm.startswith("winograd"):
+                    f_alg = winograd_gemm_flops(n_local, s.c, s.k, s.out_hw, s.out_hw, layer.e)
+                    name = (f"winograd F({layer.e},3)" if layer.algorithm == "winograd"
+                            else f"{layer.algorithm} F({layer.e},3)")
+                else:
+                    f_alg = s.flops(n_local)
+                    name = layer.algorithm
+                agg = fam.setdefault(name, {"ms": 0.0, "flops": 0.0, "launches": 0, "layers": set(),
+                                            "layer_launches": {}, "units": []})
+                agg["ms"] += sum(ts)
+                agg["flops"] += f_alg * len(idx) * reps
+                agg["launches"] += reps
+                agg["layers"].add(s.name)
+                agg["layer_launches"][s.name] = agg["layer_launches"].get(s.name, 0) + len(idx) * reps
+                agg["units"].append({"unit": s.name + (f" x{len(idx)}" if kind == "group" else ""),
+                                     "ms": round(statistics.median(ts), 4)})
+            return fam
+
     plans = load_plans(args.workload, n=n_local)
     arm = Arm(plans)
     flush = arm.work_bytes < 4 * L2_BYTES
     scratch = torch.empty(2 * L2_BYTES // 4, device=dev) if flush else None
     for _ in range(args.warmup):
         arm.step()
+        # the eager per-layer pass below launches every layer on its own: warm its
+        # per-layer state too (each launch's speculative activation scale)
+        arm.step(per_layer=True)
     torch.cuda.synchronize(dev)
 
     # ---- device-timed region: exactly K steps --------------------------------
@@ -826,7 +887,9 @@ def main() -> None:
     clk = clocks.stop()
     t_max_ms = max_over_ranks(total_ms)
     value = flops_all * args.steps / (t_max_ms / 1e3) / 1e9
-    per_layer, fam = arm.breakdown(ev, args.steps)
+    per_layer, _ = arm.breakdown(ev, args.steps)
+    # the roofline's kernel families from the timed step's own launches (grouped units)
+    fam = arm.unit_families(max(args.steps, 5), scratch)
 
     # ---- roofline of the dominant kernel (largest share of the step) ------------
     dom = max(fam, key=lambda k: fam[k]["ms"])
@@ -874,6 +937,11 @@ def main() -> None:
         }
     roofline["layers"] = sorted(d["layers"])
     roofline["share_of_step"] = round(d["ms"] / sum(f["ms"] for f in fam.values()), 3)
+    roofline["units"] = d["units"]
+    roofline["timing"] = ("per unit of the timed step (grouped launch or single layer, with its checking "
+                          "launch) as its own CUDA graph, CUDA events around each replay"
+                          + (", L2 flushed between replays" if flush else "")
+                          + "; traffic = ncu DRAM bytes per single-layer call")
     # the same family against HBM: the committed ncu DRAM bytes of its layer calls
     # over their device time (the unfused Winograd pipeline moves V and M through
     # HBM, so bandwidth, not the tensor pipe, is its ceiling)
@@ -903,6 +971,7 @@ def main() -> None:
             varm = Arm(vplans)
             for _ in range(2):
                 varm.step()
+                varm.step(per_layer=True)
             vt, vev, _ = varm.timed(args.steps, scratch)
             if not args.no_graph:   # same timing basis as the headline: graph replay
                 vg = varm.capture()
