@@ -215,9 +215,10 @@ def group_table(workload: str) -> str:
 
 
 def load_group_plans(workload: str, n: int) -> dict:
-    """``{layer name: TileConfig}`` for the grouped launches at per-layer batch ``n``:
-    the fastest measured tile for the G-layer launch (a G*n-image GEMM prefers the
-    tiles tuned at larger batches), or ``{}`` when untuned."""
+    """``{layer name: TileConfig | None}`` for the grouped launches at per-layer batch
+    ``n``: the fastest measured tile for the G-layer launch (a G*n-image GEMM prefers
+    the tiles tuned at larger batches), None where G single launches measured faster,
+    ``{}`` when untuned."""
     try:
         with open(group_table(workload)) as fh:
             tab = json.load(fh)
@@ -225,7 +226,9 @@ def load_group_plans(workload: str, n: int) -> dict:
         return {}
     out = {}
     for name, ent in tab.get("groups", {}).get(str(n), {}).items():
-        if ent.get("tile"):
+        if not ent.get("use_group", True):
+            out[name] = None
+        elif ent.get("tile"):
             out[name] = TileConfig(**ent["tile"])
     return out
 
@@ -243,6 +246,8 @@ def group_layers(layers, n: int, device, group_plans: dict | None = None) -> lis
             while (j < len(layers) and layers[j].algorithm == "igemm_3xf16" and layers[j].spec == l.spec
                    and layers[j].tile == l.tile and (layers[j].bias is None) == (l.bias is None)):
                 j += 1
+        if j - i >= 2 and group_plans and l.spec.name in group_plans and group_plans[l.spec.name] is None:
+            j = i + 1   # measured: single launches win for this group
         if j - i >= 2:
             try:
                 grp = LayerGroup(layers[i:j], n, device)

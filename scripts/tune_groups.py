@@ -1,7 +1,8 @@
 """Tune the grouped launches of a workload's repeated same-shape 3xF16 layers
 (``runner.group_layers``): for each per-layer batch n and each group of G layers, time
 the grouped launch with every igemm_3xf16 tile the per-batch tables hold for that layer
-(a G*n-image GEMM often prefers a tile tuned at a larger batch) and keep the fastest.
+(a G*n-image GEMM often prefers a tile tuned at a larger batch), keep the fastest, and
+record whether it beats G single launches on the layers' own plans.
 
     python scripts/tune_groups.py --workload resnet50 [--batches 32,64,128,256]
 
@@ -94,12 +95,20 @@ def main():
                 cands.append({"tile": t.to_dict(), "us": round(us, 2)})
             ok = [c for c in cands if "us" in c]
             best = min(ok, key=lambda c: c["us"])
+            # the alternative: G single launches, each layer on its own tuned plan
+            ys = [C.empty_act(n, specs[i].k, specs[i].out_hw, specs[i].out_hw, "HWC", device=dev) for i in idx]
+
+            def singles():
+                for j, i in enumerate(idx):
+                    layers[i].run(grp.x_of(j), out=ys[j])
+            singles_us = time_us(singles, args.reps)
             res[name] = {"layers": len(idx), "n": n, "tile": best["tile"], "us": best["us"],
                          "own_plan_us": ok[0]["us"] if cands and "us" in cands[0] else None,
+                         "singles_us": round(singles_us, 2), "use_group": best["us"] < singles_us,
                          "candidates": cands}
             grp.tile = own
-            print(f"n={n:4d} {name:12s} x{len(idx)} best {best['us']:8.2f} us (own plan {res[name]['own_plan_us']}) "
-                  f"{TileConfig(**best['tile'])}", flush=True)
+            print(f"n={n:4d} {name:12s} x{len(idx)} best {best['us']:8.2f} us (own plan {res[name]['own_plan_us']}, "
+                  f"singles {singles_us:.2f}) {TileConfig(**best['tile'])}", flush=True)
         out["groups"][str(n)] = res
         del layers, units
         torch.cuda.empty_cache()

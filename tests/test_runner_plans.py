@@ -149,4 +149,7 @@ def test_group_plans_table_gives_feasible_tiles():
             assert ent["us"] == min(c["us"] for c in measured)
             assert ent["tile"] in [c["tile"] for c in measured]
             t = plans[name]
+            if not ent.get("use_group", True):
+                assert t is None and ent["singles_us"] <= ent["us"]
+                continue
             assert t.n_zt >= 2 and t.layout == "HWC"
