@@ -5,7 +5,8 @@
 #     SM<->L2 read bytes per layer call (--cache-control none, last of 3 calls)
 #     -> gpurun_out/<ROUND>_{resnet50,vgg16}_traffic.json (bench.py reads them)
 #  2. the bench step's kernel launch list (gpu__time_duration, --clock-control none)
-#  3. one `ncu --set full` capture of each ResNet-50 layer family's tuned plan
+#  3. one `ncu --set full` capture of each ResNet-50 layer family's tuned plan, and of the
+#     bench's grouped launches of res2 x3 / res4 x5
 R=${1:-r2}
 M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,l1tex__m_xbar2l1tex_read_bytes.sum
 mkdir -p gpurun_out/traffic_$R
@@ -27,6 +28,13 @@ for L in res2_3x3 res3_3x3_s2 res3_3x3 res4_3x3; do
   timeout 400 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair" -s 2 -c 1 \
     -o gpurun_out/${R}_ncu_$L -f python scripts/run_layer.py --workload resnet50 --layer $L --reps 3 > /dev/null 2>&1
 done
+# the timed step's grouped launches (res2 x3, res4 x5 as one persistent launch each)
+for L in res2_3x3 res4_3x3; do
+  timeout 400 ncu --set full --import-source on --clock-control none -k regex:"igemm_pair" -s 2 -c 1 \
+    -o gpurun_out/${R}_ncu_group_$L -f python scripts/run_layer.py --workload resnet50 --layer $L --group --reps 3 > /dev/null 2>&1
+done
 python scripts/ncu_summary.py rep gpurun_out/${R}_ncu_*.ncu-rep --out gpurun_out/${R}_ncu_kernels.json > /dev/null 2>&1
 rm -rf gpurun_out/traffic_$R/*.csv
+# keep one full report (the grouped res4 launch) for reading back; the rest are summarised
+find gpurun_out -maxdepth 1 -name "${R}_ncu_*.ncu-rep" ! -name "${R}_ncu_group_res4_3x3.ncu-rep" -delete
 ls -la gpurun_out/${R}_*

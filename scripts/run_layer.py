@@ -27,6 +27,26 @@ def run(args):
     n = args.batch or DEFAULT_BATCH[args.workload]
     plan = load_plans(args.workload).get(spec.name)
     dev = torch.device("cuda")
+    if args.group:   # the bench's grouped launch of the layer's `count` repeats
+        from paper_2012_15667_b200.runner import group_layers, load_group_plans, prepare_layers
+        layers = [ConvLayer(spec, make_weights(spec, dev, 1000 + i), plan) for i in range(spec.count)]
+        units = group_layers(layers, n, dev, load_group_plans(args.workload, n))
+        kind, grp, _ = units[0]
+        if kind != "group":
+            raise SystemExit(f"{spec.name}: no grouped launch at n={n}")
+        for g in range(spec.count):
+            grp.x_of(g).copy_(make_input(spec, n, dev, seed=7919 + g, layout="HWC"))
+        prepare_layers(layers, dev)
+        for _ in range(args.reps):
+            grp.run()
+        torch.cuda.synchronize()
+        meta = {"layer": spec.name, "algorithm": layers[0].algorithm, "group": spec.count, "reps": args.reps,
+                "tile": grp.tile.to_dict(), "n": n}
+        if args.meta:
+            with open(args.meta, "w") as fh:
+                json.dump(meta, fh)
+        print(json.dumps(meta))
+        return
     layer = ConvLayer(spec, make_weights(spec, dev, 1000), plan)
     x = make_input(spec, n, dev, seed=7919, layout=layer.layout)
     y = C.empty_act(n, spec.k, spec.out_hw, spec.out_hw, layer.layout, device=dev)
@@ -93,6 +113,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--meta", default="", help="write the run's plan as JSON here")
+    ap.add_argument("--group", action="store_true",
+                    help="run the layer's repeats as the bench's grouped launch (runner.LayerGroup)")
     ap.add_argument("--parse", nargs="*")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
