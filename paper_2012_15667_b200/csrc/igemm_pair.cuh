@@ -1148,11 +1148,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     tmem_ld_x32_nowait(ta + (uint32_t)(2 * KOUT), r2);
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                     if (c0 == 0 && q == 0 && lane == 0) EPI_TRACE(19, t);
+#ifdef CONVIO_ABL_NOSHFL   // ablation (timing only, wrong numerics): no row shift
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        v[j] = __uint_as_float(r0[j]) + __uint_as_float(r1[j]) + __uint_as_float(r2[j]);
+#else
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
                         v[j] = __uint_as_float(r0[j]) +
                                __shfl_down_sync(0xffffffffu, __uint_as_float(r1[j]), 1) +
                                __shfl_down_sync(0xffffffffu, __uint_as_float(r2[j]), 2);
+#endif
                 } else {
                     tmem_ld_32x32b<32>(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(acc * BN + c0), v);
                     if (c0 == 0 && q == 0 && lane == 0) EPI_TRACE(19, t);
@@ -1167,23 +1173,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 // unscale (exact powers of two, two multiplies: the exponent sum may pass
                 // pow2f's range), bias, ReLU
                 const int kc = k0 + c0;
+#ifdef CONVIO_ABL_NOUNSCALE   // ablation (timing only, wrong numerics): no unscale / bias
+                if (0)
+#endif
+                if (cs_smem) {
+                    // the chunk's 32 channel scales and biases: 16 broadcast LDS.128 from the
+                    // shared-memory constants, issued together (explicit shared-space loads:
+                    // generic loads of these addresses, one dependent pair per 4 channels,
+                    // cost the fold epilogue ~14 % of res2's time)
+                    const uint32_t es = smem_u32(escale + kc), eb = smem_u32(ebias + kc);
+                    float4 c4v[8], b4v[8];
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        c4v[j4] = lds128(es + 16u * (uint32_t)j4);
+                        b4v[j4] = lds128(eb + 16u * (uint32_t)j4);
+                    }
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const float cs[4] = {c4v[j4].x, c4v[j4].y, c4v[j4].z, c4v[j4].w};
+                        const float b4[4] = {with_bias ? b4v[j4].x : 0.f, with_bias ? b4v[j4].y : 0.f,
+                                             with_bias ? b4v[j4].z : 0.f, with_bias ? b4v[j4].w : 0.f};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            float o = v[4 * j4 + u];
+                            // (rs = 1 when the tensor scale is folded into cs: o * rs is exact)
+                            if constexpr (F16X3 || F16C) o = fmaf(o * rs, cs[u], b4[u]);
+                            else o += b4[u];
+                            v[4 * j4 + u] = P.relu ? fmaxf(o, 0.f) : o;
+                        }
+                    }
+                } else {
 #pragma unroll
                 for (int j4 = 0; j4 < 8; ++j4) {
                     float4 bv = make_float4(0.f, 0.f, 0.f, 0.f);
                     float cs[4] = {1.f, 1.f, 1.f, 1.f};
-                    if (cs_smem) {   // broadcast LDS.128: every lane reads the same channels
-                        if (with_bias) bv = *reinterpret_cast<const float4 *>(ebias + kc + 4 * j4);
-                        if constexpr (F16C) {
-                            const float4 c4 = *reinterpret_cast<const float4 *>(escale + kc + 4 * j4);
-                            cs[0] = c4.x; cs[1] = c4.y; cs[2] = c4.z; cs[3] = c4.w;
-                        }
-                    } else {
-                        if (with_bias) bv = __ldg(reinterpret_cast<const float4 *>(P.bias + (int64_t)layer * P.k + kc) + j4);
-                        if constexpr (F16X3 || F16C) {
-                            const int4 ce = __ldg(reinterpret_cast<const int4 *>(
-                                P.col_exp + (P.batched ? (int64_t)grp * P.k : (int64_t)layer * P.col_stride) + kc) + j4);
-                            cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
-                        }
+                    if (with_bias) bv = __ldg(reinterpret_cast<const float4 *>(P.bias + (int64_t)layer * P.k + kc) + j4);
+                    if constexpr (F16X3 || F16C) {
+                        const int4 ce = __ldg(reinterpret_cast<const int4 *>(
+                            P.col_exp + (P.batched ? (int64_t)grp * P.k : (int64_t)layer * P.col_stride) + kc) + j4);
+                        cs[0] = pow2f(-ce.x); cs[1] = pow2f(-ce.y); cs[2] = pow2f(-ce.z); cs[3] = pow2f(-ce.w);
                     }
                     const float b4[4] = {bv.x, bv.y, bv.z, bv.w};
 #pragma unroll
@@ -1193,6 +1221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                         else o += b4[u];
                         v[4 * j4 + u] = P.relu ? fmaxf(o, 0.f) : o;
                     }
+                }
                 }
                 if (c0 == 0 && q == 0 && lane == 0) PAIR_TRACE(7, t);   // chunk 0 in registers
                 // staging box: FOLD alternates two (the store of chunk i-1 may still be reading)
