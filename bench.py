@@ -594,7 +594,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, group_layers, load_group_plans, load_plans, make_input, make_weights,
+        WORKLOADS, ConvLayer, expand, group_layers, load_group_overrides, load_group_plans, load_plans,
+        make_input, make_weights,
         prepare_layers,
         shard_range,
         tuned_table,
@@ -858,6 +859,8 @@ def main() -> None:
             return fam
 
     plans = load_plans(args.workload, n=n_local)
+    if not args.no_group:   # repeated layers whose grouped 3xF16 launch beat their own plan
+        plans.update(load_group_overrides(args.workload, n_local))
     arm = Arm(plans)
     flush = arm.work_bytes < 4 * L2_BYTES
     scratch = torch.empty(2 * L2_BYTES // 4, device=dev) if flush else None

@@ -233,6 +233,20 @@ def load_group_plans(workload: str, n: int) -> dict:
     return out
 
 
+def load_group_overrides(workload: str, n: int) -> dict:
+    """Plans ``{layer name: {"algorithm": "igemm_3xf16", "tile", "e"}}`` that replace a
+    repeated layer's own plan (e.g. res5's Winograd) because its grouped 3xF16 launch,
+    filter prep included, measured faster (``scripts/tune_groups.py``)."""
+    try:
+        with open(group_table(workload)) as fh:
+            tab = json.load(fh)
+    except (OSError, ValueError):
+        return {}
+    return {name: {"algorithm": ent["algorithm"], "tile": TileConfig(**ent["tile"]), "e": None}
+            for name, ent in tab.get("groups", {}).get(str(n), {}).items()
+            if ent.get("replaces") and ent.get("use_group", True)}
+
+
 def group_layers(layers, n: int, device, group_plans: dict | None = None) -> list:
     """Runs of consecutive layers with the same shape and the same 3xF16 implicit-GEMM
     plan (CTA-pair tiles whose image stack divides ``n``) as :class:`LayerGroup`; other

@@ -20,7 +20,7 @@ import torch  # noqa: E402
 
 from paper_2012_15667_b200 import conv as C  # noqa: E402
 from paper_2012_15667_b200.runner import (WORKLOADS, ConvLayer, expand, group_layers,  # noqa: E402
-                                           load_group_plans, load_plans, make_input, make_weights,
+                                           load_group_overrides, load_group_plans, load_plans, make_input, make_weights,
                                            prepare_layers)
 
 
@@ -65,6 +65,8 @@ def main():
     specs = expand(WORKLOADS[args.workload])
     plans = (load_plans(args.workload, allowed=tuple(args.allowed.split(",")), n=n) if args.allowed
              else load_plans(args.workload, n=n))
+    if not args.no_group and not args.allowed:
+        plans.update(load_group_overrides(args.workload, n))
     layers = [ConvLayer(s, make_weights(s, dev, 1000 + i), plans.get(s.name)) for i, s in enumerate(specs)]
     xs = [make_input(s, n, dev, seed=7919 * (i + 1), layout=l.layout) for i, (s, l) in enumerate(zip(specs, layers))]
     ys = [C.empty_act(n, s.k, s.out_hw, s.out_hw, l.layout, device=dev) for s, l in zip(specs, layers)]

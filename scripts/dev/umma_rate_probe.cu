@@ -105,6 +105,8 @@ int main() {
     rate<128, KIND_3XF16C, false, 1>(dcyc);
     rate<192, KIND_3XF16C, false, 1>(dcyc);
     rate<256, KIND_3XF16C, false, 1>(dcyc);
+    rate<64, KIND_3XF16C, true, 1>(dcyc);
+    rate<192, KIND_3XF16C, true, 1>(dcyc);
     rate<128, KIND_3XF16C, true, 1>(dcyc);
     rate<256, KIND_3XF16C, true, 1>(dcyc);
     return 0;

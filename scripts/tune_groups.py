@@ -2,7 +2,9 @@
 (``runner.group_layers``): for each per-layer batch n and each group of G layers, time
 the grouped launch with every igemm_3xf16 tile the per-batch tables hold for that layer
 (a G*n-image GEMM often prefers a tile tuned at a larger batch), keep the fastest, and
-record whether it beats G single launches on the layers' own plans.
+record whether it beats G single launches on the layers' own plans.  Repeated layers
+on another plan (Winograd) are offered the same grouped 3xF16 launch, compared with
+each side's filter prep included; a win replaces their plan (runner.load_group_overrides).
 
     python scripts/tune_groups.py --workload resnet50 [--batches 32,64,128,256]
 
@@ -59,6 +61,22 @@ def time_us(fn, reps, rounds=5):
     return statistics.median(ts)
 
 
+def time_graph_us(fn, reps, rounds=5):
+    """``fn(stream)`` captured as one CUDA graph and replayed (no host time between its
+    launches: a fair race between a 1-launch and a 4-launch alternative)."""
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn(side)
+        fn(side)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        fn(side)
+    torch.cuda.synchronize()
+    return time_us(g.replay, reps, rounds)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="resnet50")
@@ -109,6 +127,61 @@ def main():
             grp.tile = own
             print(f"n={n:4d} {name:12s} x{len(idx)} best {best['us']:8.2f} us (own plan {res[name]['own_plan_us']}, "
                   f"singles {singles_us:.2f}) {TileConfig(**best['tile'])}", flush=True)
+        # repeated layers on another plan (res5's Winograd): one grouped 3xF16 launch instead,
+        # compared WITH each side's filter prep (a Winograd U is 4x the filter, a 3xF16 pack 1x)
+        i = 0
+        while i < len(specs):
+            j = i
+            while j < len(specs) and specs[j] == specs[i]:
+                j += 1
+            idx, i = list(range(i, j)), j
+            name = specs[idx[0]].name
+            own_alg = layers[idx[0]].algorithm
+            if len(idx) < 2 or own_alg == "igemm_3xf16" or name in res:
+                continue
+            ig_plan = load_plans(args.workload, allowed=("igemm_3xf16",), n=n).get(name)
+            if not ig_plan:
+                continue
+            xs = [make_input(specs[k], n, dev, seed=7919 * (k + 1), layout="HWC") for k in idx]
+            ys = [C.empty_act(n, specs[k].k, specs[k].out_hw, specs[k].out_hw, "HWC", device=dev) for k in idx]
+            own_layers = [layers[k] for k in idx]
+
+            def own_step(st):
+                prepare_layers(own_layers, dev, st)
+                for q, l in enumerate(own_layers):
+                    l.run(xs[q], out=ys[q], stream=st)
+            own_us = time_graph_us(own_step, args.reps)
+            ig_layers = [ConvLayer(specs[k], layers[k].weight, ig_plan) for k in idx]
+            ug = group_layers(ig_layers, n, dev)
+            if not ug or ug[0][0] != "group":
+                continue
+            grp = ug[0][1]
+            for q in range(len(idx)):
+                grp.x_of(q).copy_(xs[q])
+            cands = []
+            for t in [ig_plan["tile"]] + [t for t in candidate_tiles(args.workload, name) if t != ig_plan["tile"]]:
+                grp.tile = t
+
+                def ig_step(st):
+                    prepare_layers(ig_layers, dev, st)
+                    grp.run(st)
+                try:
+                    us = time_graph_us(ig_step, args.reps)
+                except Exception as exc:  # noqa: BLE001 -- infeasible for this batch: recorded
+                    cands.append({"tile": t.to_dict(), "error": str(exc).splitlines()[0][:160]})
+                    continue
+                cands.append({"tile": t.to_dict(), "us_with_prep": round(us, 2)})
+            ok = [c for c in cands if "us_with_prep" in c]
+            if not ok:
+                continue
+            best = min(ok, key=lambda c: c["us_with_prep"])
+            if best["us_with_prep"] < 0.97 * own_us:   # a clear win only (box-to-box noise ~3 %)
+                res[name] = {"layers": len(idx), "n": n, "algorithm": "igemm_3xf16", "replaces": own_alg,
+                             "tile": best["tile"], "us_with_prep": best["us_with_prep"],
+                             "own_us_with_prep": round(own_us, 2), "use_group": True, "candidates": cands}
+            print(f"n={n:4d} {name:12s} x{len(idx)} grouped 3xF16 + pack {best['us_with_prep']:8.2f} us vs "
+                  f"{own_alg} + its prep {own_us:8.2f} us -> {'replace' if name in res else 'keep'}", flush=True)
+            del ig_layers, ug, grp
         out["groups"][str(n)] = res
         del layers, units
         torch.cuda.empty_cache()
