@@ -223,8 +223,10 @@ int convio_conv_igemm_grouped(const convio_conv_desc *desc, const convio_tile *t
                               const float *bias, int32_t relu, float *y, void *workspace, size_t workspace_bytes,
                               void *stream);
 /* The tensor-core Winograd filter transform (convio_winograd_filter_transform_tc) of
- * `count` <= 32 filters of one e and one precision in one launch (two for 3xF16:
- * the transform, then the fp16 split); fp32-U precisions (TF32, 3xTF32, 3xF16). */
+ * `count` <= 32 filters of one e and one precision in one launch; fp32-U precisions
+ * (TF32, 3xTF32, 3xF16).  3xF16 (even C) writes the fp16 hi / lo planes and exponents
+ * in one pass -- bit-identical to the per-filter transform + split -- and leaves the
+ * fp32 U region of the buffer unwritten (the GEMM never reads it). */
 int convio_winograd_filter_transform_tc_batched(int32_t count, const convio_conv_desc *descs, int32_t e,
                                                 int32_t precision, const float *const *w, void *const *u,
                                                 void *stream);
