@@ -982,6 +982,10 @@ int convio_conv_igemm_grouped(const convio_conv_desc *desc, const convio_tile *t
                   f16c_filter_bytes(desc), f16c_partials_bytes());
         return CONVIO_EINVAL;
     }
+    if ((int64_t)desc->n * layers > INT32_MAX || layer_bytes / 4 > (size_t)INT32_MAX) {
+        set_error("grouped 3xF16: layers * n (%lld) or the slice size overflows", (long long)desc->n * layers);
+        return CONVIO_EINVAL;
+    }
     convio_conv_desc dg = *desc;
     dg.n = desc->n * layers;   // the stacked batch
     IgemmPlan pl;
@@ -1041,13 +1045,9 @@ int convio_pack_filters_igemm_f16x3_batched(int32_t count, const convio_conv_des
     const int blocks = std::max(1, std::min(B.kcum[count], 148 * 8));
     if (max_crs <= kPackStageFloats) {
         const size_t smem = (size_t)((max_crs + 3) & ~3) * 4;
-        static bool attr = false;
-        if (!attr) {
-            CONVIO_CUDA_TRY(cudaFuncSetAttribute(pack_filters_f16x3_batched_kernel<true>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 kPackStageFloats * 4));
-            attr = true;
-        }
+        // (a per-device function attribute: set on every call, not cached per process)
+        CONVIO_CUDA_TRY(cudaFuncSetAttribute(pack_filters_f16x3_batched_kernel<true>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, kPackStageFloats * 4));
         CONVIO_CUDA_TRY(launch_pdl(pack_filters_f16x3_batched_kernel<true>, dim3(blocks), dim3(256), smem,
                                    (cudaStream_t)stream, B));
     } else {

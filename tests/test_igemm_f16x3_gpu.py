@@ -233,7 +233,9 @@ def test_batched_winograd_filter_transform_matches_per_filter(prec, e):
     (2, 4, 64, 56, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 4, layout="HWC")),     # halo fold
     (4, 32, 256, 14, 256, 1, TileConfig(2, 2, 256, 32768, 1, 1, 2, layout="HWC")),  # pair (+ tail split)
     (2, 32, 128, 28, 128, 2, TileConfig(2, 2, 128, 32768, 1, 1, 4, layout="HWC")),  # stride 2
-], ids=["tsa", "fold", "pair", "stride2"])
+    (2, 8, 128, 28, 128, 1, TileConfig(4, 4, 128, 32768, 1, 1, 8, layout="HWC")),   # gathered footprint
+    (3, 4, 64, 56, 64, 1, TileConfig(30, 4, 64, 32768, 2, 1, 2, layout="HWC")),     # fold, smem A, 3 layers
+], ids=["tsa", "fold", "pair", "stride2", "gather", "fold-smem-3"])
 def test_grouped_3xf16_conv_matches_per_layer_and_oracle(case):
     """convio_conv_igemm_grouped: G independent layers (own filters and biases) of one
     shape in one launch == G single-layer launches, and the oracle."""
