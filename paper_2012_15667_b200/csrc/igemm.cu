@@ -211,8 +211,12 @@ __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const _
         const float sc = pow2f(e);
         const float *src = STAGED ? stage : wr;
         const int pairs = (c + 1) / 2;
+        // (tap, pair) of t walked incrementally: one division per row, not one per pair
+        // (the per-pair division made this kernel issue-bound: 71 % issue slots busy)
+        const int dtap = (int)blockDim.x / pairs, dp = (int)blockDim.x - dtap * pairs;
+        int tap = (int)threadIdx.x / pairs, pp = (int)threadIdx.x - tap * pairs;
         for (int t = threadIdx.x; t < rs * pairs; t += blockDim.x) {
-            const int tap = t / pairs, cc = 2 * (t - tap * pairs);
+            const int cc = 2 * pp;
             __half *hrow = J.wq + ((int64_t)tap * k + kk) * c;
             const float v0 = src[cc * rs + tap] * sc;
             const float v1 = cc + 1 < c ? src[(cc + 1) * rs + tap] * sc : 0.0f;
@@ -225,6 +229,12 @@ __global__ void __launch_bounds__(256) pack_filters_f16x3_batched_kernel(const _
             } else {
                 hrow[cc] = __low2half(hi);
                 hrow[plane + cc] = __low2half(lo);
+            }
+            tap += dtap;
+            pp += dp;
+            if (pp >= pairs) {
+                pp -= pairs;
+                ++tap;
             }
         }
         if (threadIdx.x == 0) J.col_exp[kk] = e;
