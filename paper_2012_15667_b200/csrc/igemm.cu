@@ -354,6 +354,8 @@ static int plan_ring(IgemmPlan *pl, int bn, int kind, int s_b, bool pair, char *
         // na [A0 | A1] slots (released by the converters), the stages hold the filter planes
         const bool aring = pl->tsa && kind == KIND_3XF16C && !pl->halo;
         if (aring) pl->na = bn >= 256 ? 3 : (bn >= 128 ? 4 : 5);
+        if (const char *na = getenv("CONVIO_DEV_NA"))   // dev knob: A-ring depth sensitivity
+            if (aring) pl->na = std::max(2, std::min(6, atoi(na)));
         const size_t stage_bytes = (pl->tsa && kind == KIND_3XTF32) ? (size_t)(128 * 128 + 2 * (bn / 2) * 128)
                                            : (size_t)((pl->halo || aring ? 0 : 128 * 128) + (bn / 2) * 128) *
                                                  (loslot ? 1 : mult);

@@ -129,6 +129,17 @@ def test_group_layers_stacks_repeated_3xf16_layers(n):
             assert unit.x_of(g).data_ptr() == unit.x.data_ptr() + g * n * s.c * s.hw * s.hw * 4
     grouped = [idx for kind, _, idx in units if kind == "group"]
     assert grouped, "the tuned ResNet-50 tables put the repeated layers on 3xF16 pair tiles"
+    # bench.py's plans: the group table's overrides move repeated Winograd layers onto a
+    # grouped 3xF16 launch; every overridden layer then sits in a group with its tile
+    over = runner.load_group_overrides("resnet50", n)
+    plans.update(over)
+    layers = [runner.ConvLayer(s, torch.zeros(s.k, s.c, s.r, s.r), plans.get(s.name)) for s in specs]
+    gp = runner.load_group_plans("resnet50", n)
+    units = runner.group_layers(layers, n, "cpu", gp)
+    for name, plan in over.items():
+        idx = [i for i, s in enumerate(specs) if s.name == name]
+        unit = next(u for kind, u, ix in units if kind == "group" and ix == idx)
+        assert unit.tile == plan["tile"] == gp[name]
 
 
 def test_group_plans_table_gives_feasible_tiles():
