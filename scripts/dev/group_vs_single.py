@@ -14,6 +14,7 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 
 from paper_2012_15667_b200 import conv as C  # noqa: E402
+from paper_2012_15667_b200.dataflow import TileConfig  # noqa: E402
 from paper_2012_15667_b200.runner import WORKLOADS, load_plans, make_weights  # noqa: E402
 
 
@@ -36,9 +37,11 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--g", type=int, default=3)
     ap.add_argument("--plan-n", type=int, default=0)
+    ap.add_argument("--tile", default="", help="x,y,z,s_b,n_xt,n_yt,n_zt (HWC) instead of the table's")
     args = ap.parse_args()
     s = next(x for x in WORKLOADS["resnet50"] if x.name == args.layer)
-    tile = load_plans("resnet50", n=args.plan_n or args.n)[s.name]["tile"]
+    tile = (TileConfig(*[int(v) for v in args.tile.split(",")], layout="HWC") if args.tile
+            else load_plans("resnet50", n=args.plan_n or args.n)[s.name]["tile"])
     n, g = args.n, args.g
     dev = torch.device("cuda")
     w = make_weights(s, dev, 1)
