@@ -60,3 +60,36 @@ def test_plan_table_at_its_batch_matches_oracle(workload, n, plan_set):
         tol = tol_for(layer.algorithm, spec.c, layer.e)
         assert err <= tol, (spec.name, layer.algorithm, layer.tile, err, tol)
         del x, y
+
+
+@pytest.mark.parametrize("n", [256, 128, 64, 32])
+def test_grouped_units_at_bench_batch_match_oracle(n):
+    """The timed step as bench.py runs it: the group table's plan overrides and tiles,
+    each group of repeated layers in ONE grouped launch over the stacked batch, after
+    the step's batched filter prep -- every layer of every group against the C oracle
+    on its first and last two images."""
+    plans = R.load_plans("resnet50", n=n)
+    plans.update(R.load_group_overrides("resnet50", n))
+    dev = torch.device("cuda:0")
+    specs = R.expand(R.WORKLOADS["resnet50"])
+    layers = [R.ConvLayer(s, R.make_weights(s, dev, seed=1000 + i), plans.get(s.name)) for i, s in enumerate(specs)]
+    units = R.group_layers(layers, n, dev, R.load_group_plans("resnet50", n))
+    groups = [(u, idx) for kind, u, idx in units if kind == "group"]
+    assert groups, "the bench step has grouped launches at this batch"
+    for u, idx in groups:
+        for g, i in enumerate(idx):
+            u.x_of(g).copy_(R.make_input(specs[i], n, dev, seed=7919 * (i + 1), layout="HWC"))
+    R.prepare_layers(layers, dev)
+    imgs = _edge_images(n)
+    for u, idx in groups:
+        u.run()
+        torch.cuda.synchronize()
+        for g, i in enumerate(idx):
+            spec, layer = specs[i], layers[i]
+            xs = u.x_of(g)[imgs].contiguous().cpu().numpy()
+            ref = co.c_direct_conv(xs, layer.weight.cpu().numpy(), spec.stride, spec.pad)
+            err = co.rel_err(u.y_of(g)[imgs].contiguous().cpu().numpy(), ref)
+            tol = tol_for("igemm_3xf16", spec.c, None)
+            assert err <= tol, (spec.name, g, u.tile, err, tol)
+    del units, groups, layers
+    torch.cuda.empty_cache()
