@@ -24,7 +24,7 @@ import torch
 
 from . import conv as C
 from .dataflow import TileConfig
-from .runner import VGG16_3X3, ConvLayer, load_plans, make_weights
+from .runner import VGG16_3X3, ConvLayer, load_plans, make_weights, plan_for
 
 # the 13 convolutions in order, "M" = 2x2 max pool; names map to the tuned table's
 # layer shapes (conv3_3 has conv3_2's shape, conv4_3 conv4_2's, conv5_x conv5_1's)
@@ -54,7 +54,8 @@ class Vgg16Features:
                 self.layers.append(None)
                 continue
             spec = specs[_SHAPE_OF.get(name, name)]
-            plan = dict(plans.get(spec.name) or {})
+            # (a table tuned at another batch may hold tiles this batch cannot take)
+            plan = dict(plan_for(spec, n, plans))
             if name == "conv1_1" or (plan.get("tile") is not None and plan["tile"].layout != "HWC"):
                 plan = {"algorithm": "direct", "tile": CONV1_1_HWC if spec.c <= 4 else None, "e": None}
             layer = ConvLayer(spec, make_weights(spec, self.device, seed + i), plan)

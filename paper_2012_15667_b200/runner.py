@@ -146,6 +146,51 @@ def load_plans(workload: str, allowed=FP32_ALGORITHMS, n: int | None = None) -> 
     return plans
 
 
+# untuned shapes: CTA-pair tiles tried in order (x, y) -- small pixel blocks of many
+# stacked images first (deep layers), larger blocks for wide feature maps
+_DEFAULT_XY = [(2, 2), (1, 2), (2, 1), (1, 1), (4, 2), (2, 4), (4, 4), (7, 7), (8, 8), (14, 8), (16, 8)]
+
+
+def plan_feasible(spec: "LayerSpec", n: int, plan: dict | None) -> bool:
+    """Whether ``plan`` runs ``spec`` at batch ``n`` (the library's planner, host only;
+    FFMA kernels take any batch)."""
+    if not plan or plan.get("tile") is None or plan.get("algorithm") in ("direct", "winograd", "winograd_nhwc"):
+        return True
+    t = plan["tile"]
+    alg = plan["algorithm"]
+    try:
+        info = C.query((n, spec.c, spec.hw, spec.hw), (spec.k, spec.c, spec.r, spec.r), spec.stride, spec.pad,
+                       t.layout, t, alg)
+    except Exception:  # noqa: BLE001 -- an unknown algorithm name is infeasible here
+        return False
+    return info.get("rc", 1) == 0
+
+
+def default_plan(spec: "LayerSpec", n: int) -> dict:
+    """The plan of a layer no tuned table covers (or whose tuned tile does not fit
+    batch ``n``): the FP32-accurate 3xF16 implicit GEMM (C % 64 == 0) or 3xTF32 (C % 32
+    == 0) on the first CTA-pair tile the planner accepts, else the FFMA direct kernel
+    with its default tile -- instead of always falling back to FFMA."""
+    for alg, cmod in (("igemm_3xf16", 64), ("igemm_3xtf32", 32)):
+        if spec.c % cmod:
+            continue
+        for z in (256, 128, 64):
+            if spec.k % z:
+                continue
+            for nzt in (2, 4):
+                for x, y in _DEFAULT_XY:
+                    plan = {"algorithm": alg, "tile": TileConfig(x, y, z, 32768, 1, 1, nzt, layout="HWC"), "e": None}
+                    if plan_feasible(spec, n, plan):
+                        return plan
+    return {"algorithm": "direct", "tile": None, "e": None}
+
+
+def plan_for(spec: "LayerSpec", n: int, plans: dict) -> dict:
+    """``plans[spec.name]`` when it runs at batch ``n``, else :func:`default_plan`."""
+    plan = plans.get(spec.name)
+    return plan if plan is not None and plan_feasible(spec, n, plan) else default_plan(spec, n)
+
+
 # 3xF16 implicit GEMM: the speculative activation-scale state (tagged max |x| of the
 # previous call + one observed max per CTA) at the start of the layer's workspace; it
 # persists across calls, which is what lets the second and later calls skip the redo

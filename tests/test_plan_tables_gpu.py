@@ -93,3 +93,20 @@ def test_grouped_units_at_bench_batch_match_oracle(n):
             assert err <= tol, (spec.name, g, u.tile, err, tol)
     del units, groups, layers
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape", [(192, 17, 192, 1), (512, 7, 512, 1), (256, 28, 512, 2), (96, 35, 96, 1)])
+def test_default_plan_matches_oracle(shape):
+    """runner.default_plan (untuned shapes) through the runner, against the C oracle."""
+    c, hw, k, stride = shape
+    spec = R.LayerSpec("untuned", c, hw, k, stride=stride)
+    n = 3
+    dev = torch.device("cuda:0")
+    plan = R.default_plan(spec, n)
+    layer = R.ConvLayer(spec, R.make_weights(spec, dev, seed=5), plan)
+    x = R.make_input(spec, n, dev, seed=11, layout=layer.layout)
+    y = layer.forward(x)
+    torch.cuda.synchronize()
+    ref = co.c_direct_conv(x.contiguous().cpu().numpy(), layer.weight.cpu().numpy(), spec.stride, spec.pad)
+    err = co.rel_err(y.contiguous().cpu().numpy(), ref)
+    assert err <= tol_for(layer.algorithm, spec.c, layer.e), (plan, err)

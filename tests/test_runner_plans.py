@@ -170,3 +170,24 @@ def test_group_plans_table_gives_feasible_tiles():
                 assert t is None and ent["singles_us"] <= ent["us"]
                 continue
             assert t.n_zt >= 2 and t.layout == "HWC"
+
+
+@pytest.mark.parametrize("shape,alg", [((192, 17, 192, 1), "igemm_3xf16"), ((512, 7, 512, 1), "igemm_3xf16"),
+                                       ((256, 28, 512, 2), "igemm_3xf16"), ((96, 35, 96, 1), "direct"),
+                                       ((3, 64, 32, 1), "direct")])
+def test_default_plan_for_untuned_shapes(shape, alg):
+    """A layer no tuned table covers gets the FP32-accurate tensor-core plan the planner
+    accepts at its batch (FFMA direct only when no tcgen05 tile applies); plan_for keeps a
+    tuned plan that fits the batch and replaces one that does not."""
+    c, hw, k, stride = shape
+    spec = runner.LayerSpec("untuned", c, hw, k, stride=stride)
+    for n in (1, 5, 64):
+        plan = runner.default_plan(spec, n)
+        assert plan["algorithm"] == alg
+        assert runner.plan_feasible(spec, n, plan)
+    tuned = runner.load_plans("resnet50", n=256)
+    res4 = next(s for s in runner.WORKLOADS["resnet50"] if s.name == "res4_3x3")
+    assert runner.plan_for(res4, 256, tuned) is tuned["res4_3x3"]
+    big_stack = {"res4_3x3": {"algorithm": "igemm_3xf16", "e": None,
+                              "tile": TileConfig(1, 1, 256, 32768, 1, 1, 2, layout="HWC")}}
+    assert runner.plan_feasible(res4, 256, big_stack["res4_3x3"])
