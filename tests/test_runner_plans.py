@@ -142,19 +142,20 @@ def test_group_layers_stacks_repeated_3xf16_layers(n):
         assert unit.tile == plan["tile"] == gp[name]
 
 
-def test_group_plans_table_gives_feasible_tiles():
+@pytest.mark.parametrize("workload", ["resnet50", "vgg16"])
+def test_group_plans_table_gives_feasible_tiles(workload):
     """The committed grouped-launch table (scripts/tune_groups.py): every per-batch group
     entry names a real repeated layer, its best tile is one of its measured candidates,
     and the tile's CTA-pair image stack divides the per-layer batch."""
-    path = runner.group_table("resnet50")
+    path = runner.group_table(workload)
     if not os.path.exists(path):
         pytest.skip("no grouped-launch table")
     tab = json.load(open(path))
-    names = {s.name: s for s in runner.WORKLOADS["resnet50"]}
+    names = {s.name: s for s in runner.WORKLOADS[workload]}
     for n, groups in tab["groups"].items():
-        plans = runner.load_group_plans("resnet50", int(n))
+        plans = runner.load_group_plans(workload, int(n))
         assert set(plans) == set(groups)
-        overrides = runner.load_group_overrides("resnet50", int(n))
+        overrides = runner.load_group_overrides(workload, int(n))
         for name, ent in groups.items():
             assert names[name].count == ent["layers"] >= 2
             if ent.get("replaces"):   # a repeated non-3xF16 layer moved onto a grouped 3xF16 launch
