@@ -62,18 +62,19 @@ def test_plan_table_at_its_batch_matches_oracle(workload, n, plan_set):
         del x, y
 
 
-@pytest.mark.parametrize("n", [256, 128, 64, 32])
-def test_grouped_units_at_bench_batch_match_oracle(n):
+@pytest.mark.parametrize("workload,n", [("resnet50", 256), ("resnet50", 128), ("resnet50", 64), ("resnet50", 32),
+                                        ("vgg16", 32)])
+def test_grouped_units_at_bench_batch_match_oracle(workload, n):
     """The timed step as bench.py runs it: the group table's plan overrides and tiles,
     each group of repeated layers in ONE grouped launch over the stacked batch, after
     the step's batched filter prep -- every layer of every group against the C oracle
     on its first and last two images."""
-    plans = R.load_plans("resnet50", n=n)
-    plans.update(R.load_group_overrides("resnet50", n))
+    plans = R.load_plans(workload, n=n)
+    plans.update(R.load_group_overrides(workload, n))
     dev = torch.device("cuda:0")
-    specs = R.expand(R.WORKLOADS["resnet50"])
+    specs = R.expand(R.WORKLOADS[workload])
     layers = [R.ConvLayer(s, R.make_weights(s, dev, seed=1000 + i), plans.get(s.name)) for i, s in enumerate(specs)]
-    units = R.group_layers(layers, n, dev, R.load_group_plans("resnet50", n))
+    units = R.group_layers(layers, n, dev, R.load_group_plans(workload, n))
     groups = [(u, idx) for kind, u, idx in units if kind == "group"]
     assert groups, "the bench step has grouped launches at this batch"
     for u, idx in groups:
