@@ -1308,6 +1308,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                     real = PP.gather ? m < a_rows : fr < fp_rows;
                 } else {   // ARING: the A slot (the filter planes are the MMA issuer's to wait for)
                     mbar_wait(afull + sa, pha);
+                    if (warp == 8 && lane == 0) EPI_TRACE(21, it);   // (trace builds) A data here
                     row = smem_u32(aring + sa * ASLOT) + (h ? (uint32_t)A_BYTES : 0u) + (uint32_t)m * 128;
                     sw = m & 7;
                     real = m < a_rows;
@@ -1336,6 +1337,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pair_threads<BN, KIN
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(tconv_leader + (uint32_t)(ta * 8));
+                if (warp == 8 && lane == 0) EPI_TRACE(22, it);   // (trace builds) signalled
                 if (++ta == NTA) {
                     ta = 0;
                     pht ^= 1;

@@ -71,6 +71,12 @@ def main():
     if k1:
         print(f"converter: data-wait after issue (C1-P) med {med(C1[:k1] - P[:k1]):.0f} cyc, "
               f"convert (C2-C1) med {med(C2[:k1] - C1[:k1]):.0f}")
+    f21, f22 = fine[3] - t0, fine[4] - t0   # converter warp 8, CTA 0: A data seen / tconv signalled
+    if k1 and (fine[3] > 0).sum() and (fine[4] > 0).sum():
+        kk = min(k1, int((fine[3] > 0).sum()), int((fine[4] > 0).sum()))
+        print(f"converter fine (ARING): C2 -> signalled med {med(f22[:kk] - C2[:kk]):.0f}, "
+              f"signalled -> next A data med {med(f21[1:kk] - f22[:kk - 1]):.0f}, "
+              f"A data -> C1 (TMEM slot free) med {med(C1[1:kk] - f21[1:kk]):.0f}")
     gaps = [M3[i] - M4[i - 1] for i in range(1, k)]
     per = [M4[i] - M4[i - 1] for i in range(1, k)]
     print(f"MMA issuer: k-block period med {med(per):.0f} cyc, idle waiting for data med {med(gaps):.0f} "
