@@ -594,7 +594,8 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2012_15667_b200 import conv as C
     from paper_2012_15667_b200.runner import (
-        WORKLOADS, ConvLayer, expand, group_layers, load_group_overrides, load_group_plans, load_plans,
+        WORKLOADS, ConvLayer, expand, group_layers, group_table, load_group_overrides, load_group_plans,
+        load_plans,
         make_input, make_weights,
         prepare_layers,
         shard_range,
@@ -1163,6 +1164,8 @@ def main() -> None:
                          f"launch per layer and per-layer events ({eager_ms / args.steps:.4f} ms/step)"
                          if graph_used else "eager launches, one per layer"),
                 "tuned_table": os.path.basename(tuned_table(args.workload, n_local)),
+                "group_table": (os.path.basename(group_table(args.workload))
+                                if not args.no_group and os.path.exists(group_table(args.workload)) else None),
                 "plans": "per layer the fastest device-tuned FP32-accurate algorithm: direct / Winograd "
                          "(FFMA), 3xTF32 tcgen05 implicit GEMM or 3xTF32 tcgen05 Winograd "
                          "(FP32-level GEMM accuracy)",
