@@ -45,6 +45,17 @@ def candidate_tiles(workload, name):
     return tiles
 
 
+def domain_tiles(spec, n_stacked, cap):
+    """The 3xF16 tcgen05 searching domain of the STACKED problem (device_tuner.tcgen05_space
+    at batch G*n, I/O-model pruned), the ``cap`` members with the least modelled traffic."""
+    from paper_2012_15667_b200.device import shape_of
+    from paper_2012_15667_b200.device_tuner import set_padding, tcgen05_hw_model, tcgen05_io_words, tcgen05_space
+    set_padding(spec.pad)
+    shape = shape_of(n_stacked, spec.c, spec.hw, spec.hw, spec.k, spec.r, spec.stride, spec.pad)
+    space = tcgen05_space(shape, tcgen05_hw_model(), "igemm_3xf16", check_legal=False)
+    return sorted(space.members, key=lambda t: tcgen05_io_words(shape, t))[:cap]
+
+
 def time_us(fn, reps, rounds=5):
     for _ in range(3):
         fn()
@@ -77,17 +88,70 @@ def time_graph_us(fn, reps, rounds=5):
     return time_us(g.replay, reps, rounds)
 
 
+def merge(paths, out_path):
+    """Combine group tables tuned on different boxes (box-to-box spread is ~10 %): per
+    group, the tile with the least geometric-mean time over the runs that measured it in
+    all of them; a replacement only when it won in every run."""
+    import math
+    tabs = [json.load(open(p)) for p in paths]
+    out = dict(tabs[0])
+    out["method"] = tabs[0]["method"] + f"; merged over {len(tabs)} runs on different boxes (geometric mean)"
+    out["groups"] = {}
+    for n in tabs[0]["groups"]:
+        res = {}
+        for name, ent in tabs[0]["groups"][n].items():
+            ents = [t["groups"].get(n, {}).get(name) for t in tabs]
+            if any(e is None for e in ents):
+                continue
+            key = "us_with_prep" if ent.get("replaces") else "us"
+            times = {}
+            for e in ents:
+                for c in e["candidates"]:
+                    if key in c:
+                        times.setdefault(json.dumps(c["tile"], sort_keys=True), []).append(c[key])
+            full = {k: math.exp(sum(map(math.log, v)) / len(v)) for k, v in times.items() if len(v) == len(tabs)}
+            if not full:
+                continue
+            best = min(full, key=full.get)
+            merged = dict(ent)
+            merged["tile"] = json.loads(best)
+            merged[key] = round(full[best], 2)
+            merged["runs"] = [{k: e.get(k) for k in ("tile", key, "own_plan_us", "singles_us", "own_us_with_prep",
+                                                     "use_group")} for e in ents]
+            if ent.get("replaces"):
+                own = math.exp(sum(math.log(e["own_us_with_prep"]) for e in ents) / len(ents))
+                merged["own_us_with_prep"] = round(own, 2)
+                if not (all(e.get("use_group") for e in ents) and full[best] < 0.97 * own):
+                    continue   # not a clear win on every box: keep the layer's own plan
+            else:
+                singles = math.exp(sum(math.log(e["singles_us"]) for e in ents) / len(ents))
+                merged["singles_us"] = round(singles, 2)
+                merged["use_group"] = full[best] < singles
+            res[name] = merged
+        out["groups"][n] = res
+    with open(out_path, "w") as fh:
+        json.dump(out, fh, indent=1, sort_keys=True)
+    print("wrote", out_path)
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--merge":   # --merge OUT A.json B.json ...
+        merge(sys.argv[3:], sys.argv[2])
+        return
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="resnet50")
     ap.add_argument("--batches", default="32,64,128,256")
     ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--domain", type=int, default=0,
+                    help="also race this many members of the stacked problem's tcgen05 domain")
     args = ap.parse_args()
     dev = torch.device("cuda")
     specs = expand(WORKLOADS[args.workload])
     out = {"workload": args.workload, "device": torch.cuda.get_device_name(),
            "method": "grouped launch timed with CUDA events (median of 5 x reps back-to-back), "
-                     "candidates = the layer's igemm_3xf16 tiles from every per-batch table",
+                     "candidates = the layer's igemm_3xf16 tiles from every per-batch table"
+                     + (f" + {args.domain} members of the stacked problem's tcgen05 domain (least modelled "
+                        "SM<->L2 traffic first)" if args.domain else ""),
            "groups": {}}
     for n in [int(b) for b in args.batches.split(",")]:
         plans = load_plans(args.workload, n=n)
@@ -103,7 +167,10 @@ def main():
                 grp.x_of(g).copy_(make_input(specs[i], n, dev, seed=7919 * (i + 1), layout="HWC"))
             own = grp.tile
             cands = []
-            for t in [own] + [t for t in candidate_tiles(args.workload, name) if t != own]:
+            tiles = [own] + [t for t in candidate_tiles(args.workload, name) if t != own]
+            if args.domain:
+                tiles += [t for t in domain_tiles(specs[idx[0]], n * len(idx), args.domain) if t not in tiles]
+            for t in tiles:
                 grp.tile = t
                 try:
                     us = time_us(lambda: grp.run(), args.reps)
@@ -159,7 +226,10 @@ def main():
             for q in range(len(idx)):
                 grp.x_of(q).copy_(xs[q])
             cands = []
-            for t in [ig_plan["tile"]] + [t for t in candidate_tiles(args.workload, name) if t != ig_plan["tile"]]:
+            tiles = [ig_plan["tile"]] + [t for t in candidate_tiles(args.workload, name) if t != ig_plan["tile"]]
+            if args.domain:
+                tiles += [t for t in domain_tiles(specs[idx[0]], n * len(idx), args.domain) if t not in tiles]
+            for t in tiles:
                 grp.tile = t
 
                 def ig_step(st):
