@@ -292,6 +292,16 @@ def load_group_overrides(workload: str, n: int) -> dict:
             if ent.get("replaces") and ent.get("use_group", True)}
 
 
+def group_stack_ok(tile: TileConfig, n: int, layers: int) -> bool:
+    """Whether a grouped launch of ``layers`` x ``n`` images can use ``tile``: its CTA-pair
+    blocks stack ``min(128 / (x y), layers * n)`` images (1 for halo tiles), and a stack
+    must not straddle two layers (convio_conv_igemm_grouped)."""
+    if tile.n_zt < 2:
+        return False
+    imgs = 1 if tile.n_xt == 2 else max(1, min(128 // (tile.x * tile.y), layers * n))
+    return n % imgs == 0
+
+
 def group_layers(layers, n: int, device, group_plans: dict | None = None) -> list:
     """Runs of consecutive layers with the same shape and the same 3xF16 implicit-GEMM
     plan (CTA-pair tiles whose image stack divides ``n``) as :class:`LayerGroup`; other
@@ -307,11 +317,14 @@ def group_layers(layers, n: int, device, group_plans: dict | None = None) -> lis
                 j += 1
         if j - i >= 2 and group_plans and l.spec.name in group_plans and group_plans[l.spec.name] is None:
             j = i + 1   # measured: single launches win for this group
+        tile = group_plans.get(l.spec.name) if group_plans else None
+        tile = tile or l.tile
+        if j - i >= 2 and not group_stack_ok(tile, n, j - i):
+            j = i + 1   # e.g. an untabled batch whose image stacks would straddle layers
         if j - i >= 2:
             try:
                 grp = LayerGroup(layers[i:j], n, device)
-                if group_plans and l.spec.name in group_plans:
-                    grp.tile = group_plans[l.spec.name]
+                grp.tile = tile
                 units.append(("group", grp, list(range(i, j))))
             except ValueError:
                 units += [("single", layers[k], [k]) for k in range(i, j)]

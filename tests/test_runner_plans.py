@@ -194,3 +194,18 @@ def test_default_plan_for_untuned_shapes(shape, alg):
     big_stack = {"res4_3x3": {"algorithm": "igemm_3xf16", "e": None,
                               "tile": TileConfig(1, 1, 256, 32768, 1, 1, 2, layout="HWC")}}
     assert runner.plan_feasible(res4, 256, big_stack["res4_3x3"])
+
+
+def test_group_layers_skips_stacks_that_straddle_layers():
+    """At a batch no table was tuned for, a group whose tile stacks more images per CTA
+    pair than divide the per-layer batch runs as single launches instead of failing."""
+    t64 = TileConfig(1, 2, 256, 32768, 1, 1, 2, layout="HWC")      # 64 images per stack
+    assert runner.group_stack_ok(t64, 128, 5) and not runner.group_stack_ok(t64, 96, 5)
+    assert runner.group_stack_ok(TileConfig(30, 4, 64, 32768, 2, 1, 4, layout="HWC"), 7, 3)   # halo: 1 image
+    t32 = TileConfig(2, 2, 256, 32768, 1, 1, 2, layout="HWC")     # min(32, 5 x n) images per stack
+    assert runner.group_stack_ok(t32, 32, 5) and not runner.group_stack_ok(t32, 1, 5)
+    spec = next(s for s in runner.WORKLOADS["resnet50"] if s.name == "res4_3x3")
+    plan = {"algorithm": "igemm_3xf16", "tile": t64, "e": None}
+    layers = [runner.ConvLayer(spec, torch.zeros(spec.k, spec.c, 3, 3), plan) for _ in range(5)]
+    assert [k for k, _, _ in runner.group_layers(layers, 96, "cpu")] == ["single"] * 5
+    assert [k for k, _, _ in runner.group_layers(layers, 128, "cpu")] == ["group"]
