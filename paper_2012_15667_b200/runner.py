@@ -107,13 +107,34 @@ def candidate_algorithm(key: str) -> tuple[str, int | None]:
 def tuned_table(workload: str, n: int | None = None) -> str:
     """Path of the tuned table for ``workload``: the per-batch table
     ``b200_<workload>_n<n>.json`` tuned at the local batch of a sharded run
-    (strong scaling gives each rank N/G images) when one exists, else the table
-    tuned at the workload's full batch."""
-    if n is not None:
-        path = os.path.join(TUNED_DIR, f"b200_{workload}_n{n}.json")
-        if os.path.exists(path):
-            return path
-    return os.path.join(TUNED_DIR, f"b200_{workload}.json")
+    (strong scaling gives each rank N/G images) when one exists; for a batch no table
+    was tuned at, the table tuned at the nearest batch (log scale: its tiles' image
+    stacks and grid shapes were chosen for a similar work size); else the table tuned
+    at the workload's full batch."""
+    default = os.path.join(TUNED_DIR, f"b200_{workload}.json")
+    if n is None:
+        return default
+    path = os.path.join(TUNED_DIR, f"b200_{workload}_n{n}.json")
+    if os.path.exists(path):
+        return path
+    import glob
+    import math
+    cands = []
+    if os.path.exists(default):
+        try:
+            with open(default) as fh:
+                n_tune = json.load(fh).get("n_tune")
+        except (OSError, ValueError):
+            n_tune = None
+        if n_tune:
+            cands.append((int(n_tune), default))
+    for p in glob.glob(os.path.join(TUNED_DIR, f"b200_{workload}_n*.json")):
+        tail = os.path.basename(p)[len(f"b200_{workload}_n"):-len(".json")]
+        if tail.isdigit():
+            cands.append((int(tail), p))
+    if not cands or n < 1:
+        return default
+    return min(cands, key=lambda c: (abs(math.log(n / c[0])), -c[0]))[1]
 
 
 def load_plans(workload: str, allowed=FP32_ALGORITHMS, n: int | None = None) -> dict:

@@ -101,7 +101,9 @@ def test_per_batch_table_preferred_for_the_local_batch(tmp_path, monkeypatch):
     monkeypatch.setattr(runner, "TUNED_DIR", str(d))
     assert runner.load_plans("toy")["L"]["tile"].z == 256
     assert runner.load_plans("toy", n=32)["L"]["tile"].z == 128
-    assert runner.load_plans("toy", n=64)["L"]["tile"].z == 256   # no n64 table: full-batch one
+    assert runner.load_plans("toy", n=64)["L"]["tile"].z == 128   # no n64 table: the nearest batch's (32)
+    assert runner.load_plans("toy", n=200)["L"]["tile"].z == 256  # nearer the full-batch table
+    assert runner.tuned_table("toy", 8).endswith("b200_toy_n32.json")
 
 
 @pytest.mark.parametrize("n", [256, 32])
