@@ -43,9 +43,10 @@ def main():
             C.conv_igemm(x, w, padding=0, tile=tile, precision=prec, w_packed=wp, out=out, workspace=ws)
         torch.cuda.synchronize()
         return
-    for prec in ("tf32", "bf16", "3xtf32"):
-        wp = C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm(w)
-        for z, nzt in ((256, 2), (128, 2), (128, 1), (256, 1)):
+    for prec in ("tf32", "bf16", "3xtf32", "3xf16"):
+        wp = (C.pack_filter_igemm_bf16(w) if prec == "bf16" else C.pack_filter_igemm_f16x3(w) if prec == "3xf16"
+              else C.pack_filter_igemm(w))
+        for z, nzt in ((256, 2), (128, 2), (128, 1), (256, 1), (128, 4)):
             tile = TileConfig(128, 1, z, 65536, 1, 1, nzt, layout="HWC")
             try:
                 t = timeit(lambda: C.conv_igemm(x, w, padding=0, tile=tile, precision=prec,
@@ -53,7 +54,7 @@ def main():
             except Exception as exc:  # noqa: BLE001
                 print(f"{prec:7s} z={z} n_zt={nzt}: {exc}")
                 continue
-            mult = 3 if prec == "3xtf32" else 1
+            mult = 3 if prec in ("3xtf32", "3xf16") else 1
             print(f"{prec:7s} z={z:3d} n_zt={nzt}: {t * 1e3:7.3f} ms {flops / t / 1e12:7.1f} TF/s "
                   f"(MMA rate {mult * flops / t / 1e12:7.1f})", flush=True)
     a = torch.rand(m, k, device="cuda")
